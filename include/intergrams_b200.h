@@ -1,0 +1,182 @@
+/* intergrams_b200.h — the C-ABI drop-in boundary of the B200-native Intergrams
+ * top-k n-gram counter (arxiv 2511.14955).
+ *
+ * The reference exposes its hot path as the C++ API in
+ * /root/reference/proj/include/intergrams/ (no FFI of its own):
+ *   run_intergrams   intergrams.hpp:74-75   (driver, src/intergrams.cpp:68-166)
+ *   extend_pass      intergrams.hpp:70-72   (src/intergrams.cpp:44-66)
+ *   count_dense      dense_pass.hpp:25-28   (src/dense_pass.cpp:21-39)
+ *   top_k            counting.hpp:112-113   (src/counting.cpp:52-98)
+ * Every entry point below replaces one of those; the C++ drop-in headers in
+ * include/intergrams/ re-expose the reference's own signatures on top of it.
+ * Plain pointers and sizes only; no torch or STL types cross this boundary.
+ *
+ * Corpus layout (CSR): data[0..offsets[m]) bytes, offsets[m+1] u64 with
+ * offsets[0] == 0; sequence i is data[offsets[i] .. offsets[i+1]).  This is
+ * the enumeration order of Corpus::for_each (corpus.hpp:46-64).
+ *
+ * Gram keys: a gram of L <= 8 bytes is a u64, key = sum b_i << 8*(L-1-i)
+ * (big-endian), so for one L numeric order == the reference's unsigned-byte
+ * tie-break order (counting.hpp:38-41).  Output lists are canonical: count
+ * descending, then key ascending.
+ *
+ * Return codes mirror the reference's exception classes (common.hpp:12-22,
+ * cli.cpp:427-439):  IG_OK 0, IG_ECONFIG 2 (ConfigError), IG_EIO 3 (IoError),
+ * IG_EINTERNAL 4 (CUDA / collective / allocation failure), IG_EINVALID 5
+ * (std::invalid_argument from PrefixTrie::build / lookup, trie.cpp:26-46,142).
+ * On error `err` (if non-NULL) receives a NUL-terminated message.
+ *
+ * Threading: calls on one session are serialised by the caller; sessions on
+ * different devices are independent.  No global mutable state.
+ */
+#ifndef INTERGRAMS_B200_H
+#define INTERGRAMS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define IG_API __attribute__((visibility("default")))
+#else
+#define IG_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define IG_OK 0
+#define IG_ECONFIG 2
+#define IG_EIO 3
+#define IG_EINTERNAL 4
+#define IG_EINVALID 5
+
+/* CountMode (counting.hpp:19). */
+#define IG_MODE_ONCE 0
+#define IG_MODE_ALL 1
+
+/* Where ig_corpus pointers live. */
+#define IG_HOST 0
+#define IG_DEVICE 1
+
+/* Largest gram length the packed-u64 path supports.  run_intergrams with
+ * n > IG_MAX_N returns IG_ECONFIG. */
+#define IG_MAX_N 8
+
+typedef struct {
+  const uint8_t* data;      /* bytes; host or device per `location` */
+  const uint64_t* offsets;  /* num_seqs + 1 entries, same location as data */
+  uint64_t num_seqs;        /* m */
+  int32_t location;         /* IG_HOST or IG_DEVICE */
+} ig_corpus;
+
+/* IntergramConfig (intergrams.hpp:19-33).  merge / workers /
+ * flush_batch_size / frequency_ordered_trie never change results in the
+ * reference (tests/test_dense_pass.cpp:141-161, test_trie.cpp:134-150) and
+ * have no GPU meaning; flush_batch_size is still validated. */
+typedef struct {
+  uint32_t n;
+  uint64_t k;
+  double z;
+  int32_t mode;             /* IG_MODE_ONCE / IG_MODE_ALL */
+  uint64_t flush_batch_size;/* validated only (>= 1) */
+  int32_t device;           /* CUDA ordinal; -1 = current */
+} ig_params;
+
+/* PassResult (intergrams.hpp:35-47). seconds are device-event times. */
+typedef struct {
+  char label[48];
+  uint32_t gram_len;
+  double seconds;
+  uint64_t bytes_processed;
+  uint64_t candidate_space;
+  uint64_t retained;
+  int32_t retained_short;
+} ig_pass_stat;
+
+/* IntergramsResult (intergrams.hpp:49-53); library-allocated, release with
+ * ig_result_free. */
+typedef struct {
+  uint64_t len;            /* entries in keys/counts */
+  uint32_t gram_len;       /* n */
+  uint64_t* keys;          /* packed big-endian grams, canonical order */
+  uint64_t* counts;
+  ig_pass_stat* passes;
+  uint32_t num_passes;
+  char* diagnostics;       /* '\n'-separated, NUL-terminated */
+} ig_result;
+
+/* Optional cross-rank hook for multi-GPU runs (one process per GPU).  The
+ * library shards nothing itself: each rank passes its own whole-sequence
+ * shard (see ig_shard_range) and the library calls allreduce once per
+ * counting pass on the device count table (sum, in place, on `stream`).
+ * dtype: 0 = u32, 1 = u64.  bytes_total / seqs_total are the GLOBAL corpus
+ * totals (they choose the counter width identically on every rank and are
+ * what PassResult::bytes_processed reports). */
+typedef struct {
+  int32_t rank;
+  int32_t world;
+  uint64_t bytes_total;
+  uint64_t seqs_total;
+  int (*allreduce)(void* dev_buf, uint64_t count, int32_t dtype,
+                   void* cuda_stream, void* user);
+  void* user;
+} ig_collective;
+
+/* ---- one-shot entry point: run_intergrams (src/intergrams.cpp:68-166) ---- */
+IG_API int ig_topk_ngrams(const ig_corpus* corpus, const ig_params* params,
+                   ig_result* out, char* err, size_t err_len);
+IG_API void ig_result_free(ig_result* r);
+
+/* ---- session API: corpus resident in HBM across runs ---------------------
+ * ig_session_create binds a device and (optionally) a collective.  load
+ * copies a host corpus (or adopts a device corpus without copying).  run
+ * executes run_intergrams on the resident corpus.  stream: cudaStream_t or
+ * NULL for a library-owned stream. */
+typedef struct ig_session ig_session;
+IG_API int ig_session_create(int32_t device, void* cuda_stream,
+                      const ig_collective* coll, ig_session** out, char* err,
+                      size_t err_len);
+IG_API int ig_session_load(ig_session* s, const ig_corpus* corpus, char* err,
+                    size_t err_len);
+IG_API int ig_session_run(ig_session* s, const ig_params* params, ig_result* out,
+                   char* err, size_t err_len);
+/* Kernel launches issued by the last run (for launch accounting). */
+IG_API uint64_t ig_session_launches(const ig_session* s);
+IG_API void ig_session_destroy(ig_session* s);
+
+/* ---- pass-level entry points (parity of the reference's tables) ---------- */
+/* count_dense (dense_pass.cpp:21-39): table_out receives 256^n u64, n 1..3. */
+IG_API int ig_count_dense(const ig_corpus* corpus, uint32_t n, int32_t mode,
+                   int32_t device, uint64_t* table_out, char* err,
+                   size_t err_len);
+
+/* extend_pass (intergrams.cpp:44-66) over the prefix list `prefix_keys`
+ * (nprefix keys of prefix_len bytes, rank order; ordinal = index).
+ * table_out receives 256*nprefix u64 indexed ordinal*256 + last byte
+ * (candidate_id, intergrams.hpp:56-59).  An empty list is a depth-0 trie. */
+IG_API int ig_extend_pass(const ig_corpus* corpus, const uint64_t* prefix_keys,
+                   uint64_t nprefix, uint32_t prefix_len, uint32_t j,
+                   int32_t mode, int32_t device, uint64_t* table_out,
+                   uint64_t* bytes_processed, char* err, size_t err_len);
+
+/* top_k (counting.cpp:52-98) of a host u64 table whose gram key is the id
+ * (prefix_keys == NULL) or (prefix_keys[id>>8] << 8) | (id & 255).  Writes
+ * min(k, nonzero) entries; returns IG_ECONFIG for k < 1. */
+IG_API int ig_top_k(const uint64_t* table, uint64_t cap, uint64_t k,
+             const uint64_t* prefix_keys, int32_t device, uint64_t* keys_out,
+             uint64_t* counts_out, uint64_t* len_out, char* err,
+             size_t err_len);
+
+/* Byte-balanced whole-sequence shard [*first, *last) of rank r of world w:
+ * cut at the sequence boundary nearest r*total/w.  Host-only, no device. */
+IG_API void ig_shard_range(const uint64_t* offsets, uint64_t num_seqs, int32_t rank,
+                    int32_t world, uint64_t* first, uint64_t* last);
+
+/* Library version string. */
+IG_API const char* ig_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

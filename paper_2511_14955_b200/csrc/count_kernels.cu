@@ -1,0 +1,478 @@
+// count_kernels.cu — the counting passes of Intergrams on sm_100a.
+//
+// Reference semantics:
+//   dense pass     proj/src/intergrams.cpp:79-100 (= dense_pass.cpp:21-39):
+//                  every n0-gram of every sequence, id = big-endian bytes.
+//   extension pass proj/src/intergrams.cpp:44-66: every j-gram whose (j-1)-byte
+//                  prefix is a survivor p; id = p*256 + last byte.
+//   count-all      pipeline.hpp:106-113: counts[id] += 1 per occurrence.
+//   count-once     counting.hpp:48-74 + counting.cpp:27-50: counts[id] += 1 per
+//                  sequence that contains id.
+// n-grams never cross sequence boundaries (intergrams.cpp:53-57).
+//
+// B200 design:
+//   * every lane owns a 16-byte segment, read with one 128-bit load; a warp
+//     covers 512 contiguous bytes, so a 32-lane load is one fully coalesced
+//     512 B transaction.  The 8 bytes before a segment (the n-gram halo) come
+//     from the neighbouring lane by shuffle, never from a second HBM read.
+//   * n-gram keys are assembled in registers with funnel shifts / byte perms
+//     at compile-time byte offsets (the gram length is a template parameter).
+//   * count-all: one L2 reduction (RED) per occurrence; duplicate ids within a
+//     warp instruction are merged with MATCH.ANY first so hot grams do not
+//     serialise on one L2 slice.
+//   * count-once: per-sequence dedup in SHARED memory.  The candidate space
+//     is split into G owner slices (G = 16 for the 2^24 dense space); the G
+//     CTAs of a group each keep one slice's bitmap in smem, scan the same
+//     sequence, and handle only the windows they own.  A bit that is already
+//     set is detected with a plain shared load (test before set), so repeated
+//     grams cost no atomic; the first occurrence does one ATOMS.OR and one RED
+//     to the L2-resident count table.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <type_traits>
+
+#include "ig_internal.cuh"
+#include "kernels.h"
+
+namespace igb {
+
+// ------------------------------------------------------------------ helpers
+
+// Compile-time loop: f(std::integral_constant<int, I>) for I in [B, E).
+template <int B, int E, typename F>
+__device__ __forceinline__ void static_for(F&& f) {
+  if constexpr (B < E) {
+    f(std::integral_constant<int, B>{});
+    static_for<B + 1, E>(f);
+  }
+}
+
+// W[0..1] = the 8 bytes before the segment, W[2..5] = the segment, W[6] = 0.
+struct Seg {
+  uint32_t W[7];
+};
+
+// Loads lane's 16-byte segment at byte index b0 (16-aligned, may be past the
+// end: padding is readable) and its 8-byte halo from lane-1 (lane 0 loads it).
+// Requires the full warp, with lanes holding consecutive segments.
+__device__ __forceinline__ void load_seg(const uint8_t* __restrict__ data, int64_t b0, Seg& s) {
+  const uint4 v = __ldcs(reinterpret_cast<const uint4*>(data + b0));
+  s.W[2] = v.x;
+  s.W[3] = v.y;
+  s.W[4] = v.z;
+  s.W[5] = v.w;
+  s.W[6] = 0;
+  uint32_t h0 = __shfl_up_sync(0xffffffffu, v.z, 1);
+  uint32_t h1 = __shfl_up_sync(0xffffffffu, v.w, 1);
+  if ((threadIdx.x & 31) == 0) {
+    const uint2 h = *reinterpret_cast<const uint2*>(data + b0 - 8);
+    h0 = h.x;
+    h1 = h.y;
+  }
+  s.W[0] = h0;
+  s.W[1] = h1;
+}
+
+// Word q of the segment shifted back by D bytes: byte r = b[b0 + 4q + r - D].
+template <int Q, int D>
+__device__ __forceinline__ uint32_t shifted(const Seg& s) {
+  constexpr int o = 8 + 4 * Q - D;
+  constexpr int wi = o / 4, sh = 8 * (o % 4);
+  if constexpr (sh == 0) return s.W[wi];
+  else return __funnelshift_r(s.W[wi], s.W[wi + 1], sh);
+}
+
+// Big-endian key of the 8 bytes ending at segment position T.
+template <int T>
+__device__ __forceinline__ uint64_t key8_at(const Seg& s) {
+  constexpr int o = T + 1;
+  constexpr int wi = o / 4, sh = 8 * (o % 4);
+  uint32_t lo, hi;
+  if constexpr (sh == 0) {
+    lo = s.W[wi];
+    hi = s.W[wi + 1];
+  } else {
+    lo = __funnelshift_r(s.W[wi], s.W[wi + 1], sh);
+    hi = __funnelshift_r(s.W[wi + 1], s.W[wi + 2], sh);
+  }
+  return ((uint64_t)__byte_perm(lo, 0, 0x0123) << 32) | (uint64_t)__byte_perm(hi, 0, 0x0123);
+}
+
+template <int L>
+__device__ __forceinline__ uint64_t gram_mask() {
+  if constexpr (L >= 8) return ~0ull;
+  else return (1ull << (8 * L)) - 1;
+}
+
+// Per-byte zero test of y (bytes < 0x80) -> 4-bit mask, bit r = byte r == 0.
+__device__ __forceinline__ uint32_t zero_bytes4(uint32_t y) {
+  const uint32_t z = ~(((y & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | y) & 0x80808080u;
+  return (((z >> 7) * 0x00204081u) >> 21) & 0xFu;
+}
+
+// 16-bit mask of segment positions whose window belongs to owner o.
+// KIND 0 (dense, L = 3): owner = (b[i-2] ^ b[i-1] ^ b[i]) & (G-1).
+// KIND 1 (extension, prefix = b[i-L+1 .. i-1]): owner = prefix_owner(prefix).
+template <int KIND, int L, int Q>
+__device__ __forceinline__ uint32_t owner_word(const Seg& s, uint32_t gm4, uint32_t o4) {
+  uint32_t x;
+  if constexpr (KIND == 0) {
+    x = shifted<Q, 0>(s) ^ shifted<Q, 1>(s) ^ shifted<Q, 2>(s);
+  } else {
+    constexpr int P = L - 1;  // prefix length
+    if constexpr (P >= 2) x = shifted<Q, 1>(s) ^ shifted<Q, P>(s);
+    else x = shifted<Q, 1>(s);
+  }
+  return zero_bytes4((x & gm4) ^ o4) << (4 * Q);
+}
+
+template <int KIND, int L>
+__device__ __forceinline__ uint32_t owner_mask(const Seg& s, uint32_t gm4, uint32_t o4) {
+  return owner_word<KIND, L, 0>(s, gm4, o4) | owner_word<KIND, L, 1>(s, gm4, o4) |
+         owner_word<KIND, L, 2>(s, gm4, o4) | owner_word<KIND, L, 3>(s, gm4, o4);
+}
+
+// 16-bit mask of valid gram ends in [b0, b0+16) for one sequence [s0, s1).
+template <int L>
+__device__ __forceinline__ uint32_t valid_mask_one(int64_t b0, int64_t s0, int64_t s1) {
+  const int64_t lo = s0 + L - 1;  // first valid gram end
+  int64_t a = lo - b0;
+  int64_t b = s1 - b0;
+  if (a < 0) a = 0;
+  if (b > 16) b = 16;
+  if (a >= b) return 0;
+  return ((1u << b) - 1u) & ~((1u << a) - 1u);
+}
+
+// Open-addressing lookup of a prefix key in owner slice `o`.  Returns p or
+// 0xffffffff.  Slices: keys[o*S .. o*S+S).
+__device__ __forceinline__ uint32_t prefix_lookup(const uint64_t* __restrict__ hkeys,
+                                                  const uint32_t* __restrict__ hidx, uint32_t S,
+                                                  uint32_t lgS, uint32_t o, uint64_t key) {
+  const uint64_t* kk = hkeys + (size_t)o * S;
+  uint32_t h = hash_slot(key, lgS);
+  for (;;) {
+    const uint64_t k = __ldg(kk + h);
+    if (k == key) return __ldg(hidx + (size_t)o * S + h);
+    if (k == kEmptyKey) return 0xffffffffu;
+    h = (h + 1) & (S - 1);
+  }
+}
+
+// ------------------------------------------------------------------ tiles
+
+// tile_seq[t] = sequence containing byte t*512 (upper_bound(off, t*512) - 1).
+__global__ void k_tile_seq(const uint64_t* __restrict__ off, uint64_t m, uint64_t ntiles,
+                           uint32_t* __restrict__ tile_seq) {
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < ntiles;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t b = t * kTileBytes;
+    uint64_t lo = 0, hi = m + 1;  // first index with off > b
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi) >> 1;
+      if (off[mid] <= b) lo = mid + 1;
+      else hi = mid;
+    }
+    uint64_t s = lo ? lo - 1 : 0;
+    if (s >= m) s = m ? m - 1 : 0;
+    tile_seq[t] = (uint32_t)s;
+  }
+}
+
+void launch_tile_seq(const uint64_t* off, uint64_t m, uint64_t ntiles, uint32_t* tile_seq,
+                     cudaStream_t st) {
+  if (!ntiles) return;
+  const int threads = 256;
+  const uint64_t blocks = (ntiles + threads - 1) / threads;
+  k_tile_seq<<<(unsigned)(blocks < 65535 ? blocks : 65535), threads, 0, st>>>(off, m, ntiles,
+                                                                            tile_seq);
+}
+
+// ------------------------------------------------------------------ count-all
+
+// Counts every gram end in the tile range with one RED per (warp-merged) id.
+// KIND 0: dense id over L bytes.  KIND 1: extension, L = j.
+template <int KIND, int L, typename CT>
+__global__ void __launch_bounds__(512) k_count_all(DevCorpus c, DevPrefixSet ps, CT* __restrict__ table) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t t = warp; t < c.ntiles; t += nwarps) {
+    const int64_t b0 = (int64_t)t * kTileBytes + lane * 16;
+    Seg s;
+    load_seg(c.data, b0, s);
+    // validity: walk sequence boundaries from the tile's first sequence
+    uint64_t q = c.tile_seq[t];
+    int64_t s0 = (int64_t)c.off[q], s1 = (int64_t)c.off[q + 1];
+    while (s1 <= b0 && q + 1 < c.m) {
+      ++q;
+      s0 = s1;
+      s1 = (int64_t)c.off[q + 1];
+    }
+    uint32_t vm = 0;
+    if (b0 < (int64_t)c.total) {
+      if (s1 >= b0 + 16) {
+        vm = valid_mask_one<L>(b0, s0, s1);
+      } else {
+        // a sequence boundary inside the segment: per-sequence pieces
+        for (;;) {
+          vm |= valid_mask_one<L>(b0, s0, s1);
+          if (s1 >= b0 + 16 || q + 1 >= c.m) break;
+          ++q;
+          s0 = s1;
+          s1 = (int64_t)c.off[q + 1];
+        }
+      }
+    }
+    static_for<0, 16>([&](auto tc) {
+      constexpr int T = decltype(tc)::value;
+      const bool valid = (vm >> T) & 1u;
+      uint32_t id = 0xffffffffu;
+      uint64_t gid = 0;
+      if (valid) {
+        const uint64_t key = key8_at<T>(s) & gram_mask<L>();
+        if constexpr (KIND == 0) {
+          gid = key;
+          id = (uint32_t)key;
+        } else {
+          const uint32_t p = prefix_lookup(ps.hkeys, ps.hidx, ps.S, ps.lgS, 0, key >> 8);
+          if (p != 0xffffffffu) {
+            gid = (uint64_t)p * 256 + (key & 0xff);
+            id = (uint32_t)gid;  // < 2^32: 256*K with K < 2^24
+          }
+        }
+      }
+      if constexpr (KIND == 0) {
+        // merge duplicate ids of this step across the warp (hot grams)
+        const uint32_t peers = __match_any_sync(0xffffffffu, id);
+        if (id != 0xffffffffu && lane == __ffs(peers) - 1) atomicAdd(table + gid, (CT)__popc(peers));
+      } else {
+        if (id != 0xffffffffu) atomicAdd(table + gid, (CT)1);
+      }
+    });
+  }
+}
+
+// ------------------------------------------------------------------ count-once
+
+// One CTA = (group g, owner o).  For every sequence taken from owner o's
+// work counter, scan the whole sequence, mark owned windows in the smem
+// bitmap, RED the count of each id the first time it is marked, then clear.
+// local id: dense -> id >> lgG (the low lgG bits are implied by o);
+// extension -> (p - owner_start[o])*256 + last.
+template <int KIND, int L, typename CT>
+__global__ void __launch_bounds__(1024) k_count_once(DevCorpus c, DevPrefixSet ps, uint32_t G,
+                                                     uint32_t lgG, uint32_t bm_words,
+                                                     uint32_t* __restrict__ work,
+                                                     CT* __restrict__ table) {
+  extern __shared__ uint4 smem_raw[];
+  uint32_t* bm = reinterpret_cast<uint32_t*>(smem_raw);
+  __shared__ uint32_t s_seq;
+  const uint32_t o = blockIdx.x % G;
+  const uint32_t gm = G - 1;
+  const uint32_t gm4 = gm * 0x01010101u, o4 = o * 0x01010101u;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  const uint32_t ostart = (KIND == 1) ? ps.owner_start[o] : 0u;
+
+  for (uint32_t i = threadIdx.x; i < bm_words / 4; i += blockDim.x) smem_raw[i] = make_uint4(0, 0, 0, 0);
+  __syncthreads();
+  for (;;) {
+    if (threadIdx.x == 0) s_seq = atomicAdd(work + o, 1u);
+    __syncthreads();
+    const uint32_t r = s_seq;
+    if (r >= c.m) break;
+    const uint32_t q = c.order[r];
+    const int64_t s0 = (int64_t)c.off[q], s1 = (int64_t)c.off[q + 1];
+    if (s1 - s0 >= L) {
+      const int64_t first = s0 & ~int64_t(15);
+      const int64_t nseg = (s1 - first + 15) >> 4;
+      for (int64_t base = (int64_t)warp * 32; base < nseg; base += (int64_t)nwarp * 32) {
+        const int64_t b0 = first + (base + lane) * 16;
+        Seg s;
+        load_seg(c.data, b0, s);
+        uint32_t vm = valid_mask_one<L>(b0, s0, s1);
+        if (G > 1) vm &= owner_mask<KIND, L>(s, gm4, o4);
+        while (vm) {
+          const int T = __ffs(vm) - 1;
+          vm &= vm - 1;
+          // runtime T: assemble the key from the segment words
+          uint64_t key;
+          switch (T) {
+#define IGB_CASE(X) \
+  case X:           \
+    key = key8_at<X>(s); \
+    break;
+            IGB_CASE(0) IGB_CASE(1) IGB_CASE(2) IGB_CASE(3) IGB_CASE(4) IGB_CASE(5)
+            IGB_CASE(6) IGB_CASE(7) IGB_CASE(8) IGB_CASE(9) IGB_CASE(10) IGB_CASE(11)
+            IGB_CASE(12) IGB_CASE(13) IGB_CASE(14) default: key = key8_at<15>(s); break;
+#undef IGB_CASE
+          }
+          key &= gram_mask<L>();
+          uint64_t gid;
+          uint32_t local;
+          if constexpr (KIND == 0) {
+            gid = key;
+            local = (uint32_t)(key >> lgG);
+          } else {
+            const uint32_t p = prefix_lookup(ps.hkeys, ps.hidx, ps.S, ps.lgS, o, key >> 8);
+            if (p == 0xffffffffu) continue;
+            gid = (uint64_t)p * 256 + (key & 0xff);
+            local = (p - ostart) * 256 + (uint32_t)(key & 0xff);
+          }
+          const uint32_t bit = 1u << (local & 31);
+          uint32_t* w = bm + (local >> 5);
+          if (!(*(volatile uint32_t*)w & bit)) {
+            if (!(atomicOr(w, bit) & bit)) atomicAdd(table + gid, (CT)1);
+          }
+        }
+      }
+    }
+    __syncthreads();
+    // clear: the whole slice bitmap (vectorised)
+    for (uint32_t i = threadIdx.x; i < bm_words / 4; i += blockDim.x) smem_raw[i] = make_uint4(0, 0, 0, 0);
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------ launchers
+
+template <int KIND, int L, typename CT>
+static void launch_all_t(const DevCorpus& c, const DevPrefixSet& ps, CT* table, int num_sms,
+                         cudaStream_t st) {
+  if (!c.ntiles) return;
+  const int threads = 512;
+  uint64_t want = (c.ntiles * 32 + threads - 1) / threads;
+  const uint64_t cap = (uint64_t)num_sms * 4 * 8;  // 4 CTAs/SM, 8 waves of tiles max
+  unsigned blocks = (unsigned)(want < cap ? want : cap);
+  if (!blocks) blocks = 1;
+  k_count_all<KIND, L, CT><<<blocks, threads, 0, st>>>(c, ps, table);
+}
+
+template <int KIND, int L, typename CT>
+static void launch_once_t(const DevCorpus& c, const DevPrefixSet& ps, uint32_t G, uint32_t lgG,
+                          uint64_t slice_bits, uint32_t* work, CT* table, int num_sms,
+                          cudaStream_t st) {
+  if (!c.m) return;
+  uint32_t bm_words = (uint32_t)((slice_bits + 127) / 128 * 4);  // multiple of 4 words
+  size_t smem = (size_t)bm_words * 4;
+  auto kern = k_count_once<KIND, L, CT>;
+  IGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int threads = 1024;
+  int per_sm = 0;
+  IGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
+  if (per_sm < 1) throw Error(IG_EINTERNAL, "count-once bitmap does not fit in shared memory");
+  uint64_t ngroups = ((uint64_t)num_sms * per_sm) / G;
+  if (ngroups < 1) ngroups = 1;
+  if (ngroups > c.m) ngroups = c.m;
+  IGB_CUDA(cudaMemsetAsync(work, 0, G * sizeof(uint32_t), st));
+  kern<<<(unsigned)(ngroups * G), threads, smem, st>>>(c, ps, G, lgG, bm_words, work, table);
+}
+
+template <typename CT>
+void launch_count_dense(const DevCorpus& c, uint32_t n0, int mode, CT* table, uint32_t* work,
+                        int num_sms, cudaStream_t st) {
+  DevPrefixSet none{};
+  if (mode == IG_MODE_ALL) {
+    switch (n0) {
+      case 1: launch_all_t<0, 1, CT>(c, none, table, num_sms, st); break;
+      case 2: launch_all_t<0, 2, CT>(c, none, table, num_sms, st); break;
+      default: launch_all_t<0, 3, CT>(c, none, table, num_sms, st); break;
+    }
+  } else {
+    switch (n0) {
+      case 1: launch_once_t<0, 1, CT>(c, none, 1, 0, 256, work, table, num_sms, st); break;
+      case 2: launch_once_t<0, 2, CT>(c, none, 1, 0, 65536, work, table, num_sms, st); break;
+      default: launch_once_t<0, 3, CT>(c, none, 16, 4, 1u << 20, work, table, num_sms, st); break;
+    }
+  }
+}
+
+template <typename CT>
+void launch_count_extend(const DevCorpus& c, const DevPrefixSet& ps, uint32_t j, int mode,
+                         CT* table, uint32_t* work, int num_sms, cudaStream_t st) {
+  const uint64_t slice_bits = (uint64_t)ps.max_owner * 256;
+#define IGB_J(J)                                                                            \
+  case J:                                                                                   \
+    if (mode == IG_MODE_ALL) launch_all_t<1, J, CT>(c, ps, table, num_sms, st);             \
+    else launch_once_t<1, J, CT>(c, ps, ps.G, ps.lgG, slice_bits, work, table, num_sms, st); \
+    break;
+  switch (j) {
+    IGB_J(2) IGB_J(3) IGB_J(4) IGB_J(5) IGB_J(6) IGB_J(7) IGB_J(8)
+    default: throw Error(IG_ECONFIG, "gram length above 8 is not supported");
+  }
+#undef IGB_J
+}
+
+template void launch_count_dense<uint32_t>(const DevCorpus&, uint32_t, int, uint32_t*, uint32_t*,
+                                           int, cudaStream_t);
+template void launch_count_dense<unsigned long long>(const DevCorpus&, uint32_t, int,
+                                                     unsigned long long*, uint32_t*, int,
+                                                     cudaStream_t);
+template void launch_count_extend<uint32_t>(const DevCorpus&, const DevPrefixSet&, uint32_t, int,
+                                            uint32_t*, uint32_t*, int, cudaStream_t);
+template void launch_count_extend<unsigned long long>(const DevCorpus&, const DevPrefixSet&,
+                                                      uint32_t, int, unsigned long long*,
+                                                      uint32_t*, int, cudaStream_t);
+
+// ------------------------------------------------------------------ prefix set build
+
+// Pass 1: owner of every survivor key and per-owner sizes.
+__global__ void k_prefix_owner(const uint64_t* __restrict__ keys, uint32_t K, uint32_t plen,
+                               uint32_t G, uint32_t* __restrict__ owner,
+                               uint32_t* __restrict__ owner_count) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < K; i += gridDim.x * blockDim.x) {
+    const uint32_t o = prefix_owner(keys[i], plen, G);
+    owner[i] = o;
+    atomicAdd(owner_count + o, 1u);
+  }
+}
+
+// Pass 2: place survivor i at p = owner_start[o] + (stable rank within owner
+// via a per-owner cursor: order within a slice is irrelevant to results), and
+// insert it into owner o's open-addressing slice.
+__global__ void k_prefix_insert(const uint64_t* __restrict__ keys, uint32_t K,
+                                const uint32_t* __restrict__ owner,
+                                const uint32_t* __restrict__ owner_start,
+                                uint32_t* __restrict__ cursor, uint32_t S, uint32_t lgS,
+                                uint64_t* __restrict__ hkeys, uint32_t* __restrict__ hidx,
+                                uint64_t* __restrict__ pkeys, uint32_t* __restrict__ rank_of_p) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < K; i += gridDim.x * blockDim.x) {
+    const uint32_t o = owner[i];
+    const uint32_t p = owner_start[o] + atomicAdd(cursor + o, 1u);
+    const uint64_t key = keys[i];
+    pkeys[p] = key;
+    rank_of_p[p] = i;
+    unsigned long long* kk = reinterpret_cast<unsigned long long*>(hkeys + (size_t)o * S);
+    uint32_t h = hash_slot(key, lgS);
+    for (;;) {
+      const unsigned long long prev = atomicCAS(kk + h, (unsigned long long)kEmptyKey,
+                                                (unsigned long long)key);
+      if (prev == kEmptyKey) {
+        hidx[(size_t)o * S + h] = p;
+        break;
+      }
+      h = (h + 1) & (S - 1);
+    }
+  }
+}
+
+void launch_prefix_owner(const uint64_t* keys, uint32_t K, uint32_t plen, uint32_t G,
+                         uint32_t* owner, uint32_t* owner_count, cudaStream_t st) {
+  if (!K) return;
+  const unsigned blocks = (K + 255) / 256;
+  k_prefix_owner<<<blocks < 4096 ? blocks : 4096, 256, 0, st>>>(keys, K, plen, G, owner,
+                                                               owner_count);
+}
+
+void launch_prefix_insert(const uint64_t* keys, uint32_t K, const uint32_t* owner,
+                          const uint32_t* owner_start, uint32_t* cursor, uint32_t S, uint32_t lgS,
+                          uint64_t* hkeys, uint32_t* hidx, uint64_t* pkeys, uint32_t* rank_of_p,
+                          cudaStream_t st) {
+  if (!K) return;
+  const unsigned blocks = (K + 255) / 256;
+  k_prefix_insert<<<blocks < 4096 ? blocks : 4096, 256, 0, st>>>(
+      keys, K, owner, owner_start, cursor, S, lgS, hkeys, hidx, pkeys, rank_of_p);
+}
+
+}  // namespace igb

@@ -1,0 +1,118 @@
+// ig_internal.cuh — shared internals of the B200 Intergrams library.
+//
+// Layout in HBM (one session = one device):
+//   corpus   d_data  : u8[total + pad], 16 B of zero front padding so a segment's
+//                       8-byte halo load at base-8 never leaves the allocation
+//            d_off   : u64[m+1] sequence offsets (CSR)
+//            d_tile  : u32[ceil(total/512)] sequence index of each 512-byte tile
+//            d_order : u32[m] sequences by length, longest first (count-once LPT)
+//   tables   counts  : CT[capacity] (u32 when every count provably fits, else u64)
+//   prefixes pkeys   : u64[K]   survivor keys in bucket order (p = index)
+//            hkeys   : u64[G*S] open-addressing prefix set, G owner slices
+//            hidx    : u32[G*S] p of each occupied slot
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+#include <utility>
+
+#include "../../include/intergrams_b200.h"
+
+namespace igb {
+
+// Exceptions carried to the C boundary and turned into IG_* codes there.
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+inline void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
+  if (e != cudaSuccess) {
+    throw Error(IG_EINTERNAL, std::string("CUDA error in ") + what + " at " + file + ":" +
+                                  std::to_string(line) + ": " + cudaGetErrorString(e));
+  }
+}
+#define IGB_CUDA(x) ::igb::cuda_check((x), #x, __FILE__, __LINE__)
+#define IGB_LAUNCHED(sess) \
+  do {                     \
+    (sess)->launches++;    \
+    IGB_CUDA(cudaGetLastError()); \
+  } while (0)
+
+constexpr uint64_t kEmptyKey = ~0ull;  // never a key: keys have <= 56 bits in a prefix set
+constexpr int kTileBytes = 512;        // one warp x 16 B per lane
+constexpr int kFrontPad = 16;
+constexpr int kBackPad = 1024;
+
+// Grow-only device buffer.
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  void swap(DevBuf& o) noexcept {
+    std::swap(p, o.p);
+    std::swap(bytes, o.bytes);
+  }
+  void* get(size_t need) {
+    if (need > bytes) {
+      if (p) cudaFree(p);
+      p = nullptr;
+      bytes = 0;
+      IGB_CUDA(cudaMalloc(&p, need ? need : 16));
+      bytes = need ? need : 16;
+    }
+    return p;
+  }
+  template <typename T>
+  T* as(size_t count) { return static_cast<T*>(get(count * sizeof(T))); }
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+};
+
+// Device-side corpus view.
+struct DevCorpus {
+  const uint8_t* data = nullptr;  // first byte of sequence 0
+  const uint64_t* off = nullptr;  // m+1
+  const uint32_t* tile_seq = nullptr;
+  const uint32_t* order = nullptr;
+  uint64_t m = 0;
+  uint64_t total = 0;      // bytes
+  uint64_t ntiles = 0;
+};
+
+// Device prefix set for an extension pass.
+struct DevPrefixSet {
+  const uint64_t* pkeys = nullptr;   // [K] keys by p
+  const uint64_t* hkeys = nullptr;   // [G*S]
+  const uint32_t* hidx = nullptr;    // [G*S]
+  const uint32_t* owner_start = nullptr;  // [G+1] p range of each owner slice
+  uint32_t K = 0;
+  uint32_t G = 1, lgG = 0;
+  uint32_t S = 0;          // slots per owner slice (power of two)
+  uint32_t lgS = 0;
+  uint32_t plen = 0;       // prefix length (j-1)
+  uint32_t max_owner = 0;  // largest owner slice size
+};
+
+__host__ __device__ inline uint32_t hash_slot(uint64_t key, uint32_t lgS) {
+  return lgS == 0 ? 0u : (uint32_t)((key * 0x9E3779B97F4A7C15ull) >> (64 - lgS));
+}
+
+// Owner slice of a prefix key (count-once passes): first byte xor last byte.
+__host__ __device__ inline uint32_t prefix_owner(uint64_t key, uint32_t plen, uint32_t G) {
+  uint32_t last = (uint32_t)(key & 0xff);
+  uint32_t first = (uint32_t)((key >> (8 * (plen - 1))) & 0xff);
+  uint32_t x = plen >= 2 ? (first ^ last) : last;
+  return x & (G - 1);
+}
+
+// Session (the C handle).
+struct Session;
+
+}  // namespace igb

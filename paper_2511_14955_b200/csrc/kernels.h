@@ -1,0 +1,62 @@
+// kernels.h — host-side launchers of the sm_100a kernels (one translation
+// unit per family: count_kernels.cu, select_kernels.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "ig_internal.cuh"
+
+namespace igb {
+
+// --- corpus / counting (count_kernels.cu)
+void launch_tile_seq(const uint64_t* off, uint64_t m, uint64_t ntiles, uint32_t* tile_seq,
+                     cudaStream_t st);
+
+template <typename CT>
+void launch_count_dense(const DevCorpus& c, uint32_t n0, int mode, CT* table, uint32_t* work,
+                        int num_sms, cudaStream_t st);
+
+template <typename CT>
+void launch_count_extend(const DevCorpus& c, const DevPrefixSet& ps, uint32_t j, int mode,
+                         CT* table, uint32_t* work, int num_sms, cudaStream_t st);
+
+void launch_prefix_owner(const uint64_t* keys, uint32_t K, uint32_t plen, uint32_t G,
+                         uint32_t* owner, uint32_t* owner_count, cudaStream_t st);
+void launch_prefix_insert(const uint64_t* keys, uint32_t K, const uint32_t* owner,
+                          const uint32_t* owner_start, uint32_t* cursor, uint32_t S, uint32_t lgS,
+                          uint64_t* hkeys, uint32_t* hidx, uint64_t* pkeys, uint32_t* rank_of_p,
+                          cudaStream_t st);
+
+// --- selection (select_kernels.cu)
+struct SelState {
+  unsigned long long prefix;   // count digits chosen so far
+  unsigned long long r;        // rank still to place among counts
+  unsigned long long nonzero;  // nonzero entries (first pass)
+  unsigned long long T;        // count threshold
+  unsigned long long need;     // entries with count == T to take
+  unsigned long long kprefix;  // key digits chosen so far (-> Kt)
+  int take_all;
+  int pad;
+};
+
+struct SelectCtx {
+  cudaStream_t stream = nullptr;
+  int num_sms = 148;
+  SelState* state = nullptr;          // device
+  uint32_t* hist = nullptr;           // device [256]
+  unsigned long long* scalar = nullptr;  // device
+  DevBuf tmp_keys, tmp_counts, cub_tmp;
+  uint64_t launches = 0;
+};
+
+// Canonical top-k of table[0..cap) (cap % 4 == 0).  Gram key = id, or
+// (pkeys[id>>8] << 8) | (id & 255) when pkeys != nullptr.  Writes
+// min(k, nonzero) entries to out_keys/out_counts (device) and returns that
+// number.  key_bits = 8 * gram length.
+template <typename CT>
+uint64_t select_topk(SelectCtx& x, const CT* table, uint64_t cap, uint64_t k,
+                     const uint64_t* pkeys, int key_bits, uint64_t* out_keys,
+                     uint64_t* out_counts);
+
+}  // namespace igb

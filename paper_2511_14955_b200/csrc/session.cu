@@ -1,0 +1,673 @@
+// session.cu — the Intergrams driver and the C-ABI (include/intergrams_b200.h).
+//
+// Orchestration follows run_intergrams, proj/src/intergrams.cpp:68-166:
+//   validate (:37-42) -> dense n0-gram pass, n0 = min(n,3) (:76-103) ->
+//   n <= 3: top-k and return (:105-113) -> top-k' survivors + prefix set
+//   (:115-132) -> for j = 4..n: extension pass (:135-141), then top-k'
+//   (:143-157) or the final top-k (:158-163).
+// PassResult rows, labels and diagnostics are the reference's own; seconds
+// are CUDA-event times of each step on the session stream.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "ig_internal.cuh"
+#include "kernels.h"
+
+namespace igb {
+
+static constexpr size_t kOnceSmemBudget = 200 * 1024;  // bytes of bitmap per CTA
+
+struct Session {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  bool has_coll = false;
+  ig_collective coll{};
+  int num_sms = 148;
+  uint64_t launches = 0;
+
+  // corpus
+  DevBuf data, off, tile, order;
+  DevCorpus dc;
+  bool loaded = false;
+
+  // pass buffers
+  DevBuf table, work;
+  DevBuf surv_keys, surv_counts, next_keys, next_counts;
+  DevBuf pkeys, hkeys, hidx, owner, owner_cnt, owner_start, cursor, rank_of_p;
+  DevBuf sel_state, sel_hist, sel_scalar;
+  SelectCtx sel;
+  std::vector<cudaEvent_t> events;
+
+  ~Session() {
+    for (auto e : events) cudaEventDestroy(e);
+    if (own_stream && stream) cudaStreamDestroy(stream);
+  }
+};
+
+// ---------------------------------------------------------------- helpers
+
+static void set_err(char* err, size_t len, const char* msg) {
+  if (err && len) {
+    strncpy(err, msg, len - 1);
+    err[len - 1] = 0;
+  }
+}
+
+template <typename F>
+static int guarded(char* err, size_t len, F&& f) {
+  try {
+    f();
+    if (err && len) err[0] = 0;
+    return IG_OK;
+  } catch (const Error& e) {
+    set_err(err, len, e.what());
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    set_err(err, len, "host allocation failed");
+    return IG_EINTERNAL;
+  } catch (const std::exception& e) {
+    set_err(err, len, e.what());
+    return IG_EINTERNAL;
+  }
+}
+
+static void use_device(Session& s) { IGB_CUDA(cudaSetDevice(s.device)); }
+
+static void validate(const ig_params& p) {
+  // IntergramConfig::validate, intergrams.cpp:37-42
+  if (p.n < 1) throw Error(IG_ECONFIG, "gram length n must be >= 1");
+  if (p.k < 1) throw Error(IG_ECONFIG, "k must be >= 1");
+  if (!(p.z >= 1.0)) throw Error(IG_ECONFIG, "oversample factor z must be >= 1");
+  if (p.flush_batch_size < 1) throw Error(IG_ECONFIG, "flush batch size must be >= 1");
+  if (p.mode != IG_MODE_ONCE && p.mode != IG_MODE_ALL)
+    throw Error(IG_ECONFIG, "count mode must be ONCE (0) or ALL (1)");
+  if (p.n > IG_MAX_N)
+    throw Error(IG_ECONFIG, "gram length n above 8 is not supported by the packed-u64 GPU path");
+}
+
+static uint64_t k_prime(const ig_params& p) {
+  // k_prime(), intergrams.hpp:29-31: ceil(z * k)
+  const double v = std::ceil(p.z * (double)p.k);
+  if (v >= 4.0e9) return 4000000000ull;  // survivors are bounded by the table anyway
+  return (uint64_t)v;
+}
+
+static void load_corpus(Session& s, const ig_corpus& c) {
+  use_device(s);
+  const uint64_t m = c.num_seqs;
+  std::vector<uint64_t> hoff(m + 1);
+  if (c.location == IG_DEVICE) {
+    IGB_CUDA(cudaMemcpy(hoff.data(), c.offsets, (m + 1) * sizeof(uint64_t),
+                        cudaMemcpyDeviceToHost));
+  } else {
+    memcpy(hoff.data(), c.offsets, (m + 1) * sizeof(uint64_t));
+  }
+  if (hoff[0] != 0) throw Error(IG_ECONFIG, "corpus offsets must start at 0");
+  for (uint64_t i = 0; i < m; ++i)
+    if (hoff[i + 1] < hoff[i]) throw Error(IG_ECONFIG, "corpus offsets must be non-decreasing");
+  if (m >= 0xffffffffull) throw Error(IG_ECONFIG, "too many sequences");
+  const uint64_t total = hoff[m];
+  const uint64_t ntiles = (total + kTileBytes - 1) / kTileBytes;
+  const size_t alloc = kFrontPad + ntiles * kTileBytes + kBackPad;
+  uint8_t* base = s.data.as<uint8_t>(alloc);
+  IGB_CUDA(cudaMemsetAsync(base, 0, kFrontPad, s.stream));
+  IGB_CUDA(cudaMemsetAsync(base + kFrontPad + total, 0, alloc - kFrontPad - total, s.stream));
+  if (total) {
+    IGB_CUDA(cudaMemcpyAsync(base + kFrontPad, c.data, total,
+                             c.location == IG_DEVICE ? cudaMemcpyDeviceToDevice
+                                                     : cudaMemcpyHostToDevice,
+                             s.stream));
+  }
+  uint64_t* doff = s.off.as<uint64_t>(m + 1);
+  IGB_CUDA(cudaMemcpyAsync(doff, hoff.data(), (m + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice,
+                           s.stream));
+  uint32_t* dtile = s.tile.as<uint32_t>(ntiles + 1);
+  launch_tile_seq(doff, m, ntiles, dtile, s.stream);
+  s.launches++;
+  // count-once schedule: longest sequences first
+  std::vector<uint32_t> ord(m);
+  for (uint64_t i = 0; i < m; ++i) ord[i] = (uint32_t)i;
+  std::stable_sort(ord.begin(), ord.end(), [&](uint32_t a, uint32_t b) {
+    return hoff[a + 1] - hoff[a] > hoff[b + 1] - hoff[b];
+  });
+  uint32_t* dord = s.order.as<uint32_t>(m + 1);
+  if (m)
+    IGB_CUDA(cudaMemcpyAsync(dord, ord.data(), m * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                             s.stream));
+  IGB_CUDA(cudaStreamSynchronize(s.stream));
+  s.dc.data = base + kFrontPad;
+  s.dc.off = doff;
+  s.dc.tile_seq = dtile;
+  s.dc.order = dord;
+  s.dc.m = m;
+  s.dc.total = total;
+  s.dc.ntiles = ntiles;
+  s.loaded = true;
+}
+
+// Event pair per step; elapsed read at the end of the run.
+struct StepTimer {
+  Session& s;
+  size_t next = 0;
+  explicit StepTimer(Session& ss) : s(ss) {}
+  size_t begin() {
+    if (next + 2 > s.events.size()) {
+      for (int i = 0; i < 16; ++i) {
+        cudaEvent_t e;
+        IGB_CUDA(cudaEventCreate(&e));
+        s.events.push_back(e);
+      }
+    }
+    IGB_CUDA(cudaEventRecord(s.events[next], s.stream));
+    next += 2;
+    return next - 2;
+  }
+  void end(size_t i) { IGB_CUDA(cudaEventRecord(s.events[i + 1], s.stream)); }
+  double seconds(size_t i) {
+    float ms = 0;
+    IGB_CUDA(cudaEventSynchronize(s.events[i + 1]));
+    IGB_CUDA(cudaEventElapsedTime(&ms, s.events[i], s.events[i + 1]));
+    return ms * 1e-3;
+  }
+};
+
+struct Row {
+  ig_pass_stat st;
+  size_t ev;
+};
+
+static Row make_row(const std::string& label, uint32_t gl, uint64_t bytes, uint64_t cap,
+                    uint64_t retained, bool shrt, size_t ev) {
+  Row r;
+  memset(&r.st, 0, sizeof(r.st));
+  snprintf(r.st.label, sizeof(r.st.label), "%s", label.c_str());
+  r.st.gram_len = gl;
+  r.st.bytes_processed = bytes;
+  r.st.candidate_space = cap;
+  r.st.retained = retained;
+  r.st.retained_short = shrt ? 1 : 0;
+  r.ev = ev;
+  return r;
+}
+
+static void init_select(Session& s) {
+  s.sel.stream = s.stream;
+  s.sel.num_sms = s.num_sms;
+  s.sel.state = s.sel_state.as<SelState>(1);
+  s.sel.hist = s.sel_hist.as<uint32_t>(256);
+  s.sel.scalar = s.sel_scalar.as<unsigned long long>(1);
+}
+
+// Builds the device prefix set for survivors keys[0..K) of length plen.
+static DevPrefixSet build_prefix_set(Session& s, const uint64_t* keys, uint64_t K, uint32_t plen,
+                                     int mode) {
+  DevPrefixSet ps;
+  ps.K = (uint32_t)K;
+  ps.plen = plen;
+  uint32_t* owner = s.owner.as<uint32_t>(K + 1);
+  uint32_t* ocnt = s.owner_cnt.as<uint32_t>(16);
+  uint32_t* ostart = s.owner_start.as<uint32_t>(17);
+  uint32_t* cursor = s.cursor.as<uint32_t>(16);
+  uint32_t G = 1;
+  std::vector<uint32_t> cnt(16, 0);
+  if (mode == IG_MODE_ONCE) {
+    // owner16 counts, then the smallest G whose largest slice fits in smem
+    IGB_CUDA(cudaMemsetAsync(ocnt, 0, 16 * sizeof(uint32_t), s.stream));
+    launch_prefix_owner(keys, (uint32_t)K, plen, 16, owner, ocnt, s.stream);
+    s.launches++;
+    IGB_CUDA(cudaMemcpyAsync(cnt.data(), ocnt, 16 * sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                             s.stream));
+    IGB_CUDA(cudaStreamSynchronize(s.stream));
+    G = 0;
+    for (uint32_t g = 1; g <= 16; g *= 2) {
+      uint64_t mx = 0;
+      for (uint32_t o = 0; o < g; ++o) {
+        uint64_t c = 0;
+        for (uint32_t q = o; q < 16; q += g) c += cnt[q];
+        mx = std::max(mx, c);
+      }
+      if (mx * 256 / 8 <= kOnceSmemBudget) {
+        G = g;
+        break;
+      }
+    }
+    if (G == 0)
+      throw Error(IG_EINTERNAL,
+                  "count-once prefix slice exceeds shared memory (k' too large for the smem "
+                  "bitmap path)");
+  }
+  uint32_t lgG = 0;
+  while ((1u << lgG) < G) ++lgG;
+  std::vector<uint32_t> gc(G, 0), gs(G + 1, 0);
+  if (G == 1) {
+    gc[0] = (uint32_t)K;
+  } else {
+    for (uint32_t q = 0; q < 16; ++q) gc[q & (G - 1)] += cnt[q];
+  }
+  uint32_t mx = 0;
+  for (uint32_t o = 0; o < G; ++o) {
+    gs[o + 1] = gs[o] + gc[o];
+    mx = std::max(mx, gc[o]);
+  }
+  uint32_t lgS = 1;
+  while ((1ull << lgS) < 2ull * std::max<uint32_t>(mx, 1)) ++lgS;
+  const uint32_t S = 1u << lgS;
+  // recompute owners at width G (owner16 & (G-1) == owner_G)
+  launch_prefix_owner(keys, (uint32_t)K, plen, G, owner, ocnt /*scratch*/, s.stream);
+  s.launches++;
+  IGB_CUDA(cudaMemcpyAsync(ostart, gs.data(), (G + 1) * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                           s.stream));
+  IGB_CUDA(cudaMemsetAsync(cursor, 0, 16 * sizeof(uint32_t), s.stream));
+  uint64_t* hk = s.hkeys.as<uint64_t>((size_t)G * S);
+  uint32_t* hi = s.hidx.as<uint32_t>((size_t)G * S);
+  uint64_t* pk = s.pkeys.as<uint64_t>(K + 1);
+  uint32_t* rp = s.rank_of_p.as<uint32_t>(K + 1);
+  IGB_CUDA(cudaMemsetAsync(hk, 0xff, (size_t)G * S * sizeof(uint64_t), s.stream));
+  launch_prefix_insert(keys, (uint32_t)K, owner, ostart, cursor, S, lgS, hk, hi, pk, rp, s.stream);
+  s.launches++;
+  ps.pkeys = pk;
+  ps.hkeys = hk;
+  ps.hidx = hi;
+  ps.owner_start = ostart;
+  ps.G = G;
+  ps.lgG = lgG;
+  ps.S = S;
+  ps.lgS = lgS;
+  ps.max_owner = mx;
+  return ps;
+}
+
+static void allreduce(Session& s, void* buf, uint64_t count, int dtype) {
+  if (!s.has_coll || s.coll.world <= 1) return;
+  if (!s.coll.allreduce) throw Error(IG_EINTERNAL, "collective has no allreduce");
+  const int rc = s.coll.allreduce(buf, count, dtype, (void*)s.stream, s.coll.user);
+  if (rc != 0) throw Error(IG_EINTERNAL, "allreduce callback failed");
+}
+
+// Count-table dtype: u32 whenever no count can reach 2^32 (count-once counts
+// are <= m; count-all counts are <= the corpus bytes), else u64.
+static bool use_u32(Session& s, int mode) {
+  const uint64_t bytes = s.has_coll ? s.coll.bytes_total : s.dc.total;
+  const uint64_t seqs = s.has_coll ? s.coll.seqs_total : s.dc.m;
+  return mode == IG_MODE_ONCE ? seqs < 0xffffffffull : bytes < 0xffffffffull;
+}
+
+template <typename CT>
+static void run_t(Session& s, const ig_params& p, ig_result* out) {
+  init_select(s);
+  const uint64_t kp = k_prime(p);
+  const uint32_t n = p.n;
+  const uint32_t n0 = std::min<uint32_t>(n, 3);
+  const uint64_t total_bytes = s.has_coll ? s.coll.bytes_total : s.dc.total;
+  StepTimer tm(s);
+  std::vector<Row> rows;
+  std::string diag;
+  uint32_t* work = s.work.as<uint32_t>(64);
+  const uint64_t sel_before = s.sel.launches;
+
+  // ---- dense pass (intergrams.cpp:76-103)
+  const uint64_t dcap = 1ull << (8 * n0);
+  size_t ev = tm.begin();
+  CT* table = s.table.as<CT>(dcap);
+  IGB_CUDA(cudaMemsetAsync(table, 0, dcap * sizeof(CT), s.stream));
+  launch_count_dense<CT>(s.dc, n0, p.mode, table, work, s.num_sms, s.stream);
+  s.launches++;
+  IGB_CUDA(cudaGetLastError());
+  allreduce(s, table, dcap, sizeof(CT) == 4 ? 0 : 1);
+  tm.end(ev);
+  rows.push_back(make_row(std::to_string(n0) + "-gram pass", n0, total_bytes, dcap, 0, false, ev));
+
+  uint64_t* out_keys_d = nullptr;
+  uint64_t* out_counts_d = nullptr;
+  uint64_t out_len = 0;
+
+  if (n <= 3) {  // intergrams.cpp:105-113
+    ev = tm.begin();
+    out_keys_d = s.next_keys.as<uint64_t>(std::min<uint64_t>(p.k, dcap) + 1);
+    out_counts_d = s.next_counts.as<uint64_t>(std::min<uint64_t>(p.k, dcap) + 1);
+    out_len = select_topk<CT>(s.sel, table, dcap, p.k, nullptr, 8 * n0, out_keys_d, out_counts_d);
+    tm.end(ev);
+    rows.push_back(make_row("top-k " + std::to_string(n) + "-grams", n, 0, 0, out_len, false, ev));
+  } else {
+    // ---- survivors of the 3-gram pass (intergrams.cpp:115-132)
+    ev = tm.begin();
+    uint64_t scap = std::min<uint64_t>(kp, dcap);
+    uint64_t* sk = s.surv_keys.as<uint64_t>(scap + 1);
+    uint64_t* sc = s.surv_counts.as<uint64_t>(scap + 1);
+    uint64_t ns = select_topk<CT>(s.sel, table, dcap, kp, nullptr, 24, sk, sc);
+    bool shrt = ns < kp;
+    if (shrt)
+      diag += "pass 3 retained " + std::to_string(ns) + " candidates (requested " +
+              std::to_string(kp) + ")\n";
+    DevPrefixSet ps{};
+    if (ns) ps = build_prefix_set(s, sk, ns, 3, p.mode);
+    tm.end(ev);
+    rows.push_back(make_row("top-zk 3-grams/trie building", 3, 0, 0, ns, shrt, ev));
+
+    for (uint32_t j = 4; j <= n; ++j) {
+      // an empty survivor list is a depth-0 trie (trie.cpp:23) and the
+      // extension pass rejects it (intergrams.cpp:46-48)
+      if (ns == 0) throw Error(IG_ECONFIG, "extension pass needs a trie of depth j-1");
+      ev = tm.begin();
+      const uint64_t cap = 256 * ns;
+      CT* ct = s.table.as<CT>(cap);
+      IGB_CUDA(cudaMemsetAsync(ct, 0, cap * sizeof(CT), s.stream));
+      launch_count_extend<CT>(s.dc, ps, j, p.mode, ct, work, s.num_sms, s.stream);
+      s.launches++;
+      IGB_CUDA(cudaGetLastError());
+      allreduce(s, ct, cap, sizeof(CT) == 4 ? 0 : 1);
+      tm.end(ev);
+      rows.push_back(
+          make_row(std::to_string(j) + "-gram pass", j, total_bytes, cap, 0, false, ev));
+
+      ev = tm.begin();
+      if (j < n) {
+        uint64_t ncap = std::min<uint64_t>(kp, cap);
+        uint64_t* nk = s.next_keys.as<uint64_t>(ncap + 1);
+        uint64_t* nc = s.next_counts.as<uint64_t>(ncap + 1);
+        uint64_t nn = select_topk<CT>(s.sel, ct, cap, kp, ps.pkeys, 8 * j, nk, nc);
+        shrt = nn < kp;
+        if (shrt)
+          diag += "pass " + std::to_string(j) + " retained " + std::to_string(nn) +
+                  " candidates (requested " + std::to_string(kp) + ")\n";
+        s.surv_keys.swap(s.next_keys);
+        s.surv_counts.swap(s.next_counts);
+        sk = nk;
+        ns = nn;
+        if (ns) ps = build_prefix_set(s, sk, ns, j, p.mode);
+        tm.end(ev);
+        rows.push_back(make_row("top-zk " + std::to_string(j) + "-grams/trie building", j, 0, 0,
+                                ns, shrt, ev));
+      } else {
+        uint64_t ocap = std::min<uint64_t>(p.k, cap);
+        out_keys_d = s.next_keys.as<uint64_t>(ocap + 1);
+        out_counts_d = s.next_counts.as<uint64_t>(ocap + 1);
+        out_len = select_topk<CT>(s.sel, ct, cap, p.k, ps.pkeys, 8 * j, out_keys_d, out_counts_d);
+        tm.end(ev);
+        rows.push_back(
+            make_row("top-k " + std::to_string(j) + "-grams", j, 0, 0, out_len, false, ev));
+      }
+    }
+  }
+
+  // ---- results to host
+  out->len = out_len;
+  out->gram_len = n;
+  out->keys = (uint64_t*)malloc((out_len + 1) * sizeof(uint64_t));
+  out->counts = (uint64_t*)malloc((out_len + 1) * sizeof(uint64_t));
+  out->passes = (ig_pass_stat*)malloc(rows.size() * sizeof(ig_pass_stat));
+  out->diagnostics = (char*)malloc(diag.size() + 1);
+  if (!out->keys || !out->counts || !out->passes || !out->diagnostics)
+    throw Error(IG_EINTERNAL, "host allocation failed");
+  if (out_len) {
+    IGB_CUDA(cudaMemcpyAsync(out->keys, out_keys_d, out_len * sizeof(uint64_t),
+                             cudaMemcpyDeviceToHost, s.stream));
+    IGB_CUDA(cudaMemcpyAsync(out->counts, out_counts_d, out_len * sizeof(uint64_t),
+                             cudaMemcpyDeviceToHost, s.stream));
+  }
+  IGB_CUDA(cudaStreamSynchronize(s.stream));
+  for (size_t i = 0; i < rows.size(); ++i) {
+    rows[i].st.seconds = tm.seconds(rows[i].ev);
+    out->passes[i] = rows[i].st;
+  }
+  out->num_passes = (uint32_t)rows.size();
+  memcpy(out->diagnostics, diag.c_str(), diag.size() + 1);
+  s.launches += s.sel.launches - sel_before;
+}
+
+static void run(Session& s, const ig_params& p, ig_result* out) {
+  validate(p);
+  if (!s.loaded) throw Error(IG_ECONFIG, "no corpus loaded");
+  use_device(s);
+  memset(out, 0, sizeof(*out));
+  try {
+    if (use_u32(s, p.mode)) run_t<uint32_t>(s, p, out);
+    else run_t<unsigned long long>(s, p, out);
+  } catch (...) {
+    ig_result_free(out);
+    throw;
+  }
+}
+
+}  // namespace igb
+
+using namespace igb;
+
+struct ig_session : igb::Session {};
+
+namespace igb {
+static ig_session* create(int32_t device, void* stream, const ig_collective* coll) {
+  ig_session* s = new ig_session();
+  try {
+    if (device < 0) IGB_CUDA(cudaGetDevice(&device));
+    s->device = device;
+    IGB_CUDA(cudaSetDevice(device));
+    IGB_CUDA(cudaDeviceGetAttribute(&s->num_sms, cudaDevAttrMultiProcessorCount, device));
+    if (stream) {
+      s->stream = (cudaStream_t)stream;
+    } else {
+      IGB_CUDA(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+      s->own_stream = true;
+    }
+    if (coll) {
+      s->coll = *coll;
+      s->has_coll = true;
+    }
+  } catch (...) {
+    delete s;
+    throw;
+  }
+  return s;
+}
+
+}  // namespace igb
+
+extern "C" {
+
+const char* ig_version(void) { return "intergrams-b200 0.1 (sm_100a)"; }
+
+void ig_result_free(ig_result* r) {
+  if (!r) return;
+  free(r->keys);
+  free(r->counts);
+  free(r->passes);
+  free(r->diagnostics);
+  r->keys = nullptr;
+  r->counts = nullptr;
+  r->passes = nullptr;
+  r->diagnostics = nullptr;
+  r->len = 0;
+  r->num_passes = 0;
+}
+
+int ig_session_create(int32_t device, void* cuda_stream, const ig_collective* coll,
+                      ig_session** out, char* err, size_t err_len) {
+  return guarded(err, err_len, [&] {
+    if (!out) throw Error(IG_ECONFIG, "null session out-pointer");
+    *out = create(device, cuda_stream, coll);
+  });
+}
+
+int ig_session_load(ig_session* s, const ig_corpus* corpus, char* err, size_t err_len) {
+  return guarded(err, err_len, [&] {
+    if (!s || !corpus) throw Error(IG_ECONFIG, "null session or corpus");
+    load_corpus(*s, *corpus);
+  });
+}
+
+int ig_session_run(ig_session* s, const ig_params* params, ig_result* out, char* err,
+                   size_t err_len) {
+  return guarded(err, err_len, [&] {
+    if (!s || !params || !out) throw Error(IG_ECONFIG, "null argument");
+    run(*s, *params, out);
+  });
+}
+
+uint64_t ig_session_launches(const ig_session* s) { return s ? s->launches : 0; }
+
+void ig_session_destroy(ig_session* s) {
+  if (!s) return;
+  cudaSetDevice(s->device);
+  delete s;
+}
+
+int ig_topk_ngrams(const ig_corpus* corpus, const ig_params* params, ig_result* out, char* err,
+                   size_t err_len) {
+  return guarded(err, err_len, [&] {
+    if (!corpus || !params || !out) throw Error(IG_ECONFIG, "null argument");
+    validate(*params);
+    ig_session* s = create(params->device, nullptr, nullptr);
+    try {
+      load_corpus(*s, *corpus);
+      run(*s, *params, out);
+    } catch (...) {
+      delete s;
+      throw;
+    }
+    delete s;
+  });
+}
+
+int ig_count_dense(const ig_corpus* corpus, uint32_t n, int32_t mode, int32_t device,
+                   uint64_t* table_out, char* err, size_t err_len) {
+  return guarded(err, err_len, [&] {
+    // dense_capacity, dense_pass.cpp:5-10
+    if (n < 1 || n > 3) throw Error(IG_ECONFIG, "dense pass supports gram lengths 1..3");
+    if (mode != IG_MODE_ONCE && mode != IG_MODE_ALL) throw Error(IG_ECONFIG, "bad count mode");
+    ig_session* s = create(device, nullptr, nullptr);
+    try {
+      load_corpus(*s, *corpus);
+      const uint64_t cap = 1ull << (8 * n);
+      unsigned long long* t = s->table.as<unsigned long long>(cap);
+      IGB_CUDA(cudaMemsetAsync(t, 0, cap * 8, s->stream));
+      launch_count_dense<unsigned long long>(s->dc, n, mode, t, s->work.as<uint32_t>(64),
+                                             s->num_sms, s->stream);
+      IGB_CUDA(cudaGetLastError());
+      IGB_CUDA(cudaMemcpyAsync(table_out, t, cap * 8, cudaMemcpyDeviceToHost, s->stream));
+      IGB_CUDA(cudaStreamSynchronize(s->stream));
+    } catch (...) {
+      delete s;
+      throw;
+    }
+    delete s;
+  });
+}
+
+int ig_extend_pass(const ig_corpus* corpus, const uint64_t* prefix_keys, uint64_t nprefix,
+                   uint32_t prefix_len, uint32_t j, int32_t mode, int32_t device,
+                   uint64_t* table_out, uint64_t* bytes_processed, char* err, size_t err_len) {
+  return guarded(err, err_len, [&] {
+    const uint32_t depth = nprefix ? prefix_len : 0;  // trie.cpp:23
+    if (j < 2 || depth != j - 1)  // intergrams.cpp:46-48
+      throw Error(IG_ECONFIG, "extension pass needs a trie of depth j-1");
+    if (j > IG_MAX_N) throw Error(IG_ECONFIG, "gram length above 8 is not supported");
+    if (mode != IG_MODE_ONCE && mode != IG_MODE_ALL) throw Error(IG_ECONFIG, "bad count mode");
+    {  // PrefixTrie::build rejects duplicates (trie.cpp:45-46)
+      std::vector<uint64_t> v(prefix_keys, prefix_keys + nprefix);
+      std::sort(v.begin(), v.end());
+      if (std::adjacent_find(v.begin(), v.end()) != v.end())
+        throw Error(IG_EINVALID, "duplicate prefix in trie input");
+    }
+    ig_session* s = create(device, nullptr, nullptr);
+    try {
+      load_corpus(*s, *corpus);
+      uint64_t* dk = s->surv_keys.as<uint64_t>(nprefix + 1);
+      IGB_CUDA(cudaMemcpyAsync(dk, prefix_keys, nprefix * 8, cudaMemcpyHostToDevice, s->stream));
+      DevPrefixSet ps = build_prefix_set(*s, dk, nprefix, prefix_len, mode);
+      const uint64_t cap = 256 * nprefix;
+      unsigned long long* t = s->table.as<unsigned long long>(cap);
+      IGB_CUDA(cudaMemsetAsync(t, 0, cap * 8, s->stream));
+      launch_count_extend<unsigned long long>(s->dc, ps, j, mode, t, s->work.as<uint32_t>(64),
+                                              s->num_sms, s->stream);
+      IGB_CUDA(cudaGetLastError());
+      std::vector<uint64_t> tab(cap);
+      std::vector<uint32_t> rank(nprefix);
+      IGB_CUDA(cudaMemcpyAsync(tab.data(), t, cap * 8, cudaMemcpyDeviceToHost, s->stream));
+      IGB_CUDA(cudaMemcpyAsync(rank.data(), ps.hidx ? s->rank_of_p.p : nullptr, nprefix * 4,
+                               cudaMemcpyDeviceToHost, s->stream));
+      IGB_CUDA(cudaStreamSynchronize(s->stream));
+      // back to the reference layout: ordinal (rank) * 256 + last byte
+      for (uint64_t p = 0; p < nprefix; ++p)
+        memcpy(table_out + (uint64_t)rank[p] * 256, tab.data() + p * 256, 256 * 8);
+      if (bytes_processed) *bytes_processed = s->dc.total;
+    } catch (...) {
+      delete s;
+      throw;
+    }
+    delete s;
+  });
+}
+
+int ig_top_k(const uint64_t* table, uint64_t cap, uint64_t k, const uint64_t* prefix_keys,
+             int32_t device, uint64_t* keys_out, uint64_t* counts_out, uint64_t* len_out,
+             char* err, size_t err_len) {
+  return guarded(err, err_len, [&] {
+    if (k < 1) throw Error(IG_ECONFIG, "top_k requires k >= 1");  // counting.cpp:54
+    ig_session* s = create(device, nullptr, nullptr);
+    try {
+      init_select(*s);
+      const uint64_t cap4 = (cap + 255) / 256 * 256;
+      unsigned long long* t = s->table.as<unsigned long long>(cap4);
+      IGB_CUDA(cudaMemsetAsync(t, 0, cap4 * 8, s->stream));
+      IGB_CUDA(cudaMemcpyAsync(t, table, cap * 8, cudaMemcpyHostToDevice, s->stream));
+      uint64_t* pk = nullptr;
+      int key_bits = 64;
+      if (prefix_keys) {
+        const uint64_t np = cap4 / 256;
+        pk = s->pkeys.as<uint64_t>(np);
+        IGB_CUDA(cudaMemsetAsync(pk, 0, np * 8, s->stream));
+        IGB_CUDA(cudaMemcpyAsync(pk, prefix_keys, (cap + 255) / 256 * 8, cudaMemcpyHostToDevice,
+                                 s->stream));
+      } else {
+        key_bits = 0;
+        while (key_bits < 64 && (1ull << key_bits) < cap4) ++key_bits;
+      }
+      const uint64_t kk = std::min<uint64_t>(k, cap4);
+      uint64_t* ok = s->next_keys.as<uint64_t>(kk + 1);
+      uint64_t* oc = s->next_counts.as<uint64_t>(kk + 1);
+      const uint64_t n = select_topk<unsigned long long>(s->sel, t, cap4, kk, pk, key_bits, ok, oc);
+      if (n) {
+        IGB_CUDA(cudaMemcpyAsync(keys_out, ok, n * 8, cudaMemcpyDeviceToHost, s->stream));
+        IGB_CUDA(cudaMemcpyAsync(counts_out, oc, n * 8, cudaMemcpyDeviceToHost, s->stream));
+      }
+      IGB_CUDA(cudaStreamSynchronize(s->stream));
+      *len_out = n;
+    } catch (...) {
+      delete s;
+      throw;
+    }
+    delete s;
+  });
+}
+
+void ig_shard_range(const uint64_t* offsets, uint64_t num_seqs, int32_t rank, int32_t world,
+                    uint64_t* first, uint64_t* last) {
+  // cut r: the sequence boundary nearest r*total/world (ties to the lower)
+  auto cut = [&](int32_t r) -> uint64_t {
+    if (r <= 0) return 0;
+    if (r >= world) return num_seqs;
+    const uint64_t total = offsets[num_seqs];
+    const unsigned __int128 target128 = (unsigned __int128)total * (uint64_t)r / (uint64_t)world;
+    const uint64_t target = (uint64_t)target128;
+    const uint64_t* it = std::lower_bound(offsets, offsets + num_seqs + 1, target);
+    uint64_t i = (uint64_t)(it - offsets);
+    if (i > num_seqs) i = num_seqs;
+    if (i > 0 && (offsets[i] - target) > (target - offsets[i - 1])) --i;
+    return i;
+  };
+  if (world < 1) world = 1;
+  uint64_t a = cut(rank), b = cut(rank + 1);
+  if (b < a) b = a;
+  *first = a;
+  *last = b;
+}
+
+}  // extern "C"
