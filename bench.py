@@ -1,0 +1,415 @@
+#!/usr/bin/env python
+"""Benchmark of the B200-native Intergrams top-k n-gram run (BASELINE.json metric:
+input GB/s per top-k n-gram run, and % of the HBM roofline).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+
+A step is one full run_intergrams (every counting pass, every top-k' selection
+and prefix-set build, the final top-k list copied to the host) over the
+config's synthetic corpus.  N=1 runs BASELINE configs[1] (c2: 4096 x 1 MiB
+Zipf-token corpus, n=6, k=10000, count-once).  For N>1 (torchrun, one process
+per GPU) every rank holds its own 4096-sequence shard of the same generator
+(weak scaling) and the per-pass count tables are summed with NCCL all-reduce.
+
+`value` is device-timed with CUDA events on the library's stream with the corpus
+resident in HBM; `e2e` is the same metric through the public session API with
+the corpus in pinned host memory, the H2D copy and the result D2H inside the
+timed region.  `--impl reference` times the reference CPU implementation
+(compiled from its own sources into oracle/_ref) on a bounded sample.
+"""
+from __future__ import annotations
+
+import argparse
+import hashlib
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "input GB/s per top-k n-gram run (1/2/4/8 B200) and % of HBM roofline"
+UNIT = "GB/s"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# ------------------------------------------------------------------ clocks
+
+REASON_BITS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+
+class ClockSampler:
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 3:
+                try:
+                    self.samples.append((float(parts[0]), float(parts[1]), int(parts[2], 16)))
+                except ValueError:
+                    pass
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [s[0] for s in self.samples]
+        reasons = set()
+        for s in self.samples:
+            for bit, name in REASON_BITS.items():
+                if s[2] & bit and name != "gpu_idle":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(s[1] for s in self.samples),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ collective
+
+def make_collective(rank, world, bytes_total, seqs_total):
+    import ctypes as C
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2511_14955_b200 import _native as N
+
+    class _CAI:
+        def __init__(self, ptr, n, typestr):
+            self.__cuda_array_interface__ = {"data": (ptr, False), "shape": (n,),
+                                             "typestr": typestr, "version": 3, "strides": None}
+
+    def _allreduce(buf, count, dtype, stream, user):
+        try:
+            # sum of unsigned counters == sum of the same bits as signed ints (mod 2^w)
+            t = torch.as_tensor(_CAI(buf, count, "<i4" if dtype == 0 else "<i8"), device="cuda")
+            with torch.cuda.stream(torch.cuda.ExternalStream(stream)):
+                dist.all_reduce(t)
+            return 0
+        except Exception as e:  # noqa: BLE001
+            log("allreduce failed:", e)
+            return 1
+
+    cb = N.ALLREDUCE_FN(_allreduce)
+    coll = N.ig_collective(rank=rank, world=world, bytes_total=bytes_total,
+                           seqs_total=seqs_total, allreduce=cb, user=None)
+    return coll, cb
+
+
+# ------------------------------------------------------------------ reference arm
+
+def run_reference(args, cfg, rank, world):
+    from oracle import oracle as O
+    from paper_2511_14955_b200 import synth as S
+
+    if rank != 0:
+        return 0
+    try:
+        L = O.ref()
+        kind = "reference"
+        cores = int(L.igref_hardware_concurrency())
+    except Exception as e:  # noqa: BLE001
+        print(json.dumps({"impl": "reference", "unavailable": f"reference build missing: {e}"}))
+        return 0
+    sample_seqs = args.ref_sample
+    data, off = S.generate(cfg, 0, sample_seqs)
+    nbytes = int(off[-1])
+    times = []
+    for i in range(args.warmup + args.steps):
+        rc, keys, counts, rows, diag, secs, err = O.ref_run(data, off, cfg.n, cfg.k, cfg.z,
+                                                            cfg.mode, 0)
+        if rc != 0:
+            print(json.dumps({"impl": "reference", "unavailable": f"reference failed: {err}"}))
+            return 0
+        if i >= args.warmup:
+            times.append(secs)
+    t = sum(times) / len(times)
+    v = nbytes / t / 1e9
+    sample = f"first {sample_seqs} of {cfg.num_seqs or 'all'} sequences ({nbytes} B) of {cfg.name}"
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic (seeded generator, csrc/synth.c)",
+            "config": config_dict(cfg, world),
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": kind,
+                             "sample": sample},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def config_dict(cfg, world):
+    return {"workload": f"{cfg.name}: {cfg.describe()}", "n": cfg.n, "k": cfg.k, "z": cfg.z,
+            "mode": "once" if cfg.mode == 0 else "all",
+            "corpus_bytes_per_gpu": None, "parallelism": f"dp{world} (whole-sequence shards)",
+            "l2": "inputs larger than L2 (corpus >> 126 MB), no flush needed"}
+
+
+def cpu_baseline(cfg, sample_seqs):
+    """The reference CPU path (oracle/_ref) timed on this host, bounded sample."""
+    from oracle import oracle as O
+    from paper_2511_14955_b200 import synth as S
+    data, off = S.generate(cfg, 0, sample_seqs)
+    nbytes = int(off[-1])
+    try:
+        L = O.ref()
+        cores = int(L.igref_hardware_concurrency())
+        rc, keys, counts, rows, diag, secs, err = O.ref_run(data, off, cfg.n, cfg.k, cfg.z,
+                                                            cfg.mode, 0)
+        kind = "reference"
+        if rc != 0:
+            raise RuntimeError(err)
+    except Exception as e:  # noqa: BLE001
+        log("reference build unavailable, timing the C oracle port:", e)
+        t0 = time.perf_counter()
+        O.oracle_run(data, off, cfg.n, cfg.k, cfg.z, cfg.mode)
+        secs = time.perf_counter() - t0
+        kind, cores = "port", 1
+    return {"value": nbytes / secs / 1e9, "unit": UNIT, "cores": cores, "kind": kind,
+            "sample": f"first {sample_seqs} sequences ({nbytes} B) of {cfg.name}, "
+                      f"n={cfg.n} k={cfg.k} z={cfg.z} {'once' if cfg.mode == 0 else 'all'}"}
+
+
+# ------------------------------------------------------------------ our arm
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--ref-sample", type=int, default=256,
+                    help="sequences of the config the CPU reference is timed on")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--seqs", type=int, default=0, help="override sequences per GPU")
+    ap.add_argument("--profile-run", action="store_true",
+                    help="load, run once, exit (for ncu captures; prints nothing)")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+
+    from paper_2511_14955_b200 import synth as S
+    cfg = S.CONFIGS[args.config]
+    rank, world, local = dist_env()
+
+    if args.impl == "reference":
+        return run_reference(args, cfg, rank, world)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2511_14955_b200 import intergrams as ig
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    # ---- this rank's shard: weak scaling, sequences [rank*m, (rank+1)*m)
+    off_all = S.offsets(cfg)
+    m_all = off_all.size - 1
+    per = args.seqs or m_all
+    if cfg.kind == S.K_LOGNORMAL or world == 1:
+        # one corpus sharded by bytes (lognormal lengths), or the whole config at N=1
+        first, count = 0, per
+        if world > 1:
+            first, last = ig.shard_range(off_all, rank, world)
+            count = last - first
+        gen_cfg = cfg
+    else:
+        gen_cfg = S.scaled(cfg, num_seqs=per * world)
+        first, count = rank * per, per
+    t0 = time.time()
+    nbytes = int(S.offsets(gen_cfg)[first + count] - S.offsets(gen_cfg)[first])
+    host = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    data, off = S.generate(gen_cfg, first, count, out=host.numpy())
+    log(f"rank {rank}: generated {nbytes / 2**30:.2f} GiB ({count} seqs) in {time.time() - t0:.1f}s")
+    off_np = np.ascontiguousarray(off, np.uint64)
+    bytes_total = nbytes * world if cfg.kind != S.K_LOGNORMAL else int(off_all[-1])
+    if world > 1 and cfg.kind == S.K_LOGNORMAL:
+        bytes_total = int(off_all[-1])
+    seqs_total = count * world if cfg.kind != S.K_LOGNORMAL else m_all
+
+    stream = torch.cuda.Stream()
+    coll, _cb = (None, None)
+    if world > 1:
+        coll, _cb = make_collective(rank, world, bytes_total, seqs_total)
+    sess = ig.Session(device=local, stream=stream.cuda_stream, collective=coll)
+    corpus = ig.Corpus(data, off_np)
+    sess.load(corpus)
+    icfg = ig.IntergramConfig(n=cfg.n, k=cfg.k, z=cfg.z, mode=ig.CountMode(cfg.mode))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    if args.profile_run:
+        res = sess.run(icfg)
+        torch.cuda.synchronize()
+        log("profile run:", [(p.label, round(p.seconds * 1e3, 3)) for p in res.passes])
+        sess.close()
+        return 0
+
+    # ---- device-resident timing
+    for _ in range(args.warmup):
+        res = sess.run(icfg)
+    barrier()
+    l0 = sess.launches
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    rows = []
+    with ClockSampler(local) as clk:
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            res = sess.run(icfg)
+            rows.append(res.passes)
+        ev1.record(stream)
+        barrier()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    launches = (sess.launches - l0) // args.steps
+    t_max = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+    ms = float(t_max.item())
+    value = bytes_total / (ms * 1e-3) / 1e9
+
+    # ---- roofline of the dominant kernel (the counting pass with the largest share)
+    peak, peak_src = peaks()
+    passes = {}
+    for step in rows:
+        for p in step:
+            if p.bytes_processed > 0:
+                passes.setdefault(p.label, []).append(p.seconds)
+    dom_label, dom_times = max(passes.items(), key=lambda kv: sum(kv[1]))
+    dom_s = sum(dom_times) / len(dom_times)
+    local_bytes = nbytes  # algorithmic bytes per launch: this rank's corpus, read once
+    achieved = local_bytes / dom_s / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        try:
+            with open(tp) as f:
+                traffic = json.load(f).get(f"{cfg.name}:{dom_label}")
+        except Exception:
+            traffic = None
+    step_breakdown = {}
+    for step in rows:
+        for p in step:
+            step_breakdown[p.label] = step_breakdown.get(p.label, 0.0) + p.seconds * 1e3 / len(rows)
+
+    # ---- end-to-end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        barrier()
+        t_e2e = []
+        for i in range(2 + args.steps):
+            torch.cuda.synchronize()
+            ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ea.record(stream)
+            sess.load(corpus)  # H2D of the pinned corpus + offsets
+            r2 = sess.run(icfg)  # result list D2H inside
+            eb.record(stream)
+            eb.synchronize()
+            if i >= 2:
+                t_e2e.append(ea.elapsed_time(eb))
+        e_ms = sum(t_e2e) / len(t_e2e)
+        te = torch.tensor([e_ms], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e_ms = float(te.item())
+        e2e = {"value": bytes_total / (e_ms * 1e-3) / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": int(nbytes + off_np.nbytes),
+               "d2h_bytes_per_step": int(16 * len(r2.topk)), "ms_per_step": e_ms}
+        assert r2.topk == res.topk
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(cfg, args.ref_sample)
+
+    if rank == 0:
+        passes_alg = max(cfg.n, 3) - 2
+        cd = config_dict(cfg, world)
+        cd["corpus_bytes_per_gpu"] = nbytes
+        cd["sequences_per_gpu"] = count
+        cd["counting_passes"] = passes_alg
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic (seeded generator csrc/synth.c; BASELINE shapes)",
+            "config": cd,
+            "hbm_roofline_frac_full_run": (bytes_total * passes_alg / (ms * 1e-3) / 1e9)
+            / (world * peak),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": f"count pass '{dom_label}'", "peak_source": peak_src,
+                         "algorithmic_bytes_per_launch": local_bytes,
+                         "avg_launch_ms": dom_s * 1e3},
+            "step_breakdown_ms": step_breakdown,
+            "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "result_digest": hashlib.sha256(ig.topk_to_tsv(res.topk).encode()).hexdigest()[:16],
+            "topk_len": len(res.topk),
+        }
+        print(json.dumps(line), flush=True)
+    sess.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())
