@@ -145,8 +145,8 @@ __device__ __forceinline__ uint32_t valid_mask_one(int64_t b0, int64_t s0, int64
   return ((1u << b) - 1u) & ~((1u << a) - 1u);
 }
 
-// Open-addressing lookup of a prefix key in owner slice `o`.  Returns p or
-// 0xffffffff.  Slices: keys[o*S .. o*S+S).
+// Open-addressing lookup of a prefix key in owner slice `o` (global/L2).
+// Returns p or 0xffffffff.  Slices: keys[o*S .. o*S+S).
 __device__ __forceinline__ uint32_t prefix_lookup(const uint64_t* __restrict__ hkeys,
                                                   const uint32_t* __restrict__ hidx, uint32_t S,
                                                   uint32_t lgS, uint32_t o, uint64_t key) {
@@ -160,11 +160,27 @@ __device__ __forceinline__ uint32_t prefix_lookup(const uint64_t* __restrict__ h
   }
 }
 
+// Packed prefix-set slice: entry = (key << ib) | local index, kEmptyKey = empty.
+// Returns the local index (p - owner_start) or 0xffffffff.
+__device__ __forceinline__ uint32_t lookup_packed(const uint64_t* tab, uint32_t lgS, uint32_t ib,
+                                                  uint64_t key) {
+  const uint32_t mask = (1u << lgS) - 1;
+  uint32_t h = hash_slot(key, lgS);
+  for (;;) {
+    const uint64_t e = tab[h];
+    if (e == kEmptyKey) return 0xffffffffu;
+    if ((e >> ib) == key) return (uint32_t)(e & ((1ull << ib) - 1));
+    h = (h + 1) & mask;
+  }
+}
+
 // ------------------------------------------------------------------ tiles
 
-// tile_seq[t] = sequence containing byte t*512 (upper_bound(off, t*512) - 1).
-__global__ void k_tile_seq(const uint64_t* __restrict__ off, uint64_t m, uint64_t ntiles,
-                           uint32_t* __restrict__ tile_seq) {
+// tile_desc[t]: bit 31 = "fast" (the 512-byte tile lies inside one sequence
+// and starts >= 7 bytes after its start, so every position is a valid gram end
+// for any n <= 8); bits 0..30 = sequence containing byte t*512.
+__global__ void k_tile_desc(const uint64_t* __restrict__ off, uint64_t m, uint64_t ntiles,
+                            uint32_t* __restrict__ desc) {
   for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < ntiles;
        t += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t b = t * kTileBytes;
@@ -176,149 +192,265 @@ __global__ void k_tile_seq(const uint64_t* __restrict__ off, uint64_t m, uint64_
     }
     uint64_t s = lo ? lo - 1 : 0;
     if (s >= m) s = m ? m - 1 : 0;
-    tile_seq[t] = (uint32_t)s;
+    const bool fast = m && off[s + 1] >= b + kTileBytes && b >= off[s] + 7;
+    desc[t] = (uint32_t)s | (fast ? 0x80000000u : 0u);
   }
 }
 
-void launch_tile_seq(const uint64_t* off, uint64_t m, uint64_t ntiles, uint32_t* tile_seq,
+void launch_tile_seq(const uint64_t* off, uint64_t m, uint64_t ntiles, uint32_t* desc,
                      cudaStream_t st) {
   if (!ntiles) return;
   const int threads = 256;
   const uint64_t blocks = (ntiles + threads - 1) / threads;
-  k_tile_seq<<<(unsigned)(blocks < 65535 ? blocks : 65535), threads, 0, st>>>(off, m, ntiles,
-                                                                            tile_seq);
+  k_tile_desc<<<(unsigned)(blocks < 65535 ? blocks : 65535), threads, 0, st>>>(off, m, ntiles,
+                                                                             desc);
+}
+
+// Packs owner slices of the open-addressing prefix set for shared-memory staging.
+__global__ void k_pack_prefix(const uint64_t* __restrict__ hkeys, const uint32_t* __restrict__ hidx,
+                              const uint32_t* __restrict__ owner_start, uint32_t S, uint32_t ib,
+                              uint64_t total, uint64_t* __restrict__ packed) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = hkeys[i];
+    const uint32_t o = (uint32_t)(i / S);
+    packed[i] = k == kEmptyKey ? kEmptyKey : ((k << ib) | (uint64_t)(hidx[i] - owner_start[o]));
+  }
+}
+
+void launch_pack_prefix(const DevPrefixSet& ps, uint64_t* packed, cudaStream_t st) {
+  const uint64_t total = (uint64_t)ps.G * ps.S;
+  const unsigned blocks = (unsigned)((total + 255) / 256);
+  k_pack_prefix<<<blocks < 4096 ? blocks : 4096, 256, 0, st>>>(ps.hkeys, ps.hidx, ps.owner_start,
+                                                               ps.S, ps.ib, total, packed);
+}
+
+// Slow path: validity of a segment that crosses sequence boundaries.
+template <int L>
+__device__ __noinline__ uint32_t valid_mask_walk(const uint64_t* __restrict__ off, uint64_t m,
+                                                 uint64_t total, uint64_t q, int64_t b0) {
+  if (b0 >= (int64_t)total) return 0;
+  int64_t s0 = (int64_t)off[q], s1 = (int64_t)off[q + 1];
+  while (s1 <= b0 && q + 1 < m) {
+    ++q;
+    s0 = s1;
+    s1 = (int64_t)off[q + 1];
+  }
+  uint32_t vm = 0;
+  for (;;) {
+    vm |= valid_mask_one<L>(b0, s0, s1);
+    if (s1 >= b0 + 16 || q + 1 >= m) break;
+    ++q;
+    s0 = s1;
+    s1 = (int64_t)off[q + 1];
+  }
+  return vm;
 }
 
 // ------------------------------------------------------------------ count-all
 
-// Counts every gram end in the tile range with one RED per (warp-merged) id.
-// KIND 0: dense id over L bytes.  KIND 1: extension, L = j.
-template <int KIND, int L, typename CT>
-__global__ void __launch_bounds__(512) k_count_all(DevCorpus c, DevPrefixSet ps, CT* __restrict__ table) {
+// Flat scan of all 512-byte tiles; one RED per valid gram end (dense) or per
+// prefix hit (extension).  Each warp keeps the next tile's 128-bit loads in
+// flight while it counts the current one.  TAB: 0 none (dense), 1 prefix set
+// staged in shared memory (packed), 2 prefix set read from global/L2.
+template <int KIND, int L, typename CT, int TAB, bool AGG>
+__global__ void __launch_bounds__(256) k_count_all(DevCorpus c, DevPrefixSet ps,
+                                                   const uint64_t* __restrict__ packed,
+                                                   CT* __restrict__ table) {
+  extern __shared__ uint64_t s_tab[];
+  if constexpr (TAB == 1) {
+    for (uint32_t i = threadIdx.x; i < ps.S; i += blockDim.x) s_tab[i] = packed[i];
+    __syncthreads();
+  }
   const int lane = threadIdx.x & 31;
-  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  for (uint64_t t = warp; t < c.ntiles; t += nwarps) {
-    const int64_t b0 = (int64_t)t * kTileBytes + lane * 16;
+  uint64_t t = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  if (t >= c.ntiles) return;
+  uint4 v = __ldcs(reinterpret_cast<const uint4*>(c.data + t * kTileBytes + lane * 16));
+  uint2 h = make_uint2(0, 0);
+  if (lane == 0) h = *reinterpret_cast<const uint2*>(c.data + t * kTileBytes - 8);
+  uint32_t d = __ldg(c.tile_seq + t);
+  for (;;) {
+    const uint64_t tn = t + nwarps;
+    uint4 vn = make_uint4(0, 0, 0, 0);
+    uint2 hn = make_uint2(0, 0);
+    uint32_t dn = 0;
+    if (tn < c.ntiles) {
+      vn = __ldcs(reinterpret_cast<const uint4*>(c.data + tn * kTileBytes + lane * 16));
+      if (lane == 0) hn = *reinterpret_cast<const uint2*>(c.data + tn * kTileBytes - 8);
+      dn = __ldg(c.tile_seq + tn);
+    }
     Seg s;
-    load_seg(c.data, b0, s);
-    // validity: walk sequence boundaries from the tile's first sequence
-    uint64_t q = c.tile_seq[t];
-    int64_t s0 = (int64_t)c.off[q], s1 = (int64_t)c.off[q + 1];
-    while (s1 <= b0 && q + 1 < c.m) {
-      ++q;
-      s0 = s1;
-      s1 = (int64_t)c.off[q + 1];
+    s.W[2] = v.x;
+    s.W[3] = v.y;
+    s.W[4] = v.z;
+    s.W[5] = v.w;
+    s.W[6] = 0;
+    s.W[0] = __shfl_up_sync(0xffffffffu, v.z, 1);
+    s.W[1] = __shfl_up_sync(0xffffffffu, v.w, 1);
+    if (lane == 0) {
+      s.W[0] = h.x;
+      s.W[1] = h.y;
     }
-    uint32_t vm = 0;
-    if (b0 < (int64_t)c.total) {
-      if (s1 >= b0 + 16) {
-        vm = valid_mask_one<L>(b0, s0, s1);
-      } else {
-        // a sequence boundary inside the segment: per-sequence pieces
-        for (;;) {
-          vm |= valid_mask_one<L>(b0, s0, s1);
-          if (s1 >= b0 + 16 || q + 1 >= c.m) break;
-          ++q;
-          s0 = s1;
-          s1 = (int64_t)c.off[q + 1];
-        }
-      }
-    }
+    const int64_t b0 = (int64_t)t * kTileBytes + lane * 16;
+    const uint32_t vm = (d >> 31) ? 0xffffu : valid_mask_walk<L>(c.off, c.m, c.total, d & 0x7fffffffu, b0);
     static_for<0, 16>([&](auto tc) {
       constexpr int T = decltype(tc)::value;
       const bool valid = (vm >> T) & 1u;
-      uint32_t id = 0xffffffffu;
-      uint64_t gid = 0;
-      if (valid) {
-        const uint64_t key = key8_at<T>(s) & gram_mask<L>();
-        if constexpr (KIND == 0) {
-          gid = key;
-          id = (uint32_t)key;
+      if constexpr (KIND == 0) {
+        const uint32_t id = valid ? (uint32_t)(key8_at<T>(s) & gram_mask<L>()) : 0xffffffffu;
+        if constexpr (AGG) {
+          const uint32_t peers = __match_any_sync(0xffffffffu, id);
+          if (valid && lane == __ffs(peers) - 1) atomicAdd(table + id, (CT)__popc(peers));
         } else {
-          const uint32_t p = prefix_lookup(ps.hkeys, ps.hidx, ps.S, ps.lgS, 0, key >> 8);
-          if (p != 0xffffffffu) {
-            gid = (uint64_t)p * 256 + (key & 0xff);
-            id = (uint32_t)gid;  // < 2^32: 256*K with K < 2^24
-          }
+          if (valid) atomicAdd(table + id, (CT)1);
+        }
+      } else {
+        if (valid) {
+          const uint64_t key = key8_at<T>(s) & gram_mask<L>();
+          uint32_t p;
+          if constexpr (TAB == 1) p = lookup_packed(s_tab, ps.lgS, ps.ib, key >> 8);
+          else p = prefix_lookup(ps.hkeys, ps.hidx, ps.S, ps.lgS, 0, key >> 8);
+          if (p != 0xffffffffu) atomicAdd(table + ((uint64_t)p * 256 + (key & 0xff)), (CT)1);
         }
       }
-      if constexpr (KIND == 0) {
-        // merge duplicate ids of this step across the warp (hot grams)
-        const uint32_t peers = __match_any_sync(0xffffffffu, id);
-        if (id != 0xffffffffu && lane == __ffs(peers) - 1) atomicAdd(table + gid, (CT)__popc(peers));
-      } else {
-        if (id != 0xffffffffu) atomicAdd(table + gid, (CT)1);
-      }
     });
+    if (tn >= c.ntiles) break;
+    t = tn;
+    v = vn;
+    h = hn;
+    d = dn;
   }
 }
 
 // ------------------------------------------------------------------ count-once
 
-// One CTA = (group g, owner o).  For every sequence taken from owner o's
-// work counter, scan the whole sequence, mark owned windows in the smem
-// bitmap, RED the count of each id the first time it is marked, then clear.
-// local id: dense -> id >> lgG (the low lgG bits are implied by o);
-// extension -> (p - owner_start[o])*256 + last.
-template <int KIND, int L, typename CT>
-__global__ void __launch_bounds__(1024) k_count_once(DevCorpus c, DevPrefixSet ps, uint32_t G,
-                                                     uint32_t lgG, uint32_t bm_words,
-                                                     uint32_t* __restrict__ work,
-                                                     CT* __restrict__ table) {
+constexpr int kOnceThreads = 512;
+constexpr int kOnceWarps = kOnceThreads / 32;
+constexpr int kTileBufWords = 136;  // [2 unused | 2 halo | 128 tile (16-B aligned) | pad]
+
+// Big-endian key of the 8 bytes ending at tile position p (0..511) from the
+// warp's staged tile (word 0..1 = the 8 bytes before the tile).
+__device__ __forceinline__ uint64_t key8_smem(const uint32_t* buf, uint32_t p) {
+  const uint32_t o = p + 9;  // tile byte p lives at buf byte 16 + p; first of the 8 bytes
+  const uint32_t wi = o >> 2, sh = (o & 3) * 8;
+  const uint32_t w0 = buf[wi], w1 = buf[wi + 1], w2 = buf[wi + 2];
+  const uint32_t lo = __funnelshift_r(w0, w1, sh), hi = __funnelshift_r(w1, w2, sh);
+  return ((uint64_t)__byte_perm(lo, 0, 0x0123) << 32) | (uint64_t)__byte_perm(hi, 0, 0x0123);
+}
+
+// One CTA = (group g, owner o); group g takes sequences order[g], order[g+NG],
+// ... (the G CTAs of a group walk the same sequences in the same order, so a
+// sequence is read from HBM once and from L2 by the others).  Per 512-byte
+// tile a warp (1) stages the tile in smem, (2) computes the 16-bit mask of
+// valid gram ends it owns per lane in registers, (3) compacts the owned
+// positions into a warp queue, (4) drains the queue 32 positions at a time
+// with all lanes converged: key -> (prefix lookup) -> bitmap test -> first
+// occurrence: ATOMS.OR + RED.  After each sequence the slice bitmap is cleared.
+template <int KIND, int L, typename CT, int TAB>
+__global__ void __launch_bounds__(kOnceThreads) k_count_once(DevCorpus c, DevPrefixSet ps,
+                                                           const uint64_t* __restrict__ packed,
+                                                           uint32_t G, uint32_t lgG,
+                                                           uint32_t bm_words, uint32_t ngroups,
+                                                           CT* __restrict__ table) {
   extern __shared__ uint4 smem_raw[];
   uint32_t* bm = reinterpret_cast<uint32_t*>(smem_raw);
-  __shared__ uint32_t s_seq;
+  uint64_t* s_tab = reinterpret_cast<uint64_t*>(bm + bm_words);
+  const uint32_t tab_words = (TAB == 1) ? ps.S * 2 : 0;
+  uint32_t* tilebuf = bm + bm_words + tab_words;
+  uint16_t* queue = reinterpret_cast<uint16_t*>(tilebuf + kOnceWarps * kTileBufWords);
+
   const uint32_t o = blockIdx.x % G;
-  const uint32_t gm = G - 1;
-  const uint32_t gm4 = gm * 0x01010101u, o4 = o * 0x01010101u;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  const uint32_t g = blockIdx.x / G;
+  const uint32_t gm4 = (G - 1) * 0x01010101u, o4 = o * 0x01010101u;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t* buf = tilebuf + warp * kTileBufWords;
+  uint16_t* q = queue + warp * 512;
   const uint32_t ostart = (KIND == 1) ? ps.owner_start[o] : 0u;
 
   for (uint32_t i = threadIdx.x; i < bm_words / 4; i += blockDim.x) smem_raw[i] = make_uint4(0, 0, 0, 0);
+  if constexpr (TAB == 1) {
+    const uint64_t* src = packed + (size_t)o * ps.S;
+    for (uint32_t i = threadIdx.x; i < ps.S; i += blockDim.x) s_tab[i] = src[i];
+  }
+  if (lane == 0) {
+    for (int i = 132; i < kTileBufWords; ++i) buf[i] = 0;
+  }
   __syncthreads();
-  for (;;) {
-    if (threadIdx.x == 0) s_seq = atomicAdd(work + o, 1u);
-    __syncthreads();
-    const uint32_t r = s_seq;
-    if (r >= c.m) break;
-    const uint32_t q = c.order[r];
-    const int64_t s0 = (int64_t)c.off[q], s1 = (int64_t)c.off[q + 1];
+
+  for (uint64_t r = g; r < c.m; r += ngroups) {
+    const uint32_t sq = c.order[r];
+    const int64_t s0 = (int64_t)c.off[sq], s1 = (int64_t)c.off[sq + 1];
     if (s1 - s0 >= L) {
       const int64_t first = s0 & ~int64_t(15);
-      const int64_t nseg = (s1 - first + 15) >> 4;
-      for (int64_t base = (int64_t)warp * 32; base < nseg; base += (int64_t)nwarp * 32) {
-        const int64_t b0 = first + (base + lane) * 16;
+      const int64_t ntiles = (s1 - first + kTileBytes - 1) / kTileBytes;
+      int64_t t = warp;
+      uint4 v = make_uint4(0, 0, 0, 0);
+      uint2 h = make_uint2(0, 0);
+      if (t < ntiles) {
+        v = __ldcg(reinterpret_cast<const uint4*>(c.data + first + t * kTileBytes + lane * 16));
+        if (lane == 0) h = *reinterpret_cast<const uint2*>(c.data + first + t * kTileBytes - 8);
+      }
+      while (t < ntiles) {
+        const int64_t tn = t + kOnceWarps;
+        uint4 vn = make_uint4(0, 0, 0, 0);
+        uint2 hn = make_uint2(0, 0);
+        if (tn < ntiles) {
+          vn = __ldcg(reinterpret_cast<const uint4*>(c.data + first + tn * kTileBytes + lane * 16));
+          if (lane == 0) hn = *reinterpret_cast<const uint2*>(c.data + first + tn * kTileBytes - 8);
+        }
+        const int64_t b0 = first + t * kTileBytes + lane * 16;
         Seg s;
-        load_seg(c.data, b0, s);
+        s.W[2] = v.x;
+        s.W[3] = v.y;
+        s.W[4] = v.z;
+        s.W[5] = v.w;
+        s.W[6] = 0;
+        s.W[0] = __shfl_up_sync(0xffffffffu, v.z, 1);
+        s.W[1] = __shfl_up_sync(0xffffffffu, v.w, 1);
+        if (lane == 0) {
+          s.W[0] = h.x;
+          s.W[1] = h.y;
+          buf[2] = h.x;
+          buf[3] = h.y;
+        }
+        reinterpret_cast<uint4*>(buf + 4)[lane] = v;
         uint32_t vm = valid_mask_one<L>(b0, s0, s1);
         if (G > 1) vm &= owner_mask<KIND, L>(s, gm4, o4);
+        // warp exclusive scan of the owned counts -> queue slots
+        const uint32_t cnt = __popc(vm);
+        uint32_t incl = cnt;
+#pragma unroll
+        for (int dd = 1; dd < 32; dd <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, incl, dd);
+          if (lane >= dd) incl += y;
+        }
+        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+        uint32_t pos = incl - cnt;
         while (vm) {
           const int T = __ffs(vm) - 1;
           vm &= vm - 1;
-          // runtime T: assemble the key from the segment words
-          uint64_t key;
-          switch (T) {
-#define IGB_CASE(X) \
-  case X:           \
-    key = key8_at<X>(s); \
-    break;
-            IGB_CASE(0) IGB_CASE(1) IGB_CASE(2) IGB_CASE(3) IGB_CASE(4) IGB_CASE(5)
-            IGB_CASE(6) IGB_CASE(7) IGB_CASE(8) IGB_CASE(9) IGB_CASE(10) IGB_CASE(11)
-            IGB_CASE(12) IGB_CASE(13) IGB_CASE(14) default: key = key8_at<15>(s); break;
-#undef IGB_CASE
-          }
-          key &= gram_mask<L>();
+          q[pos++] = (uint16_t)(lane * 16 + T);
+        }
+        __syncwarp();
+        for (uint32_t i = lane; i < total; i += 32) {
+          const uint32_t p = q[i];
+          const uint64_t key = key8_smem(buf, p) & gram_mask<L>();
           uint64_t gid;
           uint32_t local;
           if constexpr (KIND == 0) {
             gid = key;
             local = (uint32_t)(key >> lgG);
           } else {
-            const uint32_t p = prefix_lookup(ps.hkeys, ps.hidx, ps.S, ps.lgS, o, key >> 8);
-            if (p == 0xffffffffu) continue;
-            gid = (uint64_t)p * 256 + (key & 0xff);
-            local = (p - ostart) * 256 + (uint32_t)(key & 0xff);
+            uint32_t lp;
+            if constexpr (TAB == 1) lp = lookup_packed(s_tab, ps.lgS, ps.ib, key >> 8);
+            else {
+              lp = prefix_lookup(ps.hkeys, ps.hidx, ps.S, ps.lgS, o, key >> 8);
+              if (lp != 0xffffffffu) lp -= ostart;
+            }
+            if (lp == 0xffffffffu) continue;
+            gid = (uint64_t)(ostart + lp) * 256 + (key & 0xff);
+            local = lp * 256 + (uint32_t)(key & 0xff);
           }
           const uint32_t bit = 1u << (local & 31);
           uint32_t* w = bm + (local >> 5);
@@ -326,10 +458,13 @@ __global__ void __launch_bounds__(1024) k_count_once(DevCorpus c, DevPrefixSet p
             if (!(atomicOr(w, bit) & bit)) atomicAdd(table + gid, (CT)1);
           }
         }
+        __syncwarp();
+        t = tn;
+        v = vn;
+        h = hn;
       }
     }
     __syncthreads();
-    // clear: the whole slice bitmap (vectorised)
     for (uint32_t i = threadIdx.x; i < bm_words / 4; i += blockDim.x) smem_raw[i] = make_uint4(0, 0, 0, 0);
     __syncthreads();
   }
@@ -341,36 +476,54 @@ template <int KIND, int L, typename CT>
 static void launch_all_t(const DevCorpus& c, const DevPrefixSet& ps, CT* table, int num_sms,
                          cudaStream_t st) {
   if (!c.ntiles) return;
-  const int threads = 512;
+  const int threads = 256;
   uint64_t want = (c.ntiles * 32 + threads - 1) / threads;
-  const uint64_t cap = (uint64_t)num_sms * 4 * 8;  // 4 CTAs/SM, 8 waves of tiles max
+  const uint64_t cap = (uint64_t)num_sms * 8;  // 8 CTAs (64 warps) per SM, persistent
   unsigned blocks = (unsigned)(want < cap ? want : cap);
   if (!blocks) blocks = 1;
-  k_count_all<KIND, L, CT><<<blocks, threads, 0, st>>>(c, ps, table);
+  if constexpr (KIND == 0) {
+    k_count_all<0, L, CT, 0, true><<<blocks, threads, 0, st>>>(c, ps, nullptr, table);
+  } else {
+    if (ps.packed && (size_t)ps.S * 8 <= 48 * 1024) {
+      k_count_all<1, L, CT, 1, false><<<blocks, threads, ps.S * 8, st>>>(c, ps, ps.packed, table);
+    } else {
+      k_count_all<1, L, CT, 2, false><<<blocks, threads, 0, st>>>(c, ps, nullptr, table);
+    }
+  }
+}
+
+template <int KIND, int L, typename CT, int TAB>
+static void launch_once_tt(const DevCorpus& c, const DevPrefixSet& ps, uint32_t G, uint32_t lgG,
+                           uint32_t bm_words, size_t smem, CT* table, int num_sms, cudaStream_t st) {
+  auto kern = k_count_once<KIND, L, CT, TAB>;
+  IGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  IGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kOnceThreads, smem));
+  if (per_sm < 1) throw Error(IG_EINTERNAL, "count-once slice does not fit in shared memory");
+  uint64_t ngroups = ((uint64_t)num_sms * per_sm) / G;
+  if (ngroups < 1) ngroups = 1;
+  if (ngroups > c.m) ngroups = c.m;
+  kern<<<(unsigned)(ngroups * G), kOnceThreads, smem, st>>>(c, ps, ps.packed, G, lgG, bm_words,
+                                                            (uint32_t)ngroups, table);
 }
 
 template <int KIND, int L, typename CT>
 static void launch_once_t(const DevCorpus& c, const DevPrefixSet& ps, uint32_t G, uint32_t lgG,
-                          uint64_t slice_bits, uint32_t* work, CT* table, int num_sms,
-                          cudaStream_t st) {
+                          uint64_t slice_bits, CT* table, int num_sms, cudaStream_t st) {
   if (!c.m) return;
-  uint32_t bm_words = (uint32_t)((slice_bits + 127) / 128 * 4);  // multiple of 4 words
-  size_t smem = (size_t)bm_words * 4;
-  auto kern = k_count_once<KIND, L, CT>;
-  IGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const int threads = 1024;
-  int per_sm = 0;
-  IGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
-  if (per_sm < 1) throw Error(IG_EINTERNAL, "count-once bitmap does not fit in shared memory");
-  uint64_t ngroups = ((uint64_t)num_sms * per_sm) / G;
-  if (ngroups < 1) ngroups = 1;
-  if (ngroups > c.m) ngroups = c.m;
-  IGB_CUDA(cudaMemsetAsync(work, 0, G * sizeof(uint32_t), st));
-  kern<<<(unsigned)(ngroups * G), threads, smem, st>>>(c, ps, G, lgG, bm_words, work, table);
+  const uint32_t bm_words = (uint32_t)((slice_bits + 127) / 128 * 4);  // multiple of 4 words
+  const size_t fixed = (size_t)bm_words * 4 + (size_t)kOnceWarps * (kTileBufWords * 4 + 1024);
+  const size_t tab = (KIND == 1 && ps.packed) ? (size_t)ps.S * 8 : 0;
+  if (tab && fixed + tab <= kMaxOnceSmem) {
+    launch_once_tt<KIND, L, CT, 1>(c, ps, G, lgG, bm_words, fixed + tab, table, num_sms, st);
+  } else {
+    launch_once_tt<KIND, L, CT, (KIND == 1 ? 2 : 0)>(c, ps, G, lgG, bm_words, fixed, table,
+                                                     num_sms, st);
+  }
 }
 
 template <typename CT>
-void launch_count_dense(const DevCorpus& c, uint32_t n0, int mode, CT* table, uint32_t* work,
+void launch_count_dense(const DevCorpus& c, uint32_t n0, int mode, CT* table, uint32_t* /*work*/,
                         int num_sms, cudaStream_t st) {
   DevPrefixSet none{};
   if (mode == IG_MODE_ALL) {
@@ -381,21 +534,21 @@ void launch_count_dense(const DevCorpus& c, uint32_t n0, int mode, CT* table, ui
     }
   } else {
     switch (n0) {
-      case 1: launch_once_t<0, 1, CT>(c, none, 1, 0, 256, work, table, num_sms, st); break;
-      case 2: launch_once_t<0, 2, CT>(c, none, 1, 0, 65536, work, table, num_sms, st); break;
-      default: launch_once_t<0, 3, CT>(c, none, 16, 4, 1u << 20, work, table, num_sms, st); break;
+      case 1: launch_once_t<0, 1, CT>(c, none, 1, 0, 256, table, num_sms, st); break;
+      case 2: launch_once_t<0, 2, CT>(c, none, 1, 0, 65536, table, num_sms, st); break;
+      default: launch_once_t<0, 3, CT>(c, none, 16, 4, 1u << 20, table, num_sms, st); break;
     }
   }
 }
 
 template <typename CT>
 void launch_count_extend(const DevCorpus& c, const DevPrefixSet& ps, uint32_t j, int mode,
-                         CT* table, uint32_t* work, int num_sms, cudaStream_t st) {
+                         CT* table, uint32_t* /*work*/, int num_sms, cudaStream_t st) {
   const uint64_t slice_bits = (uint64_t)ps.max_owner * 256;
-#define IGB_J(J)                                                                            \
-  case J:                                                                                   \
-    if (mode == IG_MODE_ALL) launch_all_t<1, J, CT>(c, ps, table, num_sms, st);             \
-    else launch_once_t<1, J, CT>(c, ps, ps.G, ps.lgG, slice_bits, work, table, num_sms, st); \
+#define IGB_J(J)                                                                        \
+  case J:                                                                               \
+    if (mode == IG_MODE_ALL) launch_all_t<1, J, CT>(c, ps, table, num_sms, st);         \
+    else launch_once_t<1, J, CT>(c, ps, ps.G, ps.lgG, slice_bits, table, num_sms, st);  \
     break;
   switch (j) {
     IGB_J(2) IGB_J(3) IGB_J(4) IGB_J(5) IGB_J(6) IGB_J(7) IGB_J(8)
@@ -428,9 +581,9 @@ __global__ void k_prefix_owner(const uint64_t* __restrict__ keys, uint32_t K, ui
   }
 }
 
-// Pass 2: place survivor i at p = owner_start[o] + (stable rank within owner
-// via a per-owner cursor: order within a slice is irrelevant to results), and
-// insert it into owner o's open-addressing slice.
+// Pass 2: place survivor i at p = owner_start[o] + cursor (order inside a
+// slice is irrelevant to results: selection orders by gram key), and insert it
+// into owner o's open-addressing slice.
 __global__ void k_prefix_insert(const uint64_t* __restrict__ keys, uint32_t K,
                                 const uint32_t* __restrict__ owner,
                                 const uint32_t* __restrict__ owner_start,

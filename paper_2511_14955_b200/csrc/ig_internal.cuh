@@ -42,10 +42,14 @@ inline void cuda_check(cudaError_t e, const char* what, const char* file, int li
     IGB_CUDA(cudaGetLastError()); \
   } while (0)
 
-constexpr uint64_t kEmptyKey = ~0ull;  // never a key: keys have <= 56 bits in a prefix set
+constexpr uint64_t kEmptyKey = ~0ull;
+constexpr uint64_t kCuckooMul1 = 0x9E3779B97F4A7C15ull;  // prefix-set bucket hashes
+constexpr uint64_t kCuckooMul2 = 0xC2B2AE3D27D4EB4Full;
+constexpr uint64_t kOwnerMul = 0xD6E8FEB86659FD93ull;    // count-once owner of a prefix  // never a key: keys have <= 56 bits in a prefix set
 constexpr int kTileBytes = 512;        // one warp x 16 B per lane
 constexpr int kFrontPad = 16;
 constexpr int kBackPad = 1024;
+constexpr size_t kMaxOnceSmem = 227 * 1024;  // dynamic smem per CTA (sm_100a)
 
 // Grow-only device buffer.
 struct DevBuf {
@@ -98,6 +102,8 @@ struct DevPrefixSet {
   uint32_t lgS = 0;
   uint32_t plen = 0;       // prefix length (j-1)
   uint32_t max_owner = 0;  // largest owner slice size
+  uint32_t ib = 0;         // local-index bits of a packed entry
+  const uint64_t* packed = nullptr;  // [G*S] (key << ib) | local, or null
 };
 
 __host__ __device__ inline uint32_t hash_slot(uint64_t key, uint32_t lgS) {

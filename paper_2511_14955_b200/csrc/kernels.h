@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <vector>
+
 #include "ig_internal.cuh"
 
 namespace igb {
@@ -27,6 +29,50 @@ void launch_prefix_insert(const uint64_t* keys, uint32_t K, const uint32_t* owne
                           const uint32_t* owner_start, uint32_t* cursor, uint32_t S, uint32_t lgS,
                           uint64_t* hkeys, uint32_t* hidx, uint64_t* pkeys, uint32_t* rank_of_p,
                           cudaStream_t st);
+
+void launch_pack_prefix(const DevPrefixSet& ps, uint64_t* packed, cudaStream_t st);
+
+// --- count-once route-then-count (route_kernels.cu)
+struct RouteUnit {  // <= 1 MiB of gram ends of one sequence: byte range [b0, b1)
+  uint32_t q;
+  uint32_t pad;
+  uint64_t b0, b1;
+};
+
+struct RouteView {
+  const RouteUnit* units;
+  const uint32_t* unit_first;  // [m+1] first unit of each sequence
+  uint32_t nunits;
+};
+
+struct RouteParams {
+  uint32_t lgc = 2, lgl = 2, NO = 1;  // dense: permuted id space 2^lgc; 2^lgl ids per owner
+  uint64_t cmask = 3, mult = 1, minv = 1;
+  // extension passes: owner = hash(prefix) >> (64-lgno); p numbered owner by
+  // owner (ostart[o] .. ostart[o+1]); bucketized cuckoo prefix set
+  bool ext = false;
+  bool packed = false;  // slots = (key << 24) | p, else slots = key and pidx[slot] = p
+  uint32_t lgno = 0;
+  uint32_t nbk = 0;
+  const uint64_t* slots = nullptr;
+  const uint32_t* pidx = nullptr;
+  const uint32_t* ostart = nullptr;
+};
+
+struct RouteCtx {
+  const RouteUnit* units = nullptr;
+  const uint32_t* unit_first = nullptr;
+  uint32_t nunits = 0;
+  DevBuf cnt, actual, base, entries, cub_tmp;
+  uint64_t launches = 0;
+};
+
+void make_route_params(uint64_t cap, RouteParams& rp);
+void build_cuckoo_prefix(const std::vector<uint64_t>& keys, std::vector<uint64_t>& slots,
+                         std::vector<uint32_t>& slot_p, uint32_t& nbk);
+template <typename CT>
+void route_count_once(RouteCtx& x, const DevCorpus& c, int kind, uint32_t L, const RouteParams& rp,
+                      CT* table, int num_sms, cudaStream_t st);
 
 // --- selection (select_kernels.cu)
 struct SelState {
@@ -54,9 +100,15 @@ struct SelectCtx {
 // (pkeys[id>>8] << 8) | (id & 255) when pkeys != nullptr.  Writes
 // min(k, nonzero) entries to out_keys/out_counts (device) and returns that
 // number.  key_bits = 8 * gram length.
+// Table index -> gram key: id = (index * minv) & cmask (identity when
+// minv == 0), then key = id, or (pkeys[id>>8] << 8) | (id & 255).
+struct KeyMap {
+  const uint64_t* pkeys = nullptr;
+  uint64_t minv = 0, cmask = ~0ull;
+};
+
 template <typename CT>
-uint64_t select_topk(SelectCtx& x, const CT* table, uint64_t cap, uint64_t k,
-                     const uint64_t* pkeys, int key_bits, uint64_t* out_keys,
-                     uint64_t* out_counts);
+uint64_t select_topk(SelectCtx& x, const CT* table, uint64_t cap, uint64_t k, KeyMap km,
+                     int key_bits, uint64_t* out_keys, uint64_t* out_counts);
 
 }  // namespace igb

@@ -1,0 +1,589 @@
+// route_kernels.cu — count-once passes as route-then-count (sm_100a).
+//
+// Reference semantics: counting.hpp:48-74 + counting.cpp:27-50 (a gram adds 1
+// per sequence containing it), over the candidates of the dense pass
+// (intergrams.cpp:79-100) or of an extension pass (intergrams.cpp:44-66).
+//
+// Design.  Per-sequence dedup needs a bitmap over the whole
+// candidate space (2 MiB for the 2^24 dense 3-grams), far more than one SM's
+// shared memory.  Every candidate occurrence is therefore computed once and
+// routed to the owner of its id slice:
+//   dense:     id' = (id * M) mod 2^24 (odd M: a bijection that spreads hot
+//              grams), owner = id' >> 14, local = id' & 16383
+//   extension: owner = hash(prefix) (<= 64 prefixes per owner), prefixes are
+//              numbered owner by owner, local = (p - ostart[owner])*256 + last
+// Work unit = <= 1 MiB of gram ends of one sequence.
+//   1. k_route_count    per unit: owner histogram in smem -> cnt[o][u] (for
+//                       extension passes an upper bound: no prefix lookup)
+//   2. exclusive scan   cnt -> base: unit u owns [base[o][u], base[o][u+1]) of
+//                       owner o's region (owner-major, no reservation atomics)
+//   3. k_route_scatter  per unit, 8K positions at a time: drop repeats of the
+//                       same gram inside the chunk (smem cache, before any
+//                       lookup; an optimisation only, the consumer is exact),
+//                       look the prefix up, counting-sort by owner in smem, copy
+//                       each owner's run out coalesced; actual[o][u] = written
+//   4. k_consume_once   CTA per (owner, block of sequences): a warp streams one
+//                       sequence's runs (uint4 = 8 entries per load), dedups in
+//                       a warp-private smem bitmap, counts first occurrences in
+//                       smem u16 counters; the CTA flushes nonzero counters with
+//                       coalesced REDs.
+// Extension prefixes live in a host-built bucketized cuckoo table (2 buckets x
+// 4 slots of (key << 24 | p)): a lookup is two 32-byte loads and eight
+// compares with no divergence.
+#include <cub/cub.cuh>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <type_traits>
+#include <vector>
+
+#include "ig_internal.cuh"
+#include "kernels.h"
+
+namespace igb {
+
+namespace {
+
+template <int B, int E, typename F>
+__device__ __forceinline__ void static_for(F&& f) {
+  if constexpr (B < E) {
+    f(std::integral_constant<int, B>{});
+    static_for<B + 1, E>(f);
+  }
+}
+
+template <int T>
+__device__ __forceinline__ uint64_t key8(const uint32_t (&W)[7]) {
+  constexpr int o = T + 1;
+  constexpr int wi = o / 4, sh = 8 * (o % 4);
+  uint32_t lo, hi;
+  if constexpr (sh == 0) {
+    lo = W[wi];
+    hi = W[wi + 1];
+  } else {
+    lo = __funnelshift_r(W[wi], W[wi + 1], sh);
+    hi = __funnelshift_r(W[wi + 1], W[wi + 2], sh);
+  }
+  return ((uint64_t)__byte_perm(lo, 0, 0x0123) << 32) | (uint64_t)__byte_perm(hi, 0, 0x0123);
+}
+
+template <int L>
+__device__ __forceinline__ uint64_t gmask() {
+  if constexpr (L >= 8) return ~0ull;
+  else return (1ull << (8 * L)) - 1;
+}
+
+__device__ __forceinline__ uint32_t ck_bucket(uint64_t key, uint64_t mul, uint32_t nbk) {
+  return (uint32_t)((((key * mul) >> 32) & 0xffffffffull) * (uint64_t)nbk >> 32);
+}
+
+// Bucketized cuckoo prefix set (2 buckets x 4 slots).  Packed slots hold
+// (key << 24) | p (prefixes of <= 5 bytes); empty = ~0.  Unpacked slots hold the
+// key and p lives in pidx[slot].  Returns p or 0xffffffff.
+template <bool PACKED>
+__device__ __forceinline__ uint32_t cuckoo_lookup(const uint64_t* slots, const uint32_t* pidx,
+                                                  uint32_t nbk, uint64_t key) {
+  const uint32_t b1 = ck_bucket(key, kCuckooMul1, nbk);
+  const uint32_t b2 = ck_bucket(key, kCuckooMul2, nbk);
+  const ulonglong2* p1 = reinterpret_cast<const ulonglong2*>(slots + 4 * (size_t)b1);
+  const ulonglong2* p2 = reinterpret_cast<const ulonglong2*>(slots + 4 * (size_t)b2);
+  const ulonglong2 a0 = p1[0], a1 = p1[1], c0 = p2[0], c1 = p2[1];
+  const uint64_t e[8] = {a0.x, a0.y, a1.x, a1.y, c0.x, c0.y, c1.x, c1.y};
+  if constexpr (PACKED) {
+    const uint64_t kk = key << 24;
+    uint32_t best = 0xffffffu;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if ((e[i] & 0xffffffffff000000ull) == kk) best = min(best, (uint32_t)e[i] & 0xffffffu);
+    return best == 0xffffffu ? 0xffffffffu : best;
+  } else {
+    uint32_t r = 0xffffffffu;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (e[i] == key) r = (i < 4 ? 4 * b1 : 4 * b2) + (i & 3);
+    return r == 0xffffffffu ? r : __ldg(pidx + r);
+  }
+}
+
+// Owner of an extension prefix (count-once routing): multiplicative hash.
+__device__ __forceinline__ uint32_t prefix_owner_hash(uint64_t pkey, uint32_t lgno) {
+  return lgno ? (uint32_t)((pkey * kOwnerMul) >> (64 - lgno)) : 0u;
+}
+
+constexpr int kRouteThreads = 1024;
+constexpr int kChunk = kRouteThreads * 16;  // positions per scatter chunk
+constexpr int kDedupSlots = 2048;
+
+// The 16-byte segment at b0 plus its 8-byte halo (full warp, consecutive lanes).
+__device__ __forceinline__ void seg_load(const uint8_t* __restrict__ data, int64_t b0, int lane,
+                                         uint32_t (&W)[7]) {
+  const uint4 v = __ldcs(reinterpret_cast<const uint4*>(data + b0));
+  W[2] = v.x;
+  W[3] = v.y;
+  W[4] = v.z;
+  W[5] = v.w;
+  W[6] = 0;
+  uint32_t h0 = __shfl_up_sync(0xffffffffu, v.z, 1);
+  uint32_t h1 = __shfl_up_sync(0xffffffffu, v.w, 1);
+  if (lane == 0) {
+    const uint2 h = *reinterpret_cast<const uint2*>(data + b0 - 8);
+    h0 = h.x;
+    h1 = h.y;
+  }
+  W[0] = h0;
+  W[1] = h1;
+}
+
+__device__ __forceinline__ uint32_t vmask(int64_t b0, int64_t lo, int64_t hi) {
+  int64_t a = lo - b0, b = hi - b0;
+  if (a < 0) a = 0;
+  if (b > 16) b = 16;
+  if (a >= b) return 0;
+  return ((1u << b) - 1u) & ~((1u << a) - 1u);
+}
+
+// Dense: (owner << 16 | local) of a dense id via the odd-multiplier permutation.
+__device__ __forceinline__ uint32_t dense_route(uint64_t id, const RouteParams& rp) {
+  const uint64_t idp = (id * rp.mult) & rp.cmask;
+  return ((uint32_t)(idp >> rp.lgl) << 16) | (uint32_t)(idp & ((1u << rp.lgl) - 1));
+}
+
+// Count pass owner of the gram ending at T (no prefix lookup: an upper bound
+// for extension passes, exact for the dense pass).
+template <int KIND, int L, int T>
+__device__ __forceinline__ uint32_t count_owner(const uint32_t (&W)[7], const RouteParams& rp) {
+  const uint64_t key = key8<T>(W) & gmask<L>();
+  if constexpr (KIND == 0) return dense_route(key, rp) >> 16;
+  else return prefix_owner_hash(key >> 8, rp.lgno);
+}
+
+// Scatter pass: (owner << 16 | local) of a gram key, or ~0 (prefix miss).
+template <int KIND, bool PACKED>
+__device__ __forceinline__ uint32_t scatter_route(uint64_t key, const RouteParams& rp,
+                                                  const uint64_t* slots) {
+  if constexpr (KIND == 0) {
+    return dense_route(key, rp);
+  } else {
+    const uint64_t pk = key >> 8;
+    const uint32_t p = cuckoo_lookup<PACKED>(slots, rp.pidx, rp.nbk, pk);
+    if (p == 0xffffffffu) return 0xffffffffu;
+    const uint32_t o = prefix_owner_hash(pk, rp.lgno);
+    return (o << 16) | ((p - __ldg(rp.ostart + o)) * 256 + (uint32_t)(key & 0xff));
+  }
+}
+
+template <int TAB>
+__device__ __forceinline__ const uint64_t* stage_table(const RouteParams& rp, uint64_t* s_slots) {
+  if constexpr (TAB == 1) {
+    const uint32_t n = 4 * rp.nbk;
+    for (uint32_t i = threadIdx.x; i < n / 2; i += blockDim.x)
+      reinterpret_cast<ulonglong2*>(s_slots)[i] = reinterpret_cast<const ulonglong2*>(rp.slots)[i];
+    __syncthreads();
+    return s_slots;
+  } else {
+    return rp.slots;
+  }
+}
+
+__host__ __device__ inline size_t align16(size_t b) { return (b + 15) & ~size_t(15); }
+
+}  // namespace
+
+// ------------------------------------------------------------------ 1. count
+
+template <int KIND, int L>
+__global__ void __launch_bounds__(kRouteThreads) k_route_count(DevCorpus c, RouteView uv,
+                                                               RouteParams rp,
+                                                               uint32_t* __restrict__ cnt) {
+  extern __shared__ uint4 smem4[];
+  uint32_t* hist = reinterpret_cast<uint32_t*>(smem4);
+  const int lane = threadIdx.x & 31;
+  for (uint32_t u = blockIdx.x; u < uv.nunits; u += gridDim.x) {
+    for (uint32_t i = threadIdx.x; i < rp.NO; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    const RouteUnit U = uv.units[u];
+    const int64_t s0 = (int64_t)c.off[U.q];
+    const int64_t lo = max((int64_t)U.b0, s0 + L - 1), hi = (int64_t)U.b1;
+    const int64_t first = (int64_t)U.b0 & ~int64_t(15);
+    const int64_t nseg = (hi - first + 15) >> 4;
+    const int64_t nseg_r = (nseg + 31) & ~int64_t(31);  // whole warps
+    for (int64_t sgi = threadIdx.x; sgi < nseg_r; sgi += blockDim.x) {
+      const int64_t b0 = first + sgi * 16;
+      uint32_t W[7];
+      seg_load(c.data, b0, lane, W);
+      const uint32_t vm = sgi < nseg ? vmask(b0, lo, hi) : 0u;
+      static_for<0, 16>([&](auto tc) {
+        constexpr int T = decltype(tc)::value;
+        if ((vm >> T) & 1u) atomicAdd(hist + count_owner<KIND, L, T>(W, rp), 1u);
+      });
+    }
+    __syncthreads();
+    for (uint32_t o = threadIdx.x; o < rp.NO; o += blockDim.x)
+      cnt[(size_t)o * uv.nunits + u] = hist[o];
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------ 3. scatter
+
+constexpr int kScatterThreads = 512;
+constexpr int kSChunk = kScatterThreads * 16;  // positions per chunk
+
+// TAB: 0 dense (no table), 1 packed table staged in smem, 2 packed table in
+// global memory, 3 unpacked table (key slots + pidx) in global memory.
+template <int KIND, int L, int TAB>
+__global__ void __launch_bounds__(kScatterThreads) k_route_scatter(
+    DevCorpus c, RouteView uv, RouteParams rp, const unsigned long long* __restrict__ base,
+    uint32_t* __restrict__ actual, uint16_t* __restrict__ entries) {
+  constexpr bool PACKED = TAB != 3;
+  extern __shared__ uint4 smem4[];
+  char* sp = reinterpret_cast<char*>(smem4);
+  uint32_t* staging = reinterpret_cast<uint32_t*>(sp);  // kSChunk x (owner<<16|local)
+  sp += (size_t)kSChunk * 4;
+  uint64_t* cache = reinterpret_cast<uint64_t*>(sp);  // kDedupSlots gram keys
+  sp += (size_t)kDedupSlots * 8;
+  unsigned long long* res = reinterpret_cast<unsigned long long*>(sp);  // NO
+  sp += align16((size_t)rp.NO * 8);
+  uint32_t* lhist = reinterpret_cast<uint32_t*>(sp);  // NO
+  sp += align16((size_t)rp.NO * 4);
+  uint32_t* lbase = reinterpret_cast<uint32_t*>(sp);  // NO + 1
+  sp += align16((size_t)(rp.NO + 1) * 4);
+  uint64_t* s_slots = reinterpret_cast<uint64_t*>(sp);
+  __shared__ uint32_t s_total;
+  using BlockScan = cub::BlockScan<uint32_t, kScatterThreads>;
+  __shared__ typename BlockScan::TempStorage scan_tmp;
+  const uint64_t* slots = stage_table<TAB == 1 ? 1 : 2>(rp, s_slots);
+  const int lane = threadIdx.x & 31;
+  for (uint32_t u = blockIdx.x; u < uv.nunits; u += gridDim.x) {
+    const RouteUnit U = uv.units[u];
+    __syncthreads();
+    for (uint32_t o = threadIdx.x; o < rp.NO; o += blockDim.x) res[o] = base[(size_t)o * uv.nunits + u];
+    const int64_t s0 = (int64_t)c.off[U.q];
+    const int64_t lo = max((int64_t)U.b0, s0 + L - 1), hi = (int64_t)U.b1;
+    const int64_t first = (int64_t)U.b0 & ~int64_t(15);
+    const int64_t nseg = (hi - first + 15) >> 4;
+    for (int64_t cs = 0; cs < nseg; cs += kScatterThreads) {
+      for (uint32_t i = threadIdx.x; i < rp.NO; i += blockDim.x) lhist[i] = 0;
+      for (uint32_t i = threadIdx.x; i < kDedupSlots; i += blockDim.x) cache[i] = ~0ull;
+      __syncthreads();
+      const int64_t sgi = cs + threadIdx.x;
+      const int64_t b0 = first + sgi * 16;
+      uint32_t W[7] = {0, 0, 0, 0, 0, 0, 0};
+      if (cs + (int64_t)(threadIdx.x & ~31u) < nseg) seg_load(c.data, b0, lane, W);  // warp-uniform
+      const uint32_t vm = sgi < nseg ? vmask(b0, lo, hi) : 0u;
+      uint32_t r[16];
+      static_for<0, 16>([&](auto tc) {
+        constexpr int T = decltype(tc)::value;
+        uint32_t v = 0xffffffffu;
+        if ((vm >> T) & 1u) {
+          const uint64_t key = key8<T>(W) & gmask<L>();
+          // a gram already routed from this chunk adds nothing (count-once):
+          // drop it before the prefix lookup.  Races only cost a duplicate.
+          const uint32_t slot = (uint32_t)((key * 0x9E3779B97F4A7C15ull) >> (64 - 11));
+          if (cache[slot] != key) {
+            cache[slot] = key;
+            v = scatter_route<KIND, PACKED>(key, rp, slots);
+            if (v != 0xffffffffu) atomicAdd(lhist + (v >> 16), 1u);
+          }
+        }
+        r[T] = v;
+      });
+      __syncthreads();
+      {  // exclusive scan lhist -> lbase; each thread owns a contiguous run of owners
+        const uint32_t per = (rp.NO + kScatterThreads - 1) / kScatterThreads;
+        const uint32_t a = threadIdx.x * per, e = min(rp.NO, a + per);
+        uint32_t sum = 0;
+        for (uint32_t o = a; o < e; ++o) sum += lhist[o];
+        uint32_t ex, tot;
+        BlockScan(scan_tmp).ExclusiveSum(sum, ex, tot);
+        for (uint32_t o = a; o < e; ++o) {
+          lbase[o] = ex;
+          ex += lhist[o];
+        }
+        if (threadIdx.x == 0) {
+          lbase[rp.NO] = tot;
+          s_total = tot;
+        }
+      }
+      __syncthreads();
+      for (uint32_t i = threadIdx.x; i < rp.NO; i += blockDim.x) lhist[i] = lbase[i];
+      __syncthreads();
+      static_for<0, 16>([&](auto tc) {
+        constexpr int T = decltype(tc)::value;
+        if (r[T] != 0xffffffffu) staging[atomicAdd(lhist + (r[T] >> 16), 1u)] = r[T];
+      });
+      __syncthreads();
+      const uint32_t total = s_total;
+      for (uint32_t i = threadIdx.x; i < total; i += blockDim.x) {
+        const uint32_t e = staging[i];
+        const uint32_t o = e >> 16;
+        entries[res[o] + (i - lbase[o])] = (uint16_t)(e & 0xffffu);
+      }
+      __syncthreads();
+      for (uint32_t o = threadIdx.x; o < rp.NO; o += blockDim.x) res[o] += lbase[o + 1] - lbase[o];
+    }
+    __syncthreads();
+    for (uint32_t o = threadIdx.x; o < rp.NO; o += blockDim.x)
+      actual[(size_t)o * uv.nunits + u] = (uint32_t)(res[o] - base[(size_t)o * uv.nunits + u]);
+  }
+}
+
+// ------------------------------------------------------------------ 4. consume
+
+constexpr int kConsumeThreads = 512;
+constexpr int kConsumeWarps = kConsumeThreads / 32;
+
+__device__ __forceinline__ void consume_entry(uint32_t local, uint32_t* bm, uint32_t* cnt) {
+  const uint32_t bit = 1u << (local & 31);
+  uint32_t* w = bm + (local >> 5);
+  if (!(*(volatile uint32_t*)w & bit)) {
+    if (!(atomicOr(w, bit) & bit)) atomicAdd(cnt + (local >> 1), 1u << (16 * (local & 1)));
+  }
+}
+
+template <typename CT>
+__global__ void __launch_bounds__(kConsumeThreads) k_consume_once(
+    RouteView uv, uint64_t m, RouteParams rp, uint32_t seq_block, uint32_t nblocks,
+    const unsigned long long* __restrict__ base, const uint32_t* __restrict__ actual,
+    const uint16_t* __restrict__ entries, CT* __restrict__ table) {
+  extern __shared__ uint4 smem4[];
+  const uint32_t ipo = 1u << rp.lgl;                   // ids per owner
+  const uint32_t cntw = (uint32_t)(align16((size_t)(ipo + 1) / 2 * 4) / 4);
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(smem4);  // u16 pairs
+  uint32_t* bms = cnt + cntw;                          // kConsumeWarps x bmw4 words
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t bmw4 = ((ipo + 31) / 32 + 3) & ~3u;
+  uint32_t* bm = bms + warp * bmw4;
+  const uint32_t nitems = rp.NO * nblocks;
+  for (uint32_t i = threadIdx.x; i < bmw4 * kConsumeWarps; i += blockDim.x) bms[i] = 0;
+  for (uint32_t item = blockIdx.x; item < nitems; item += gridDim.x) {
+    const uint32_t o = item / nblocks, b = item % nblocks;
+    for (uint32_t i = threadIdx.x; i < cntw; i += blockDim.x) cnt[i] = 0;
+    __syncthreads();
+    const uint64_t q0 = (uint64_t)b * seq_block;
+    const uint64_t q1 = min(m, q0 + seq_block);
+    for (uint64_t q = q0 + warp; q < q1; q += kConsumeWarps) {
+      const uint32_t u0 = uv.unit_first[q], u1 = uv.unit_first[q + 1];
+      for (uint32_t u = u0; u < u1; ++u) {
+        const size_t ix = (size_t)o * uv.nunits + u;
+        const uint64_t e0 = base[ix], e1 = e0 + actual[ix];
+        // uint4-aligned body: 8 entries per lane per load
+        const uint64_t a0 = (e0 + 7) & ~7ull, a1 = e1 & ~7ull;
+        if (a0 >= a1) {
+          for (uint64_t e = e0 + lane; e < e1; e += 32) consume_entry(entries[e], bm, cnt);
+        } else {
+          if (e0 + lane < a0) consume_entry(entries[e0 + lane], bm, cnt);
+          if (a1 + lane < e1) consume_entry(entries[a1 + lane], bm, cnt);
+          const uint4* v4 = reinterpret_cast<const uint4*>(entries + a0);
+          const uint64_t nv = (a1 - a0) >> 3;
+          for (uint64_t i = lane; i < nv; i += 32) {
+            const uint4 v = __ldcs(v4 + i);
+            const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              consume_entry(w[k] & 0xffffu, bm, cnt);
+              consume_entry(w[k] >> 16, bm, cnt);
+            }
+          }
+        }
+      }
+      __syncwarp();
+      for (uint32_t i = lane; i < bmw4 / 4; i += 32) reinterpret_cast<uint4*>(bm)[i] = make_uint4(0, 0, 0, 0);
+      __syncwarp();
+    }
+    __syncthreads();
+    // owner o's ids start at o << lgl (dense, permuted) or ostart[o]*256 (extension)
+    CT* dst = table + (rp.ext ? (size_t)rp.ostart[o] * 256 : ((size_t)o << rp.lgl));
+    const uint32_t lim = rp.ext ? (rp.ostart[o + 1] - rp.ostart[o]) * 256 : ipo;
+    for (uint32_t i = threadIdx.x; i < (lim + 1) / 2; i += blockDim.x) {
+      const uint32_t v = cnt[i];
+      if (v & 0xffffu) atomicAdd(dst + 2 * i, (CT)(v & 0xffffu));
+      if ((v >> 16) && 2 * i + 1 < lim) atomicAdd(dst + 2 * i + 1, (CT)(v >> 16));
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------ host
+
+static size_t table_bytes(const RouteParams& rp) { return (size_t)4 * rp.nbk * 8; }
+
+template <int KIND, int L, int TAB, typename CT>
+static void route_once_t(RouteCtx& x, const DevCorpus& c, const RouteParams& rp, CT* table,
+                         int num_sms, cudaStream_t st) {
+  const RouteView uv{x.units, x.unit_first, x.nunits};
+  const size_t tab = TAB == 1 ? table_bytes(rp) : 0;
+  const size_t ncnt = (size_t)rp.NO * x.nunits + 1;
+  uint32_t* cnt = x.cnt.as<uint32_t>(ncnt);
+  uint32_t* act = x.actual.as<uint32_t>(ncnt);
+  unsigned long long* base = x.base.as<unsigned long long>(ncnt);
+  // 1. count (upper bounds per owner and unit)
+  {
+    const size_t smem = align16((size_t)rp.NO * 4);
+    auto k = k_route_count<KIND, L>;
+    IGB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per = 0;
+    IGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, kRouteThreads, smem));
+    if (per < 1) throw Error(IG_EINTERNAL, "route count does not fit in shared memory");
+    const unsigned grid = (unsigned)std::min<uint64_t>(x.nunits, (uint64_t)num_sms * per);
+    IGB_CUDA(cudaMemsetAsync(cnt + ncnt - 1, 0, 4, st));
+    k<<<grid, kRouteThreads, smem, st>>>(c, uv, rp, cnt);
+    x.launches++;
+  }
+  // 2. owner-major exclusive scan -> base
+  {
+    size_t need = 0;
+    IGB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, need, cnt, base, (int64_t)ncnt, st));
+    void* tmp = x.cub_tmp.get(need);
+    IGB_CUDA(cub::DeviceScan::ExclusiveSum(tmp, need, cnt, base, (int64_t)ncnt, st));
+  }
+  // 3. scatter
+  uint16_t* ent = x.entries.as<uint16_t>(c.total + 64);
+  {
+    const size_t smem = (size_t)kSChunk * 4 + (size_t)kDedupSlots * 8 + align16((size_t)rp.NO * 8) +
+                        align16((size_t)rp.NO * 4) + align16((size_t)(rp.NO + 1) * 4) + tab;
+    auto k = k_route_scatter<KIND, L, TAB>;
+    IGB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per = 0;
+    IGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, kScatterThreads, smem));
+    if (per < 1) throw Error(IG_EINTERNAL, "route scatter does not fit in shared memory");
+    const unsigned grid = (unsigned)std::min<uint64_t>(x.nunits, (uint64_t)num_sms * per);
+    k<<<grid, kScatterThreads, smem, st>>>(c, uv, rp, base, act, ent);
+    x.launches++;
+  }
+  // 4. consume
+  {
+    const uint32_t ipo = 1u << rp.lgl;
+    const uint32_t bmw4 = ((ipo + 31) / 32 + 3) & ~3u;
+    const size_t smem = align16((size_t)(ipo + 1) / 2 * 4) + (size_t)kConsumeWarps * bmw4 * 4;
+    auto k = k_consume_once<CT>;
+    IGB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per = 0;
+    IGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, kConsumeThreads, smem));
+    if (per < 1) throw Error(IG_EINTERNAL, "route consume does not fit in shared memory");
+    const uint64_t slots = (uint64_t)num_sms * per;
+    uint64_t nblocks = (slots * 4 + rp.NO - 1) / rp.NO;
+    if (nblocks > c.m) nblocks = c.m;
+    if (nblocks < 1) nblocks = 1;
+    uint64_t sb = (c.m + nblocks - 1) / nblocks;
+    if (sb > 65535) sb = 65535;  // u16 smem counters: <= 65535 sequences per item
+    if (sb < 1) sb = 1;
+    nblocks = (c.m + sb - 1) / sb;
+    if (nblocks < 1) nblocks = 1;
+    const uint64_t nitems = (uint64_t)rp.NO * nblocks;
+    const unsigned grid = (unsigned)std::min<uint64_t>(nitems, slots);
+    k<<<grid, kConsumeThreads, smem, st>>>(uv, c.m, rp, (uint32_t)sb, (uint32_t)nblocks, base, act,
+                                            ent, table);
+    x.launches++;
+  }
+  IGB_CUDA(cudaGetLastError());
+}
+
+template <int KIND, int L, typename CT>
+static void route_once_l(RouteCtx& x, const DevCorpus& c, const RouteParams& rp, CT* table,
+                         int num_sms, cudaStream_t st) {
+  if constexpr (KIND == 0) {
+    route_once_t<0, L, 0, CT>(x, c, rp, table, num_sms, st);
+  } else {
+    const size_t scatter_fixed = (size_t)kSChunk * 4 + (size_t)kDedupSlots * 8 +
+                                 (size_t)rp.NO * 16 + 256 + 4 * 1024;  // + static smem
+    if (!rp.packed) route_once_t<1, L, 3, CT>(x, c, rp, table, num_sms, st);
+    else if (scatter_fixed + table_bytes(rp) <= kMaxOnceSmem)
+      route_once_t<1, L, 1, CT>(x, c, rp, table, num_sms, st);
+    else
+      route_once_t<1, L, 2, CT>(x, c, rp, table, num_sms, st);
+  }
+}
+
+template <typename CT>
+void route_count_once(RouteCtx& x, const DevCorpus& c, int kind, uint32_t L, const RouteParams& rp,
+                      CT* table, int num_sms, cudaStream_t st) {
+  if (!c.m || !x.nunits) return;
+  if (kind == 0) {
+    switch (L) {
+      case 1: route_once_l<0, 1, CT>(x, c, rp, table, num_sms, st); break;
+      case 2: route_once_l<0, 2, CT>(x, c, rp, table, num_sms, st); break;
+      default: route_once_l<0, 3, CT>(x, c, rp, table, num_sms, st); break;
+    }
+  } else {
+    switch (L) {
+      case 2: route_once_l<1, 2, CT>(x, c, rp, table, num_sms, st); break;
+      case 3: route_once_l<1, 3, CT>(x, c, rp, table, num_sms, st); break;
+      case 4: route_once_l<1, 4, CT>(x, c, rp, table, num_sms, st); break;
+      case 5: route_once_l<1, 5, CT>(x, c, rp, table, num_sms, st); break;
+      case 6: route_once_l<1, 6, CT>(x, c, rp, table, num_sms, st); break;
+      case 7: route_once_l<1, 7, CT>(x, c, rp, table, num_sms, st); break;
+      case 8: route_once_l<1, 8, CT>(x, c, rp, table, num_sms, st); break;
+      default: throw Error(IG_ECONFIG, "gram length above 8 is not supported");
+    }
+  }
+}
+
+template void route_count_once<uint32_t>(RouteCtx&, const DevCorpus&, int, uint32_t,
+                                         const RouteParams&, uint32_t*, int, cudaStream_t);
+template void route_count_once<unsigned long long>(RouteCtx&, const DevCorpus&, int, uint32_t,
+                                                   const RouteParams&, unsigned long long*, int,
+                                                   cudaStream_t);
+
+// ------------------------------------------------------------------ prefix set (host)
+
+static uint32_t host_bucket(uint64_t key, uint64_t mul, uint32_t nbk) {
+  return (uint32_t)((((key * mul) >> 32) & 0xffffffffull) * (uint64_t)nbk >> 32);
+}
+
+// Bucketized cuckoo insertion (deterministic random walk).  False on failure.
+static bool cuckoo_try(const std::vector<uint64_t>& keys, uint32_t nbk, std::vector<uint64_t>& slots,
+                       std::vector<uint32_t>& slot_rank) {
+  slots.assign((size_t)4 * nbk, kEmptyKey);
+  slot_rank.assign((size_t)4 * nbk, 0xffffffffu);
+  uint64_t rng = 0x853c49e6748fea9bull;
+  for (uint32_t r = 0; r < keys.size(); ++r) {
+    uint64_t cur = keys[r];
+    uint32_t cur_rank = r;
+    bool placed = false;
+    for (int kick = 0; kick < 2000 && !placed; ++kick) {
+      const uint32_t b[2] = {host_bucket(cur, kCuckooMul1, nbk), host_bucket(cur, kCuckooMul2, nbk)};
+      for (int t = 0; t < 2 && !placed; ++t)
+        for (int i = 0; i < 4; ++i)
+          if (slots[4 * (size_t)b[t] + i] == kEmptyKey) {
+            slots[4 * (size_t)b[t] + i] = cur;
+            slot_rank[4 * (size_t)b[t] + i] = cur_rank;
+            placed = true;
+            break;
+          }
+      if (placed) break;
+      rng ^= rng << 13;
+      rng ^= rng >> 7;
+      rng ^= rng << 17;
+      const size_t s = 4 * (size_t)b[rng & 1] + ((rng >> 1) & 3);
+      std::swap(cur, slots[s]);
+      std::swap(cur_rank, slot_rank[s]);
+    }
+    if (!placed) return false;
+  }
+  return true;
+}
+
+void build_cuckoo_prefix(const std::vector<uint64_t>& keys, std::vector<uint64_t>& slots,
+                         std::vector<uint32_t>& slot_p, uint32_t& nbk) {
+  nbk = (uint32_t)std::max<uint64_t>(1, (keys.size() * 10 + 35) / 36);  // ~90% load
+  while (!cuckoo_try(keys, nbk, slots, slot_p)) nbk = nbk + nbk / 10 + 1;
+}
+
+// Host: the permuted id space of a candidate space of `cap` ids.
+void make_route_params(uint64_t cap, RouteParams& rp) {
+  uint32_t lgc = 0;
+  while ((1ull << lgc) < cap) ++lgc;
+  if (lgc < 2) lgc = 2;
+  rp.lgc = lgc;
+  rp.lgl = lgc < 14 ? lgc : 14;
+  rp.NO = 1u << (lgc - rp.lgl);
+  rp.cmask = lgc >= 64 ? ~0ull : ((1ull << lgc) - 1);
+  rp.mult = (0x9E3779B97F4A7C15ull & rp.cmask) | 1ull;
+  uint64_t inv = rp.mult;  // Newton: inv = inv * (2 - mult * inv) mod 2^64
+  for (int i = 0; i < 6; ++i) inv *= 2ull - rp.mult * inv;
+  rp.minv = inv & rp.cmask;
+}
+
+}  // namespace igb

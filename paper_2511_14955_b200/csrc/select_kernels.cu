@@ -27,7 +27,9 @@ namespace igb {
 
 struct KeyFn {
   const uint64_t* pkeys;  // nullptr: key = id
-  __device__ __forceinline__ uint64_t operator()(uint64_t id) const {
+  uint64_t minv, cmask;   // permuted table index -> id (minv == 0: identity)
+  __device__ __forceinline__ uint64_t operator()(uint64_t i) const {
+    const uint64_t id = minv ? ((i * minv) & cmask) : i;
     return pkeys ? ((__ldg(pkeys + (id >> 8)) << 8) | (id & 255)) : id;
   }
 };
@@ -178,12 +180,11 @@ __global__ void k_invert(const uint64_t* __restrict__ in, uint64_t* __restrict__
 static int bits_of(uint64_t v) { return v ? 64 - __builtin_clzll(v) : 0; }
 
 template <typename CT>
-uint64_t select_topk(SelectCtx& x, const CT* table, uint64_t cap, uint64_t k,
-                     const uint64_t* pkeys, int key_bits, uint64_t* out_keys,
-                     uint64_t* out_counts) {
+uint64_t select_topk(SelectCtx& x, const CT* table, uint64_t cap, uint64_t k, KeyMap km,
+                     int key_bits, uint64_t* out_keys, uint64_t* out_counts) {
   cudaStream_t s = x.stream;
-  const uint64_t cap4 = cap / 4;  // cap is a multiple of 256
-  const KeyFn kf{pkeys};
+  const uint64_t cap4 = cap / 4;  // cap is a multiple of 4
+  const KeyFn kf{km.pkeys, km.minv, km.cmask};
   const int threads = 512;
   unsigned blocks = (unsigned)((cap4 + threads - 1) / threads);
   const unsigned maxb = (unsigned)x.num_sms * 4;
@@ -255,10 +256,9 @@ uint64_t select_topk(SelectCtx& x, const CT* table, uint64_t cap, uint64_t k,
   return nsel;
 }
 
-template uint64_t select_topk<uint32_t>(SelectCtx&, const uint32_t*, uint64_t, uint64_t,
-                                        const uint64_t*, int, uint64_t*, uint64_t*);
+template uint64_t select_topk<uint32_t>(SelectCtx&, const uint32_t*, uint64_t, uint64_t, KeyMap,
+                                        int, uint64_t*, uint64_t*);
 template uint64_t select_topk<unsigned long long>(SelectCtx&, const unsigned long long*, uint64_t,
-                                                  uint64_t, const uint64_t*, int, uint64_t*,
-                                                  uint64_t*);
+                                                  uint64_t, KeyMap, int, uint64_t*, uint64_t*);
 
 }  // namespace igb

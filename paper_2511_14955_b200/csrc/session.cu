@@ -23,6 +23,8 @@
 namespace igb {
 
 static constexpr size_t kOnceSmemBudget = 200 * 1024;  // bytes of bitmap per CTA
+static constexpr uint64_t kUnitBytes = 1ull << 20;     // count-once work unit
+static constexpr uint32_t kPrefixesPerOwner = 64;       // count-once ext: 64*256 ids/owner
 
 struct Session {
   int device = 0;
@@ -41,9 +43,10 @@ struct Session {
   // pass buffers
   DevBuf table, work;
   DevBuf surv_keys, surv_counts, next_keys, next_counts;
-  DevBuf pkeys, hkeys, hidx, owner, owner_cnt, owner_start, cursor, rank_of_p;
-  DevBuf sel_state, sel_hist, sel_scalar;
+  DevBuf pkeys, hkeys, hidx, hpacked, owner, owner_cnt, owner_start, cursor, rank_of_p;
+  DevBuf sel_state, sel_hist, sel_scalar, units, unit_first;
   SelectCtx sel;
+  RouteCtx rc;
   std::vector<cudaEvent_t> events;
 
   ~Session() {
@@ -142,6 +145,30 @@ static void load_corpus(Session& s, const ig_corpus& c) {
   if (m)
     IGB_CUDA(cudaMemcpyAsync(dord, ord.data(), m * sizeof(uint32_t), cudaMemcpyHostToDevice,
                              s.stream));
+  // count-once work units: <= 1 MiB of gram ends of one sequence
+  std::vector<RouteUnit> units;
+  std::vector<uint32_t> ufirst(m + 1, 0);
+  for (uint64_t q = 0; q < m; ++q) {
+    ufirst[q] = (uint32_t)units.size();
+    for (uint64_t b = hoff[q]; b < hoff[q + 1]; b += kUnitBytes) {
+      RouteUnit u{};
+      u.q = (uint32_t)q;
+      u.b0 = b;
+      u.b1 = std::min<uint64_t>(b + kUnitBytes, hoff[q + 1]);
+      units.push_back(u);
+    }
+  }
+  RouteUnit* dun = s.units.as<RouteUnit>(units.size() + 1);
+  if (!units.empty())
+    IGB_CUDA(cudaMemcpyAsync(dun, units.data(), units.size() * sizeof(RouteUnit),
+                             cudaMemcpyHostToDevice, s.stream));
+  ufirst[m] = (uint32_t)units.size();
+  uint32_t* duf = s.unit_first.as<uint32_t>(m + 1);
+  IGB_CUDA(cudaMemcpyAsync(duf, ufirst.data(), (m + 1) * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                           s.stream));
+  s.rc.units = dun;
+  s.rc.unit_first = duf;
+  s.rc.nunits = (uint32_t)units.size();
   IGB_CUDA(cudaStreamSynchronize(s.stream));
   s.dc.data = base + kFrontPad;
   s.dc.off = doff;
@@ -282,6 +309,16 @@ static DevPrefixSet build_prefix_set(Session& s, const uint64_t* keys, uint64_t 
   ps.S = S;
   ps.lgS = lgS;
   ps.max_owner = mx;
+  // packed copy for shared-memory staging when key and local index fit in 64 bits
+  uint32_t ib = 1;
+  while ((1ull << ib) <= mx) ++ib;
+  if (8 * plen + ib <= 64) {
+    ps.ib = ib;
+    uint64_t* pk2 = s.hpacked.as<uint64_t>((size_t)G * S);
+    ps.packed = pk2;
+    launch_pack_prefix(ps, pk2, s.stream);
+    s.launches++;
+  }
   return ps;
 }
 
@@ -290,6 +327,130 @@ static void allreduce(Session& s, void* buf, uint64_t count, int dtype) {
   if (!s.coll.allreduce) throw Error(IG_EINTERNAL, "collective has no allreduce");
   const int rc = s.coll.allreduce(buf, count, dtype, (void*)s.stream, s.coll.user);
   if (rc != 0) throw Error(IG_EINTERNAL, "allreduce callback failed");
+}
+
+// Survivor prefix structure for the next extension pass: the bucketed (CSR)
+// set for count-once routing, the open-addressing set for count-all.
+struct Prefix {
+  DevPrefixSet ps;
+  RouteParams rp;
+  bool csr = false;  // cuckoo prefix set (count-once)
+  uint64_t K = 0;
+  std::vector<uint32_t> rank_of_p;  // count-once: p -> survivor rank
+  const uint64_t* pkeys = nullptr;   // count-once: keys by p
+};
+
+static Prefix prepare_prefix(Session& s, const uint64_t* keys, uint64_t K, uint32_t plen,
+                             int mode) {
+  Prefix P;
+  P.K = K;
+  if (!K) return P;
+  if (mode == IG_MODE_ONCE) {
+    // count-once routing: owners = hash(prefix) with <= 64 prefixes each,
+    // prefixes numbered owner by owner (stable by rank), bucketized cuckoo set
+    std::vector<uint64_t> hk(K);
+    IGB_CUDA(cudaMemcpyAsync(hk.data(), keys, K * 8, cudaMemcpyDeviceToHost, s.stream));
+    IGB_CUDA(cudaStreamSynchronize(s.stream));
+    auto owner_of = [](uint64_t key, uint32_t lgno) -> uint32_t {
+      return lgno ? (uint32_t)((key * kOwnerMul) >> (64 - lgno)) : 0u;
+    };
+    uint32_t lgno = 0;
+    std::vector<uint32_t> cnt;
+    for (;; ++lgno) {
+      cnt.assign((size_t)1 << lgno, 0);
+      uint32_t mx = 0;
+      for (uint64_t i = 0; i < K; ++i) mx = std::max(mx, ++cnt[owner_of(hk[i], lgno)]);
+      if (mx <= kPrefixesPerOwner) break;
+    }
+    const uint32_t NO = 1u << lgno;
+    std::vector<uint32_t> ostart(NO + 1, 0);
+    for (uint32_t o = 0; o < NO; ++o) ostart[o + 1] = ostart[o] + cnt[o];
+    std::vector<uint32_t> cur(ostart.begin(), ostart.end() - 1);
+    std::vector<uint64_t> pk(K);
+    P.rank_of_p.assign(K, 0);
+    for (uint64_t i = 0; i < K; ++i) {
+      const uint32_t pp = cur[owner_of(hk[i], lgno)]++;
+      pk[pp] = hk[i];
+      P.rank_of_p[pp] = (uint32_t)i;
+    }
+    std::vector<uint64_t> slots;
+    std::vector<uint32_t> slot_p;
+    uint32_t nbk = 0;
+    build_cuckoo_prefix(pk, slots, slot_p, nbk);
+    const bool packed = 8 * plen + 24 <= 64 && K < 0xffffffull;
+    if (packed)
+      for (size_t i = 0; i < slots.size(); ++i)
+        if (slots[i] != kEmptyKey) slots[i] = (slots[i] << 24) | slot_p[i];
+    uint64_t* dpk = s.pkeys.as<uint64_t>(K + 1);
+    uint64_t* ds = s.hkeys.as<uint64_t>(slots.size() + 2);
+    uint32_t* dpi = s.hidx.as<uint32_t>(slot_p.size() + 2);
+    uint32_t* dos = s.owner_start.as<uint32_t>(NO + 1);
+    IGB_CUDA(cudaMemcpyAsync(dpk, pk.data(), K * 8, cudaMemcpyHostToDevice, s.stream));
+    IGB_CUDA(cudaMemcpyAsync(ds, slots.data(), slots.size() * 8, cudaMemcpyHostToDevice, s.stream));
+    IGB_CUDA(cudaMemcpyAsync(dpi, slot_p.data(), slot_p.size() * 4, cudaMemcpyHostToDevice,
+                             s.stream));
+    IGB_CUDA(cudaMemcpyAsync(dos, ostart.data(), (NO + 1) * 4, cudaMemcpyHostToDevice, s.stream));
+    RouteParams& rp = P.rp;
+    rp.ext = true;
+    rp.packed = packed;
+    rp.lgno = lgno;
+    rp.NO = NO;
+    rp.lgl = 14;  // kPrefixesPerOwner * 256 ids per owner
+    rp.nbk = nbk;
+    rp.slots = ds;
+    rp.pidx = dpi;
+    rp.ostart = dos;
+    rp.minv = 0;  // table index = p * 256 + last byte
+    P.pkeys = dpk;
+    P.csr = true;
+  } else {
+    P.ps = build_prefix_set(s, keys, K, plen, mode);
+  }
+  return P;
+}
+
+// One counting pass.  Returns the device table (tcap entries) and how table
+// indices map to gram keys.
+template <typename CT>
+static CT* count_pass(Session& s, bool dense, uint32_t L, int mode, const Prefix* P,
+                      uint64_t& tcap, KeyMap& km) {
+  if (mode == IG_MODE_ONCE) {
+    RouteParams rp;
+    if (dense) make_route_params(1ull << (8 * L), rp);
+    else rp = P->rp;
+    tcap = dense ? (1ull << rp.lgc) : 256 * P->K;
+    CT* t = s.table.as<CT>(tcap);
+    IGB_CUDA(cudaMemsetAsync(t, 0, tcap * sizeof(CT), s.stream));
+    const uint64_t l0 = s.rc.launches;
+    route_count_once<CT>(s.rc, s.dc, dense ? 0 : 1, L, rp, t, s.num_sms, s.stream);
+    s.launches += s.rc.launches - l0;
+    km = KeyMap{};
+    if (dense) {
+      km.minv = rp.minv;
+      km.cmask = rp.cmask;
+    } else {
+      km.pkeys = P->pkeys;
+    }
+    return t;
+  }
+  uint32_t* work = s.work.as<uint32_t>(64);
+  if (dense) {
+    tcap = 1ull << (8 * L);
+    CT* t = s.table.as<CT>(tcap);
+    IGB_CUDA(cudaMemsetAsync(t, 0, tcap * sizeof(CT), s.stream));
+    launch_count_dense<CT>(s.dc, L, mode, t, work, s.num_sms, s.stream);
+    s.launches++;
+    km = KeyMap{};
+    return t;
+  }
+  tcap = 256 * P->K;
+  CT* t = s.table.as<CT>(tcap);
+  IGB_CUDA(cudaMemsetAsync(t, 0, tcap * sizeof(CT), s.stream));
+  launch_count_extend<CT>(s.dc, P->ps, L, mode, t, work, s.num_sms, s.stream);
+  s.launches++;
+  km = KeyMap{};
+  km.pkeys = P->ps.pkeys;
+  return t;
 }
 
 // Count-table dtype: u32 whenever no count can reach 2^32 (count-once counts
@@ -310,18 +471,16 @@ static void run_t(Session& s, const ig_params& p, ig_result* out) {
   StepTimer tm(s);
   std::vector<Row> rows;
   std::string diag;
-  uint32_t* work = s.work.as<uint32_t>(64);
   const uint64_t sel_before = s.sel.launches;
 
   // ---- dense pass (intergrams.cpp:76-103)
   const uint64_t dcap = 1ull << (8 * n0);
   size_t ev = tm.begin();
-  CT* table = s.table.as<CT>(dcap);
-  IGB_CUDA(cudaMemsetAsync(table, 0, dcap * sizeof(CT), s.stream));
-  launch_count_dense<CT>(s.dc, n0, p.mode, table, work, s.num_sms, s.stream);
-  s.launches++;
+  uint64_t tcap = 0;
+  KeyMap km;
+  CT* table = count_pass<CT>(s, true, n0, p.mode, nullptr, tcap, km);
   IGB_CUDA(cudaGetLastError());
-  allreduce(s, table, dcap, sizeof(CT) == 4 ? 0 : 1);
+  allreduce(s, table, tcap, sizeof(CT) == 4 ? 0 : 1);
   tm.end(ev);
   rows.push_back(make_row(std::to_string(n0) + "-gram pass", n0, total_bytes, dcap, 0, false, ev));
 
@@ -333,7 +492,7 @@ static void run_t(Session& s, const ig_params& p, ig_result* out) {
     ev = tm.begin();
     out_keys_d = s.next_keys.as<uint64_t>(std::min<uint64_t>(p.k, dcap) + 1);
     out_counts_d = s.next_counts.as<uint64_t>(std::min<uint64_t>(p.k, dcap) + 1);
-    out_len = select_topk<CT>(s.sel, table, dcap, p.k, nullptr, 8 * n0, out_keys_d, out_counts_d);
+    out_len = select_topk<CT>(s.sel, table, tcap, p.k, km, 8 * n0, out_keys_d, out_counts_d);
     tm.end(ev);
     rows.push_back(make_row("top-k " + std::to_string(n) + "-grams", n, 0, 0, out_len, false, ev));
   } else {
@@ -342,13 +501,12 @@ static void run_t(Session& s, const ig_params& p, ig_result* out) {
     uint64_t scap = std::min<uint64_t>(kp, dcap);
     uint64_t* sk = s.surv_keys.as<uint64_t>(scap + 1);
     uint64_t* sc = s.surv_counts.as<uint64_t>(scap + 1);
-    uint64_t ns = select_topk<CT>(s.sel, table, dcap, kp, nullptr, 24, sk, sc);
+    uint64_t ns = select_topk<CT>(s.sel, table, tcap, kp, km, 24, sk, sc);
     bool shrt = ns < kp;
     if (shrt)
       diag += "pass 3 retained " + std::to_string(ns) + " candidates (requested " +
               std::to_string(kp) + ")\n";
-    DevPrefixSet ps{};
-    if (ns) ps = build_prefix_set(s, sk, ns, 3, p.mode);
+    Prefix P = prepare_prefix(s, sk, ns, 3, p.mode);
     tm.end(ev);
     rows.push_back(make_row("top-zk 3-grams/trie building", 3, 0, 0, ns, shrt, ev));
 
@@ -358,12 +516,9 @@ static void run_t(Session& s, const ig_params& p, ig_result* out) {
       if (ns == 0) throw Error(IG_ECONFIG, "extension pass needs a trie of depth j-1");
       ev = tm.begin();
       const uint64_t cap = 256 * ns;
-      CT* ct = s.table.as<CT>(cap);
-      IGB_CUDA(cudaMemsetAsync(ct, 0, cap * sizeof(CT), s.stream));
-      launch_count_extend<CT>(s.dc, ps, j, p.mode, ct, work, s.num_sms, s.stream);
-      s.launches++;
+      CT* ct = count_pass<CT>(s, false, j, p.mode, &P, tcap, km);
       IGB_CUDA(cudaGetLastError());
-      allreduce(s, ct, cap, sizeof(CT) == 4 ? 0 : 1);
+      allreduce(s, ct, tcap, sizeof(CT) == 4 ? 0 : 1);
       tm.end(ev);
       rows.push_back(
           make_row(std::to_string(j) + "-gram pass", j, total_bytes, cap, 0, false, ev));
@@ -373,7 +528,7 @@ static void run_t(Session& s, const ig_params& p, ig_result* out) {
         uint64_t ncap = std::min<uint64_t>(kp, cap);
         uint64_t* nk = s.next_keys.as<uint64_t>(ncap + 1);
         uint64_t* nc = s.next_counts.as<uint64_t>(ncap + 1);
-        uint64_t nn = select_topk<CT>(s.sel, ct, cap, kp, ps.pkeys, 8 * j, nk, nc);
+        uint64_t nn = select_topk<CT>(s.sel, ct, tcap, kp, km, 8 * j, nk, nc);
         shrt = nn < kp;
         if (shrt)
           diag += "pass " + std::to_string(j) + " retained " + std::to_string(nn) +
@@ -382,7 +537,7 @@ static void run_t(Session& s, const ig_params& p, ig_result* out) {
         s.surv_counts.swap(s.next_counts);
         sk = nk;
         ns = nn;
-        if (ns) ps = build_prefix_set(s, sk, ns, j, p.mode);
+        P = prepare_prefix(s, sk, ns, j, p.mode);
         tm.end(ev);
         rows.push_back(make_row("top-zk " + std::to_string(j) + "-grams/trie building", j, 0, 0,
                                 ns, shrt, ev));
@@ -390,7 +545,7 @@ static void run_t(Session& s, const ig_params& p, ig_result* out) {
         uint64_t ocap = std::min<uint64_t>(p.k, cap);
         out_keys_d = s.next_keys.as<uint64_t>(ocap + 1);
         out_counts_d = s.next_counts.as<uint64_t>(ocap + 1);
-        out_len = select_topk<CT>(s.sel, ct, cap, p.k, ps.pkeys, 8 * j, out_keys_d, out_counts_d);
+        out_len = select_topk<CT>(s.sel, ct, tcap, p.k, km, 8 * j, out_keys_d, out_counts_d);
         tm.end(ev);
         rows.push_back(
             make_row("top-k " + std::to_string(j) + "-grams", j, 0, 0, out_len, false, ev));
@@ -546,13 +701,23 @@ int ig_count_dense(const ig_corpus* corpus, uint32_t n, int32_t mode, int32_t de
     try {
       load_corpus(*s, *corpus);
       const uint64_t cap = 1ull << (8 * n);
-      unsigned long long* t = s->table.as<unsigned long long>(cap);
-      IGB_CUDA(cudaMemsetAsync(t, 0, cap * 8, s->stream));
-      launch_count_dense<unsigned long long>(s->dc, n, mode, t, s->work.as<uint32_t>(64),
-                                             s->num_sms, s->stream);
+      uint64_t tcap = 0;
+      KeyMap km;
+      unsigned long long* t = count_pass<unsigned long long>(*s, true, n, mode, nullptr, tcap, km);
       IGB_CUDA(cudaGetLastError());
-      IGB_CUDA(cudaMemcpyAsync(table_out, t, cap * 8, cudaMemcpyDeviceToHost, s->stream));
+      std::vector<uint64_t> tab(tcap);
+      IGB_CUDA(cudaMemcpyAsync(tab.data(), t, tcap * 8, cudaMemcpyDeviceToHost, s->stream));
       IGB_CUDA(cudaStreamSynchronize(s->stream));
+      // back to the reference layout: table index = dense id (dense_pass.cpp:12-19)
+      if (km.minv) {
+        // index = (id * mult) & cmask; recover mult from minv
+        uint64_t mult = km.minv;
+        for (int it = 0; it < 6; ++it) mult *= 2ull - km.minv * mult;
+        mult &= km.cmask;
+        for (uint64_t id = 0; id < cap; ++id) table_out[id] = tab[(id * mult) & km.cmask];
+      } else {
+        memcpy(table_out, tab.data(), cap * 8);
+      }
     } catch (...) {
       delete s;
       throw;
@@ -581,22 +746,37 @@ int ig_extend_pass(const ig_corpus* corpus, const uint64_t* prefix_keys, uint64_
       load_corpus(*s, *corpus);
       uint64_t* dk = s->surv_keys.as<uint64_t>(nprefix + 1);
       IGB_CUDA(cudaMemcpyAsync(dk, prefix_keys, nprefix * 8, cudaMemcpyHostToDevice, s->stream));
-      DevPrefixSet ps = build_prefix_set(*s, dk, nprefix, prefix_len, mode);
-      const uint64_t cap = 256 * nprefix;
-      unsigned long long* t = s->table.as<unsigned long long>(cap);
-      IGB_CUDA(cudaMemsetAsync(t, 0, cap * 8, s->stream));
-      launch_count_extend<unsigned long long>(s->dc, ps, j, mode, t, s->work.as<uint32_t>(64),
-                                              s->num_sms, s->stream);
+      Prefix P = prepare_prefix(*s, dk, nprefix, prefix_len, mode);
+      uint64_t tcap = 0;
+      KeyMap km;
+      unsigned long long* t = count_pass<unsigned long long>(*s, false, j, mode, &P, tcap, km);
       IGB_CUDA(cudaGetLastError());
-      std::vector<uint64_t> tab(cap);
-      std::vector<uint32_t> rank(nprefix);
-      IGB_CUDA(cudaMemcpyAsync(tab.data(), t, cap * 8, cudaMemcpyDeviceToHost, s->stream));
-      IGB_CUDA(cudaMemcpyAsync(rank.data(), ps.hidx ? s->rank_of_p.p : nullptr, nprefix * 4,
-                               cudaMemcpyDeviceToHost, s->stream));
+      std::vector<uint64_t> tab(tcap);
+      IGB_CUDA(cudaMemcpyAsync(tab.data(), t, tcap * 8, cudaMemcpyDeviceToHost, s->stream));
+      std::vector<uint32_t> rank;  // p -> survivor rank
+      if (P.csr) {
+        rank = P.rank_of_p;
+      } else {
+        rank.resize(nprefix);
+        IGB_CUDA(cudaMemcpyAsync(rank.data(), s->rank_of_p.p, nprefix * 4,
+                                 cudaMemcpyDeviceToHost, s->stream));
+      }
       IGB_CUDA(cudaStreamSynchronize(s->stream));
-      // back to the reference layout: ordinal (rank) * 256 + last byte
-      for (uint64_t p = 0; p < nprefix; ++p)
-        memcpy(table_out + (uint64_t)rank[p] * 256, tab.data() + p * 256, 256 * 8);
+      uint64_t mult = 1;
+      if (km.minv) {
+        mult = km.minv;
+        for (int it = 0; it < 6; ++it) mult *= 2ull - km.minv * mult;
+        mult &= km.cmask;
+      }
+      // back to the reference layout: ordinal (rank) * 256 + last byte (candidate_id)
+      memset(table_out, 0, nprefix * 256 * 8);
+      for (uint64_t p = 0; p < rank.size(); ++p) {
+        if (rank[p] == 0xffffffffu) continue;  // empty cuckoo slot
+        for (uint64_t b = 0; b < 256; ++b) {
+          const uint64_t id = p * 256 + b;
+          table_out[(uint64_t)rank[p] * 256 + b] = tab[km.minv ? ((id * mult) & km.cmask) : id];
+        }
+      }
       if (bytes_processed) *bytes_processed = s->dc.total;
     } catch (...) {
       delete s;
@@ -633,7 +813,9 @@ int ig_top_k(const uint64_t* table, uint64_t cap, uint64_t k, const uint64_t* pr
       const uint64_t kk = std::min<uint64_t>(k, cap4);
       uint64_t* ok = s->next_keys.as<uint64_t>(kk + 1);
       uint64_t* oc = s->next_counts.as<uint64_t>(kk + 1);
-      const uint64_t n = select_topk<unsigned long long>(s->sel, t, cap4, kk, pk, key_bits, ok, oc);
+      KeyMap km;
+      km.pkeys = pk;
+      const uint64_t n = select_topk<unsigned long long>(s->sel, t, cap4, kk, km, key_bits, ok, oc);
       if (n) {
         IGB_CUDA(cudaMemcpyAsync(keys_out, ok, n * 8, cudaMemcpyDeviceToHost, s->stream));
         IGB_CUDA(cudaMemcpyAsync(counts_out, oc, n * 8, cudaMemcpyDeviceToHost, s->stream));
