@@ -589,10 +589,13 @@ __global__ void k_prefix_insert(const uint64_t* __restrict__ keys, uint32_t K,
                                 const uint32_t* __restrict__ owner_start,
                                 uint32_t* __restrict__ cursor, uint32_t S, uint32_t lgS,
                                 uint64_t* __restrict__ hkeys, uint32_t* __restrict__ hidx,
-                                uint64_t* __restrict__ pkeys, uint32_t* __restrict__ rank_of_p) {
+                                uint64_t* __restrict__ pkeys, uint32_t* __restrict__ rank_of_p,
+                                bool S_single) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < K; i += gridDim.x * blockDim.x) {
     const uint32_t o = owner[i];
-    const uint32_t p = owner_start[o] + atomicAdd(cursor + o, 1u);
+    // single slice (count-all): p = rank, identical on every rank of a
+    // multi-GPU run so per-rank tables can be summed element-wise
+    const uint32_t p = S_single ? i : owner_start[o] + atomicAdd(cursor + o, 1u);
     const uint64_t key = keys[i];
     pkeys[p] = key;
     rank_of_p[p] = i;
@@ -625,7 +628,8 @@ void launch_prefix_insert(const uint64_t* keys, uint32_t K, const uint32_t* owne
   if (!K) return;
   const unsigned blocks = (K + 255) / 256;
   k_prefix_insert<<<blocks < 4096 ? blocks : 4096, 256, 0, st>>>(
-      keys, K, owner, owner_start, cursor, S, lgS, hkeys, hidx, pkeys, rank_of_p);
+      keys, K, owner, owner_start, cursor, S, lgS, hkeys, hidx, pkeys, rank_of_p,
+      owner_start == nullptr);
 }
 
 }  // namespace igb

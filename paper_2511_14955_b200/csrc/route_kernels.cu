@@ -281,7 +281,7 @@ __global__ void __launch_bounds__(kScatterThreads) k_route_scatter(
           // a gram already routed from this chunk adds nothing (count-once):
           // drop it before the prefix lookup.  Races only cost a duplicate.
           const uint32_t slot = (uint32_t)((key * 0x9E3779B97F4A7C15ull) >> (64 - 11));
-          if (cache[slot] != key) {
+          if (key == ~0ull || cache[slot] != key) {  // ~0 is the empty marker
             cache[slot] = key;
             v = scatter_route<KIND, PACKED>(key, rp, slots);
             if (v != 0xffffffffu) atomicAdd(lhist + (v >> 16), 1u);

@@ -298,7 +298,8 @@ static DevPrefixSet build_prefix_set(Session& s, const uint64_t* keys, uint64_t 
   uint64_t* pk = s.pkeys.as<uint64_t>(K + 1);
   uint32_t* rp = s.rank_of_p.as<uint32_t>(K + 1);
   IGB_CUDA(cudaMemsetAsync(hk, 0xff, (size_t)G * S * sizeof(uint64_t), s.stream));
-  launch_prefix_insert(keys, (uint32_t)K, owner, ostart, cursor, S, lgS, hk, hi, pk, rp, s.stream);
+  launch_prefix_insert(keys, (uint32_t)K, owner, G == 1 ? nullptr : ostart, cursor, S, lgS, hk, hi,
+                       pk, rp, s.stream);
   s.launches++;
   ps.pkeys = pk;
   ps.hkeys = hk;

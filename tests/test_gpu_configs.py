@@ -1,0 +1,71 @@
+"""BASELINE config shapes on the GPU.  Reduced-size samples of every config are
+compared with the C oracle bit for bit; at full size (c1 entirely; c2 at 4 GiB)
+the run is checked through size-independent properties: canonical order,
+count bounds (count-once <= m; extension counts <= prefix counts), prefix
+consistency with the previous pass, and determinism across runs."""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2511_14955_b200 import intergrams as ig
+from paper_2511_14955_b200 import synth as S
+
+pytestmark = pytest.mark.gpu
+
+
+def run_both(cfg, n, k, mode, z=1.5):
+    data, off = S.generate(cfg)
+    r = ig.run_intergrams(ig.Corpus(data, off), ig.IntergramConfig(n=n, k=k, z=z,
+                                                                   mode=ig.CountMode(mode)))
+    rc, keys, counts, rows, diag = O.oracle_run(data, off, n, k, z, mode)
+    assert rc == 0
+    return r, keys, counts, diag
+
+
+@pytest.mark.parametrize("name,extra", [
+    ("c1", {}),  # full size: 256 x 256 KiB
+    ("c2", {"num_seqs": 96}),
+    ("c3", {"total": 96 << 20}),
+    ("c4", {"num_seqs": 24}),
+    ("c5", {"num_seqs": 64}),
+])
+def test_config_sample_equals_oracle(gpu_lib, name, extra):
+    base = S.CONFIGS[name]
+    cfg = S.scaled(base, **extra)
+    k = base.k if name in ("c1", "c2") else min(base.k, 2000)
+    r, keys, counts, diag = run_both(cfg, base.n, k, base.mode)
+    assert np.array_equal(r.keys, keys) and np.array_equal(r.counts, counts)
+    assert r.diagnostics == diag
+
+
+def check_canonical(r):
+    c = r.counts.astype(np.int64)
+    k = r.keys
+    assert (np.diff(c) <= 0).all()
+    same = np.diff(c) == 0
+    assert (k[1:][same] > k[:-1][same]).all()
+
+
+@pytest.mark.slow
+def test_c2_full_size_properties(gpu_lib):
+    cfg = S.CONFIGS["c2"]
+    data, off = S.generate(cfg)
+    corpus = ig.Corpus(data, off)
+    sess = ig.Session(device=0)
+    sess.load(corpus)
+    c6 = ig.IntergramConfig(n=6, k=10000, z=1.5, mode=ig.CountMode.kOnce)
+    r1 = sess.run(c6)
+    r2 = sess.run(c6)
+    assert r1.topk == r2.topk  # determinism
+    assert len(r1.topk) == 10000
+    check_canonical(r1)
+    assert int(r1.counts.max()) <= cfg.num_seqs  # count-once bound
+    # prefix consistency: every 6-gram's 5-prefix is a 5-gram survivor, and its
+    # count never exceeds the prefix count (test_intergrams.cpp:163-208)
+    r5 = sess.run(ig.IntergramConfig(n=5, k=15000, z=1.5, mode=ig.CountMode.kOnce))
+    pc = {g.gram: g.count for g in r5.topk}
+    for g in r1.topk:
+        assert g.gram[:5] in pc and g.count <= pc[g.gram[:5]]
+    passes = [p for p in r1.passes if p.bytes_processed]
+    assert len(passes) == 4 and all(p.bytes_processed == 4 << 30 for p in passes)
+    sess.close()

@@ -82,3 +82,49 @@ def test_run_equals_c_oracle(gpu_lib, n, mode):
                  p.retained_short) for p in r.passes] == \
                [(q["label"], q["gram_len"], q["bytes_processed"], q["candidate_space"],
                  q["retained"], q["retained_short"]) for q in rows]
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_extend_pass_table_equals_oracle(gpu_lib, seed):
+    # tests/test_intergrams.cpp:69-110: random prefix subsets, both modes
+    rng = O.Mt64(606 + seed)
+    seqs = O.random_corpus(rng, 10, 120, 6)
+    d, off = O.csr(seqs)
+    j = 4 + seed % 2
+    allp, _ = O.oracle_naive(d, off, j - 1, int(ONCE), 1 << 20)
+    kept = [int(x) for x in allp if rng() % 2 == 0] or [int(allp[0])]
+    pre = [ig.key_to_gram(x, j - 1) for x in kept]
+    for mode in (ONCE, ALL):
+        t, bp = ig.extend_pass(seqs, pre, j, mode)
+        rc, t2, b2 = O.oracle_extend(d, off, np.array(kept, np.uint64), j - 1, j, int(mode))
+        assert rc == 0 and np.array_equal(t, t2) and bp == b2
+
+
+def test_extend_pass_rejects_wrong_depth(gpu_lib):
+    # tests/test_intergrams.cpp:112-117
+    with pytest.raises(ig.ConfigError):
+        ig.extend_pass([b"abcd"], [b"ab"], 4, ONCE)
+    with pytest.raises(ig.ConfigError):
+        ig.extend_pass([b"abcd"], [], 4, ONCE)
+
+
+def test_extend_pass_kat(gpu_lib):
+    # tests/test_intergrams.cpp:48-67
+    t, _ = ig.extend_pass([b"abab"], [b"aba"], 4, ONCE)
+    assert t.size == 256 and t[ig.candidate_id(0, ord("b"))] == 1 and t.sum() == 1
+    t, _ = ig.extend_pass([b"abab"], [b"bab"], 4, ONCE)
+    assert t.sum() == 0
+
+
+@pytest.mark.parametrize("seed", [99, 123, 7])
+def test_top_k_api_equals_oracle(gpu_lib, seed):
+    # tests/test_counting.cpp:149-171 (k beyond capacity included)
+    rng = O.Mt64(seed)
+    t = np.array([rng() % 16 for _ in range(1000)], np.uint64)
+    for k in (1, 10, 999, 5000):
+        keys, counts = ig.top_k(t, k)
+        k2, c2 = O.oracle_top_k(t, k)
+        assert np.array_equal(keys, k2) and np.array_equal(counts, c2)
+    with pytest.raises(ig.ConfigError):
+        ig.top_k(t, 0)
+    assert ig.top_k(np.zeros(100, np.uint64), 5)[0].size == 0  # test_counting.cpp:144-147
