@@ -1,0 +1,131 @@
+// intergrams/intergrams.hpp — drop-in for
+// /root/reference/proj/include/intergrams/intergrams.hpp: the same
+// IntergramConfig (:19-33), PassResult (:35-47), IntergramsResult (:49-53),
+// candidate_id (:56-59) and run_intergrams (:74-75), executed by the sm_100a
+// library through the C-ABI in include/intergrams_b200.h.  Header-only; link
+// with paper_2511_14955_b200/_lib/libintergrams_b200.so.
+#pragma once
+
+#include <cassert>
+#include <cmath>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "intergrams/common.hpp"
+#include "intergrams/corpus.hpp"
+#include "intergrams/counting.hpp"
+#include "intergrams_b200.h"
+
+namespace intergrams {
+
+struct IntergramConfig {
+  size_t n = 6;
+  size_t k = 10000;
+  double z = 1.5;  // k' = ceil(z*k)
+  CountMode mode = CountMode::kOnce;
+  MergeStrategy merge = MergeStrategy::kBatchedFlush;  // no effect on the GPU
+  size_t workers = 1;                                   // no effect on the GPU
+  size_t flush_batch_size = 8;                          // validated only
+  bool frequency_ordered_trie = true;                   // no effect on results
+  int device = -1;                                      // CUDA ordinal (-1: current)
+
+  size_t k_prime() const { return static_cast<size_t>(std::ceil(z * static_cast<double>(k))); }
+  void validate() const {
+    if (n < 1) throw ConfigError("gram length n must be >= 1");
+    if (k < 1) throw ConfigError("k must be >= 1");
+    if (!(z >= 1.0)) throw ConfigError("oversample factor z must be >= 1");
+    if (flush_batch_size < 1) throw ConfigError("flush batch size must be >= 1");
+  }
+};
+
+struct PassResult {
+  std::string label;
+  size_t gram_len = 0;
+  double seconds = 0.0;
+  uint64_t bytes_processed = 0;
+  size_t candidate_space = 0;
+  size_t retained = 0;
+  bool retained_short = false;
+
+  double throughput_bps() const {
+    return seconds > 0.0 ? static_cast<double>(bytes_processed) / seconds : 0.0;
+  }
+};
+
+struct IntergramsResult {
+  TopKList topk;
+  std::vector<PassResult> passes;
+  std::vector<std::string> diagnostics;
+};
+
+inline size_t candidate_id(size_t prefix_ordinal, unsigned last_byte) {
+  assert(last_byte <= 255);
+  return prefix_ordinal * 256 + last_byte;
+}
+
+namespace detail {
+
+inline void raise(int rc, const char* err) {
+  switch (rc) {
+    case IG_OK: return;
+    case IG_ECONFIG: throw ConfigError(err);
+    case IG_EIO: throw IoError(err);
+    case IG_EINVALID: throw std::invalid_argument(err);
+    default: throw DeviceError(err);
+  }
+}
+
+inline IntergramsResult convert(const ig_result& r) {
+  IntergramsResult out;
+  out.topk.reserve(r.len);
+  for (uint64_t i = 0; i < r.len; ++i) {
+    std::string g(r.gram_len, '\0');
+    for (uint32_t b = 0; b < r.gram_len; ++b)
+      g[b] = static_cast<char>((r.keys[i] >> (8 * (r.gram_len - 1 - b))) & 0xff);
+    out.topk.push_back(GramCount{std::move(g), r.counts[i]});
+  }
+  for (uint32_t i = 0; i < r.num_passes; ++i) {
+    const ig_pass_stat& p = r.passes[i];
+    out.passes.push_back(PassResult{p.label, p.gram_len, p.seconds, p.bytes_processed,
+                                    p.candidate_space, p.retained, p.retained_short != 0});
+  }
+  std::string d = r.diagnostics ? r.diagnostics : "";
+  size_t s = 0;
+  while (s < d.size()) {
+    size_t e = d.find('\n', s);
+    if (e == std::string::npos) e = d.size();
+    if (e > s) out.diagnostics.push_back(d.substr(s, e - s));
+    s = e + 1;
+  }
+  return out;
+}
+
+inline ig_params params_of(const IntergramConfig& cfg) {
+  ig_params p{};
+  p.n = static_cast<uint32_t>(cfg.n);
+  p.k = cfg.k;
+  p.z = cfg.z;
+  p.mode = cfg.mode == CountMode::kAll ? IG_MODE_ALL : IG_MODE_ONCE;
+  p.flush_batch_size = cfg.flush_batch_size;
+  p.device = cfg.device;
+  return p;
+}
+
+}  // namespace detail
+
+// run_intergrams (intergrams.hpp:74-75) on the GPU.
+inline IntergramsResult run_intergrams(const Corpus& corpus, const IntergramConfig& cfg) {
+  cfg.validate();
+  const CorpusCSR csr = corpus.materialize();
+  ig_corpus c{csr.data.data(), csr.offsets.data(), csr.offsets.size() - 1, IG_HOST};
+  const ig_params p = detail::params_of(cfg);
+  ig_result r{};
+  char err[1024] = {0};
+  detail::raise(ig_topk_ngrams(&c, &p, &r, err, sizeof(err)), err);
+  IntergramsResult out = detail::convert(r);
+  ig_result_free(&r);
+  return out;
+}
+
+}  // namespace intergrams
