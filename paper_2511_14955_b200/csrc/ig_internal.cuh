@@ -43,7 +43,7 @@ inline void cuda_check(cudaError_t e, const char* what, const char* file, int li
   } while (0)
 
 constexpr uint64_t kEmptyKey = ~0ull;
-constexpr uint64_t kCuckooMul1 = 0x9E3779B97F4A7C15ull;  // prefix-set bucket hashes
+constexpr uint64_t kCuckooMul1 = 0x9E3779B97F4A7C15ull;  // prefix-set hashes
 constexpr uint64_t kCuckooMul2 = 0xC2B2AE3D27D4EB4Full;
 constexpr uint64_t kOwnerMul = 0xD6E8FEB86659FD93ull;    // count-once owner of a prefix  // never a key: keys have <= 56 bits in a prefix set
 constexpr int kTileBytes = 512;        // one warp x 16 B per lane

@@ -49,13 +49,14 @@ struct RouteParams {
   uint32_t lgc = 2, lgl = 2, NO = 1;  // dense: permuted id space 2^lgc; 2^lgl ids per owner
   uint64_t cmask = 3, mult = 1, minv = 1;
   // extension passes: owner = hash(prefix) >> (64-lgno); p numbered owner by
-  // owner (ostart[o] .. ostart[o+1]); bucketized cuckoo prefix set
+  // owner (ostart[o] .. ostart[o+1]); CHD perfect-hash prefix set
   bool ext = false;
   bool packed = false;  // slots = (key << 24) | p, else slots = key and pidx[slot] = p
   uint32_t lgno = 0;
-  uint32_t nbk = 0;
-  const uint64_t* slots = nullptr;
-  const uint32_t* pidx = nullptr;
+  uint32_t nb = 0, nslots = 0;         // perfect-hash buckets / slots
+  const uint64_t* slots = nullptr;     // [nslots]
+  const uint16_t* disp = nullptr;      // [nb]
+  const uint32_t* pidx = nullptr;      // [nslots] (unpacked only)
   const uint32_t* ostart = nullptr;
 };
 
@@ -68,11 +69,12 @@ struct RouteCtx {
 };
 
 void make_route_params(uint64_t cap, RouteParams& rp);
-void build_cuckoo_prefix(const std::vector<uint64_t>& keys, std::vector<uint64_t>& slots,
-                         std::vector<uint32_t>& slot_p, uint32_t& nbk);
+void build_prefix_mphf(const std::vector<uint64_t>& keys, std::vector<uint32_t>& slot_of_key,
+                       std::vector<uint16_t>& disp, uint32_t& nb, uint32_t& nslots);
+// stage 1: count + scan (owner function only); stage 2: scatter + consume.
 template <typename CT>
-void route_count_once(RouteCtx& x, const DevCorpus& c, int kind, uint32_t L, const RouteParams& rp,
-                      CT* table, int num_sms, cudaStream_t st);
+void route_count_once(int stage, RouteCtx& x, const DevCorpus& c, int kind, uint32_t L,
+                      const RouteParams& rp, CT* table, int num_sms, cudaStream_t st);
 
 // --- selection (select_kernels.cu)
 struct SelState {

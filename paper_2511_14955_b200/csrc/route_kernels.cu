@@ -27,14 +27,14 @@
 //                       a warp-private smem bitmap, counts first occurrences in
 //                       smem u16 counters; the CTA flushes nonzero counters with
 //                       coalesced REDs.
-// Extension prefixes live in a host-built bucketized cuckoo table (2 buckets x
-// 4 slots of (key << 24 | p)): a lookup is two 32-byte loads and eight
-// compares with no divergence.
+// Extension prefixes live in a host-built CHD perfect-hash table: a lookup is
+// one 16-bit displacement load and one 8-byte slot load, with no divergence.
 #include <cub/cub.cuh>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 #include <vector>
 
@@ -74,35 +74,35 @@ __device__ __forceinline__ uint64_t gmask() {
   else return (1ull << (8 * L)) - 1;
 }
 
-__device__ __forceinline__ uint32_t ck_bucket(uint64_t key, uint64_t mul, uint32_t nbk) {
-  return (uint32_t)((((key * mul) >> 32) & 0xffffffffull) * (uint64_t)nbk >> 32);
+// CHD perfect-hash prefix set (host-built): bucket b = hash1(key) of nb,
+// slot = range(s + d[b] * t) of nslots with (s, t) = hash2(key); every survivor
+// owns exactly one slot.  Packed slots hold (key << 24) | v (prefixes of <= 5
+// bytes; empty = ~0), unpacked slots hold the key and v lives in pidx[slot].
+// A lookup is one u16 and one u64 shared-memory load: no probing, no divergence.
+// Returns v = (owner << 6 | index of the prefix in its owner) or 0xffffffff.
+__host__ __device__ __forceinline__ uint32_t mphf_slot(uint64_t key, uint32_t nb,
+                                                       uint32_t nslots, const uint16_t* disp,
+                                                       uint32_t* bucket_out) {
+  const uint64_t x = key * kCuckooMul1;
+  const uint32_t b = (uint32_t)(((x >> 32) * (uint64_t)nb) >> 32);
+  if (bucket_out) *bucket_out = b;
+  const uint64_t y = key * kCuckooMul2;
+  const uint32_t d = disp ? disp[b] : 0u;
+  const uint32_t h = (uint32_t)(y >> 32) + d * ((uint32_t)y | 1u);
+  return (uint32_t)(((uint64_t)h * nslots) >> 32);
 }
 
-// Bucketized cuckoo prefix set (2 buckets x 4 slots).  Packed slots hold
-// (key << 24) | p (prefixes of <= 5 bytes); empty = ~0.  Unpacked slots hold the
-// key and p lives in pidx[slot].  Returns p or 0xffffffff.
 template <bool PACKED>
-__device__ __forceinline__ uint32_t cuckoo_lookup(const uint64_t* slots, const uint32_t* pidx,
-                                                  uint32_t nbk, uint64_t key) {
-  const uint32_t b1 = ck_bucket(key, kCuckooMul1, nbk);
-  const uint32_t b2 = ck_bucket(key, kCuckooMul2, nbk);
-  const ulonglong2* p1 = reinterpret_cast<const ulonglong2*>(slots + 4 * (size_t)b1);
-  const ulonglong2* p2 = reinterpret_cast<const ulonglong2*>(slots + 4 * (size_t)b2);
-  const ulonglong2 a0 = p1[0], a1 = p1[1], c0 = p2[0], c1 = p2[1];
-  const uint64_t e[8] = {a0.x, a0.y, a1.x, a1.y, c0.x, c0.y, c1.x, c1.y};
+__device__ __forceinline__ uint32_t prefix_lookup_v(const uint64_t* slots, const uint16_t* disp,
+                                                    const uint32_t* pidx, uint32_t nb,
+                                                    uint32_t nslots, uint64_t key) {
+  const uint32_t sl = mphf_slot(key, nb, nslots, disp, nullptr);
+  const uint64_t e = slots[sl];
   if constexpr (PACKED) {
-    const uint64_t kk = key << 24;
-    uint32_t best = 0xffffffu;
-#pragma unroll
-    for (int i = 0; i < 8; ++i)
-      if ((e[i] & 0xffffffffff000000ull) == kk) best = min(best, (uint32_t)e[i] & 0xffffffu);
-    return best == 0xffffffu ? 0xffffffffu : best;
+    const uint32_t v = (uint32_t)e & 0xffffffu;
+    return ((e >> 24) == key && v != 0xffffffu) ? v : 0xffffffffu;
   } else {
-    uint32_t r = 0xffffffffu;
-#pragma unroll
-    for (int i = 0; i < 8; ++i)
-      if (e[i] == key) r = (i < 4 ? 4 * b1 : 4 * b2) + (i & 3);
-    return r == 0xffffffffu ? r : __ldg(pidx + r);
+    return e == key ? __ldg(pidx + sl) : 0xffffffffu;
   }
 }
 
@@ -159,29 +159,35 @@ __device__ __forceinline__ uint32_t count_owner(const uint32_t (&W)[7], const Ro
 }
 
 // Scatter pass: (owner << 16 | local) of a gram key, or ~0 (prefix miss).
+// Extension: the slot value is (owner << 6 | index of the prefix inside its
+// owner), so local = value_lo6 * 256 + last byte with no second lookup.
 template <int KIND, bool PACKED>
 __device__ __forceinline__ uint32_t scatter_route(uint64_t key, const RouteParams& rp,
-                                                  const uint64_t* slots) {
+                                                  const uint64_t* slots, const uint16_t* disp) {
   if constexpr (KIND == 0) {
     return dense_route(key, rp);
   } else {
-    const uint64_t pk = key >> 8;
-    const uint32_t p = cuckoo_lookup<PACKED>(slots, rp.pidx, rp.nbk, pk);
-    if (p == 0xffffffffu) return 0xffffffffu;
-    const uint32_t o = prefix_owner_hash(pk, rp.lgno);
-    return (o << 16) | ((p - __ldg(rp.ostart + o)) * 256 + (uint32_t)(key & 0xff));
+    const uint32_t v =
+        prefix_lookup_v<PACKED>(slots, disp, rp.pidx, rp.nb, rp.nslots, key >> 8);
+    if (v == 0xffffffffu) return 0xffffffffu;
+    return ((v >> 6) << 16) | ((v & 63u) * 256 + (uint32_t)(key & 0xff));
   }
 }
 
+// Stages the perfect-hash prefix set (slots, then displacements) in smem
+// (TAB == 1) or points at global memory.
 template <int TAB>
-__device__ __forceinline__ const uint64_t* stage_table(const RouteParams& rp, uint64_t* s_slots) {
+__device__ __forceinline__ const uint64_t* stage_table(const RouteParams& rp, uint64_t* s_slots,
+                                                       const uint16_t*& disp) {
   if constexpr (TAB == 1) {
-    const uint32_t n = 4 * rp.nbk;
-    for (uint32_t i = threadIdx.x; i < n / 2; i += blockDim.x)
-      reinterpret_cast<ulonglong2*>(s_slots)[i] = reinterpret_cast<const ulonglong2*>(rp.slots)[i];
+    for (uint32_t i = threadIdx.x; i < rp.nslots; i += blockDim.x) s_slots[i] = rp.slots[i];
+    uint16_t* s_disp = reinterpret_cast<uint16_t*>(s_slots + rp.nslots);
+    for (uint32_t i = threadIdx.x; i < rp.nb; i += blockDim.x) s_disp[i] = rp.disp[i];
     __syncthreads();
+    disp = s_disp;
     return s_slots;
   } else {
+    disp = rp.disp;
     return rp.slots;
   }
 }
@@ -253,7 +259,8 @@ __global__ void __launch_bounds__(kScatterThreads) k_route_scatter(
   __shared__ uint32_t s_total;
   using BlockScan = cub::BlockScan<uint32_t, kScatterThreads>;
   __shared__ typename BlockScan::TempStorage scan_tmp;
-  const uint64_t* slots = stage_table<TAB == 1 ? 1 : 2>(rp, s_slots);
+  const uint16_t* disp = nullptr;
+  const uint64_t* slots = KIND == 1 ? stage_table<TAB == 1 ? 1 : 2>(rp, s_slots, disp) : nullptr;
   const int lane = threadIdx.x & 31;
   for (uint32_t u = blockIdx.x; u < uv.nunits; u += gridDim.x) {
     const RouteUnit U = uv.units[u];
@@ -280,10 +287,11 @@ __global__ void __launch_bounds__(kScatterThreads) k_route_scatter(
           const uint64_t key = key8<T>(W) & gmask<L>();
           // a gram already routed from this chunk adds nothing (count-once):
           // drop it before the prefix lookup.  Races only cost a duplicate.
-          const uint32_t slot = (uint32_t)((key * 0x9E3779B97F4A7C15ull) >> (64 - 11));
+          const uint32_t slot =
+              (((uint32_t)key ^ ((uint32_t)(key >> 32) * 0x85EBCA6Bu)) * 0x9E3779B1u) >> (32 - 11);
           if (key == ~0ull || cache[slot] != key) {  // ~0 is the empty marker
             cache[slot] = key;
-            v = scatter_route<KIND, PACKED>(key, rp, slots);
+            v = scatter_route<KIND, PACKED>(key, rp, slots, disp);
             if (v != 0xffffffffu) atomicAdd(lhist + (v >> 16), 1u);
           }
         }
@@ -407,38 +415,45 @@ __global__ void __launch_bounds__(kConsumeThreads) k_consume_once(
 
 // ------------------------------------------------------------------ host
 
-static size_t table_bytes(const RouteParams& rp) { return (size_t)4 * rp.nbk * 8; }
+static size_t table_bytes(const RouteParams& rp) {
+  return align16((size_t)rp.nslots * 8 + (size_t)rp.nb * 2);
+}
 
+// Stage 1: count kernel + owner-major scan (needs only the owner function).
+template <int KIND, int L>
+static void route_stage1_t(RouteCtx& x, const DevCorpus& c, const RouteParams& rp, int num_sms,
+                           cudaStream_t st) {
+  const RouteView uv{x.units, x.unit_first, x.nunits};
+  const size_t ncnt = (size_t)rp.NO * x.nunits + 1;
+  uint32_t* cnt = x.cnt.as<uint32_t>(ncnt);
+  x.actual.as<uint32_t>(ncnt);
+  unsigned long long* base = x.base.as<unsigned long long>(ncnt);
+  const size_t smem = align16((size_t)rp.NO * 4);
+  auto k = k_route_count<KIND, L>;
+  IGB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per = 0;
+  IGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, kRouteThreads, smem));
+  if (per < 1) throw Error(IG_EINTERNAL, "route count does not fit in shared memory");
+  const unsigned grid = (unsigned)std::min<uint64_t>(x.nunits, (uint64_t)num_sms * per);
+  IGB_CUDA(cudaMemsetAsync(cnt + ncnt - 1, 0, 4, st));
+  k<<<grid, kRouteThreads, smem, st>>>(c, uv, rp, cnt);
+  x.launches++;
+  size_t need = 0;
+  IGB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, need, cnt, base, (int64_t)ncnt, st));
+  void* tmp = x.cub_tmp.get(need);
+  IGB_CUDA(cub::DeviceScan::ExclusiveSum(tmp, need, cnt, base, (int64_t)ncnt, st));
+  IGB_CUDA(cudaGetLastError());
+}
+
+// Stage 2: scatter + consume (needs the prefix table for extension passes).
 template <int KIND, int L, int TAB, typename CT>
-static void route_once_t(RouteCtx& x, const DevCorpus& c, const RouteParams& rp, CT* table,
-                         int num_sms, cudaStream_t st) {
+static void route_stage2_t(RouteCtx& x, const DevCorpus& c, const RouteParams& rp, CT* table,
+                           int num_sms, cudaStream_t st) {
   const RouteView uv{x.units, x.unit_first, x.nunits};
   const size_t tab = TAB == 1 ? table_bytes(rp) : 0;
   const size_t ncnt = (size_t)rp.NO * x.nunits + 1;
-  uint32_t* cnt = x.cnt.as<uint32_t>(ncnt);
   uint32_t* act = x.actual.as<uint32_t>(ncnt);
   unsigned long long* base = x.base.as<unsigned long long>(ncnt);
-  // 1. count (upper bounds per owner and unit)
-  {
-    const size_t smem = align16((size_t)rp.NO * 4);
-    auto k = k_route_count<KIND, L>;
-    IGB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int per = 0;
-    IGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, kRouteThreads, smem));
-    if (per < 1) throw Error(IG_EINTERNAL, "route count does not fit in shared memory");
-    const unsigned grid = (unsigned)std::min<uint64_t>(x.nunits, (uint64_t)num_sms * per);
-    IGB_CUDA(cudaMemsetAsync(cnt + ncnt - 1, 0, 4, st));
-    k<<<grid, kRouteThreads, smem, st>>>(c, uv, rp, cnt);
-    x.launches++;
-  }
-  // 2. owner-major exclusive scan -> base
-  {
-    size_t need = 0;
-    IGB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, need, cnt, base, (int64_t)ncnt, st));
-    void* tmp = x.cub_tmp.get(need);
-    IGB_CUDA(cub::DeviceScan::ExclusiveSum(tmp, need, cnt, base, (int64_t)ncnt, st));
-  }
-  // 3. scatter
   uint16_t* ent = x.entries.as<uint16_t>(c.total + 64);
   {
     const size_t smem = (size_t)kSChunk * 4 + (size_t)kDedupSlots * 8 + align16((size_t)rp.NO * 8) +
@@ -452,7 +467,6 @@ static void route_once_t(RouteCtx& x, const DevCorpus& c, const RouteParams& rp,
     k<<<grid, kScatterThreads, smem, st>>>(c, uv, rp, base, act, ent);
     x.launches++;
   }
-  // 4. consume
   {
     const uint32_t ipo = 1u << rp.lgl;
     const uint32_t bmw4 = ((ipo + 31) / 32 + 3) & ~3u;
@@ -481,94 +495,124 @@ static void route_once_t(RouteCtx& x, const DevCorpus& c, const RouteParams& rp,
 }
 
 template <int KIND, int L, typename CT>
-static void route_once_l(RouteCtx& x, const DevCorpus& c, const RouteParams& rp, CT* table,
-                         int num_sms, cudaStream_t st) {
-  if constexpr (KIND == 0) {
-    route_once_t<0, L, 0, CT>(x, c, rp, table, num_sms, st);
+static void route_stage_l(int stage, RouteCtx& x, const DevCorpus& c, const RouteParams& rp,
+                          CT* table, int num_sms, cudaStream_t st) {
+  if (stage == 1) {
+    route_stage1_t<KIND, L>(x, c, rp, num_sms, st);
+  } else if constexpr (KIND == 0) {
+    route_stage2_t<0, L, 0, CT>(x, c, rp, table, num_sms, st);
   } else {
     const size_t scatter_fixed = (size_t)kSChunk * 4 + (size_t)kDedupSlots * 8 +
                                  (size_t)rp.NO * 16 + 256 + 4 * 1024;  // + static smem
-    if (!rp.packed) route_once_t<1, L, 3, CT>(x, c, rp, table, num_sms, st);
-    else if (scatter_fixed + table_bytes(rp) <= kMaxOnceSmem)
-      route_once_t<1, L, 1, CT>(x, c, rp, table, num_sms, st);
+    static const bool force_global = getenv("IG_SCATTER_TABLE_GLOBAL") != nullptr;
+    if (!rp.packed) route_stage2_t<1, L, 3, CT>(x, c, rp, table, num_sms, st);
+    else if (!force_global && scatter_fixed + table_bytes(rp) <= kMaxOnceSmem)
+      route_stage2_t<1, L, 1, CT>(x, c, rp, table, num_sms, st);
     else
-      route_once_t<1, L, 2, CT>(x, c, rp, table, num_sms, st);
+      route_stage2_t<1, L, 2, CT>(x, c, rp, table, num_sms, st);
   }
 }
 
 template <typename CT>
-void route_count_once(RouteCtx& x, const DevCorpus& c, int kind, uint32_t L, const RouteParams& rp,
-                      CT* table, int num_sms, cudaStream_t st) {
+void route_count_once(int stage, RouteCtx& x, const DevCorpus& c, int kind, uint32_t L,
+                      const RouteParams& rp, CT* table, int num_sms, cudaStream_t st) {
   if (!c.m || !x.nunits) return;
   if (kind == 0) {
     switch (L) {
-      case 1: route_once_l<0, 1, CT>(x, c, rp, table, num_sms, st); break;
-      case 2: route_once_l<0, 2, CT>(x, c, rp, table, num_sms, st); break;
-      default: route_once_l<0, 3, CT>(x, c, rp, table, num_sms, st); break;
+      case 1: route_stage_l<0, 1, CT>(stage, x, c, rp, table, num_sms, st); break;
+      case 2: route_stage_l<0, 2, CT>(stage, x, c, rp, table, num_sms, st); break;
+      default: route_stage_l<0, 3, CT>(stage, x, c, rp, table, num_sms, st); break;
     }
   } else {
     switch (L) {
-      case 2: route_once_l<1, 2, CT>(x, c, rp, table, num_sms, st); break;
-      case 3: route_once_l<1, 3, CT>(x, c, rp, table, num_sms, st); break;
-      case 4: route_once_l<1, 4, CT>(x, c, rp, table, num_sms, st); break;
-      case 5: route_once_l<1, 5, CT>(x, c, rp, table, num_sms, st); break;
-      case 6: route_once_l<1, 6, CT>(x, c, rp, table, num_sms, st); break;
-      case 7: route_once_l<1, 7, CT>(x, c, rp, table, num_sms, st); break;
-      case 8: route_once_l<1, 8, CT>(x, c, rp, table, num_sms, st); break;
+      case 2: route_stage_l<1, 2, CT>(stage, x, c, rp, table, num_sms, st); break;
+      case 3: route_stage_l<1, 3, CT>(stage, x, c, rp, table, num_sms, st); break;
+      case 4: route_stage_l<1, 4, CT>(stage, x, c, rp, table, num_sms, st); break;
+      case 5: route_stage_l<1, 5, CT>(stage, x, c, rp, table, num_sms, st); break;
+      case 6: route_stage_l<1, 6, CT>(stage, x, c, rp, table, num_sms, st); break;
+      case 7: route_stage_l<1, 7, CT>(stage, x, c, rp, table, num_sms, st); break;
+      case 8: route_stage_l<1, 8, CT>(stage, x, c, rp, table, num_sms, st); break;
       default: throw Error(IG_ECONFIG, "gram length above 8 is not supported");
     }
   }
 }
 
-template void route_count_once<uint32_t>(RouteCtx&, const DevCorpus&, int, uint32_t,
+template void route_count_once<uint32_t>(int, RouteCtx&, const DevCorpus&, int, uint32_t,
                                          const RouteParams&, uint32_t*, int, cudaStream_t);
-template void route_count_once<unsigned long long>(RouteCtx&, const DevCorpus&, int, uint32_t,
+template void route_count_once<unsigned long long>(int, RouteCtx&, const DevCorpus&, int, uint32_t,
                                                    const RouteParams&, unsigned long long*, int,
                                                    cudaStream_t);
 
 // ------------------------------------------------------------------ prefix set (host)
 
-static uint32_t host_bucket(uint64_t key, uint64_t mul, uint32_t nbk) {
-  return (uint32_t)((((key * mul) >> 32) & 0xffffffffull) * (uint64_t)nbk >> 32);
-}
-
-// Bucketized cuckoo insertion (deterministic random walk).  False on failure.
-static bool cuckoo_try(const std::vector<uint64_t>& keys, uint32_t nbk, std::vector<uint64_t>& slots,
-                       std::vector<uint32_t>& slot_rank) {
-  slots.assign((size_t)4 * nbk, kEmptyKey);
-  slot_rank.assign((size_t)4 * nbk, 0xffffffffu);
-  uint64_t rng = 0x853c49e6748fea9bull;
-  for (uint32_t r = 0; r < keys.size(); ++r) {
-    uint64_t cur = keys[r];
-    uint32_t cur_rank = r;
-    bool placed = false;
-    for (int kick = 0; kick < 2000 && !placed; ++kick) {
-      const uint32_t b[2] = {host_bucket(cur, kCuckooMul1, nbk), host_bucket(cur, kCuckooMul2, nbk)};
-      for (int t = 0; t < 2 && !placed; ++t)
-        for (int i = 0; i < 4; ++i)
-          if (slots[4 * (size_t)b[t] + i] == kEmptyKey) {
-            slots[4 * (size_t)b[t] + i] = cur;
-            slot_rank[4 * (size_t)b[t] + i] = cur_rank;
-            placed = true;
-            break;
-          }
-      if (placed) break;
-      rng ^= rng << 13;
-      rng ^= rng >> 7;
-      rng ^= rng << 17;
-      const size_t s = 4 * (size_t)b[rng & 1] + ((rng >> 1) & 3);
-      std::swap(cur, slots[s]);
-      std::swap(cur_rank, slot_rank[s]);
+// CHD construction: buckets by decreasing size, each takes the first
+// displacement that sends all its keys to free slots.  Per-key hashes are
+// computed once; buckets are a counting sort.  False on failure.
+static bool mphf_try(const std::vector<uint64_t>& keys, uint32_t nb, uint32_t nslots,
+                     std::vector<uint16_t>& disp, std::vector<uint32_t>& slot_of_key) {
+  const uint32_t K = (uint32_t)keys.size();
+  std::vector<uint32_t> kb(K), ks(K), kt(K), boff(nb + 1, 0), idx(K);
+  for (uint32_t i = 0; i < K; ++i) {
+    const uint64_t x = keys[i] * kCuckooMul1, y = keys[i] * kCuckooMul2;
+    kb[i] = (uint32_t)(((x >> 32) * (uint64_t)nb) >> 32);
+    ks[i] = (uint32_t)(y >> 32);
+    kt[i] = (uint32_t)y | 1u;
+    ++boff[kb[i] + 1];
+  }
+  uint32_t maxsz = 0;
+  for (uint32_t b = 0; b < nb; ++b) {
+    maxsz = std::max(maxsz, boff[b + 1]);
+    boff[b + 1] += boff[b];
+  }
+  {
+    std::vector<uint32_t> cur(boff.begin(), boff.end() - 1);
+    for (uint32_t i = 0; i < K; ++i) idx[cur[kb[i]]++] = i;
+  }
+  // buckets ordered by decreasing size (counting sort on size)
+  std::vector<uint32_t> szoff(maxsz + 2, 0), order(nb);
+  for (uint32_t b = 0; b < nb; ++b) ++szoff[maxsz - (boff[b + 1] - boff[b]) + 1];
+  for (uint32_t z = 0; z <= maxsz; ++z) szoff[z + 1] += szoff[z];
+  for (uint32_t b = 0; b < nb; ++b) order[szoff[maxsz - (boff[b + 1] - boff[b])]++] = b;
+  std::vector<uint8_t> used(nslots, 0);
+  disp.assign(nb, 0);
+  slot_of_key.assign(K, 0);
+  uint32_t cand[64];
+  for (uint32_t b : order) {
+    const uint32_t a0 = boff[b], n = boff[b + 1] - a0;
+    if (n == 0) break;
+    if (n > 64) return false;
+    bool ok = false;
+    for (uint32_t d = 0; d < 65536 && !ok; ++d) {
+      ok = true;
+      for (uint32_t t = 0; t < n && ok; ++t) {
+        const uint32_t i = idx[a0 + t];
+        const uint32_t h = ks[i] + d * kt[i];
+        const uint32_t sl = (uint32_t)(((uint64_t)h * nslots) >> 32);
+        if (used[sl]) ok = false;
+        for (uint32_t u = 0; u < t && ok; ++u)
+          if (cand[u] == sl) ok = false;
+        cand[t] = sl;
+      }
+      if (ok) disp[b] = (uint16_t)d;
     }
-    if (!placed) return false;
+    if (!ok) return false;
+    for (uint32_t t = 0; t < n; ++t) {
+      used[cand[t]] = 1;
+      slot_of_key[idx[a0 + t]] = cand[t];
+    }
   }
   return true;
 }
 
-void build_cuckoo_prefix(const std::vector<uint64_t>& keys, std::vector<uint64_t>& slots,
-                         std::vector<uint32_t>& slot_p, uint32_t& nbk) {
-  nbk = (uint32_t)std::max<uint64_t>(1, (keys.size() * 10 + 35) / 36);  // ~90% load
-  while (!cuckoo_try(keys, nbk, slots, slot_p)) nbk = nbk + nbk / 10 + 1;
+void build_prefix_mphf(const std::vector<uint64_t>& keys, std::vector<uint32_t>& slot_of_key,
+                       std::vector<uint16_t>& disp, uint32_t& nb, uint32_t& nslots) {
+  const uint64_t K = keys.size();
+  nb = (uint32_t)std::max<uint64_t>(1, (K + 2) / 3);
+  nslots = (uint32_t)std::max<uint64_t>(1, K + K / 8 + 1);  // ~89% load
+  while (!mphf_try(keys, nb, nslots, disp, slot_of_key)) {
+    nslots += nslots / 20 + 1;
+    nb += nb / 10 + 1;
+  }
 }
 
 // Host: the permuted id space of a candidate space of `cap` ids.

@@ -335,10 +335,13 @@ static void allreduce(Session& s, void* buf, uint64_t count, int dtype) {
 struct Prefix {
   DevPrefixSet ps;
   RouteParams rp;
-  bool csr = false;  // cuckoo prefix set (count-once)
+  bool csr = false;  // perfect-hash prefix set (count-once)
   uint64_t K = 0;
   std::vector<uint32_t> rank_of_p;  // count-once: p -> survivor rank
   const uint64_t* pkeys = nullptr;   // count-once: keys by p
+  std::vector<uint64_t> pk;          // count-once: host keys by p
+  std::vector<uint32_t> ostart;      // count-once: host owner ranges
+  uint32_t plen = 0;
 };
 
 static Prefix prepare_prefix(Session& s, const uint64_t* keys, uint64_t K, uint32_t plen,
@@ -348,7 +351,7 @@ static Prefix prepare_prefix(Session& s, const uint64_t* keys, uint64_t K, uint3
   if (!K) return P;
   if (mode == IG_MODE_ONCE) {
     // count-once routing: owners = hash(prefix) with <= 64 prefixes each,
-    // prefixes numbered owner by owner (stable by rank), bucketized cuckoo set
+    // prefixes numbered owner by owner (stable by rank), CHD perfect-hash set
     std::vector<uint64_t> hk(K);
     IGB_CUDA(cudaMemcpyAsync(hk.data(), keys, K * 8, cudaMemcpyDeviceToHost, s.stream));
     IGB_CUDA(cudaStreamSynchronize(s.stream));
@@ -374,32 +377,18 @@ static Prefix prepare_prefix(Session& s, const uint64_t* keys, uint64_t K, uint3
       pk[pp] = hk[i];
       P.rank_of_p[pp] = (uint32_t)i;
     }
-    std::vector<uint64_t> slots;
-    std::vector<uint32_t> slot_p;
-    uint32_t nbk = 0;
-    build_cuckoo_prefix(pk, slots, slot_p, nbk);
-    const bool packed = 8 * plen + 24 <= 64 && K < 0xffffffull;
-    if (packed)
-      for (size_t i = 0; i < slots.size(); ++i)
-        if (slots[i] != kEmptyKey) slots[i] = (slots[i] << 24) | slot_p[i];
     uint64_t* dpk = s.pkeys.as<uint64_t>(K + 1);
-    uint64_t* ds = s.hkeys.as<uint64_t>(slots.size() + 2);
-    uint32_t* dpi = s.hidx.as<uint32_t>(slot_p.size() + 2);
     uint32_t* dos = s.owner_start.as<uint32_t>(NO + 1);
     IGB_CUDA(cudaMemcpyAsync(dpk, pk.data(), K * 8, cudaMemcpyHostToDevice, s.stream));
-    IGB_CUDA(cudaMemcpyAsync(ds, slots.data(), slots.size() * 8, cudaMemcpyHostToDevice, s.stream));
-    IGB_CUDA(cudaMemcpyAsync(dpi, slot_p.data(), slot_p.size() * 4, cudaMemcpyHostToDevice,
-                             s.stream));
     IGB_CUDA(cudaMemcpyAsync(dos, ostart.data(), (NO + 1) * 4, cudaMemcpyHostToDevice, s.stream));
+    P.pk = std::move(pk);
+    P.ostart = std::move(ostart);
+    P.plen = plen;
     RouteParams& rp = P.rp;
     rp.ext = true;
-    rp.packed = packed;
     rp.lgno = lgno;
     rp.NO = NO;
     rp.lgl = 14;  // kPrefixesPerOwner * 256 ids per owner
-    rp.nbk = nbk;
-    rp.slots = ds;
-    rp.pidx = dpi;
     rp.ostart = dos;
     rp.minv = 0;  // table index = p * 256 + last byte
     P.pkeys = dpk;
@@ -408,6 +397,49 @@ static Prefix prepare_prefix(Session& s, const uint64_t* keys, uint64_t K, uint3
     P.ps = build_prefix_set(s, keys, K, plen, mode);
   }
   return P;
+}
+
+// The perfect-hash table of a count-once prefix set (host build + upload).  Run
+// while the pass's count kernel (which needs only the owner function) is in
+// flight.
+static void build_prefix_table(Session& s, Prefix& P) {
+  const uint64_t K = P.K;
+  const uint32_t lgno = P.rp.lgno;
+  auto owner_of = [](uint64_t key, uint32_t lg) -> uint32_t {
+    return lg ? (uint32_t)((key * kOwnerMul) >> (64 - lg)) : 0u;
+  };
+  const std::vector<uint64_t>& pk = P.pk;
+  const std::vector<uint32_t>& ostart = P.ostart;
+  // perfect-hash slots; slot value: owner << 6 | index of the prefix in its owner
+  std::vector<uint32_t> slot_of_key;
+  std::vector<uint16_t> disp;
+  uint32_t nb = 0, nslots = 0;
+  build_prefix_mphf(pk, slot_of_key, disp, nb, nslots);
+  std::vector<uint64_t> slots(nslots, kEmptyKey);
+  std::vector<uint32_t> slot_v(nslots, 0xffffffu);
+  for (uint64_t pp = 0; pp < K; ++pp) {
+    const uint32_t o = owner_of(pk[pp], lgno);
+    slots[slot_of_key[pp]] = pk[pp];
+    slot_v[slot_of_key[pp]] = (o << 6) | (uint32_t)(pp - ostart[o]);
+  }
+  const bool packed = 8 * P.plen + 24 <= 64 && lgno <= 17;
+  if (packed)
+    for (size_t i = 0; i < slots.size(); ++i)
+      if (slots[i] != kEmptyKey) slots[i] = (slots[i] << 24) | slot_v[i];
+  uint64_t* ds = s.hkeys.as<uint64_t>(slots.size() + 2);
+  uint32_t* dpi = s.hidx.as<uint32_t>(slot_v.size() + 2);
+  uint16_t* ddisp = s.hpacked.as<uint16_t>(disp.size() + 8);
+  IGB_CUDA(cudaMemcpyAsync(ds, slots.data(), slots.size() * 8, cudaMemcpyHostToDevice, s.stream));
+  IGB_CUDA(cudaMemcpyAsync(dpi, slot_v.data(), slot_v.size() * 4, cudaMemcpyHostToDevice,
+                           s.stream));
+  IGB_CUDA(cudaMemcpyAsync(ddisp, disp.data(), disp.size() * 2, cudaMemcpyHostToDevice, s.stream));
+  IGB_CUDA(cudaStreamSynchronize(s.stream));  // host vectors die here
+  P.rp.packed = packed;
+  P.rp.nb = nb;
+  P.rp.nslots = nslots;
+  P.rp.slots = ds;
+  P.rp.disp = ddisp;
+  P.rp.pidx = dpi;
 }
 
 // One counting pass.  Returns the device table (tcap entries) and how table
@@ -423,7 +455,12 @@ static CT* count_pass(Session& s, bool dense, uint32_t L, int mode, const Prefix
     CT* t = s.table.as<CT>(tcap);
     IGB_CUDA(cudaMemsetAsync(t, 0, tcap * sizeof(CT), s.stream));
     const uint64_t l0 = s.rc.launches;
-    route_count_once<CT>(s.rc, s.dc, dense ? 0 : 1, L, rp, t, s.num_sms, s.stream);
+    route_count_once<CT>(1, s.rc, s.dc, dense ? 0 : 1, L, rp, t, s.num_sms, s.stream);
+    if (!dense) {  // the host table build overlaps the count kernel
+      build_prefix_table(s, *const_cast<Prefix*>(P));
+      rp = P->rp;
+    }
+    route_count_once<CT>(2, s.rc, s.dc, dense ? 0 : 1, L, rp, t, s.num_sms, s.stream);
     s.launches += s.rc.launches - l0;
     km = KeyMap{};
     if (dense) {
@@ -772,7 +809,7 @@ int ig_extend_pass(const ig_corpus* corpus, const uint64_t* prefix_keys, uint64_
       // back to the reference layout: ordinal (rank) * 256 + last byte (candidate_id)
       memset(table_out, 0, nprefix * 256 * 8);
       for (uint64_t p = 0; p < rank.size(); ++p) {
-        if (rank[p] == 0xffffffffu) continue;  // empty cuckoo slot
+        if (rank[p] == 0xffffffffu) continue;  // no prefix at this p
         for (uint64_t b = 0; b < 256; ++b) {
           const uint64_t id = p * 256 + b;
           table_out[(uint64_t)rank[p] * 256 + b] = tab[km.minv ? ((id * mult) & km.cmask) : id];
