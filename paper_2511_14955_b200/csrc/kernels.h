@@ -51,6 +51,7 @@ struct RouteParams {
   // extension passes: owner = hash(prefix) >> (64-lgno); p numbered owner by
   // owner (ostart[o] .. ostart[o+1]); CHD perfect-hash prefix set
   bool ext = false;
+  bool dedup = true;    // scatter drops repeats inside a chunk (optimisation only)
   bool packed = false;  // slots = (key << 24) | p, else slots = key and pidx[slot] = p
   uint32_t lgno = 0;
   uint32_t nb = 0, nslots = 0;         // perfect-hash buckets / slots

@@ -113,7 +113,7 @@ __device__ __forceinline__ uint32_t prefix_owner_hash(uint64_t pkey, uint32_t lg
 
 constexpr int kRouteThreads = 1024;
 constexpr int kChunk = kRouteThreads * 16;  // positions per scatter chunk
-constexpr int kDedupSlots = 2048;
+constexpr int kDedupSlots = 4096;
 
 // The 16-byte segment at b0 plus its 8-byte halo (full warp, consecutive lanes).
 __device__ __forceinline__ void seg_load(const uint8_t* __restrict__ data, int64_t b0, int lane,
@@ -261,6 +261,7 @@ __global__ void __launch_bounds__(kScatterThreads) k_route_scatter(
   __shared__ typename BlockScan::TempStorage scan_tmp;
   const uint16_t* disp = nullptr;
   const uint64_t* slots = KIND == 1 ? stage_table<TAB == 1 ? 1 : 2>(rp, s_slots, disp) : nullptr;
+  const bool dedup = rp.dedup;
   const int lane = threadIdx.x & 31;
   for (uint32_t u = blockIdx.x; u < uv.nunits; u += gridDim.x) {
     const RouteUnit U = uv.units[u];
@@ -270,9 +271,11 @@ __global__ void __launch_bounds__(kScatterThreads) k_route_scatter(
     const int64_t lo = max((int64_t)U.b0, s0 + L - 1), hi = (int64_t)U.b1;
     const int64_t first = (int64_t)U.b0 & ~int64_t(15);
     const int64_t nseg = (hi - first + 15) >> 4;
+    // the dedup cache lives for the whole unit: every chunk of a unit belongs to
+    // the same sequence, so a gram seen anywhere earlier in it adds nothing
+    for (uint32_t i = threadIdx.x; i < kDedupSlots; i += blockDim.x) cache[i] = ~0ull;
     for (int64_t cs = 0; cs < nseg; cs += kScatterThreads) {
       for (uint32_t i = threadIdx.x; i < rp.NO; i += blockDim.x) lhist[i] = 0;
-      for (uint32_t i = threadIdx.x; i < kDedupSlots; i += blockDim.x) cache[i] = ~0ull;
       __syncthreads();
       const int64_t sgi = cs + threadIdx.x;
       const int64_t b0 = first + sgi * 16;
@@ -288,8 +291,8 @@ __global__ void __launch_bounds__(kScatterThreads) k_route_scatter(
           // a gram already routed from this chunk adds nothing (count-once):
           // drop it before the prefix lookup.  Races only cost a duplicate.
           const uint32_t slot =
-              (((uint32_t)key ^ ((uint32_t)(key >> 32) * 0x85EBCA6Bu)) * 0x9E3779B1u) >> (32 - 11);
-          if (key == ~0ull || cache[slot] != key) {  // ~0 is the empty marker
+              (((uint32_t)key ^ ((uint32_t)(key >> 32) * 0x85EBCA6Bu)) * 0x9E3779B1u) >> (32 - 12);
+          if (!dedup || key == ~0ull || cache[slot] != key) {  // ~0 is the empty marker
             cache[slot] = key;
             v = scatter_route<KIND, PACKED>(key, rp, slots, disp);
             if (v != 0xffffffffu) atomicAdd(lhist + (v >> 16), 1u);
@@ -504,9 +507,12 @@ static void route_stage_l(int stage, RouteCtx& x, const DevCorpus& c, const Rout
   } else {
     const size_t scatter_fixed = (size_t)kSChunk * 4 + (size_t)kDedupSlots * 8 +
                                  (size_t)rp.NO * 16 + 256 + 4 * 1024;  // + static smem
-    static const bool force_global = getenv("IG_SCATTER_TABLE_GLOBAL") != nullptr;
+    // the table is L1-cached from global memory by default (more CTAs per SM
+    // measured faster than staging it in shared memory); IG_SCATTER_TABLE_SMEM=1
+    // stages it when it fits
+    static const bool force_smem = getenv("IG_SCATTER_TABLE_SMEM") != nullptr;
     if (!rp.packed) route_stage2_t<1, L, 3, CT>(x, c, rp, table, num_sms, st);
-    else if (!force_global && scatter_fixed + table_bytes(rp) <= kMaxOnceSmem)
+    else if (force_smem && scatter_fixed + table_bytes(rp) <= kMaxOnceSmem)
       route_stage2_t<1, L, 1, CT>(x, c, rp, table, num_sms, st);
     else
       route_stage2_t<1, L, 2, CT>(x, c, rp, table, num_sms, st);

@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -451,6 +452,8 @@ static CT* count_pass(Session& s, bool dense, uint32_t L, int mode, const Prefix
     RouteParams rp;
     if (dense) make_route_params(1ull << (8 * L), rp);
     else rp = P->rp;
+    static const char* nd = getenv("IG_NO_DEDUP");  // experiment switch: 1 dense, 2 all
+    if (nd && (nd[0] == '2' || dense)) rp.dedup = false;
     tcap = dense ? (1ull << rp.lgc) : 256 * P->K;
     CT* t = s.table.as<CT>(tcap);
     IGB_CUDA(cudaMemsetAsync(t, 0, tcap * sizeof(CT), s.stream));
@@ -458,7 +461,9 @@ static CT* count_pass(Session& s, bool dense, uint32_t L, int mode, const Prefix
     route_count_once<CT>(1, s.rc, s.dc, dense ? 0 : 1, L, rp, t, s.num_sms, s.stream);
     if (!dense) {  // the host table build overlaps the count kernel
       build_prefix_table(s, *const_cast<Prefix*>(P));
+      const bool dd = rp.dedup;
       rp = P->rp;
+      rp.dedup = dd;
     }
     route_count_once<CT>(2, s.rc, s.dc, dense ? 0 : 1, L, rp, t, s.num_sms, s.stream);
     s.launches += s.rc.launches - l0;
