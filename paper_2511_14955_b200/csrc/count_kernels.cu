@@ -249,78 +249,104 @@ __device__ __noinline__ uint32_t valid_mask_walk(const uint64_t* __restrict__ of
 
 // ------------------------------------------------------------------ count-all
 
-// Flat scan of all 512-byte tiles; one RED per valid gram end (dense) or per
+// Flat scan of all 512-byte tiles; one count per valid gram end (dense) or per
 // prefix hit (extension).  Each warp keeps the next tile's 128-bit loads in
 // flight while it counts the current one.  TAB: 0 none (dense), 1 prefix set
 // staged in shared memory (packed), 2 prefix set read from global/L2.
+//
+// Hot grams: a Zipf corpus sends a few percent of all occurrences to single
+// ids, and one L2 address absorbs only ~0.1 G reductions/s.  Every CTA
+// therefore keeps a direct-mapped shared-memory count cache (kHotSlots ids):
+// the first id to claim a slot owns it for the CTA's lifetime and is counted
+// with shared-memory atomics; everything else is a RED to L2.  The cache is
+// flushed with one RED per claimed slot when the CTA retires.
+constexpr int kHotSlots = 4096;
+constexpr uint32_t kNoId = 0xffffffffu;
+
+template <typename CT>
+__device__ __forceinline__ void count_one(uint32_t id, uint32_t* tag, uint32_t* hcnt,
+                                          CT* __restrict__ table) {
+  const uint32_t h = (id * 0x9E3779B1u) >> (32 - 12);
+  uint32_t t = tag[h];
+  if (t == kNoId) {
+    t = atomicCAS(tag + h, kNoId, id);
+    if (t == kNoId) t = id;
+  }
+  if (t == id) atomicAdd(hcnt + h, 1u);
+  else atomicAdd(table + id, (CT)1);
+}
+
 template <int KIND, int L, typename CT, int TAB, bool AGG>
-__global__ void __launch_bounds__(256) k_count_all(DevCorpus c, DevPrefixSet ps,
+__global__ void __launch_bounds__(512) k_count_all(DevCorpus c, DevPrefixSet ps,
                                                    const uint64_t* __restrict__ packed,
                                                    CT* __restrict__ table) {
   extern __shared__ uint64_t s_tab[];
+  __shared__ uint32_t tag[kHotSlots];
+  __shared__ uint32_t hcnt[kHotSlots];
+  for (uint32_t i = threadIdx.x; i < kHotSlots; i += blockDim.x) {
+    tag[i] = kNoId;
+    hcnt[i] = 0;
+  }
   if constexpr (TAB == 1) {
     for (uint32_t i = threadIdx.x; i < ps.S; i += blockDim.x) s_tab[i] = packed[i];
-    __syncthreads();
   }
+  __syncthreads();
   const int lane = threadIdx.x & 31;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   uint64_t t = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
-  if (t >= c.ntiles) return;
-  uint4 v = __ldcs(reinterpret_cast<const uint4*>(c.data + t * kTileBytes + lane * 16));
-  uint2 h = make_uint2(0, 0);
-  if (lane == 0) h = *reinterpret_cast<const uint2*>(c.data + t * kTileBytes - 8);
-  uint32_t d = __ldg(c.tile_seq + t);
-  for (;;) {
-    const uint64_t tn = t + nwarps;
-    uint4 vn = make_uint4(0, 0, 0, 0);
-    uint2 hn = make_uint2(0, 0);
-    uint32_t dn = 0;
-    if (tn < c.ntiles) {
-      vn = __ldcs(reinterpret_cast<const uint4*>(c.data + tn * kTileBytes + lane * 16));
-      if (lane == 0) hn = *reinterpret_cast<const uint2*>(c.data + tn * kTileBytes - 8);
-      dn = __ldg(c.tile_seq + tn);
-    }
-    Seg s;
-    s.W[2] = v.x;
-    s.W[3] = v.y;
-    s.W[4] = v.z;
-    s.W[5] = v.w;
-    s.W[6] = 0;
-    s.W[0] = __shfl_up_sync(0xffffffffu, v.z, 1);
-    s.W[1] = __shfl_up_sync(0xffffffffu, v.w, 1);
-    if (lane == 0) {
-      s.W[0] = h.x;
-      s.W[1] = h.y;
-    }
-    const int64_t b0 = (int64_t)t * kTileBytes + lane * 16;
-    const uint32_t vm = (d >> 31) ? 0xffffu : valid_mask_walk<L>(c.off, c.m, c.total, d & 0x7fffffffu, b0);
-    static_for<0, 16>([&](auto tc) {
-      constexpr int T = decltype(tc)::value;
-      const bool valid = (vm >> T) & 1u;
-      if constexpr (KIND == 0) {
-        const uint32_t id = valid ? (uint32_t)(key8_at<T>(s) & gram_mask<L>()) : 0xffffffffu;
-        if constexpr (AGG) {
-          const uint32_t peers = __match_any_sync(0xffffffffu, id);
-          if (valid && lane == __ffs(peers) - 1) atomicAdd(table + id, (CT)__popc(peers));
-        } else {
-          if (valid) atomicAdd(table + id, (CT)1);
-        }
-      } else {
-        if (valid) {
-          const uint64_t key = key8_at<T>(s) & gram_mask<L>();
-          uint32_t p;
-          if constexpr (TAB == 1) p = lookup_packed(s_tab, ps.lgS, ps.ib, key >> 8);
-          else p = prefix_lookup(ps.hkeys, ps.hidx, ps.S, ps.lgS, 0, key >> 8);
-          if (p != 0xffffffffu) atomicAdd(table + ((uint64_t)p * 256 + (key & 0xff)), (CT)1);
-        }
+  if (t < c.ntiles) {
+    uint4 v = __ldcs(reinterpret_cast<const uint4*>(c.data + t * kTileBytes + lane * 16));
+    uint2 h = make_uint2(0, 0);
+    if (lane == 0) h = *reinterpret_cast<const uint2*>(c.data + t * kTileBytes - 8);
+    uint32_t d = __ldg(c.tile_seq + t);
+    for (;;) {
+      const uint64_t tn = t + nwarps;
+      uint4 vn = make_uint4(0, 0, 0, 0);
+      uint2 hn = make_uint2(0, 0);
+      uint32_t dn = 0;
+      if (tn < c.ntiles) {
+        vn = __ldcs(reinterpret_cast<const uint4*>(c.data + tn * kTileBytes + lane * 16));
+        if (lane == 0) hn = *reinterpret_cast<const uint2*>(c.data + tn * kTileBytes - 8);
+        dn = __ldg(c.tile_seq + tn);
       }
-    });
-    if (tn >= c.ntiles) break;
-    t = tn;
-    v = vn;
-    h = hn;
-    d = dn;
+      Seg s;
+      s.W[2] = v.x;
+      s.W[3] = v.y;
+      s.W[4] = v.z;
+      s.W[5] = v.w;
+      s.W[6] = 0;
+      s.W[0] = __shfl_up_sync(0xffffffffu, v.z, 1);
+      s.W[1] = __shfl_up_sync(0xffffffffu, v.w, 1);
+      if (lane == 0) {
+        s.W[0] = h.x;
+        s.W[1] = h.y;
+      }
+      const int64_t b0 = (int64_t)t * kTileBytes + lane * 16;
+      const uint32_t vm = (d >> 31) ? 0xffffu : valid_mask_walk<L>(c.off, c.m, c.total, d & 0x7fffffffu, b0);
+      static_for<0, 16>([&](auto tc) {
+        constexpr int T = decltype(tc)::value;
+        if ((vm >> T) & 1u) {
+          const uint64_t key = key8_at<T>(s) & gram_mask<L>();
+          if constexpr (KIND == 0) {
+            count_one<CT>((uint32_t)key, tag, hcnt, table);
+          } else {
+            uint32_t p;
+            if constexpr (TAB == 1) p = lookup_packed(s_tab, ps.lgS, ps.ib, key >> 8);
+            else p = prefix_lookup(ps.hkeys, ps.hidx, ps.S, ps.lgS, 0, key >> 8);
+            if (p != 0xffffffffu) count_one<CT>(p * 256 + (uint32_t)(key & 0xff), tag, hcnt, table);
+          }
+        }
+      });
+      if (tn >= c.ntiles) break;
+      t = tn;
+      v = vn;
+      h = hn;
+      d = dn;
+    }
   }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < kHotSlots; i += blockDim.x)
+    if (tag[i] != kNoId && hcnt[i]) atomicAdd(table + tag[i], (CT)hcnt[i]);
 }
 
 // ------------------------------------------------------------------ count-once
@@ -476,19 +502,22 @@ template <int KIND, int L, typename CT>
 static void launch_all_t(const DevCorpus& c, const DevPrefixSet& ps, CT* table, int num_sms,
                          cudaStream_t st) {
   if (!c.ntiles) return;
-  const int threads = 256;
-  uint64_t want = (c.ntiles * 32 + threads - 1) / threads;
-  const uint64_t cap = (uint64_t)num_sms * 8;  // 8 CTAs (64 warps) per SM, persistent
-  unsigned blocks = (unsigned)(want < cap ? want : cap);
-  if (!blocks) blocks = 1;
+  const int threads = 512;
+  const uint64_t want = (c.ntiles * 32 + threads - 1) / threads;
+  auto go = [&](auto kern, size_t smem, const uint64_t* pk) {
+    IGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per = 0;
+    IGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, threads, smem));
+    const uint64_t cap = (uint64_t)num_sms * (per > 0 ? per : 1);  // persistent
+    unsigned blocks = (unsigned)(want < cap ? want : cap);
+    if (!blocks) blocks = 1;
+    kern<<<blocks, threads, smem, st>>>(c, ps, pk, table);
+  };
   if constexpr (KIND == 0) {
-    k_count_all<0, L, CT, 0, true><<<blocks, threads, 0, st>>>(c, ps, nullptr, table);
+    go(k_count_all<0, L, CT, 0, false>, 0, nullptr);
   } else {
-    if (ps.packed && (size_t)ps.S * 8 <= 48 * 1024) {
-      k_count_all<1, L, CT, 1, false><<<blocks, threads, ps.S * 8, st>>>(c, ps, ps.packed, table);
-    } else {
-      k_count_all<1, L, CT, 2, false><<<blocks, threads, 0, st>>>(c, ps, nullptr, table);
-    }
+    if (ps.packed && (size_t)ps.S * 8 <= 64 * 1024) go(k_count_all<1, L, CT, 1, false>, ps.S * 8, ps.packed);
+    else go(k_count_all<1, L, CT, 2, false>, 0, nullptr);
   }
 }
 
