@@ -30,6 +30,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <type_traits>
 
 #include "ig_internal.cuh"
@@ -293,7 +294,7 @@ __global__ void __launch_bounds__(512) k_count_all(DevCorpus c, DevPrefixSet ps,
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  uint64_t t = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  uint64_t t = c.tile0 + ((blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5);
   if (t < c.ntiles) {
     uint4 v = __ldcs(reinterpret_cast<const uint4*>(c.data + t * kTileBytes + lane * 16));
     uint2 h = make_uint2(0, 0);
@@ -347,6 +348,30 @@ __global__ void __launch_bounds__(512) k_count_all(DevCorpus c, DevPrefixSet ps,
   __syncthreads();
   for (uint32_t i = threadIdx.x; i < kHotSlots; i += blockDim.x)
     if (tag[i] != kNoId && hcnt[i]) atomicAdd(table + tag[i], (CT)hcnt[i]);
+}
+
+// table64[i] += scratch32[i] (count-all segments of < 2^32 positions).
+__global__ void k_widen_add(const uint32_t* __restrict__ src, unsigned long long* __restrict__ dst,
+                            uint64_t n4) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n4;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint4 v = reinterpret_cast<const uint4*>(src)[i];
+    ulonglong2* d = reinterpret_cast<ulonglong2*>(dst) + 2 * i;
+    ulonglong2 a = d[0], b = d[1];
+    a.x += v.x;
+    a.y += v.y;
+    b.x += v.z;
+    b.y += v.w;
+    d[0] = a;
+    d[1] = b;
+  }
+}
+
+void launch_widen_add(const uint32_t* src, unsigned long long* dst, uint64_t n, cudaStream_t st) {
+  const uint64_t n4 = n / 4;  // table capacities are multiples of 256
+  if (!n4) return;
+  const unsigned blocks = (unsigned)std::min<uint64_t>((n4 + 255) / 256, 148 * 16);
+  k_widen_add<<<blocks, 256, 0, st>>>(src, dst, n4);
 }
 
 // ------------------------------------------------------------------ count-once
@@ -501,9 +526,9 @@ __global__ void __launch_bounds__(kOnceThreads) k_count_once(DevCorpus c, DevPre
 template <int KIND, int L, typename CT>
 static void launch_all_t(const DevCorpus& c, const DevPrefixSet& ps, CT* table, int num_sms,
                          cudaStream_t st) {
-  if (!c.ntiles) return;
+  if (c.ntiles <= c.tile0) return;
   const int threads = 512;
-  const uint64_t want = (c.ntiles * 32 + threads - 1) / threads;
+  const uint64_t want = ((c.ntiles - c.tile0) * 32 + threads - 1) / threads;
   auto go = [&](auto kern, size_t smem, const uint64_t* pk) {
     IGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per = 0;

@@ -87,7 +87,8 @@ struct DevCorpus {
   const uint32_t* order = nullptr;
   uint64_t m = 0;
   uint64_t total = 0;      // bytes
-  uint64_t ntiles = 0;
+  uint64_t ntiles = 0;     // tiles [tile0, ntiles) are counted by count-all kernels
+  uint64_t tile0 = 0;
 };
 
 // Device prefix set for an extension pass.

@@ -30,6 +30,7 @@ void launch_prefix_insert(const uint64_t* keys, uint32_t K, const uint32_t* owne
                           uint64_t* hkeys, uint32_t* hidx, uint64_t* pkeys, uint32_t* rank_of_p,
                           cudaStream_t st);
 
+void launch_widen_add(const uint32_t* src, unsigned long long* dst, uint64_t n, cudaStream_t st);
 void launch_pack_prefix(const DevPrefixSet& ps, uint64_t* packed, cudaStream_t st);
 
 // --- count-once route-then-count (route_kernels.cu)

@@ -12,6 +12,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -42,7 +43,7 @@ struct Session {
   bool loaded = false;
 
   // pass buffers
-  DevBuf table, work;
+  DevBuf table, work, scratch32;
   DevBuf surv_keys, surv_counts, next_keys, next_counts;
   DevBuf pkeys, hkeys, hidx, hpacked, owner, owner_cnt, owner_start, cursor, rank_of_p;
   DevBuf sel_state, sel_hist, sel_scalar, units, unit_first;
@@ -477,22 +478,34 @@ static CT* count_pass(Session& s, bool dense, uint32_t L, int mode, const Prefix
     return t;
   }
   uint32_t* work = s.work.as<uint32_t>(64);
-  if (dense) {
-    tcap = 1ull << (8 * L);
-    CT* t = s.table.as<CT>(tcap);
-    IGB_CUDA(cudaMemsetAsync(t, 0, tcap * sizeof(CT), s.stream));
-    launch_count_dense<CT>(s.dc, L, mode, t, work, s.num_sms, s.stream);
-    s.launches++;
-    km = KeyMap{};
-    return t;
-  }
-  tcap = 256 * P->K;
+  tcap = dense ? (1ull << (8 * L)) : 256 * P->K;
   CT* t = s.table.as<CT>(tcap);
   IGB_CUDA(cudaMemsetAsync(t, 0, tcap * sizeof(CT), s.stream));
-  launch_count_extend<CT>(s.dc, P->ps, L, mode, t, work, s.num_sms, s.stream);
-  s.launches++;
+  auto launch = [&](const DevCorpus& dc, auto* tab) {
+    using T = std::remove_pointer_t<decltype(tab)>;
+    if (dense) launch_count_dense<T>(dc, L, mode, tab, work, s.num_sms, s.stream);
+    else launch_count_extend<T>(dc, P->ps, L, mode, tab, work, s.num_sms, s.stream);
+    s.launches++;
+  };
+  if constexpr (sizeof(CT) == 8) {
+    // 64-bit totals: count each < 2^32-byte corpus segment into an
+    // L2-friendly u32 scratch table, then widen-accumulate into the u64 table
+    uint32_t* scratch = s.scratch32.as<uint32_t>(tcap);
+    const uint64_t seg_tiles = (0xF0000000ull / kTileBytes);
+    for (uint64_t t0 = 0; t0 < s.dc.ntiles; t0 += seg_tiles) {
+      DevCorpus dc = s.dc;
+      dc.tile0 = t0;
+      dc.ntiles = std::min<uint64_t>(s.dc.ntiles, t0 + seg_tiles);
+      IGB_CUDA(cudaMemsetAsync(scratch, 0, tcap * 4, s.stream));
+      launch(dc, scratch);
+      launch_widen_add(scratch, t, tcap, s.stream);
+      s.launches++;
+    }
+  } else {
+    launch(s.dc, t);
+  }
   km = KeyMap{};
-  km.pkeys = P->ps.pkeys;
+  if (!dense) km.pkeys = P->ps.pkeys;
   return t;
 }
 
