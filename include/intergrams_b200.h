@@ -141,8 +141,20 @@ IG_API int ig_session_load(ig_session* s, const ig_corpus* corpus, char* err,
                     size_t err_len);
 IG_API int ig_session_run(ig_session* s, const ig_params* params, ig_result* out,
                    char* err, size_t err_len);
-/* Kernel launches issued by the last run (for launch accounting). */
+/* Kernel launches issued by the session so far (for launch accounting). */
 IG_API uint64_t ig_session_launches(const ig_session* s);
+
+/* Per-kernel-family device timing (CUDA events on the session stream; off by
+ * default).  ig_session_kernel_stats fills ms[i] / launches[i] for families
+ * i < n (IG_KF_*) accumulated since the last reset. */
+#define IG_KF_ROUTE_COUNT 0   /* count-once: owner histogram pass        */
+#define IG_KF_ROUTE_SCATTER 1 /* count-once: dedup + lookup + route       */
+#define IG_KF_ROUTE_CONSUME 2 /* count-once: per-sequence dedup + counts  */
+#define IG_KF_COUNT_ALL 3     /* count-all counting kernels               */
+#define IG_KF_SELECT 4        /* canonical top-k selection (all kernels)  */
+IG_API void ig_session_set_profiling(ig_session* s, int32_t on);
+IG_API int ig_session_kernel_stats(ig_session* s, double* ms, uint64_t* launches, int32_t n,
+                                   int32_t reset);
 IG_API void ig_session_destroy(ig_session* s);
 
 /* ---- pass-level entry points (parity of the reference's tables) ---------- */

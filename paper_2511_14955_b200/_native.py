@@ -16,6 +16,7 @@ IG_OK, IG_ECONFIG, IG_EIO, IG_EINTERNAL, IG_EINVALID = 0, 2, 3, 4, 5
 IG_MODE_ONCE, IG_MODE_ALL = 0, 1
 IG_HOST, IG_DEVICE = 0, 1
 IG_MAX_N = 8
+KERNEL_FAMILIES = ["route_count", "route_scatter", "route_consume", "count_all", "select"]
 
 
 class ig_corpus(C.Structure):
@@ -63,6 +64,9 @@ SYMBOLS = [
     ("ig_session_run", C.c_int, [C.c_void_p, C.POINTER(ig_params), C.POINTER(ig_result),
                                  C.c_char_p, C.c_size_t]),
     ("ig_session_launches", C.c_uint64, [C.c_void_p]),
+    ("ig_session_set_profiling", None, [C.c_void_p, C.c_int32]),
+    ("ig_session_kernel_stats", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32,
+                                          C.c_int32]),
     ("ig_session_destroy", None, [C.c_void_p]),
     ("ig_count_dense", C.c_int, [C.POINTER(ig_corpus), C.c_uint32, C.c_int32, C.c_int32,
                                  C.c_void_p, C.c_char_p, C.c_size_t]),

@@ -18,6 +18,7 @@
 #include <stdexcept>
 #include <string>
 #include <utility>
+#include <vector>
 
 #include "../../include/intergrams_b200.h"
 
@@ -76,6 +77,51 @@ struct DevBuf {
   T* as(size_t count) { return static_cast<T*>(get(count * sizeof(T))); }
   ~DevBuf() {
     if (p) cudaFree(p);
+  }
+};
+
+// Optional per-kernel-family device timing (CUDA events on the launching
+// stream), for the roofline numbers.  Families: see IG_KF_* in the C header.
+struct KernelTimer {
+  bool on = false;
+  std::vector<cudaEvent_t> pool;
+  std::vector<std::pair<int, size_t>> pending;  // family, index of the begin event
+  size_t used = 0;
+  double ms[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  uint64_t n[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  size_t begin(int fam, cudaStream_t st) {
+    if (!on) return 0;
+    while (used + 2 > pool.size()) {
+      cudaEvent_t e;
+      IGB_CUDA(cudaEventCreate(&e));
+      pool.push_back(e);
+    }
+    IGB_CUDA(cudaEventRecord(pool[used], st));
+    pending.emplace_back(fam, used);
+    used += 2;
+    return used - 2;
+  }
+  void end(size_t i, cudaStream_t st) {
+    if (on) IGB_CUDA(cudaEventRecord(pool[i + 1], st));
+  }
+  void collect() {  // after a stream sync
+    for (auto& p : pending) {
+      float t = 0;
+      IGB_CUDA(cudaEventElapsedTime(&t, pool[p.second], pool[p.second + 1]));
+      ms[p.first] += t;
+      n[p.first] += 1;
+    }
+    pending.clear();
+    used = 0;
+  }
+  void reset() {
+    for (int i = 0; i < 8; ++i) {
+      ms[i] = 0;
+      n[i] = 0;
+    }
+  }
+  ~KernelTimer() {
+    for (auto e : pool) cudaEventDestroy(e);
   }
 };
 

@@ -68,6 +68,7 @@ struct RouteCtx {
   uint32_t nunits = 0;
   DevBuf cnt, actual, base, entries, cub_tmp;
   uint64_t launches = 0;
+  KernelTimer* kt = nullptr;
 };
 
 void make_route_params(uint64_t cap, RouteParams& rp);

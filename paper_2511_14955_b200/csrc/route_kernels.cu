@@ -439,7 +439,9 @@ static void route_stage1_t(RouteCtx& x, const DevCorpus& c, const RouteParams& r
   if (per < 1) throw Error(IG_EINTERNAL, "route count does not fit in shared memory");
   const unsigned grid = (unsigned)std::min<uint64_t>(x.nunits, (uint64_t)num_sms * per);
   IGB_CUDA(cudaMemsetAsync(cnt + ncnt - 1, 0, 4, st));
+  const size_t ev = x.kt ? x.kt->begin(IG_KF_ROUTE_COUNT, st) : 0;
   k<<<grid, kRouteThreads, smem, st>>>(c, uv, rp, cnt);
+  if (x.kt) x.kt->end(ev, st);
   x.launches++;
   size_t need = 0;
   IGB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, need, cnt, base, (int64_t)ncnt, st));
@@ -467,7 +469,9 @@ static void route_stage2_t(RouteCtx& x, const DevCorpus& c, const RouteParams& r
     IGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, kScatterThreads, smem));
     if (per < 1) throw Error(IG_EINTERNAL, "route scatter does not fit in shared memory");
     const unsigned grid = (unsigned)std::min<uint64_t>(x.nunits, (uint64_t)num_sms * per);
+    const size_t ev = x.kt ? x.kt->begin(IG_KF_ROUTE_SCATTER, st) : 0;
     k<<<grid, kScatterThreads, smem, st>>>(c, uv, rp, base, act, ent);
+    if (x.kt) x.kt->end(ev, st);
     x.launches++;
   }
   {
@@ -490,8 +494,10 @@ static void route_stage2_t(RouteCtx& x, const DevCorpus& c, const RouteParams& r
     if (nblocks < 1) nblocks = 1;
     const uint64_t nitems = (uint64_t)rp.NO * nblocks;
     const unsigned grid = (unsigned)std::min<uint64_t>(nitems, slots);
+    const size_t ev = x.kt ? x.kt->begin(IG_KF_ROUTE_CONSUME, st) : 0;
     k<<<grid, kConsumeThreads, smem, st>>>(uv, c.m, rp, (uint32_t)sb, (uint32_t)nblocks, base, act,
                                             ent, table);
+    if (x.kt) x.kt->end(ev, st);
     x.launches++;
   }
   IGB_CUDA(cudaGetLastError());

@@ -49,6 +49,7 @@ struct Session {
   DevBuf sel_state, sel_hist, sel_scalar, units, unit_first;
   SelectCtx sel;
   RouteCtx rc;
+  KernelTimer kt;
   std::vector<cudaEvent_t> events;
 
   ~Session() {
@@ -483,8 +484,10 @@ static CT* count_pass(Session& s, bool dense, uint32_t L, int mode, const Prefix
   IGB_CUDA(cudaMemsetAsync(t, 0, tcap * sizeof(CT), s.stream));
   auto launch = [&](const DevCorpus& dc, auto* tab) {
     using T = std::remove_pointer_t<decltype(tab)>;
+    const size_t ev = s.kt.begin(IG_KF_COUNT_ALL, s.stream);
     if (dense) launch_count_dense<T>(dc, L, mode, tab, work, s.num_sms, s.stream);
     else launch_count_extend<T>(dc, P->ps, L, mode, tab, work, s.num_sms, s.stream);
+    s.kt.end(ev, s.stream);
     s.launches++;
   };
   if constexpr (sizeof(CT) == 8) {
@@ -509,6 +512,15 @@ static CT* count_pass(Session& s, bool dense, uint32_t L, int mode, const Prefix
   return t;
 }
 
+template <typename CT>
+static uint64_t timed_select(Session& s, const CT* table, uint64_t cap, uint64_t k, KeyMap km,
+                             int key_bits, uint64_t* ok, uint64_t* oc) {
+  const size_t ev = s.kt.begin(IG_KF_SELECT, s.stream);
+  const uint64_t n = select_topk<CT>(s.sel, table, cap, k, km, key_bits, ok, oc);
+  s.kt.end(ev, s.stream);
+  return n;
+}
+
 // Count-table dtype: u32 whenever no count can reach 2^32 (count-once counts
 // are <= m; count-all counts are <= the corpus bytes), else u64.
 static bool use_u32(Session& s, int mode) {
@@ -520,6 +532,7 @@ static bool use_u32(Session& s, int mode) {
 template <typename CT>
 static void run_t(Session& s, const ig_params& p, ig_result* out) {
   init_select(s);
+  s.rc.kt = &s.kt;
   const uint64_t kp = k_prime(p);
   const uint32_t n = p.n;
   const uint32_t n0 = std::min<uint32_t>(n, 3);
@@ -548,7 +561,7 @@ static void run_t(Session& s, const ig_params& p, ig_result* out) {
     ev = tm.begin();
     out_keys_d = s.next_keys.as<uint64_t>(std::min<uint64_t>(p.k, dcap) + 1);
     out_counts_d = s.next_counts.as<uint64_t>(std::min<uint64_t>(p.k, dcap) + 1);
-    out_len = select_topk<CT>(s.sel, table, tcap, p.k, km, 8 * n0, out_keys_d, out_counts_d);
+    out_len = timed_select<CT>(s, table, tcap, p.k, km, 8 * n0, out_keys_d, out_counts_d);
     tm.end(ev);
     rows.push_back(make_row("top-k " + std::to_string(n) + "-grams", n, 0, 0, out_len, false, ev));
   } else {
@@ -557,7 +570,7 @@ static void run_t(Session& s, const ig_params& p, ig_result* out) {
     uint64_t scap = std::min<uint64_t>(kp, dcap);
     uint64_t* sk = s.surv_keys.as<uint64_t>(scap + 1);
     uint64_t* sc = s.surv_counts.as<uint64_t>(scap + 1);
-    uint64_t ns = select_topk<CT>(s.sel, table, tcap, kp, km, 24, sk, sc);
+    uint64_t ns = timed_select<CT>(s, table, tcap, kp, km, 24, sk, sc);
     bool shrt = ns < kp;
     if (shrt)
       diag += "pass 3 retained " + std::to_string(ns) + " candidates (requested " +
@@ -584,7 +597,7 @@ static void run_t(Session& s, const ig_params& p, ig_result* out) {
         uint64_t ncap = std::min<uint64_t>(kp, cap);
         uint64_t* nk = s.next_keys.as<uint64_t>(ncap + 1);
         uint64_t* nc = s.next_counts.as<uint64_t>(ncap + 1);
-        uint64_t nn = select_topk<CT>(s.sel, ct, tcap, kp, km, 8 * j, nk, nc);
+        uint64_t nn = timed_select<CT>(s, ct, tcap, kp, km, 8 * j, nk, nc);
         shrt = nn < kp;
         if (shrt)
           diag += "pass " + std::to_string(j) + " retained " + std::to_string(nn) +
@@ -601,7 +614,7 @@ static void run_t(Session& s, const ig_params& p, ig_result* out) {
         uint64_t ocap = std::min<uint64_t>(p.k, cap);
         out_keys_d = s.next_keys.as<uint64_t>(ocap + 1);
         out_counts_d = s.next_counts.as<uint64_t>(ocap + 1);
-        out_len = select_topk<CT>(s.sel, ct, tcap, p.k, km, 8 * j, out_keys_d, out_counts_d);
+        out_len = timed_select<CT>(s, ct, tcap, p.k, km, 8 * j, out_keys_d, out_counts_d);
         tm.end(ev);
         rows.push_back(
             make_row("top-k " + std::to_string(j) + "-grams", j, 0, 0, out_len, false, ev));
@@ -630,6 +643,7 @@ static void run_t(Session& s, const ig_params& p, ig_result* out) {
     out->passes[i] = rows[i].st;
   }
   out->num_passes = (uint32_t)rows.size();
+  s.kt.collect();
   memcpy(out->diagnostics, diag.c_str(), diag.size() + 1);
   s.launches += s.sel.launches - sel_before;
 }
@@ -723,6 +737,20 @@ int ig_session_run(ig_session* s, const ig_params* params, ig_result* out, char*
 }
 
 uint64_t ig_session_launches(const ig_session* s) { return s ? s->launches : 0; }
+
+void ig_session_set_profiling(ig_session* s, int32_t on) {
+  if (s) s->kt.on = on != 0;
+}
+
+int ig_session_kernel_stats(ig_session* s, double* ms, uint64_t* launches, int32_t n, int32_t reset) {
+  if (!s) return IG_ECONFIG;
+  for (int i = 0; i < n && i < 8; ++i) {
+    if (ms) ms[i] = s->kt.ms[i];
+    if (launches) launches[i] = s->kt.n[i];
+  }
+  if (reset) s->kt.reset();
+  return IG_OK;
+}
 
 void ig_session_destroy(ig_session* s) {
   if (!s) return;

@@ -366,6 +366,19 @@ class Session:
     def launches(self) -> int:
         return int(self._lib.ig_session_launches(self._h))
 
+    def set_profiling(self, on: bool) -> None:
+        """Per-kernel-family device timing (CUDA events on the session stream)."""
+        self._lib.ig_session_set_profiling(self._h, 1 if on else 0)
+
+    def kernel_stats(self, reset: bool = False) -> dict:
+        """{family: (total_ms, launches)} accumulated since the last reset."""
+        n = len(N.KERNEL_FAMILIES)
+        ms = np.zeros(n, np.float64)
+        cnt = np.zeros(n, np.uint64)
+        self._lib.ig_session_kernel_stats(self._h, ms.ctypes.data, cnt.ctypes.data, n,
+                                          1 if reset else 0)
+        return {f: (float(ms[i]), int(cnt[i])) for i, f in enumerate(N.KERNEL_FAMILIES)}
+
     def close(self) -> None:
         if self._h:
             self._lib.ig_session_destroy(self._h)
