@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(NT) k_route_scatter(
           const uint64_t key = key8<T>(W) & gmask<L>();
           // a gram already routed from this chunk adds nothing (count-once):
           // drop it before the prefix lookup.  Races only cost a duplicate.
-          constexpr int kLgSlots = DSLOTS == 4096 ? 12 : 11;
+          constexpr int kLgSlots = DSLOTS == 8192 ? 13 : DSLOTS == 4096 ? 12 : 11;
           const uint32_t slot =
               (((uint32_t)key ^ ((uint32_t)(key >> 32) * 0x85EBCA6Bu)) * 0x9E3779B1u) >> (32 - kLgSlots);
           if (!dedup || key == ~0ull || cache[slot] != key) {  // ~0 is the empty marker
@@ -459,15 +459,17 @@ static void route_stage2_t(RouteCtx& x, const DevCorpus& c, const RouteParams& r
   const RouteView uv{x.units, x.unit_first, x.nunits};
   const size_t tab = TAB == 1 ? table_bytes(rp) : 0;
   const size_t ncnt = (size_t)rp.NO * x.nunits + 1;
-  uint32_t* act = x.actual.as<uint32_t>(ncnt);
+  uint32_t* act = x.actual.as<uint32_t>(ncnt);  // TAB 10/11: dense with 1024/768 threads
   unsigned long long* base = x.base.as<unsigned long long>(ncnt);
   uint16_t* ent = x.entries.as<uint16_t>(c.total + 64);
   {
-    constexpr int NT = TAB == 1 ? kScatterThreadsBig : kScatterThreads;
-    constexpr int DS = TAB == 1 ? 2048 : kDedupSlots;
+    constexpr int NT = TAB == 1 || TAB == 11 ? kScatterThreadsBig
+                       : (TAB == 10 || TAB == 12) ? 1024 : kScatterThreads;
+    constexpr int DS = TAB == 1 ? 2048 : TAB == 12 ? 8192 : kDedupSlots;
+    constexpr int KT = TAB >= 10 ? 0 : TAB;  // dense variants carry no table
     const size_t smem = (size_t)NT * 16 * 4 + (size_t)DS * 8 + align16((size_t)rp.NO * 8) +
                         align16((size_t)rp.NO * 4) + align16((size_t)(rp.NO + 1) * 4) + tab;
-    auto k = k_route_scatter<KIND, L, TAB, NT, DS>;
+    auto k = k_route_scatter<KIND, L, KT, NT, DS>;
     IGB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per = 0;
     IGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, NT, smem));
@@ -513,7 +515,9 @@ static void route_stage_l(int stage, RouteCtx& x, const DevCorpus& c, const Rout
   if (stage == 1) {
     route_stage1_t<KIND, L>(x, c, rp, num_sms, st);
   } else if constexpr (KIND == 0) {
-    route_stage2_t<0, L, 0, CT>(x, c, rp, table, num_sms, st);
+    // dense: one 1024-thread CTA per SM with an 8192-slot dedup cache
+    // (measured best of 512/768/1024 threads and 4096/8192 slots)
+    route_stage2_t<0, L, 12, CT>(x, c, rp, table, num_sms, st);
   } else {
     const size_t scatter_fixed = (size_t)kScatterThreadsBig * 64 + 2048 * 8 +
                                  (size_t)rp.NO * 16 + 256 + 8 * 1024;  // + static smem
