@@ -60,15 +60,21 @@ struct RouteParams {
   const uint16_t* disp = nullptr;      // [nb]
   const uint32_t* pidx = nullptr;      // [nslots] (unpacked only)
   const uint32_t* ostart = nullptr;
+  // fused count of the NEXT pass (owner = hash(this pass's gram) >> (64 - next_lgno));
+  // -1: not requested
+  int32_t next_lgno = -1;
+  uint32_t* next_cnt = nullptr;
 };
 
 struct RouteCtx {
   const RouteUnit* units = nullptr;
   const uint32_t* unit_first = nullptr;
   uint32_t nunits = 0;
-  DevBuf cnt, actual, base, entries, cub_tmp;
+  DevBuf cnt, actual, base, entries, cub_tmp, cnt_next;
   uint64_t launches = 0;
   KernelTimer* kt = nullptr;
+  bool have_next = false;   // cnt_next holds the next pass's counts (fused in the scatter)
+  int32_t next_lgno = -1;
 };
 
 void make_route_params(uint64_t cap, RouteParams& rp);

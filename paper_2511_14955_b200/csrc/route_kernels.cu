@@ -256,6 +256,10 @@ __global__ void __launch_bounds__(NT) k_route_scatter(
   sp += align16((size_t)rp.NO * 4);
   uint32_t* lbase = reinterpret_cast<uint32_t*>(sp);  // NO + 1
   sp += align16((size_t)(rp.NO + 1) * 4);
+  const bool nextc = rp.next_lgno >= 0;
+  const uint32_t nno = nextc ? (1u << rp.next_lgno) : 0u;
+  uint32_t* nhist = reinterpret_cast<uint32_t*>(sp);  // next pass's owner histogram
+  sp += align16((size_t)nno * 4);
   uint64_t* s_slots = reinterpret_cast<uint64_t*>(sp);
   __shared__ uint32_t s_total;
   using BlockScan = cub::BlockScan<uint32_t, NT>;
@@ -268,6 +272,7 @@ __global__ void __launch_bounds__(NT) k_route_scatter(
     const RouteUnit U = uv.units[u];
     __syncthreads();
     for (uint32_t o = threadIdx.x; o < rp.NO; o += blockDim.x) res[o] = base[(size_t)o * uv.nunits + u];
+    for (uint32_t o = threadIdx.x; o < nno; o += blockDim.x) nhist[o] = 0;
     const int64_t s0 = (int64_t)c.off[U.q];
     const int64_t lo = max((int64_t)U.b0, s0 + L - 1), hi = (int64_t)U.b1;
     const int64_t first = (int64_t)U.b0 & ~int64_t(15);
@@ -289,6 +294,15 @@ __global__ void __launch_bounds__(NT) k_route_scatter(
         uint32_t v = 0xffffffffu;
         if ((vm >> T) & 1u) {
           const uint64_t key = key8<T>(W) & gmask<L>();
+          if (nextc) {
+            // the next pass's gram ending at b0+T+1 has this gram as its prefix
+            const int64_t nxt_end = b0 + T + 1;
+            if (nxt_end < hi) {
+              atomicAdd(nhist + prefix_owner_hash(key, rp.next_lgno), 1u);
+            } else if (nxt_end < (int64_t)c.off[U.q + 1]) {  // first position of unit u+1
+              atomicAdd(rp.next_cnt + (size_t)prefix_owner_hash(key, rp.next_lgno) * uv.nunits + u + 1, 1u);
+            }
+          }
           // a gram already routed from this chunk adds nothing (count-once):
           // drop it before the prefix lookup.  Races only cost a duplicate.
           constexpr int kLgSlots = DSLOTS == 8192 ? 13 : DSLOTS == 4096 ? 12 : 11;
@@ -339,6 +353,8 @@ __global__ void __launch_bounds__(NT) k_route_scatter(
     __syncthreads();
     for (uint32_t o = threadIdx.x; o < rp.NO; o += blockDim.x)
       actual[(size_t)o * uv.nunits + u] = (uint32_t)(res[o] - base[(size_t)o * uv.nunits + u]);
+    for (uint32_t o = threadIdx.x; o < nno; o += blockDim.x)
+      if (nhist[o]) atomicAdd(rp.next_cnt + (size_t)o * uv.nunits + u, nhist[o]);
   }
 }
 
@@ -430,9 +446,21 @@ static void route_stage1_t(RouteCtx& x, const DevCorpus& c, const RouteParams& r
                            cudaStream_t st) {
   const RouteView uv{x.units, x.unit_first, x.nunits};
   const size_t ncnt = (size_t)rp.NO * x.nunits + 1;
-  uint32_t* cnt = x.cnt.as<uint32_t>(ncnt);
   x.actual.as<uint32_t>(ncnt);
   unsigned long long* base = x.base.as<unsigned long long>(ncnt);
+  if (KIND == 1 && x.have_next && x.next_lgno == (int32_t)rp.lgno) {
+    // the previous pass's scatter already histogrammed this pass's owners
+    x.cnt.swap(x.cnt_next);
+    x.have_next = false;
+    uint32_t* cnt = x.cnt.as<uint32_t>(ncnt);
+    size_t need = 0;
+    IGB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, need, cnt, base, (int64_t)ncnt, st));
+    void* tmp = x.cub_tmp.get(need);
+    IGB_CUDA(cub::DeviceScan::ExclusiveSum(tmp, need, cnt, base, (int64_t)ncnt, st));
+    return;
+  }
+  x.have_next = false;
+  uint32_t* cnt = x.cnt.as<uint32_t>(ncnt);
   const size_t smem = align16((size_t)rp.NO * 4);
   auto k = k_route_count<KIND, L>;
   IGB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -462,13 +490,22 @@ static void route_stage2_t(RouteCtx& x, const DevCorpus& c, const RouteParams& r
   uint32_t* act = x.actual.as<uint32_t>(ncnt);  // TAB 10/11: dense with 1024/768 threads
   unsigned long long* base = x.base.as<unsigned long long>(ncnt);
   uint16_t* ent = x.entries.as<uint16_t>(c.total + 64);
+  RouteParams rq = rp;
+  if (rp.next_lgno >= 0) {
+    const size_t nn = ((size_t)1 << rp.next_lgno) * x.nunits + 1;
+    rq.next_cnt = x.cnt_next.as<uint32_t>(nn);
+    IGB_CUDA(cudaMemsetAsync(rq.next_cnt, 0, nn * 4, st));
+    x.have_next = true;
+    x.next_lgno = rp.next_lgno;
+  }
   {
     constexpr int NT = TAB == 1 || TAB == 11 ? kScatterThreadsBig
                        : (TAB == 10 || TAB == 12) ? 1024 : kScatterThreads;
     constexpr int DS = TAB == 1 ? 2048 : TAB == 12 ? 8192 : kDedupSlots;
     constexpr int KT = TAB >= 10 ? 0 : TAB;  // dense variants carry no table
+    const size_t nxt = rp.next_lgno >= 0 ? align16(((size_t)1 << rp.next_lgno) * 4) : 0;
     const size_t smem = (size_t)NT * 16 * 4 + (size_t)DS * 8 + align16((size_t)rp.NO * 8) +
-                        align16((size_t)rp.NO * 4) + align16((size_t)(rp.NO + 1) * 4) + tab;
+                        align16((size_t)rp.NO * 4) + align16((size_t)(rp.NO + 1) * 4) + nxt + tab;
     auto k = k_route_scatter<KIND, L, KT, NT, DS>;
     IGB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per = 0;
@@ -476,7 +513,7 @@ static void route_stage2_t(RouteCtx& x, const DevCorpus& c, const RouteParams& r
     if (per < 1) throw Error(IG_EINTERNAL, "route scatter does not fit in shared memory");
     const unsigned grid = (unsigned)std::min<uint64_t>(x.nunits, (uint64_t)num_sms * per);
     const size_t ev = x.kt ? x.kt->begin(IG_KF_ROUTE_SCATTER, st) : 0;
-    k<<<grid, NT, smem, st>>>(c, uv, rp, base, act, ent);
+    k<<<grid, NT, smem, st>>>(c, uv, rq, base, act, ent);
     if (x.kt) x.kt->end(ev, st);
     x.launches++;
   }

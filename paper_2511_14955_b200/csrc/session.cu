@@ -333,6 +333,16 @@ static void allreduce(Session& s, void* buf, uint64_t count, int dtype) {
   if (rc != 0) throw Error(IG_EINTERNAL, "allreduce callback failed");
 }
 
+// Owner-hash width the count-once extension passes use for k' survivors: ~40
+// prefixes per owner on average (at most kPrefixesPerOwner after the check in
+// prepare_prefix).  Known before the survivors are, so the previous pass's
+// scatter can histogram the next pass's owners (fused count).
+static uint32_t predicted_lgno(uint64_t kp) {
+  uint32_t lg = 0;
+  while ((kp + (1ull << lg) - 1) / (1ull << lg) > 40) ++lg;
+  return lg;
+}
+
 // Survivor prefix structure for the next extension pass: the bucketed (CSR)
 // set for count-once routing, the open-addressing set for count-all.
 struct Prefix {
@@ -348,7 +358,7 @@ struct Prefix {
 };
 
 static Prefix prepare_prefix(Session& s, const uint64_t* keys, uint64_t K, uint32_t plen,
-                             int mode) {
+                             int mode, uint32_t lgno_start = 0) {
   Prefix P;
   P.K = K;
   if (!K) return P;
@@ -361,7 +371,7 @@ static Prefix prepare_prefix(Session& s, const uint64_t* keys, uint64_t K, uint3
     auto owner_of = [](uint64_t key, uint32_t lgno) -> uint32_t {
       return lgno ? (uint32_t)((key * kOwnerMul) >> (64 - lgno)) : 0u;
     };
-    uint32_t lgno = 0;
+    uint32_t lgno = lgno_start;
     std::vector<uint32_t> cnt;
     for (;; ++lgno) {
       cnt.assign((size_t)1 << lgno, 0);
@@ -449,7 +459,7 @@ static void build_prefix_table(Session& s, Prefix& P) {
 // indices map to gram keys.
 template <typename CT>
 static CT* count_pass(Session& s, bool dense, uint32_t L, int mode, const Prefix* P,
-                      uint64_t& tcap, KeyMap& km) {
+                      uint64_t& tcap, KeyMap& km, int32_t next_lgno = -1) {
   if (mode == IG_MODE_ONCE) {
     RouteParams rp;
     if (dense) make_route_params(1ull << (8 * L), rp);
@@ -467,6 +477,7 @@ static CT* count_pass(Session& s, bool dense, uint32_t L, int mode, const Prefix
       rp = P->rp;
       rp.dedup = dd;
     }
+    rp.next_lgno = next_lgno;
     route_count_once<CT>(2, s.rc, s.dc, dense ? 0 : 1, L, rp, t, s.num_sms, s.stream);
     s.launches += s.rc.launches - l0;
     km = KeyMap{};
@@ -547,7 +558,9 @@ static void run_t(Session& s, const ig_params& p, ig_result* out) {
   size_t ev = tm.begin();
   uint64_t tcap = 0;
   KeyMap km;
-  CT* table = count_pass<CT>(s, true, n0, p.mode, nullptr, tcap, km);
+  const int32_t fuse_lg = (p.mode == IG_MODE_ONCE && n > 3 && !getenv("IG_NO_FUSED_COUNT"))
+                             ? (int32_t)predicted_lgno(kp) : -1;
+  CT* table = count_pass<CT>(s, true, n0, p.mode, nullptr, tcap, km, fuse_lg);
   IGB_CUDA(cudaGetLastError());
   allreduce(s, table, tcap, sizeof(CT) == 4 ? 0 : 1);
   tm.end(ev);
@@ -575,7 +588,7 @@ static void run_t(Session& s, const ig_params& p, ig_result* out) {
     if (shrt)
       diag += "pass 3 retained " + std::to_string(ns) + " candidates (requested " +
               std::to_string(kp) + ")\n";
-    Prefix P = prepare_prefix(s, sk, ns, 3, p.mode);
+    Prefix P = prepare_prefix(s, sk, ns, 3, p.mode, fuse_lg > 0 ? (uint32_t)fuse_lg : 0u);
     tm.end(ev);
     rows.push_back(make_row("top-zk 3-grams/trie building", 3, 0, 0, ns, shrt, ev));
 
@@ -585,7 +598,7 @@ static void run_t(Session& s, const ig_params& p, ig_result* out) {
       if (ns == 0) throw Error(IG_ECONFIG, "extension pass needs a trie of depth j-1");
       ev = tm.begin();
       const uint64_t cap = 256 * ns;
-      CT* ct = count_pass<CT>(s, false, j, p.mode, &P, tcap, km);
+      CT* ct = count_pass<CT>(s, false, j, p.mode, &P, tcap, km, j < n ? fuse_lg : -1);
       IGB_CUDA(cudaGetLastError());
       allreduce(s, ct, tcap, sizeof(CT) == 4 ? 0 : 1);
       tm.end(ev);
@@ -606,7 +619,7 @@ static void run_t(Session& s, const ig_params& p, ig_result* out) {
         s.surv_counts.swap(s.next_counts);
         sk = nk;
         ns = nn;
-        P = prepare_prefix(s, sk, ns, j, p.mode);
+        P = prepare_prefix(s, sk, ns, j, p.mode, fuse_lg > 0 ? (uint32_t)fuse_lg : 0u);
         tm.end(ev);
         rows.push_back(make_row("top-zk " + std::to_string(j) + "-grams/trie building", j, 0, 0,
                                 ns, shrt, ev));
