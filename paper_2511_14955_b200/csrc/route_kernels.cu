@@ -440,6 +440,20 @@ static size_t table_bytes(const RouteParams& rp) {
   return align16((size_t)rp.nslots * 8 + (size_t)rp.nb * 2);
 }
 
+// Exclusive prefix sum of u32 region sizes into u64 offsets, accumulated in 64
+// bits (a corpus can route more than 2^32 positions).
+struct WidenU64 {
+  __host__ __device__ unsigned long long operator()(uint32_t v) const { return v; }
+};
+static void scan_u32_to_u64(RouteCtx& x, const uint32_t* cnt, unsigned long long* base, size_t n,
+                            cudaStream_t st) {
+  cub::TransformInputIterator<unsigned long long, WidenU64, const uint32_t*> in(cnt, WidenU64{});
+  size_t need = 0;
+  IGB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, need, in, base, (int64_t)n, st));
+  void* tmp = x.cub_tmp.get(need);
+  IGB_CUDA(cub::DeviceScan::ExclusiveSum(tmp, need, in, base, (int64_t)n, st));
+}
+
 // Stage 1: count kernel + owner-major scan (needs only the owner function).
 template <int KIND, int L>
 static void route_stage1_t(RouteCtx& x, const DevCorpus& c, const RouteParams& rp, int num_sms,
@@ -453,10 +467,7 @@ static void route_stage1_t(RouteCtx& x, const DevCorpus& c, const RouteParams& r
     x.cnt.swap(x.cnt_next);
     x.have_next = false;
     uint32_t* cnt = x.cnt.as<uint32_t>(ncnt);
-    size_t need = 0;
-    IGB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, need, cnt, base, (int64_t)ncnt, st));
-    void* tmp = x.cub_tmp.get(need);
-    IGB_CUDA(cub::DeviceScan::ExclusiveSum(tmp, need, cnt, base, (int64_t)ncnt, st));
+    scan_u32_to_u64(x, cnt, base, ncnt, st);
     return;
   }
   x.have_next = false;
@@ -473,10 +484,7 @@ static void route_stage1_t(RouteCtx& x, const DevCorpus& c, const RouteParams& r
   k<<<grid, kRouteThreads, smem, st>>>(c, uv, rp, cnt);
   if (x.kt) x.kt->end(ev, st);
   x.launches++;
-  size_t need = 0;
-  IGB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, need, cnt, base, (int64_t)ncnt, st));
-  void* tmp = x.cub_tmp.get(need);
-  IGB_CUDA(cub::DeviceScan::ExclusiveSum(tmp, need, cnt, base, (int64_t)ncnt, st));
+  scan_u32_to_u64(x, cnt, base, ncnt, st);
   IGB_CUDA(cudaGetLastError());
 }
 

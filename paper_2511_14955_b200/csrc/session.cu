@@ -25,7 +25,7 @@
 namespace igb {
 
 static constexpr size_t kOnceSmemBudget = 200 * 1024;  // bytes of bitmap per CTA
-static constexpr uint64_t kUnitBytes = 1ull << 20;     // count-once work unit
+static constexpr uint64_t kUnitBytes = 4ull << 20;     // count-once work unit
 static constexpr uint32_t kPrefixesPerOwner = 64;       // count-once ext: 64*256 ids/owner
 
 struct Session {

@@ -69,3 +69,25 @@ def test_c2_full_size_properties(gpu_lib):
     passes = [p for p in r1.passes if p.bytes_processed]
     assert len(passes) == 4 and all(p.bytes_processed == 4 << 30 for p in passes)
     sess.close()
+
+
+@pytest.mark.slow
+def test_more_than_2_32_routed_positions_doubling(gpu_lib):
+    # A count-once corpus of two identical halves has every count exactly
+    # doubled and the same list: a size-independent check past 2^32 routed
+    # positions (the route offsets and scans must be 64-bit).
+    cfg = S.scaled(S.CONFIGS["c2"], num_seqs=2200)
+    data, off = S.generate(cfg)
+    half = ig.Corpus(data, off)
+    off2 = np.concatenate([off, off[1:] + off[-1]]).astype(np.uint64)
+    doubled = ig.Corpus(np.concatenate([data, data]), off2)
+    assert int(off2[-1]) > (1 << 32)
+    icfg = ig.IntergramConfig(n=6, k=3000, z=1.5, mode=ig.CountMode.kOnce)
+    sess = ig.Session(device=0)
+    sess.load(half)
+    r1 = sess.run(icfg)
+    sess.load(doubled)
+    r2 = sess.run(icfg)
+    assert [g.gram for g in r2.topk] == [g.gram for g in r1.topk]
+    assert [g.count for g in r2.topk] == [2 * g.count for g in r1.topk]
+    sess.close()
