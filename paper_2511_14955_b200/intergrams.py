@@ -212,14 +212,16 @@ def dense_gram(gid: int, n: int) -> bytes:
 
 # ----------------------------------------------------------------- results
 
-def _result(r: N.ig_result) -> IntergramsResult:
+def _result(r: N.ig_result, materialize: bool = True) -> IntergramsResult:
+    """materialize=False keeps the list as numpy keys/counts only (topk = [])."""
     n = int(r.len)
     gl = int(r.gram_len)
     keys = np.ctypeslib.as_array(r.keys, shape=(max(n, 1),))[:n].copy() if n else \
         np.zeros(0, np.uint64)
     counts = np.ctypeslib.as_array(r.counts, shape=(max(n, 1),))[:n].copy() if n else \
         np.zeros(0, np.uint64)
-    topk = [GramCount(key_to_gram(int(k), gl), int(c)) for k, c in zip(keys, counts)]
+    topk = [GramCount(key_to_gram(int(k), gl), int(c)) for k, c in zip(keys, counts)] \
+        if materialize else []
     passes = []
     for i in range(int(r.num_passes)):
         p = r.passes[i]
@@ -316,6 +318,13 @@ def shard_range(offsets: np.ndarray, rank: int, world: int) -> Tuple[int, int]:
     return int(a.value), int(b.value)
 
 
+def run_result_topk(r: IntergramsResult, n: int) -> List[GramCount]:
+    """The GramCount list of a result (materialised from keys/counts if needed)."""
+    if r.topk or r.keys is None:
+        return r.topk
+    return [GramCount(key_to_gram(int(k), n), int(c)) for k, c in zip(r.keys, r.counts)]
+
+
 def topk_to_tsv(topk: Sequence[GramCount]) -> str:
     """metrics.cpp:202-211: lowercase hex, TAB, decimal count, LF."""
     return "".join(f"{g.gram.hex()}\t{g.count}\n" for g in topk)
@@ -350,7 +359,10 @@ class Session:
         rc = self._lib.ig_session_load(self._h, C.byref(view), err, len(err))
         _raise(rc, err)
 
-    def run(self, cfg: IntergramConfig) -> IntergramsResult:
+    def run(self, cfg: IntergramConfig, materialize: bool = True) -> IntergramsResult:
+        """run_intergrams on the resident corpus.  materialize=False returns the
+        list as numpy `keys`/`counts` (big-endian packed grams) without building
+        per-gram Python objects."""
         cfg.validate()
         err = C.create_string_buffer(1024)
         out = N.ig_result()
@@ -358,7 +370,7 @@ class Session:
         rc = self._lib.ig_session_run(self._h, C.byref(params), C.byref(out), err, len(err))
         _raise(rc, err)
         try:
-            return _result(out)
+            return _result(out, materialize)
         finally:
             self._lib.ig_result_free(C.byref(out))
 
