@@ -141,6 +141,10 @@ IG_API int ig_session_load(ig_session* s, const ig_corpus* corpus, char* err,
                     size_t err_len);
 IG_API int ig_session_run(ig_session* s, const ig_params* params, ig_result* out,
                    char* err, size_t err_len);
+/* load + run with the host->device copy pipelined under the dense pass (the
+ * corpus stays resident afterwards, as after ig_session_load). */
+IG_API int ig_session_run_host(ig_session* s, const ig_corpus* corpus, const ig_params* params,
+                               ig_result* out, char* err, size_t err_len);
 /* Kernel launches issued by the session so far (for launch accounting). */
 IG_API uint64_t ig_session_launches(const ig_session* s);
 

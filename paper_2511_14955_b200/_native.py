@@ -63,6 +63,8 @@ SYMBOLS = [
     ("ig_session_load", C.c_int, [C.c_void_p, C.POINTER(ig_corpus), C.c_char_p, C.c_size_t]),
     ("ig_session_run", C.c_int, [C.c_void_p, C.POINTER(ig_params), C.POINTER(ig_result),
                                  C.c_char_p, C.c_size_t]),
+    ("ig_session_run_host", C.c_int, [C.c_void_p, C.POINTER(ig_corpus), C.POINTER(ig_params),
+                                      C.POINTER(ig_result), C.c_char_p, C.c_size_t]),
     ("ig_session_launches", C.c_uint64, [C.c_void_p]),
     ("ig_session_set_profiling", None, [C.c_void_p, C.c_int32]),
     ("ig_session_kernel_stats", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32,

@@ -43,7 +43,9 @@ struct RouteUnit {  // <= 1 MiB of gram ends of one sequence: byte range [b0, b1
 struct RouteView {
   const RouteUnit* units;
   const uint32_t* unit_first;  // [m+1] first unit of each sequence
-  uint32_t nunits;
+  uint32_t nunits;             // all units (layout of fused next-pass counts)
+  uint32_t u0, nb;             // units [u0, u0+nb) of this launch
+  uint32_t q0, q1;             // their sequences [q0, q1)
 };
 
 struct RouteParams {
@@ -75,6 +77,9 @@ struct RouteCtx {
   KernelTimer* kt = nullptr;
   bool have_next = false;   // cnt_next holds the next pass's counts (fused in the scatter)
   int32_t next_lgno = -1;
+  // range of the current launch (whole corpus unless a pipelined load batches it)
+  uint32_t u0 = 0, u1 = 0, q0 = 0, q1 = 0;
+  RouteView view() const { return RouteView{units, unit_first, nunits, u0, u1 - u0, q0, q1}; }
 };
 
 void make_route_params(uint64_t cap, RouteParams& rp);

@@ -205,7 +205,8 @@ __global__ void __launch_bounds__(kRouteThreads) k_route_count(DevCorpus c, Rout
   extern __shared__ uint4 smem4[];
   uint32_t* hist = reinterpret_cast<uint32_t*>(smem4);
   const int lane = threadIdx.x & 31;
-  for (uint32_t u = blockIdx.x; u < uv.nunits; u += gridDim.x) {
+  for (uint32_t ui = blockIdx.x; ui < uv.nb; ui += gridDim.x) {
+    const uint32_t u = uv.u0 + ui;
     for (uint32_t i = threadIdx.x; i < rp.NO; i += blockDim.x) hist[i] = 0;
     __syncthreads();
     const RouteUnit U = uv.units[u];
@@ -226,7 +227,7 @@ __global__ void __launch_bounds__(kRouteThreads) k_route_count(DevCorpus c, Rout
     }
     __syncthreads();
     for (uint32_t o = threadIdx.x; o < rp.NO; o += blockDim.x)
-      cnt[(size_t)o * uv.nunits + u] = hist[o];
+      cnt[(size_t)o * uv.nb + ui] = hist[o];
     __syncthreads();
   }
 }
@@ -268,10 +269,11 @@ __global__ void __launch_bounds__(NT) k_route_scatter(
   const uint64_t* slots = KIND == 1 ? stage_table<TAB == 1 ? 1 : 2>(rp, s_slots, disp) : nullptr;
   const bool dedup = rp.dedup;
   const int lane = threadIdx.x & 31;
-  for (uint32_t u = blockIdx.x; u < uv.nunits; u += gridDim.x) {
+  for (uint32_t ui = blockIdx.x; ui < uv.nb; ui += gridDim.x) {
+    const uint32_t u = uv.u0 + ui;
     const RouteUnit U = uv.units[u];
     __syncthreads();
-    for (uint32_t o = threadIdx.x; o < rp.NO; o += blockDim.x) res[o] = base[(size_t)o * uv.nunits + u];
+    for (uint32_t o = threadIdx.x; o < rp.NO; o += blockDim.x) res[o] = base[(size_t)o * uv.nb + ui];
     for (uint32_t o = threadIdx.x; o < nno; o += blockDim.x) nhist[o] = 0;
     const int64_t s0 = (int64_t)c.off[U.q];
     const int64_t lo = max((int64_t)U.b0, s0 + L - 1), hi = (int64_t)U.b1;
@@ -352,7 +354,7 @@ __global__ void __launch_bounds__(NT) k_route_scatter(
     }
     __syncthreads();
     for (uint32_t o = threadIdx.x; o < rp.NO; o += blockDim.x)
-      actual[(size_t)o * uv.nunits + u] = (uint32_t)(res[o] - base[(size_t)o * uv.nunits + u]);
+      actual[(size_t)o * uv.nb + ui] = (uint32_t)(res[o] - base[(size_t)o * uv.nb + ui]);
     for (uint32_t o = threadIdx.x; o < nno; o += blockDim.x)
       if (nhist[o]) atomicAdd(rp.next_cnt + (size_t)o * uv.nunits + u, nhist[o]);
   }
@@ -373,7 +375,7 @@ __device__ __forceinline__ void consume_entry(uint32_t local, uint32_t* bm, uint
 
 template <typename CT>
 __global__ void __launch_bounds__(kConsumeThreads) k_consume_once(
-    RouteView uv, uint64_t m, RouteParams rp, uint32_t seq_block, uint32_t nblocks,
+    RouteView uv, RouteParams rp, uint32_t seq_block, uint32_t nblocks,
     const unsigned long long* __restrict__ base, const uint32_t* __restrict__ actual,
     const uint16_t* __restrict__ entries, CT* __restrict__ table) {
   extern __shared__ uint4 smem4[];
@@ -390,12 +392,12 @@ __global__ void __launch_bounds__(kConsumeThreads) k_consume_once(
     const uint32_t o = item / nblocks, b = item % nblocks;
     for (uint32_t i = threadIdx.x; i < cntw; i += blockDim.x) cnt[i] = 0;
     __syncthreads();
-    const uint64_t q0 = (uint64_t)b * seq_block;
-    const uint64_t q1 = min(m, q0 + seq_block);
+    const uint64_t q0 = uv.q0 + (uint64_t)b * seq_block;
+    const uint64_t q1 = min((uint64_t)uv.q1, q0 + seq_block);
     for (uint64_t q = q0 + warp; q < q1; q += kConsumeWarps) {
       const uint32_t u0 = uv.unit_first[q], u1 = uv.unit_first[q + 1];
       for (uint32_t u = u0; u < u1; ++u) {
-        const size_t ix = (size_t)o * uv.nunits + u;
+        const size_t ix = (size_t)o * uv.nb + (u - uv.u0);
         const uint64_t e0 = base[ix], e1 = e0 + actual[ix];
         // uint4-aligned body: 8 entries per lane per load
         const uint64_t a0 = (e0 + 7) & ~7ull, a1 = e1 & ~7ull;
@@ -458,8 +460,8 @@ static void scan_u32_to_u64(RouteCtx& x, const uint32_t* cnt, unsigned long long
 template <int KIND, int L>
 static void route_stage1_t(RouteCtx& x, const DevCorpus& c, const RouteParams& rp, int num_sms,
                            cudaStream_t st) {
-  const RouteView uv{x.units, x.unit_first, x.nunits};
-  const size_t ncnt = (size_t)rp.NO * x.nunits + 1;
+  const RouteView uv = x.view();
+  const size_t ncnt = (size_t)rp.NO * uv.nb + 1;
   x.actual.as<uint32_t>(ncnt);
   unsigned long long* base = x.base.as<unsigned long long>(ncnt);
   if (KIND == 1 && x.have_next && x.next_lgno == (int32_t)rp.lgno) {
@@ -478,7 +480,7 @@ static void route_stage1_t(RouteCtx& x, const DevCorpus& c, const RouteParams& r
   int per = 0;
   IGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, kRouteThreads, smem));
   if (per < 1) throw Error(IG_EINTERNAL, "route count does not fit in shared memory");
-  const unsigned grid = (unsigned)std::min<uint64_t>(x.nunits, (uint64_t)num_sms * per);
+  const unsigned grid = (unsigned)std::min<uint64_t>(uv.nb, (uint64_t)num_sms * per);
   IGB_CUDA(cudaMemsetAsync(cnt + ncnt - 1, 0, 4, st));
   const size_t ev = x.kt ? x.kt->begin(IG_KF_ROUTE_COUNT, st) : 0;
   k<<<grid, kRouteThreads, smem, st>>>(c, uv, rp, cnt);
@@ -492,9 +494,9 @@ static void route_stage1_t(RouteCtx& x, const DevCorpus& c, const RouteParams& r
 template <int KIND, int L, int TAB, typename CT>
 static void route_stage2_t(RouteCtx& x, const DevCorpus& c, const RouteParams& rp, CT* table,
                            int num_sms, cudaStream_t st) {
-  const RouteView uv{x.units, x.unit_first, x.nunits};
+  const RouteView uv = x.view();
   const size_t tab = TAB == 1 ? table_bytes(rp) : 0;
-  const size_t ncnt = (size_t)rp.NO * x.nunits + 1;
+  const size_t ncnt = (size_t)rp.NO * uv.nb + 1;
   uint32_t* act = x.actual.as<uint32_t>(ncnt);  // TAB 10/11: dense with 1024/768 threads
   unsigned long long* base = x.base.as<unsigned long long>(ncnt);
   uint16_t* ent = x.entries.as<uint16_t>(c.total + 64);
@@ -502,7 +504,8 @@ static void route_stage2_t(RouteCtx& x, const DevCorpus& c, const RouteParams& r
   if (rp.next_lgno >= 0) {
     const size_t nn = ((size_t)1 << rp.next_lgno) * x.nunits + 1;
     rq.next_cnt = x.cnt_next.as<uint32_t>(nn);
-    IGB_CUDA(cudaMemsetAsync(rq.next_cnt, 0, nn * 4, st));
+    // batched (pipelined) dense passes accumulate into one next-pass histogram
+    if (x.u0 == 0) IGB_CUDA(cudaMemsetAsync(rq.next_cnt, 0, nn * 4, st));
     x.have_next = true;
     x.next_lgno = rp.next_lgno;
   }
@@ -519,7 +522,7 @@ static void route_stage2_t(RouteCtx& x, const DevCorpus& c, const RouteParams& r
     int per = 0;
     IGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, NT, smem));
     if (per < 1) throw Error(IG_EINTERNAL, "route scatter does not fit in shared memory");
-    const unsigned grid = (unsigned)std::min<uint64_t>(x.nunits, (uint64_t)num_sms * per);
+    const unsigned grid = (unsigned)std::min<uint64_t>(uv.nb, (uint64_t)num_sms * per);
     const size_t ev = x.kt ? x.kt->begin(IG_KF_ROUTE_SCATTER, st) : 0;
     k<<<grid, NT, smem, st>>>(c, uv, rq, base, act, ent);
     if (x.kt) x.kt->end(ev, st);
@@ -535,18 +538,19 @@ static void route_stage2_t(RouteCtx& x, const DevCorpus& c, const RouteParams& r
     IGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, kConsumeThreads, smem));
     if (per < 1) throw Error(IG_EINTERNAL, "route consume does not fit in shared memory");
     const uint64_t slots = (uint64_t)num_sms * per;
+    const uint64_t mq = uv.q1 - uv.q0;
     uint64_t nblocks = (slots * 4 + rp.NO - 1) / rp.NO;
-    if (nblocks > c.m) nblocks = c.m;
+    if (nblocks > mq) nblocks = mq;
     if (nblocks < 1) nblocks = 1;
-    uint64_t sb = (c.m + nblocks - 1) / nblocks;
+    uint64_t sb = (mq + nblocks - 1) / nblocks;
     if (sb > 65535) sb = 65535;  // u16 smem counters: <= 65535 sequences per item
     if (sb < 1) sb = 1;
-    nblocks = (c.m + sb - 1) / sb;
+    nblocks = (mq + sb - 1) / sb;
     if (nblocks < 1) nblocks = 1;
     const uint64_t nitems = (uint64_t)rp.NO * nblocks;
     const unsigned grid = (unsigned)std::min<uint64_t>(nitems, slots);
     const size_t ev = x.kt ? x.kt->begin(IG_KF_ROUTE_CONSUME, st) : 0;
-    k<<<grid, kConsumeThreads, smem, st>>>(uv, c.m, rp, (uint32_t)sb, (uint32_t)nblocks, base, act,
+    k<<<grid, kConsumeThreads, smem, st>>>(uv, rp, (uint32_t)sb, (uint32_t)nblocks, base, act,
                                             ent, table);
     if (x.kt) x.kt->end(ev, st);
     x.launches++;
@@ -581,7 +585,7 @@ static void route_stage_l(int stage, RouteCtx& x, const DevCorpus& c, const Rout
 template <typename CT>
 void route_count_once(int stage, RouteCtx& x, const DevCorpus& c, int kind, uint32_t L,
                       const RouteParams& rp, CT* table, int num_sms, cudaStream_t st) {
-  if (!c.m || !x.nunits) return;
+  if (!c.m || !x.nunits || x.u1 <= x.u0) return;
   if (kind == 0) {
     switch (L) {
       case 1: route_stage_l<0, 1, CT>(stage, x, c, rp, table, num_sms, st); break;

@@ -50,10 +50,23 @@ struct Session {
   SelectCtx sel;
   RouteCtx rc;
   KernelTimer kt;
+  // pipelined host load: the dense pass runs batch by batch as the H2D copies land
+  struct Batch {
+    uint64_t t0, t1;           // count-all tiles whose bytes are all in the batch
+    uint32_t u0, u1, q0, q1;   // count-once units / sequences
+    cudaEvent_t ready;         // copy of the batch's bytes done (null: resident)
+  };
+  std::vector<Batch> batches;
+  std::vector<cudaEvent_t> batch_events;
+  std::vector<uint64_t> hoff;  // host offsets of the loaded corpus
+  std::vector<uint32_t> hufirst;
+  cudaStream_t copy_stream = nullptr;
   std::vector<cudaEvent_t> events;
 
   ~Session() {
     for (auto e : events) cudaEventDestroy(e);
+    for (auto e : batch_events) cudaEventDestroy(e);
+    if (copy_stream) cudaStreamDestroy(copy_stream);
     if (own_stream && stream) cudaStreamDestroy(stream);
   }
 };
@@ -106,7 +119,7 @@ static uint64_t k_prime(const ig_params& p) {
   return (uint64_t)v;
 }
 
-static void load_corpus(Session& s, const ig_corpus& c) {
+static void load_corpus(Session& s, const ig_corpus& c, bool copy_data = true) {
   use_device(s);
   const uint64_t m = c.num_seqs;
   std::vector<uint64_t> hoff(m + 1);
@@ -126,7 +139,7 @@ static void load_corpus(Session& s, const ig_corpus& c) {
   uint8_t* base = s.data.as<uint8_t>(alloc);
   IGB_CUDA(cudaMemsetAsync(base, 0, kFrontPad, s.stream));
   IGB_CUDA(cudaMemsetAsync(base + kFrontPad + total, 0, alloc - kFrontPad - total, s.stream));
-  if (total) {
+  if (total && copy_data) {
     IGB_CUDA(cudaMemcpyAsync(base + kFrontPad, c.data, total,
                              c.location == IG_DEVICE ? cudaMemcpyDeviceToDevice
                                                      : cudaMemcpyHostToDevice,
@@ -172,7 +185,14 @@ static void load_corpus(Session& s, const ig_corpus& c) {
   s.rc.units = dun;
   s.rc.unit_first = duf;
   s.rc.nunits = (uint32_t)units.size();
+  s.rc.u0 = 0;
+  s.rc.u1 = s.rc.nunits;
+  s.rc.q0 = 0;
+  s.rc.q1 = (uint32_t)m;
   IGB_CUDA(cudaStreamSynchronize(s.stream));
+  s.hoff.swap(hoff);
+  s.hufirst.swap(ufirst);
+  s.batches.clear();
   s.dc.data = base + kFrontPad;
   s.dc.off = doff;
   s.dc.tile_seq = dtile;
@@ -470,15 +490,33 @@ static CT* count_pass(Session& s, bool dense, uint32_t L, int mode, const Prefix
     CT* t = s.table.as<CT>(tcap);
     IGB_CUDA(cudaMemsetAsync(t, 0, tcap * sizeof(CT), s.stream));
     const uint64_t l0 = s.rc.launches;
-    route_count_once<CT>(1, s.rc, s.dc, dense ? 0 : 1, L, rp, t, s.num_sms, s.stream);
-    if (!dense) {  // the host table build overlaps the count kernel
-      build_prefix_table(s, *const_cast<Prefix*>(P));
-      const bool dd = rp.dedup;
-      rp = P->rp;
-      rp.dedup = dd;
+    if (dense && !s.batches.empty()) {
+      // pipelined load: route each batch as soon as its bytes have landed
+      rp.next_lgno = next_lgno;
+      for (const auto& b : s.batches) {
+        if (b.ready) IGB_CUDA(cudaStreamWaitEvent(s.stream, b.ready, 0));
+        s.rc.u0 = b.u0;
+        s.rc.u1 = b.u1;
+        s.rc.q0 = b.q0;
+        s.rc.q1 = b.q1;
+        route_count_once<CT>(1, s.rc, s.dc, 0, L, rp, t, s.num_sms, s.stream);
+        route_count_once<CT>(2, s.rc, s.dc, 0, L, rp, t, s.num_sms, s.stream);
+      }
+      s.rc.u0 = 0;
+      s.rc.u1 = s.rc.nunits;
+      s.rc.q0 = 0;
+      s.rc.q1 = (uint32_t)s.dc.m;
+    } else {
+      route_count_once<CT>(1, s.rc, s.dc, dense ? 0 : 1, L, rp, t, s.num_sms, s.stream);
+      if (!dense) {  // the host table build overlaps the count kernel
+        build_prefix_table(s, *const_cast<Prefix*>(P));
+        const bool dd = rp.dedup;
+        rp = P->rp;
+        rp.dedup = dd;
+      }
+      rp.next_lgno = next_lgno;
+      route_count_once<CT>(2, s.rc, s.dc, dense ? 0 : 1, L, rp, t, s.num_sms, s.stream);
     }
-    rp.next_lgno = next_lgno;
-    route_count_once<CT>(2, s.rc, s.dc, dense ? 0 : 1, L, rp, t, s.num_sms, s.stream);
     s.launches += s.rc.launches - l0;
     km = KeyMap{};
     if (dense) {
@@ -501,22 +539,40 @@ static CT* count_pass(Session& s, bool dense, uint32_t L, int mode, const Prefix
     s.kt.end(ev, s.stream);
     s.launches++;
   };
-  if constexpr (sizeof(CT) == 8) {
-    // 64-bit totals: count each < 2^32-byte corpus segment into an
-    // L2-friendly u32 scratch table, then widen-accumulate into the u64 table
-    uint32_t* scratch = s.scratch32.as<uint32_t>(tcap);
-    const uint64_t seg_tiles = (0xF0000000ull / kTileBytes);
-    for (uint64_t t0 = 0; t0 < s.dc.ntiles; t0 += seg_tiles) {
-      DevCorpus dc = s.dc;
-      dc.tile0 = t0;
-      dc.ntiles = std::min<uint64_t>(s.dc.ntiles, t0 + seg_tiles);
-      IGB_CUDA(cudaMemsetAsync(scratch, 0, tcap * 4, s.stream));
-      launch(dc, scratch);
-      launch_widen_add(scratch, t, tcap, s.stream);
-      s.launches++;
+  // tile ranges: the pipelined load's batches (dense pass only), else all
+  std::vector<std::pair<uint64_t, uint64_t>> ranges;
+  std::vector<cudaEvent_t> waits;
+  if (dense && !s.batches.empty()) {
+    for (const auto& b : s.batches) {
+      ranges.emplace_back(b.t0, b.t1);
+      waits.push_back(b.ready);
     }
   } else {
-    launch(s.dc, t);
+    ranges.emplace_back(0, s.dc.ntiles);
+    waits.push_back(nullptr);
+  }
+  for (size_t r = 0; r < ranges.size(); ++r) {
+    if (waits[r]) IGB_CUDA(cudaStreamWaitEvent(s.stream, waits[r], 0));
+    if constexpr (sizeof(CT) == 8) {
+      // 64-bit totals: count each < 2^32-byte corpus segment into an
+      // L2-friendly u32 scratch table, then widen-accumulate into the u64 table
+      uint32_t* scratch = s.scratch32.as<uint32_t>(tcap);
+      const uint64_t seg_tiles = (0xF0000000ull / kTileBytes);
+      for (uint64_t t0 = ranges[r].first; t0 < ranges[r].second; t0 += seg_tiles) {
+        DevCorpus dc = s.dc;
+        dc.tile0 = t0;
+        dc.ntiles = std::min<uint64_t>(ranges[r].second, t0 + seg_tiles);
+        IGB_CUDA(cudaMemsetAsync(scratch, 0, tcap * 4, s.stream));
+        launch(dc, scratch);
+        launch_widen_add(scratch, t, tcap, s.stream);
+        s.launches++;
+      }
+    } else {
+      DevCorpus dc = s.dc;
+      dc.tile0 = ranges[r].first;
+      dc.ntiles = ranges[r].second;
+      launch(dc, t);
+    }
   }
   km = KeyMap{};
   if (!dense) km.pkeys = P->ps.pkeys;
@@ -682,6 +738,63 @@ using namespace igb;
 struct ig_session : igb::Session {};
 
 namespace igb {
+// Host corpus: offsets/units/tiles first, then the bytes in sequence-aligned
+// batches on a copy stream (one event per batch); the dense pass consumes the
+// batches as they land, so most of the H2D hides behind counting.
+static void load_and_run(Session& s, const ig_corpus& c, const ig_params& p, ig_result* out) {
+  validate(p);
+  if (c.location == IG_DEVICE) {
+    load_corpus(s, c, true);
+    run(s, p, out);
+    return;
+  }
+  load_corpus(s, c, false);
+  const uint64_t m = s.dc.m, total = s.dc.total;
+  if (!s.copy_stream) IGB_CUDA(cudaStreamCreateWithFlags(&s.copy_stream, cudaStreamNonBlocking));
+  const uint64_t want = std::max<uint64_t>(256ull << 20, (total + 7) / 8);
+  s.batches.clear();
+  uint64_t q = 0;
+  uint64_t prev_t1 = 0;
+  size_t nb = 0;
+  while (q < m || (m == 0 && nb == 0)) {
+    const uint64_t q0 = q;
+    const uint64_t b0 = s.hoff[q0];
+    while (q < m && s.hoff[q + 1] - b0 < want) ++q;
+    if (q == q0 && q < m) ++q;  // one long sequence
+    const uint64_t b1 = s.hoff[q];
+    if (nb >= s.batch_events.size()) {
+      cudaEvent_t e;
+      IGB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      s.batch_events.push_back(e);
+    }
+    cudaEvent_t ev = s.batch_events[nb];
+    if (b1 > b0)
+      IGB_CUDA(cudaMemcpyAsync(const_cast<uint8_t*>(s.dc.data) + b0, c.data + b0, b1 - b0,
+                               cudaMemcpyHostToDevice, s.copy_stream));
+    IGB_CUDA(cudaEventRecord(ev, s.copy_stream));
+    Session::Batch b{};
+    b.q0 = (uint32_t)q0;
+    b.q1 = (uint32_t)q;
+    b.u0 = s.hufirst[q0];
+    b.u1 = s.hufirst[q];
+    b.t0 = prev_t1;
+    b.t1 = q >= m ? s.dc.ntiles : std::min<uint64_t>(s.dc.ntiles, b1 / kTileBytes);
+    if (b.t1 < b.t0) b.t1 = b.t0;
+    prev_t1 = b.t1;
+    b.ready = ev;
+    s.batches.push_back(b);
+    ++nb;
+    if (m == 0) break;
+  }
+  try {
+    run(s, p, out);
+  } catch (...) {
+    s.batches.clear();
+    throw;
+  }
+  s.batches.clear();
+}
+
 static ig_session* create(int32_t device, void* stream, const ig_collective* coll) {
   ig_session* s = new ig_session();
   try {
@@ -741,6 +854,14 @@ int ig_session_load(ig_session* s, const ig_corpus* corpus, char* err, size_t er
   });
 }
 
+int ig_session_run_host(ig_session* s, const ig_corpus* corpus, const ig_params* params,
+                        ig_result* out, char* err, size_t err_len) {
+  return guarded(err, err_len, [&] {
+    if (!s || !corpus || !params || !out) throw Error(IG_ECONFIG, "null argument");
+    load_and_run(*s, *corpus, *params, out);
+  });
+}
+
 int ig_session_run(ig_session* s, const ig_params* params, ig_result* out, char* err,
                    size_t err_len) {
   return guarded(err, err_len, [&] {
@@ -778,8 +899,7 @@ int ig_topk_ngrams(const ig_corpus* corpus, const ig_params* params, ig_result* 
     validate(*params);
     ig_session* s = create(params->device, nullptr, nullptr);
     try {
-      load_corpus(*s, *corpus);
-      run(*s, *params, out);
+      load_and_run(*s, *corpus, *params, out);
     } catch (...) {
       delete s;
       throw;

@@ -374,6 +374,25 @@ class Session:
         finally:
             self._lib.ig_result_free(C.byref(out))
 
+    def load_and_run(self, corpus, cfg: IntergramConfig,
+                     materialize: bool = True) -> IntergramsResult:
+        """Host corpus -> result, with the H2D copy pipelined under the dense
+        pass (ig_session_run_host).  The corpus stays resident afterwards."""
+        cfg.validate()
+        c = as_corpus(corpus)
+        self._corpus = c
+        view = c._view()
+        err = C.create_string_buffer(1024)
+        out = N.ig_result()
+        params = cfg._params()
+        rc = self._lib.ig_session_run_host(self._h, C.byref(view), C.byref(params), C.byref(out),
+                                           err, len(err))
+        _raise(rc, err)
+        try:
+            return _result(out, materialize)
+        finally:
+            self._lib.ig_result_free(C.byref(out))
+
     @property
     def launches(self) -> int:
         return int(self._lib.ig_session_launches(self._h))

@@ -91,3 +91,25 @@ def test_more_than_2_32_routed_positions_doubling(gpu_lib):
     assert [g.gram for g in r2.topk] == [g.gram for g in r1.topk]
     assert [g.count for g in r2.topk] == [2 * g.count for g in r1.topk]
     sess.close()
+
+
+@pytest.mark.parametrize("name,extra,k", [("c2", {"num_seqs": 600, "seq_len": 1 << 20}, 1000),
+                                          ("c1", {}, 1024),
+                                          ("c3", {"total": 700 << 20}, 2000)])
+def test_pipelined_host_load_equals_resident(gpu_lib, name, extra, k):
+    # ig_session_run_host (batched H2D under the dense pass) == load + run
+    base = S.CONFIGS[name]
+    cfg = S.scaled(base, **extra)
+    data, off = S.generate(cfg)
+    corpus = ig.Corpus(data, off)
+    icfg = ig.IntergramConfig(n=base.n, k=k, z=1.5, mode=ig.CountMode(base.mode))
+    s1 = ig.Session(device=0)
+    r1 = s1.load_and_run(corpus, icfg)
+    r1b = s1.run(icfg)  # resident afterwards
+    s1.close()
+    s2 = ig.Session(device=0)
+    s2.load(corpus)
+    r2 = s2.run(icfg)
+    s2.close()
+    assert r1.topk == r2.topk == r1b.topk
+    assert [p.bytes_processed for p in r1.passes] == [p.bytes_processed for p in r2.passes]
