@@ -184,6 +184,57 @@ IG_API int ig_top_k(const uint64_t* table, uint64_t cap, uint64_t k,
              uint64_t* counts_out, uint64_t* len_out, char* err,
              size_t err_len);
 
+/* ---- exact counting paths (sort-based, same sm_100a library) ------------ */
+/* naive_count + naive_topk (proj/src/oracle.cpp:7-47, oracle.hpp:17-27):
+ * exact counts of every n-gram, canonical top-k.  A corpus of more than
+ * max_corpus_bytes is a ConfigError, like the reference's guard; pass
+ * IG_ORACLE_GUARD for the reference default.  out->passes is empty. */
+#define IG_ORACLE_GUARD (256ull << 20)
+IG_API int ig_naive_topk(const ig_corpus* corpus, uint32_t n, uint64_t k, int32_t mode,
+                         uint64_t max_corpus_bytes, int32_t device, ig_result* out,
+                         char* err, size_t err_len);
+
+/* HashgramConfig (hashgram.hpp:19-31).  merge / workers / flush_batch_size /
+ * trie_second_pass never change results and are accepted unused. */
+typedef struct {
+  uint64_t buckets;          /* B */
+  uint32_t n;
+  uint64_t k;
+  int32_t mode;
+  uint64_t seed;
+  uint64_t flush_batch_size;
+  int32_t trie_second_pass;
+  int32_t device;
+} ig_hashgram_params;
+
+/* run_hashgram (hashgram.cpp:325-383): bucket pass, top-k buckets (count
+ * desc, bucket asc), exact pass over grams of kept buckets, top-k grams.
+ * out->passes holds the reference's four rows ("hash pass", "top-k buckets",
+ * "exact pass", "top-k grams"). */
+IG_API int ig_hashgram_topk(const ig_corpus* corpus, const ig_hashgram_params* params,
+                            ig_result* out, char* err, size_t err_len);
+
+/* mix64 (hashgram.cpp:22-59, MurmurHash64A).  Host-only. */
+IG_API uint64_t ig_mix64(const uint8_t* bytes, uint64_t len, uint64_t seed);
+
+/* FeatureMatrix (metrics.hpp:39-46): rows = sequences, cols = vocabulary
+ * entries, (row[i], col[i]) the set entries sorted by row then col. */
+typedef struct {
+  uint64_t rows;
+  uint64_t cols;
+  uint64_t nnz;
+  uint64_t* row;
+  uint32_t* col;
+} ig_matrix;
+
+/* featurize (metrics.cpp:83-132): entry (r, j) when vocabulary gram j (a
+ * packed key of gram_len bytes) occurs in sequence r.  A repeated vocabulary
+ * gram maps to its first column.  Release with ig_matrix_free. */
+IG_API int ig_featurize(const ig_corpus* corpus, const uint64_t* vocab_keys, uint64_t ncols,
+                        uint32_t gram_len, int32_t device, ig_matrix* out, char* err,
+                        size_t err_len);
+IG_API void ig_matrix_free(ig_matrix* m);
+
 /* Byte-balanced whole-sequence shard [*first, *last) of rank r of world w:
  * cut at the sequence boundary nearest r*total/w.  Host-only, no device. */
 IG_API void ig_shard_range(const uint64_t* offsets, uint64_t num_seqs, int32_t rank,

@@ -435,3 +435,202 @@ int igo_naive_topk(const uint8_t* data, const uint64_t* off, uint64_t m,
   free(e);
   return IGO_OK;
 }
+
+/* ------------------------------------------------------ hash-gramming
+ * The two-pass baseline (run_hashgram, hashgram.cpp:325-383).  Bucket
+ * tables are kept sparse here (sorted bucket ids), which gives the same
+ * counts as the reference's dense CountTable(B). */
+
+/* mix64, hashgram.cpp:22-59 (MurmurHash64A over little-endian 8-byte blocks). */
+uint64_t igo_mix64(const uint8_t* bytes, uint64_t len, uint64_t seed) {
+  const uint64_t mm = 0xc6a4a7935bd1e995ULL;
+  const int r = 47;
+  uint64_t h = seed ^ (len * mm);
+  while (len >= 8) {
+    uint64_t k = 0;
+    for (int b = 7; b >= 0; --b) k = (k << 8) | bytes[b];
+    k *= mm;
+    k ^= k >> r;
+    k *= mm;
+    h ^= k;
+    h *= mm;
+    bytes += 8;
+    len -= 8;
+  }
+  uint64_t tail = 0;
+  for (uint64_t i = len; i-- > 0;) tail = (tail << 8) | bytes[i];
+  if (len > 0) {
+    h ^= tail;
+    h *= mm;
+  }
+  h ^= h >> r;
+  h *= mm;
+  h ^= h >> r;
+  return h;
+}
+
+typedef struct {
+  uint32_t n;
+  uint64_t seed, buckets;
+  const uint64_t* kept; /* sorted kept buckets (pass 2), or NULL */
+  uint64_t nkept;
+  int bucket_ids;       /* 1: emit bucket ids (pass 1), 0: emit gram keys */
+} hg_ctx;
+
+static int kept_has(const hg_ctx* c, uint64_t b) {
+  uint64_t lo = 0, hi = c->nkept;
+  while (lo < hi) {
+    uint64_t mid = (lo + hi) / 2;
+    if (c->kept[mid] < b) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo < c->nkept && c->kept[lo] == b;
+}
+
+/* Exact counts of the ids a hash-gramming pass emits; ONCE dedups per
+ * sequence (count_sequences' SeenBitset for pass 1, the last-seen stamp of
+ * MapDictionary for pass 2, hashgram.cpp:136-148).  Returns entries sorted
+ * by id; *ne receives their number. */
+static entry_t* hg_count(const uint8_t* data, const uint64_t* off, uint64_t m,
+                         int mode, const hg_ctx* c, uint64_t* ne) {
+  const uint32_t n = c->n;
+  uint64_t total = 0;
+  for (uint64_t q = 0; q < m; ++q) {
+    uint64_t len = off[q + 1] - off[q];
+    if (len >= n) total += len - n + 1;
+  }
+  uint64_t* ids = (uint64_t*)malloc((total ? total : 1) * sizeof(uint64_t));
+  uint64_t ni = 0;
+  for (uint64_t q = 0; q < m; ++q) {
+    const uint8_t* b = data + off[q];
+    uint64_t len = off[q + 1] - off[q];
+    if (len < n) continue;
+    uint64_t start = ni;
+    for (uint64_t pos = 0; pos + n <= len; ++pos) {
+      uint64_t bucket = igo_mix64(b + pos, n, c->seed) % c->buckets;
+      if (c->bucket_ids) {
+        ids[ni++] = bucket;
+      } else if (kept_has(c, bucket)) {
+        uint64_t key = 0;
+        for (uint32_t i = 0; i < n; ++i) key = (key << 8) | b[pos + i];
+        ids[ni++] = key;
+      }
+    }
+    if (mode == IGO_ONCE) {
+      qsort(ids + start, ni - start, sizeof(uint64_t), cmp_u64);
+      uint64_t u = start;
+      for (uint64_t i = start; i < ni; ++i)
+        if (i == start || ids[i] != ids[i - 1]) ids[u++] = ids[i];
+      ni = u;
+    }
+  }
+  qsort(ids, ni, sizeof(uint64_t), cmp_u64);
+  entry_t* e = (entry_t*)malloc((ni ? ni : 1) * sizeof(entry_t));
+  uint64_t k = 0;
+  for (uint64_t i = 0; i < ni;) {
+    uint64_t j = i;
+    while (j < ni && ids[j] == ids[i]) ++j;
+    e[k].key = ids[i];
+    e[k].count = j - i;
+    ++k;
+    i = j;
+  }
+  free(ids);
+  *ne = k;
+  return e;
+}
+
+int igo_hashgram_topk(const uint8_t* data, const uint64_t* off, uint64_t m,
+                      uint32_t n, uint64_t k, int mode, uint64_t buckets,
+                      uint64_t seed, uint64_t* out_keys, uint64_t* out_counts,
+                      uint64_t* out_len, uint64_t* kept_buckets,
+                      uint64_t* exact_size) {
+  if (buckets < 1 || n < 1 || k < 1 || n > 8) return IGO_CONFIG; /* :16-20 */
+  hg_ctx c = {n, seed, buckets, NULL, 0, 1};
+  uint64_t ne = 0;
+  entry_t* e = hg_count(data, off, m, mode, &c, &ne); /* pass 1, :336-351 */
+  qsort(e, ne, sizeof(entry_t), cmp_canonical);      /* topk_buckets, :74-98 */
+  uint64_t nk = ne < k ? ne : k;
+  uint64_t* kept = (uint64_t*)malloc((nk ? nk : 1) * sizeof(uint64_t));
+  for (uint64_t i = 0; i < nk; ++i) kept[i] = e[i].key;
+  free(e);
+  qsort(kept, nk, sizeof(uint64_t), cmp_u64);
+  *kept_buckets = nk;
+  c.bucket_ids = 0;
+  c.kept = kept;
+  c.nkept = nk;
+  e = hg_count(data, off, m, mode, &c, &ne); /* pass 2, :364-375 */
+  *exact_size = ne;
+  qsort(e, ne, sizeof(entry_t), cmp_canonical); /* naive_topk, :377-380 */
+  uint64_t out = ne < k ? ne : k;
+  for (uint64_t i = 0; i < out; ++i) {
+    out_keys[i] = e[i].key;
+    out_counts[i] = e[i].count;
+  }
+  *out_len = out;
+  free(e);
+  free(kept);
+  return IGO_OK;
+}
+
+/* ---------------------------------------------------------- featurize
+ * metrics.cpp:83-132: entry (row, col) when vocabulary gram col occurs in
+ * sequence row; a repeated vocabulary gram keeps its first column
+ * (columns.emplace, :101-104).  Entries sorted by row then col (:130).
+ * Returns a malloc'd array of (row << 32 | col) (free with igo_free). */
+uint64_t* igo_featurize(const uint8_t* data, const uint64_t* off, uint64_t m,
+                        const uint64_t* vocab, uint64_t ncols, uint32_t n,
+                        uint64_t* nnz) {
+  /* sorted (key, first column) pairs */
+  entry_t* v = (entry_t*)malloc((ncols ? ncols : 1) * sizeof(entry_t));
+  for (uint64_t j = 0; j < ncols; ++j) {
+    v[j].key = vocab[j];
+    v[j].count = j; /* column */
+  }
+  /* stable by key then column: sort on (key, column) */
+  for (uint64_t a = 1; a < ncols; ++a) { /* insertion sort is fine for tests */
+    entry_t t = v[a];
+    uint64_t b = a;
+    while (b > 0 && (v[b - 1].key > t.key ||
+                     (v[b - 1].key == t.key && v[b - 1].count > t.count))) {
+      v[b] = v[b - 1];
+      --b;
+    }
+    v[b] = t;
+  }
+  uint64_t cap = 1024, cnt = 0;
+  uint64_t* out = (uint64_t*)malloc(cap * sizeof(uint64_t));
+  for (uint64_t q = 0; q < m && ncols; ++q) {
+    const uint8_t* b = data + off[q];
+    uint64_t len = off[q + 1] - off[q];
+    if (len < n) continue;
+    uint64_t start = cnt;
+    for (uint64_t pos = 0; pos + n <= len; ++pos) {
+      uint64_t key = 0;
+      for (uint32_t i = 0; i < n; ++i) key = (key << 8) | b[pos + i];
+      uint64_t lo = 0, hi = ncols;
+      while (lo < hi) {
+        uint64_t mid = (lo + hi) / 2;
+        if (v[mid].key < key) lo = mid + 1;
+        else hi = mid;
+      }
+      if (lo < ncols && v[lo].key == key) {
+        if (cnt == cap) {
+          cap *= 2;
+          out = (uint64_t*)realloc(out, cap * sizeof(uint64_t));
+        }
+        out[cnt++] = (q << 32) | v[lo].count;
+      }
+    }
+    qsort(out + start, cnt - start, sizeof(uint64_t), cmp_u64);
+    uint64_t u = start;
+    for (uint64_t i = start; i < cnt; ++i)
+      if (i == start || out[i] != out[i - 1]) out[u++] = out[i];
+    cnt = u;
+  }
+  free(v);
+  *nnz = cnt;
+  return out;
+}
+
+void igo_free(void* p) { free(p); }

@@ -90,6 +90,22 @@ int igo_naive_topk(const uint8_t* data, const uint64_t* off, uint64_t m,
                    uint32_t n, int mode, uint64_t k, uint64_t* out_keys,
                    uint64_t* out_counts, uint64_t* out_len);
 
+/* run_hashgram (hashgram.cpp:325-383) for n <= 8: top-k grams plus the
+ * retained counts of its "top-k buckets" and "exact pass" rows. */
+uint64_t igo_mix64(const uint8_t* bytes, uint64_t len, uint64_t seed);
+int igo_hashgram_topk(const uint8_t* data, const uint64_t* off, uint64_t m,
+                      uint32_t n, uint64_t k, int mode, uint64_t buckets,
+                      uint64_t seed, uint64_t* out_keys, uint64_t* out_counts,
+                      uint64_t* out_len, uint64_t* kept_buckets,
+                      uint64_t* exact_size);
+
+/* featurize (metrics.cpp:83-132) for grams of n <= 8 bytes: malloc'd
+ * (row << 32 | col) entries sorted by row then col; free with igo_free. */
+uint64_t* igo_featurize(const uint8_t* data, const uint64_t* off, uint64_t m,
+                        const uint64_t* vocab, uint64_t ncols, uint32_t n,
+                        uint64_t* nnz);
+void igo_free(void* p);
+
 #ifdef __cplusplus
 }
 #endif

@@ -81,6 +81,16 @@ def c_oracle() -> C.CDLL:
                                          C.c_char_p, C.c_size_t]
         L.igo_naive_topk.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32, C.c_int,
                                      C.c_uint64, C.c_void_p, C.c_void_p, C.POINTER(C.c_uint64)]
+        L.igo_mix64.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64]
+        L.igo_mix64.restype = C.c_uint64
+        L.igo_hashgram_topk.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32,
+                                        C.c_uint64, C.c_int, C.c_uint64, C.c_uint64, C.c_void_p,
+                                        C.c_void_p, C.POINTER(C.c_uint64),
+                                        C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
+        L.igo_featurize.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64,
+                                    C.c_uint32, C.POINTER(C.c_uint64)]
+        L.igo_featurize.restype = C.c_void_p
+        L.igo_free.argtypes = [C.c_void_p]
         _oracle = L
     return _oracle
 
@@ -111,6 +121,20 @@ def ref() -> C.CDLL:
         L.igref_naive_topk.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32, C.c_int,
                                        C.c_uint64, C.c_void_p, C.c_void_p,
                                        C.POINTER(C.c_uint64), C.c_char_p, C.c_size_t]
+        L.igref_mix64.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64]
+        L.igref_mix64.restype = C.c_uint64
+        L.igref_hashgram.argtypes = [
+            C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32, C.c_uint64, C.c_int, C.c_uint64,
+            C.c_uint64, C.c_uint32, C.c_int, C.c_void_p, C.c_void_p, C.POINTER(C.c_uint64),
+            C.c_void_p, C.c_uint32, C.POINTER(C.c_uint32), C.c_char_p, C.c_size_t]
+        L.igref_featurize.argtypes = [
+            C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64, C.c_uint32, C.c_uint32,
+            C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.c_char_p,
+            C.c_size_t]
+        L.igref_jaccard_tsv.argtypes = [C.c_char_p, C.c_char_p]
+        L.igref_jaccard_tsv.restype = C.c_double
+        L.igref_report.argtypes = [C.c_char_p, C.c_char_p, C.c_void_p, C.c_uint32, C.c_int,
+                                   C.c_double, C.c_int, C.c_char_p, C.c_size_t]
         _ref = L
     return _ref
 
@@ -273,3 +297,99 @@ def ref_naive(data, off, n: int, mode: int, k: int):
     keys = np.array([int.from_bytes(grams[i * n:(i + 1) * n].tobytes(), "big") for i in range(m)],
                     dtype=np.uint64)
     return keys, counts[:m]
+
+
+# ------------------------------------------------------- hash-gramming / featurize
+
+def oracle_mix64(b: bytes, seed: int) -> int:
+    buf = np.frombuffer(b + b"\0", np.uint8)
+    return int(c_oracle().igo_mix64(buf.ctypes.data, len(b), seed))
+
+
+def oracle_hashgram(data, off, n: int, k: int, mode: int, buckets: int, seed: int):
+    """igo_hashgram_topk -> (rc, keys, counts, kept_buckets, exact_size)."""
+    keys = np.zeros(k, np.uint64)
+    counts = np.zeros(k, np.uint64)
+    ln, kept, ex = C.c_uint64(0), C.c_uint64(0), C.c_uint64(0)
+    rc = c_oracle().igo_hashgram_topk(_ptr(data), off.ctypes.data, off.size - 1, n, k, mode,
+                                      buckets, seed, keys.ctypes.data, counts.ctypes.data,
+                                      C.byref(ln), C.byref(kept), C.byref(ex))
+    return rc, keys[:ln.value], counts[:ln.value], kept.value, ex.value
+
+
+def oracle_featurize(data, off, vocab_keys, n: int) -> np.ndarray:
+    """igo_featurize -> sorted (row << 32 | col) entries."""
+    v = np.ascontiguousarray(vocab_keys, np.uint64)
+    nnz = C.c_uint64(0)
+    L = c_oracle()
+    p = L.igo_featurize(_ptr(data), off.ctypes.data, off.size - 1, _ptr(v), v.size, n,
+                        C.byref(nnz))
+    out = np.ctypeslib.as_array(C.cast(p, C.POINTER(C.c_uint64)), (max(nnz.value, 1),))
+    out = out[:nnz.value].copy()
+    L.igo_free(p)
+    return out
+
+
+def ref_mix64(b: bytes, seed: int) -> int:
+    buf = np.frombuffer(b + b"\0", np.uint8)
+    return int(ref().igref_mix64(buf.ctypes.data, len(b), seed))
+
+
+def ref_hashgram(data, off, n: int, k: int, mode: int, buckets: int, seed: int,
+                 workers: int = 1, trie: bool = False):
+    """ig_ref::run_hashgram -> (rc, keys, counts, rows, err)."""
+    grams = np.zeros(max(k * n, 1), np.uint8)
+    counts = np.zeros(k, np.uint64)
+    ln = C.c_uint64(0)
+    passes = (igref_pass * 8)()
+    np_ = C.c_uint32(0)
+    err = C.create_string_buffer(512)
+    rc = ref().igref_hashgram(_ptr(data), off.ctypes.data, off.size - 1, n, k, mode, buckets,
+                              seed, workers, int(trie), grams.ctypes.data, counts.ctypes.data,
+                              C.byref(ln), passes, 8, C.byref(np_), err, len(err))
+    m = ln.value
+    keys = np.array([int.from_bytes(grams[i * n:(i + 1) * n].tobytes(), "big") for i in range(m)],
+                    dtype=np.uint64)
+    rows = [dict(label=passes[i].label.decode(), gram_len=passes[i].gram_len,
+                 seconds=passes[i].seconds, bytes_processed=passes[i].bytes_processed,
+                 candidate_space=passes[i].candidate_space, retained=passes[i].retained,
+                 retained_short=bool(passes[i].retained_short)) for i in range(np_.value)]
+    return rc, keys, counts[:m], rows, err.value.decode()
+
+
+def ref_featurize(data, off, vocab: Sequence[bytes], workers: int = 1):
+    """ig_ref::featurize -> (rc, entries (row << 32 | col), rows, err)."""
+    n = len(vocab[0]) if vocab else 0
+    flat = np.frombuffer(b"".join(vocab) + b"\0", np.uint8)[:-1].copy()
+    cap = int(off[-1]) + int(off.size) + 16
+    ent = np.zeros(cap, np.uint64)
+    nnz, rows = C.c_uint64(0), C.c_uint64(0)
+    err = C.create_string_buffer(512)
+    rc = ref().igref_featurize(_ptr(data), off.ctypes.data, off.size - 1, _ptr(flat), len(vocab),
+                               n, workers, ent.ctypes.data, cap, C.byref(nnz), C.byref(rows), err,
+                               len(err))
+    return rc, ent[:nnz.value].copy(), rows.value, err.value.decode()
+
+
+def ref_jaccard_tsv(a: str, b: str) -> float:
+    return float(ref().igref_jaccard_tsv(a.encode(), b.encode()))
+
+
+def ref_report(algorithm: str, echo: str, rows, jaccard: Optional[float] = None,
+               json: bool = False) -> str:
+    """RunReport(algorithm, echo, rows).to_tsv() / to_json() of the reference."""
+    arr = (igref_pass * max(len(rows), 1))()
+    for i, r in enumerate(rows):
+        arr[i].label = r["label"].encode()
+        arr[i].gram_len = r["gram_len"]
+        arr[i].seconds = r["seconds"]
+        arr[i].bytes_processed = r["bytes_processed"]
+        arr[i].candidate_space = r["candidate_space"]
+        arr[i].retained = r["retained"]
+        arr[i].retained_short = int(r["retained_short"])
+    out = C.create_string_buffer(1 << 20)
+    rc = ref().igref_report(algorithm.encode(), echo.encode(), arr, len(rows),
+                            int(jaccard is not None), float(jaccard or 0.0), int(json), out,
+                            len(out))
+    assert rc == 0, out.value
+    return out.value.decode()

@@ -9,6 +9,10 @@
 //   count_dense      proj/src/dense_pass.cpp:21-39
 //   extend_pass      proj/src/intergrams.cpp:44-66
 //   naive_count/topk proj/src/oracle.cpp:7-47
+//   run_hashgram     proj/src/hashgram.cpp:325-383 (and mix64 :22-59)
+//   featurize        proj/src/metrics.cpp:83-132
+//   jaccard          proj/src/metrics.cpp:16-31
+//   RunReport        proj/src/metrics.cpp:134-200 (to_tsv / to_json)
 // No reference source is copied into this repository.
 #include <chrono>
 #include <cstdint>
@@ -19,6 +23,8 @@
 #include <vector>
 
 #include "intergrams/dense_pass.hpp"
+#include "intergrams/hashgram.hpp"
+#include "intergrams/metrics.hpp"
 #include "intergrams/intergrams.hpp"
 #include "intergrams/oracle.hpp"
 
@@ -182,6 +188,100 @@ int igref_naive_topk(const uint8_t* data, const uint64_t* off, uint64_t m,
       std::memcpy(grams + i * n, top[i].gram.data(), n);
       counts[i] = top[i].count;
     }
+  });
+}
+
+uint64_t igref_mix64(const uint8_t* bytes, uint64_t len, uint64_t seed) {
+  return mix64(std::string_view(reinterpret_cast<const char*>(bytes), len), seed);
+}
+
+// ig_ref::run_hashgram.  grams: k*n bytes.
+int igref_hashgram(const uint8_t* data, const uint64_t* off, uint64_t m,
+                   uint32_t n, uint64_t k, int mode, uint64_t buckets,
+                   uint64_t seed, uint32_t workers, int trie, uint8_t* grams,
+                   uint64_t* counts, uint64_t* out_len, igref_pass* passes,
+                   uint32_t max_passes, uint32_t* num_passes, char* err,
+                   size_t err_len) {
+  return guarded(err, err_len, [&] {
+    const Corpus corpus = make_corpus(data, off, m);
+    HashgramConfig cfg;
+    cfg.buckets = buckets;
+    cfg.n = n;
+    cfg.k = k;
+    cfg.mode = to_mode(mode);
+    cfg.seed = seed;
+    cfg.workers = workers ? workers : 1;
+    cfg.trie_second_pass = trie != 0;
+    const HashgramResult r = run_hashgram(corpus, cfg);
+    *out_len = r.topk.size();
+    for (size_t i = 0; i < r.topk.size(); ++i) {
+      std::memcpy(grams + i * n, r.topk[i].gram.data(), n);
+      counts[i] = r.topk[i].count;
+    }
+    uint32_t np = 0;
+    for (const auto& p : r.passes) {
+      if (np >= max_passes) break;
+      igref_pass& o = passes[np++];
+      std::memset(&o, 0, sizeof(o));
+      std::strncpy(o.label, p.label.c_str(), sizeof(o.label) - 1);
+      o.gram_len = static_cast<uint32_t>(p.gram_len);
+      o.seconds = p.seconds;
+      o.bytes_processed = p.bytes_processed;
+      o.candidate_space = p.candidate_space;
+      o.retained = p.retained;
+      o.retained_short = p.retained_short;
+    }
+    *num_passes = np;
+  });
+}
+
+// ig_ref::featurize.  vocab: ncols grams of n bytes.  entries: (row << 32) |
+// col, capacity cap; *nnz the number written; *rows the matrix rows.
+int igref_featurize(const uint8_t* data, const uint64_t* off, uint64_t m,
+                    const uint8_t* vocab, uint64_t ncols, uint32_t n,
+                    uint32_t workers, uint64_t* entries, uint64_t cap,
+                    uint64_t* nnz, uint64_t* rows, char* err, size_t err_len) {
+  return guarded(err, err_len, [&] {
+    const Corpus corpus = make_corpus(data, off, m);
+    TopKList v;
+    for (uint64_t j = 0; j < ncols; ++j)
+      v.push_back(GramCount{std::string(reinterpret_cast<const char*>(vocab + j * n), n), 1});
+    const FeatureMatrix mat = featurize(corpus, v, workers ? workers : 1);
+    if (mat.entries.size() > cap) throw std::runtime_error("entries capacity too small");
+    for (size_t i = 0; i < mat.entries.size(); ++i)
+      entries[i] = (mat.entries[i].first << 32) | mat.entries[i].second;
+    *nnz = mat.entries.size();
+    *rows = mat.rows;
+  });
+}
+
+// ig_ref::jaccard of two result TSV texts.
+double igref_jaccard_tsv(const char* a, const char* b) {
+  return jaccard(topk_from_tsv(a), topk_from_tsv(b));
+}
+
+// RunReport::to_tsv / to_json (json != 0) of the given rows into out.
+int igref_report(const char* algorithm, const char* echo, const igref_pass* passes,
+                 uint32_t np, int has_jaccard, double jacc, int json, char* out,
+                 size_t out_len) {
+  return guarded(out, out_len, [&] {
+    std::vector<PassResult> rows;
+    for (uint32_t i = 0; i < np; ++i) {
+      PassResult r;
+      r.label = passes[i].label;
+      r.gram_len = passes[i].gram_len;
+      r.seconds = passes[i].seconds;
+      r.bytes_processed = passes[i].bytes_processed;
+      r.candidate_space = passes[i].candidate_space;
+      r.retained = passes[i].retained;
+      r.retained_short = passes[i].retained_short != 0;
+      rows.push_back(r);
+    }
+    RunReport rep = make_report(algorithm, echo, rows);
+    if (has_jaccard) rep.jaccard_vs_reference = jacc;
+    const std::string s = json ? rep.to_json() : rep.to_tsv();
+    if (s.size() + 1 > out_len) throw std::runtime_error("report buffer too small");
+    std::memcpy(out, s.c_str(), s.size() + 1);
   });
 }
 

@@ -44,6 +44,19 @@ class ig_result(C.Structure):
                 ("diagnostics", C.c_char_p)]
 
 
+class ig_hashgram_params(C.Structure):
+    _fields_ = [("buckets", C.c_uint64), ("n", C.c_uint32), ("k", C.c_uint64),
+                ("mode", C.c_int32), ("seed", C.c_uint64), ("flush_batch_size", C.c_uint64),
+                ("trie_second_pass", C.c_int32), ("device", C.c_int32)]
+
+
+class ig_matrix(C.Structure):
+    _fields_ = [("rows", C.c_uint64), ("cols", C.c_uint64), ("nnz", C.c_uint64),
+                ("row", C.POINTER(C.c_uint64)), ("col", C.POINTER(C.c_uint32))]
+
+
+IG_ORACLE_GUARD = 256 << 20
+
 ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_uint64, C.c_int32, C.c_void_p, C.c_void_p)
 
 
@@ -78,6 +91,15 @@ SYMBOLS = [
     ("ig_top_k", C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p, C.c_int32,
                            C.c_void_p, C.c_void_p, C.POINTER(C.c_uint64), C.c_char_p,
                            C.c_size_t]),
+    ("ig_naive_topk", C.c_int, [C.POINTER(ig_corpus), C.c_uint32, C.c_uint64, C.c_int32,
+                                C.c_uint64, C.c_int32, C.POINTER(ig_result), C.c_char_p,
+                                C.c_size_t]),
+    ("ig_hashgram_topk", C.c_int, [C.POINTER(ig_corpus), C.POINTER(ig_hashgram_params),
+                                   C.POINTER(ig_result), C.c_char_p, C.c_size_t]),
+    ("ig_mix64", C.c_uint64, [C.c_void_p, C.c_uint64, C.c_uint64]),
+    ("ig_featurize", C.c_int, [C.POINTER(ig_corpus), C.c_void_p, C.c_uint64, C.c_uint32,
+                               C.c_int32, C.POINTER(ig_matrix), C.c_char_p, C.c_size_t]),
+    ("ig_matrix_free", None, [C.POINTER(ig_matrix)]),
     ("ig_shard_range", None, [C.c_void_p, C.c_uint64, C.c_int32, C.c_int32,
                               C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     ("ig_version", C.c_char_p, []),

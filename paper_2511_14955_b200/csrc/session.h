@@ -1,0 +1,153 @@
+// session.h — the session object behind the C handle, shared by the
+// Intergrams driver (session.cu) and the exact/hashgram/featurize paths
+// (exact.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "ig_internal.cuh"
+#include "kernels.h"
+
+namespace igb {
+
+// Buffers of the sort-based exact counter (exact.cu).
+struct ExactBufs {
+  DevBuf keys, keys2, vals, vals2, chunk_cnt, chunk_base, uniq, runs, nruns, flags;
+  DevBuf acc_keys, acc_counts, mrg_keys, mrg_counts, mrg_keys2, mrg_counts2;
+  DevBuf kept, vocab_keys, vocab_cols, cub_tmp;
+};
+
+struct Session {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  bool has_coll = false;
+  ig_collective coll{};
+  int num_sms = 148;
+  uint64_t launches = 0;
+
+  // corpus
+  DevBuf data, off, tile, order;
+  DevCorpus dc;
+  bool loaded = false;
+
+  // pass buffers
+  DevBuf table, work, scratch32;
+  DevBuf surv_keys, surv_counts, next_keys, next_counts;
+  DevBuf pkeys, hkeys, hidx, hpacked, owner, owner_cnt, owner_start, cursor, rank_of_p;
+  DevBuf sel_state, sel_hist, sel_scalar, units, unit_first;
+  SelectCtx sel;
+  ExactBufs ex;
+  RouteCtx rc;
+  KernelTimer kt;
+  // pipelined host load: the dense pass runs batch by batch as the H2D copies land
+  struct Batch {
+    uint64_t t0, t1;           // count-all tiles whose bytes are all in the batch
+    uint32_t u0, u1, q0, q1;   // count-once units / sequences
+    cudaEvent_t ready;         // copy of the batch's bytes done (null: resident)
+  };
+  std::vector<Batch> batches;
+  std::vector<cudaEvent_t> batch_events;
+  std::vector<uint64_t> hoff;  // host offsets of the loaded corpus
+  std::vector<uint32_t> hufirst;
+  cudaStream_t copy_stream = nullptr;
+  std::vector<cudaEvent_t> events;
+
+  ~Session() {
+    for (auto e : events) cudaEventDestroy(e);
+    for (auto e : batch_events) cudaEventDestroy(e);
+    if (copy_stream) cudaStreamDestroy(copy_stream);
+    if (own_stream && stream) cudaStreamDestroy(stream);
+  }
+};
+
+inline void set_err(char* err, size_t len, const char* msg) {
+  if (err && len) {
+    strncpy(err, msg, len - 1);
+    err[len - 1] = 0;
+  }
+}
+
+template <typename F>
+inline int guarded(char* err, size_t len, F&& f) {
+  try {
+    f();
+    if (err && len) err[0] = 0;
+    return IG_OK;
+  } catch (const Error& e) {
+    set_err(err, len, e.what());
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    set_err(err, len, "host allocation failed");
+    return IG_EINTERNAL;
+  } catch (const std::exception& e) {
+    set_err(err, len, e.what());
+    return IG_EINTERNAL;
+  }
+}
+
+
+// Event pair per step; elapsed read at the end of the run.
+struct StepTimer {
+  Session& s;
+  size_t next = 0;
+  explicit StepTimer(Session& ss) : s(ss) {}
+  size_t begin() {
+    if (next + 2 > s.events.size()) {
+      for (int i = 0; i < 16; ++i) {
+        cudaEvent_t e;
+        IGB_CUDA(cudaEventCreate(&e));
+        s.events.push_back(e);
+      }
+    }
+    IGB_CUDA(cudaEventRecord(s.events[next], s.stream));
+    next += 2;
+    return next - 2;
+  }
+  void end(size_t i) { IGB_CUDA(cudaEventRecord(s.events[i + 1], s.stream)); }
+  double seconds(size_t i) {
+    float ms = 0;
+    IGB_CUDA(cudaEventSynchronize(s.events[i + 1]));
+    IGB_CUDA(cudaEventElapsedTime(&ms, s.events[i], s.events[i + 1]));
+    return ms * 1e-3;
+  }
+};
+
+struct Row {
+  ig_pass_stat st;
+  size_t ev;
+};
+
+inline Row make_row(const std::string& label, uint32_t gl, uint64_t bytes, uint64_t cap,
+                    uint64_t retained, bool shrt, size_t ev) {
+  Row r;
+  memset(&r.st, 0, sizeof(r.st));
+  snprintf(r.st.label, sizeof(r.st.label), "%s", label.c_str());
+  r.st.gram_len = gl;
+  r.st.bytes_processed = bytes;
+  r.st.candidate_space = cap;
+  r.st.retained = retained;
+  r.st.retained_short = shrt ? 1 : 0;
+  r.ev = ev;
+  return r;
+}
+
+void use_device(Session& s);
+void validate(const ig_params& p);
+void load_corpus(Session& s, const ig_corpus& c, bool copy_data = true);
+void init_select(Session& s);
+
+}  // namespace igb
+
+// The opaque C handle.
+struct ig_session : igb::Session {};
+
+namespace igb {
+ig_session* create(int32_t device, void* stream, const ig_collective* coll);
+}  // namespace igb

@@ -9,6 +9,8 @@ tests read like its own doctest suite:
   CountMode         counting.hpp:19           top_k           counting.hpp:112-113
   GramCount         counting.hpp:27-33        candidate_id    intergrams.hpp:56-59
   ConfigError/IoError common.hpp:12-22        make_memory_corpus corpus.hpp:67
+  naive_topk        oracle.cpp:7-47           run_hashgram    hashgram.hpp:19-75
+  featurize         metrics.hpp:39-49         mix64           hashgram.hpp:33-39
 
 Every call goes through the C-ABI (include/intergrams_b200.h) into the sm_100a
 kernels; nothing here computes counts on the CPU.
@@ -328,6 +330,127 @@ def run_result_topk(r: IntergramsResult, n: int) -> List[GramCount]:
 def topk_to_tsv(topk: Sequence[GramCount]) -> str:
     """metrics.cpp:202-211: lowercase hex, TAB, decimal count, LF."""
     return "".join(f"{g.gram.hex()}\t{g.count}\n" for g in topk)
+
+
+# ------------------------------------------------- exact / hashgram / featurize
+
+kOracleCorpusGuard = N.IG_ORACLE_GUARD  # oracle.hpp:17
+
+
+def naive_topk(corpus, n: int, mode: CountMode, k: int,
+               max_corpus_bytes: int = kOracleCorpusGuard, device: int = -1) -> List[GramCount]:
+    """naive_topk(naive_count(corpus, n, mode, guard), k) (oracle.cpp:7-47),
+    counted exactly on the GPU (sort + run-length reduction)."""
+    c = as_corpus(corpus)
+    err = C.create_string_buffer(1024)
+    out = N.ig_result()
+    view = c._view()
+    rc = N.lib().ig_naive_topk(C.byref(view), int(n), int(k), int(mode), int(max_corpus_bytes),
+                               device, C.byref(out), err, len(err))
+    _raise(rc, err)
+    try:
+        return _result(out).topk
+    finally:
+        N.lib().ig_result_free(C.byref(out))
+
+
+@dataclass
+class HashgramConfig:
+    """hashgram.hpp:19-31 (same defaults)."""
+    buckets: int = 1 << 31
+    n: int = 6
+    k: int = 10000
+    mode: CountMode = CountMode.kOnce
+    seed: int = 0
+    merge: MergeStrategy = MergeStrategy.kBatchedFlush
+    workers: int = 1
+    flush_batch_size: int = 8
+    trie_second_pass: bool = False
+    device: int = -1
+
+
+@dataclass
+class HashgramResult:
+    """hashgram.hpp:69-72."""
+    topk: List[GramCount]
+    passes: List[PassResult]
+
+
+def run_hashgram(corpus, cfg: HashgramConfig) -> HashgramResult:
+    """run_hashgram (hashgram.cpp:325-383) on the GPU."""
+    c = as_corpus(corpus)
+    p = N.ig_hashgram_params(buckets=int(cfg.buckets), n=int(cfg.n), k=int(cfg.k),
+                             mode=int(cfg.mode), seed=int(cfg.seed),
+                             flush_batch_size=int(cfg.flush_batch_size),
+                             trie_second_pass=int(bool(cfg.trie_second_pass)),
+                             device=int(cfg.device))
+    err = C.create_string_buffer(1024)
+    out = N.ig_result()
+    view = c._view()
+    rc = N.lib().ig_hashgram_topk(C.byref(view), C.byref(p), C.byref(out), err, len(err))
+    _raise(rc, err)
+    try:
+        r = _result(out)
+        return HashgramResult(r.topk, r.passes)
+    finally:
+        N.lib().ig_result_free(C.byref(out))
+
+
+def mix64(gram: bytes, seed: int) -> int:
+    """mix64 (hashgram.cpp:22-59), host-side."""
+    buf = (C.c_uint8 * max(len(gram), 1)).from_buffer_copy(gram or b"\0")
+    return int(N.lib().ig_mix64(C.addressof(buf), len(gram), seed))
+
+
+def hash_ngram(gram: bytes, seed: int, buckets: int) -> int:
+    """hashgram.hpp:36-39."""
+    return mix64(gram, seed) % buckets
+
+
+class FeatureMatrix:
+    """metrics.hpp:39-46: (row, col) entries sorted by row then col, held as
+    numpy arrays (``row``, ``col``); ``entries`` materialises the pair list."""
+
+    def __init__(self, rows: int, cols: int, row: np.ndarray, col: np.ndarray):
+        self.rows = rows
+        self.cols = cols
+        self.row = row
+        self.col = col
+
+    @property
+    def entries(self) -> List[Tuple[int, int]]:
+        return list(zip(self.row.tolist(), self.col.tolist()))
+
+    def column_popcounts(self) -> List[int]:
+        """metrics.cpp:77-81."""
+        return np.bincount(self.col.astype(np.int64), minlength=self.cols).tolist()
+
+
+def featurize(corpus, vocab: Sequence[GramCount], workers: int = 1,
+              device: int = -1) -> FeatureMatrix:
+    """featurize (metrics.cpp:83-132) on the GPU.  `workers` has no GPU meaning."""
+    c = as_corpus(corpus)
+    grams = [g.gram if isinstance(g, GramCount) else bytes(g) for g in vocab]
+    n = len(grams[0]) if grams else 0
+    for g in grams:
+        if len(g) != n:
+            raise ValueError("featurize: vocab grams must share one length")
+    if grams and n > N.IG_MAX_N:
+        raise ConfigError("featurize: gram length above 8 is not supported by the GPU path")
+    keys = np.array([gram_to_key(g) for g in grams], dtype=np.uint64)
+    err = C.create_string_buffer(1024)
+    out = N.ig_matrix()
+    view = c._view()
+    rc = N.lib().ig_featurize(C.byref(view), keys.ctypes.data if keys.size else None,
+                              len(grams), n, device, C.byref(out), err, len(err))
+    _raise(rc, err)
+    try:
+        nnz = int(out.nnz)
+        rows = np.ctypeslib.as_array(out.row, shape=(nnz,)).copy() if nnz else np.zeros(0, np.uint64)
+        cols = np.ctypeslib.as_array(out.col, shape=(nnz,)).copy() if nnz else np.zeros(0, np.uint32)
+        return FeatureMatrix(int(out.rows), int(out.cols), rows, cols)
+    finally:
+        N.lib().ig_matrix_free(C.byref(out))
 
 
 # ----------------------------------------------------------------- session

@@ -124,9 +124,67 @@ def main():
                 tables.append({"corpus": rec, "n": n, "mode": mode,
                                "sha256": hashlib.sha256(t.astype("<u8").tobytes()).hexdigest(),
                                "total": int(t.sum()), "nonzero": int((t != 0).sum())})
+    # hash-gramming (run_hashgram, hashgram.cpp:325-383) and featurize
+    # (metrics.cpp:83-132), §8(f) rows 3-4
+    hashgram = []
+    seed = 9100
+    for n in (1, 2, 3, 4, 6, 8):
+        for mode in (ONCE, ALL):
+            for B, k, hseed in ((1, 3, 0), (7, 4, 1), (97, 10, 0), (1 << 20, 25, 12345),
+                                (1 << 31, 40, 0), (1 << 40, 30, 99)):
+                seed += 1
+                if B > (1 << 33):  # the reference's dense CountTable(B) cannot be allocated
+                    continue
+                rec = {"kind": "random", "seed": seed, "max_m": 10, "max_len": 300,
+                       "alphabet": 5 if n > 3 else 64}
+                data, off = corpus_from(rec)
+                rc, keys, counts, rows, err = O.ref_hashgram(data, off, n, k, mode, B, hseed)
+                case = {"corpus": rec, "n": n, "k": k, "mode": mode, "buckets": B,
+                        "seed": hseed, "rc": rc}
+                if rc == 0:
+                    case["tsv"] = tsv(keys, counts, n)
+                    case["passes"] = [{kk: r[kk] for kk in ("label", "gram_len",
+                                                             "bytes_processed",
+                                                             "candidate_space", "retained",
+                                                             "retained_short")} for r in rows]
+                hashgram.append(case)
+    mix = []
+    for s in (b"", b"a", b"ab", b"abcdefg", b"abcdefgh", b"abcdefghi", bytes(range(200, 217))):
+        for hs in (0, 1, 0xDEADBEEF, (1 << 64) - 1):
+            mix.append({"hex": s.hex(), "seed": hs, "mix64": O.ref_mix64(s, hs)})
+    feats = []
+    seed = 9500
+    for n in (1, 2, 3, 4, 5, 8):
+        for vocab_kind in ("sampled", "with_dups", "absent"):
+            seed += 1
+            rec = {"kind": "random", "seed": seed, "max_m": 16, "max_len": 250, "alphabet": 4}
+            data, off = corpus_from(rec)
+            seqs = [bytes(data[int(off[i]):int(off[i + 1])]) for i in range(off.size - 1)]
+            grams = sorted({s[i:i + n] for s in seqs for i in range(0, max(len(s) - n + 1, 0), 5)})
+            vocab = grams[: 12]
+            if vocab_kind == "with_dups":
+                vocab = vocab + vocab[:4][::-1]
+            elif vocab_kind == "absent":
+                vocab = [bytes([250 + (i % 6)]) * n for i in range(3)] + vocab[:2]
+            rc, ent, nrows, err = O.ref_featurize(data, off, vocab)
+            feats.append({"corpus": rec, "n": n, "vocab": [v.hex() for v in vocab], "rc": rc,
+                          "rows": nrows, "entries": [int(e) for e in ent]})
+    rec = {"kind": "literal", "hex": [b"abcabc".hex(), b"".hex(), b"xyz".hex()]}
+    data, off = corpus_from(rec)
+    rc, ent, nrows, err = O.ref_featurize(data, off, [b"bc", b"ab", b"zz", b"bc"])
+    feats.append({"corpus": rec, "n": 2, "vocab": ["6263", "6162", "7a7a", "6263"], "rc": rc,
+                  "rows": nrows, "entries": [int(e) for e in ent]})
+    rc, ent, nrows, err = O.ref_featurize(data, off, [])
+    feats.append({"corpus": rec, "n": 0, "vocab": [], "rc": rc, "rows": nrows,
+                  "entries": [int(e) for e in ent]})
     out = {"generator": "tests/golden/make_golden.py (reference compiled from "
                         "/root/reference/proj/src via oracle/Makefile)",
            "cases": cases, "dense_tables": tables}
+    extra = {"generator": out["generator"], "hashgram": hashgram, "mix64": mix,
+             "featurize": feats}
+    with open(os.path.join(ROOT, "tests", "golden", "golden_extra.json"), "w") as f:
+        json.dump(extra, f, indent=1)
+    print(f"wrote {len(hashgram)} hashgram, {len(mix)} mix64, {len(feats)} featurize cases")
     path = os.path.join(ROOT, "tests", "golden", "golden.json")
     with open(path, "w") as f:
         json.dump(out, f, indent=1)
