@@ -186,7 +186,7 @@ inline std::string json_double(double x) {
   out += d.substr(0, 1);
   if (k > 1) out += "." + d.substr(1);
   const int e = n - 1;
-  char eb[8];
+  char eb[16];
   std::snprintf(eb, sizeof(eb), "e%c%02d", e < 0 ? '-' : '+', e < 0 ? -e : e);
   return out + eb;
 }

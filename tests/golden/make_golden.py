@@ -180,8 +180,28 @@ def main():
     out = {"generator": "tests/golden/make_golden.py (reference compiled from "
                         "/root/reference/proj/src via oracle/Makefile)",
            "cases": cases, "dense_tables": tables}
+    # RunReport::to_tsv / to_json (metrics.cpp:134-200) of fixed rows, incl.
+    # doubles that exercise every branch of the JSON number formatting
+    reports = []
+    secs = [0.0, 1.5, 2.0, 0.1 + 0.2, 1e-5, 3.25e-7, 123456.789, 1e15, 1e16, 1.2345678901234567e21,
+            0.0001, 0.00012345, 7.0 / 3.0, 1e-300, 5e-324, 9007199254740993.0, 42.0]
+    for i in range(0, len(secs), 3):
+        rows = [dict(label=f"{3 + j}-gram pass" if j % 2 == 0 else f"top-zk {3 + j}-grams/trie building",
+                     gram_len=3 + j, seconds=s, bytes_processed=(j + 1) * 1000003 if j % 2 == 0 else 0,
+                     candidate_space=1 << (8 + j), retained=17 * j, retained_short=j % 3 == 1)
+                for j, s in enumerate(secs[i:i + 3])]
+        for js in (False, True):
+            for jac in (None, 0.123456789, 1.0):
+                reports.append({"algorithm": "intergrams", "echo": "algorithm=intergrams n=6 k=10 z=1.5",
+                                "rows": [dict(r, seconds=r["seconds"].hex()) for r in rows],
+                                "json": js, "jaccard": None if jac is None else jac.hex(),
+                                "text": O.ref_report("intergrams", "algorithm=intergrams n=6 k=10 z=1.5",
+                                                     rows, jac, js)})
+    reports.append({"algorithm": "naive", "echo": "algorithm=naive n=3 k=2 mode=once", "rows": [],
+                    "json": True, "jaccard": None,
+                    "text": O.ref_report("naive", "algorithm=naive n=3 k=2 mode=once", [], None, True)})
     extra = {"generator": out["generator"], "hashgram": hashgram, "mix64": mix,
-             "featurize": feats}
+             "featurize": feats, "reports": reports}
     with open(os.path.join(ROOT, "tests", "golden", "golden_extra.json"), "w") as f:
         json.dump(extra, f, indent=1)
     print(f"wrote {len(hashgram)} hashgram, {len(mix)} mix64, {len(feats)} featurize cases")
