@@ -47,6 +47,10 @@ constexpr uint64_t kEmptyKey = ~0ull;
 constexpr uint64_t kCuckooMul1 = 0x9E3779B97F4A7C15ull;  // prefix-set hashes
 constexpr uint64_t kCuckooMul2 = 0xC2B2AE3D27D4EB4Full;
 constexpr uint64_t kOwnerMul = 0xD6E8FEB86659FD93ull;    // count-once owner of a prefix  // never a key: keys have <= 56 bits in a prefix set
+constexpr uint32_t kOwnerMul32 = 0x9E3779B1u;       // ... of a prefix of <= 4 bytes
+constexpr uint32_t kNarrowMul1 = 0x85EBCA6Bu;       // perfect-hash hashes of <= 4-byte keys
+constexpr uint32_t kNarrowMul2 = 0xC2B2AE35u;
+constexpr uint32_t kNarrowMul3 = 0x27D4EB2Fu;
 constexpr int kTileBytes = 512;        // one warp x 16 B per lane
 constexpr int kFrontPad = 16;
 constexpr int kBackPad = 1024;
@@ -164,6 +168,52 @@ __host__ __device__ inline uint32_t prefix_owner(uint64_t key, uint32_t plen, ui
   uint32_t x = plen >= 2 ? (first ^ last) : last;
   return x & (G - 1);
 }
+
+// Owner slice of a count-once extension prefix of plen bytes (host and
+// device agree on it): multiplicative hash (top bits of key * odd constant,
+// in 32-bit arithmetic for prefixes of <= 4 bytes).
+__host__ __device__ inline uint32_t owner_hash(uint64_t pkey, uint32_t plen, uint32_t lgno) {
+  if (!lgno) return 0u;
+  if (plen <= 4) return ((uint32_t)pkey * kOwnerMul32) >> (32 - lgno);
+  return (uint32_t)((pkey * kOwnerMul) >> (64 - lgno));
+}
+
+// Predicated shared-memory operations.  `if (p) atomicAdd(smem, 1)` compiles
+// to a branch around the ATOMS (BSSY/BRA/BSYNC, ~7 issue slots); these emit
+// a single predicated instruction instead.
+#ifdef __CUDACC__
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void red_add_shared_if(bool p, const uint32_t* a, uint32_t v) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %0, 0;\n @q red.shared.add.u32 [%1], %2;\n}"
+               :: "r"((uint32_t)p), "r"(smem_u32(a)), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_inc_shared_if(bool p, const uint32_t* a) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %0, 0;\n @q red.shared.add.u32 [%1], 1;\n}"
+               :: "r"((uint32_t)p), "r"(smem_u32(a)) : "memory");
+}
+__device__ __forceinline__ uint32_t atom_add_shared_if(bool p, const uint32_t* a, uint32_t v) {
+  uint32_t old = 0;
+  asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %1, 0;\n @q atom.shared.add.u32 %0, [%2], %3;\n}"
+               : "+r"(old) : "r"((uint32_t)p), "r"(smem_u32(a)), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ uint32_t atom_or_shared_if(bool p, const uint32_t* a, uint32_t v) {
+  uint32_t old = 0;
+  asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %1, 0;\n @q atom.shared.or.b32 %0, [%2], %3;\n}"
+               : "+r"(old) : "r"((uint32_t)p), "r"(smem_u32(a)), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ void st_shared_u32_if(bool p, const uint32_t* a, uint32_t v) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %0, 0;\n @q st.shared.u32 [%1], %2;\n}"
+               :: "r"((uint32_t)p), "r"(smem_u32(a)), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_shared_u64_if(bool p, const uint64_t* a, uint64_t v) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %0, 0;\n @q st.shared.u64 [%1], %2;\n}"
+               :: "r"((uint32_t)p), "r"(smem_u32(a)), "l"(v) : "memory");
+}
+#endif
 
 // Session (the C handle).
 struct Session;

@@ -83,8 +83,10 @@ struct RouteCtx {
 };
 
 void make_route_params(uint64_t cap, RouteParams& rp);
-void build_prefix_mphf(const std::vector<uint64_t>& keys, std::vector<uint32_t>& slot_of_key,
-                       std::vector<uint16_t>& disp, uint32_t& nb, uint32_t& nslots);
+// narrow: keys of <= 4 bytes (32-bit hashes, (key << 32) | v slots)
+void build_prefix_mphf(const std::vector<uint64_t>& keys, bool narrow,
+                       std::vector<uint32_t>& slot_of_key, std::vector<uint16_t>& disp,
+                       uint32_t& nb, uint32_t& nslots);
 // stage 1: count + scan (owner function only); stage 2: scatter + consume.
 template <typename CT>
 void route_count_once(int stage, RouteCtx& x, const DevCorpus& c, int kind, uint32_t L,

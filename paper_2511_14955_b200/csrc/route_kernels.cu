@@ -76,39 +76,55 @@ __device__ __forceinline__ uint64_t gmask() {
 
 // CHD perfect-hash prefix set (host-built): bucket b = hash1(key) of nb,
 // slot = range(s + d[b] * t) of nslots with (s, t) = hash2(key); every survivor
-// owns exactly one slot.  Packed slots hold (key << 24) | v (prefixes of <= 5
-// bytes; empty = ~0), unpacked slots hold the key and v lives in pidx[slot].
-// A lookup is one u16 and one u64 shared-memory load: no probing, no divergence.
+// owns exactly one slot.  Keys of <= 4 bytes (NARROW) hash with 32-bit
+// multiplies (bijections of the key) and sit in packed slots as
+// (key << 32) | v; other packed slots
+// hold (key << 24) | v (prefixes of <= 5 bytes); empty = ~0.  Unpacked slots
+// hold the key and v lives in pidx[slot].  A lookup is one u16 and one u64
+// shared-memory load: no probing, no divergence.
 // Returns v = (owner << 6 | index of the prefix in its owner) or 0xffffffff.
-__host__ __device__ __forceinline__ uint32_t mphf_slot(uint64_t key, uint32_t nb,
-                                                       uint32_t nslots, const uint16_t* disp,
-                                                       uint32_t* bucket_out) {
-  const uint64_t x = key * kCuckooMul1;
-  const uint32_t b = (uint32_t)(((x >> 32) * (uint64_t)nb) >> 32);
-  if (bucket_out) *bucket_out = b;
-  const uint64_t y = key * kCuckooMul2;
-  const uint32_t d = disp ? disp[b] : 0u;
-  const uint32_t h = (uint32_t)(y >> 32) + d * ((uint32_t)y | 1u);
-  return (uint32_t)(((uint64_t)h * nslots) >> 32);
+struct MphfHash {
+  uint32_t b, s, t;
+};
+template <bool NARROW>
+__host__ __device__ __forceinline__ MphfHash mphf_hash(uint64_t key, uint32_t nb) {
+  MphfHash h;
+  if constexpr (NARROW) {
+    const uint32_t k = (uint32_t)key;
+    h.b = (uint32_t)(((uint64_t)(k * kNarrowMul1) * nb) >> 32);
+    h.s = k * kNarrowMul2;
+    h.t = (k * kNarrowMul3) | 1u;
+  } else {
+    const uint64_t x = key * kCuckooMul1;
+    const uint64_t y = key * kCuckooMul2;
+    h.b = (uint32_t)(((x >> 32) * (uint64_t)nb) >> 32);
+    h.s = (uint32_t)(y >> 32);
+    h.t = (uint32_t)y | 1u;
+  }
+  return h;
 }
 
-template <bool PACKED>
+__host__ __device__ __forceinline__ uint32_t mphf_place(const MphfHash& h, uint32_t d,
+                                                        uint32_t nslots) {
+  return (uint32_t)(((uint64_t)(h.s + d * h.t) * nslots) >> 32);
+}
+
+template <bool PACKED, bool NARROW>
 __device__ __forceinline__ uint32_t prefix_lookup_v(const uint64_t* slots, const uint16_t* disp,
                                                     const uint32_t* pidx, uint32_t nb,
                                                     uint32_t nslots, uint64_t key) {
-  const uint32_t sl = mphf_slot(key, nb, nslots, disp, nullptr);
+  const MphfHash h = mphf_hash<NARROW>(key, nb);
+  const uint32_t sl = mphf_place(h, disp[h.b], nslots);
   const uint64_t e = slots[sl];
-  if constexpr (PACKED) {
+  if constexpr (PACKED && NARROW) {
+    const uint32_t v = (uint32_t)e;
+    return ((uint32_t)(e >> 32) == (uint32_t)key && v != 0xffffffffu) ? v : 0xffffffffu;
+  } else if constexpr (PACKED) {
     const uint32_t v = (uint32_t)e & 0xffffffu;
     return ((e >> 24) == key && v != 0xffffffu) ? v : 0xffffffffu;
   } else {
     return e == key ? __ldg(pidx + sl) : 0xffffffffu;
   }
-}
-
-// Owner of an extension prefix (count-once routing): multiplicative hash.
-__device__ __forceinline__ uint32_t prefix_owner_hash(uint64_t pkey, uint32_t lgno) {
-  return lgno ? (uint32_t)((pkey * kOwnerMul) >> (64 - lgno)) : 0u;
 }
 
 constexpr int kRouteThreads = 1024;
@@ -155,20 +171,20 @@ template <int KIND, int L, int T>
 __device__ __forceinline__ uint32_t count_owner(const uint32_t (&W)[7], const RouteParams& rp) {
   const uint64_t key = key8<T>(W) & gmask<L>();
   if constexpr (KIND == 0) return dense_route(key, rp) >> 16;
-  else return prefix_owner_hash(key >> 8, rp.lgno);
+  else return owner_hash(key >> 8, L - 1, rp.lgno);
 }
 
 // Scatter pass: (owner << 16 | local) of a gram key, or ~0 (prefix miss).
 // Extension: the slot value is (owner << 6 | index of the prefix inside its
 // owner), so local = value_lo6 * 256 + last byte with no second lookup.
-template <int KIND, bool PACKED>
+template <int KIND, int L, bool PACKED>
 __device__ __forceinline__ uint32_t scatter_route(uint64_t key, const RouteParams& rp,
                                                   const uint64_t* slots, const uint16_t* disp) {
   if constexpr (KIND == 0) {
     return dense_route(key, rp);
   } else {
     const uint32_t v =
-        prefix_lookup_v<PACKED>(slots, disp, rp.pidx, rp.nb, rp.nslots, key >> 8);
+        prefix_lookup_v<PACKED, (L - 1 <= 4)>(slots, disp, rp.pidx, rp.nb, rp.nslots, key >> 8);
     if (v == 0xffffffffu) return 0xffffffffu;
     return ((v >> 6) << 16) | ((v & 63u) * 256 + (uint32_t)(key & 0xff));
   }
@@ -293,27 +309,31 @@ __global__ void __launch_bounds__(NT) k_route_scatter(
       uint32_t r[16];
       static_for<0, 16>([&](auto tc) {
         constexpr int T = decltype(tc)::value;
-        uint32_t v = 0xffffffffu;
-        if ((vm >> T) & 1u) {
-          const uint64_t key = key8<T>(W) & gmask<L>();
-          if (nextc) {
-            // the next pass's gram ending at b0+T+1 has this gram as its prefix
-            const int64_t nxt_end = b0 + T + 1;
-            if (nxt_end < hi) {
-              atomicAdd(nhist + prefix_owner_hash(key, rp.next_lgno), 1u);
-            } else if (nxt_end < (int64_t)c.off[U.q + 1]) {  // first position of unit u+1
-              atomicAdd(rp.next_cnt + (size_t)prefix_owner_hash(key, rp.next_lgno) * uv.nunits + u + 1, 1u);
-            }
-          }
-          // a gram already routed from this chunk adds nothing (count-once):
-          // drop it before the prefix lookup.  Races only cost a duplicate.
-          constexpr int kLgSlots = DSLOTS == 8192 ? 13 : DSLOTS == 4096 ? 12 : 11;
-          const uint32_t slot =
-              (((uint32_t)key ^ ((uint32_t)(key >> 32) * 0x85EBCA6Bu)) * 0x9E3779B1u) >> (32 - kLgSlots);
-          if (!dedup || key == ~0ull || cache[slot] != key) {  // ~0 is the empty marker
-            cache[slot] = key;
-            v = scatter_route<KIND, PACKED>(key, rp, slots, disp);
-            if (v != 0xffffffffu) atomicAdd(lhist + (v >> 16), 1u);
+        // branch-free: a warp almost never has all 32 lanes on the cheap side
+        // of a test, so every step is computed and the results predicated
+        const bool valid = (vm >> T) & 1u;
+        const uint64_t key = key8<T>(W) & gmask<L>();
+        // a gram already routed from this unit adds nothing (count-once):
+        // drop it.  Races only cost a duplicate.
+        constexpr int kLgSlots = DSLOTS == 8192 ? 13 : DSLOTS == 4096 ? 12 : 11;
+        const uint32_t slot =
+            (((uint32_t)key ^ ((uint32_t)(key >> 32) * 0x85EBCA6Bu)) * 0x9E3779B1u) >> (32 - kLgSlots);
+        const uint64_t seen = cache[slot];
+        const bool fresh = valid && (!dedup || key == ~0ull || seen != key);  // ~0: empty marker
+        st_shared_u64_if(fresh, cache + slot, key);
+        uint32_t v = scatter_route<KIND, L, PACKED>(key, rp, slots, disp);
+        v = fresh ? v : 0xffffffffu;
+        red_inc_shared_if(v != 0xffffffffu, lhist + (v >> 16));
+        if (nextc) {
+          // the next pass's gram ending at b0+T+1 has this gram as its prefix;
+          // it can be routed only if this gram is a candidate: a lookup hit,
+          // or a repeat (counted conservatively: the count is an upper bound)
+          const bool cand = valid && (KIND == 0 || v != 0xffffffffu || !fresh);
+          const int64_t nxt_end = b0 + T + 1;
+          const uint32_t no = owner_hash(key, L, rp.next_lgno);
+          red_inc_shared_if(cand && nxt_end < hi, nhist + no);
+          if (cand && nxt_end >= hi && nxt_end < (int64_t)c.off[U.q + 1]) {  // first position of unit u+1
+            atomicAdd(rp.next_cnt + (size_t)no * uv.nunits + u + 1, 1u);
           }
         }
         r[T] = v;
@@ -340,7 +360,9 @@ __global__ void __launch_bounds__(NT) k_route_scatter(
       __syncthreads();
       static_for<0, 16>([&](auto tc) {
         constexpr int T = decltype(tc)::value;
-        if (r[T] != 0xffffffffu) staging[atomicAdd(lhist + (r[T] >> 16), 1u)] = r[T];
+        const bool h = r[T] != 0xffffffffu;
+        const uint32_t at = atom_add_shared_if(h, lhist + (r[T] >> 16), 1u);
+        st_shared_u32_if(h, staging + at, r[T]);
       });
       __syncthreads();
       const uint32_t total = s_total;
@@ -617,15 +639,15 @@ template void route_count_once<unsigned long long>(int, RouteCtx&, const DevCorp
 // CHD construction: buckets by decreasing size, each takes the first
 // displacement that sends all its keys to free slots.  Per-key hashes are
 // computed once; buckets are a counting sort.  False on failure.
-static bool mphf_try(const std::vector<uint64_t>& keys, uint32_t nb, uint32_t nslots,
+static bool mphf_try(const std::vector<uint64_t>& keys, uint32_t nb, uint32_t nslots, bool narrow,
                      std::vector<uint16_t>& disp, std::vector<uint32_t>& slot_of_key) {
   const uint32_t K = (uint32_t)keys.size();
   std::vector<uint32_t> kb(K), ks(K), kt(K), boff(nb + 1, 0), idx(K);
   for (uint32_t i = 0; i < K; ++i) {
-    const uint64_t x = keys[i] * kCuckooMul1, y = keys[i] * kCuckooMul2;
-    kb[i] = (uint32_t)(((x >> 32) * (uint64_t)nb) >> 32);
-    ks[i] = (uint32_t)(y >> 32);
-    kt[i] = (uint32_t)y | 1u;
+    const MphfHash h = narrow ? mphf_hash<true>(keys[i], nb) : mphf_hash<false>(keys[i], nb);
+    kb[i] = h.b;
+    ks[i] = h.s;
+    kt[i] = h.t;
     ++boff[kb[i] + 1];
   }
   uint32_t maxsz = 0;
@@ -655,8 +677,7 @@ static bool mphf_try(const std::vector<uint64_t>& keys, uint32_t nb, uint32_t ns
       ok = true;
       for (uint32_t t = 0; t < n && ok; ++t) {
         const uint32_t i = idx[a0 + t];
-        const uint32_t h = ks[i] + d * kt[i];
-        const uint32_t sl = (uint32_t)(((uint64_t)h * nslots) >> 32);
+        const uint32_t sl = mphf_place(MphfHash{kb[i], ks[i], kt[i]}, d, nslots);
         if (used[sl]) ok = false;
         for (uint32_t u = 0; u < t && ok; ++u)
           if (cand[u] == sl) ok = false;
@@ -673,12 +694,13 @@ static bool mphf_try(const std::vector<uint64_t>& keys, uint32_t nb, uint32_t ns
   return true;
 }
 
-void build_prefix_mphf(const std::vector<uint64_t>& keys, std::vector<uint32_t>& slot_of_key,
-                       std::vector<uint16_t>& disp, uint32_t& nb, uint32_t& nslots) {
+void build_prefix_mphf(const std::vector<uint64_t>& keys, bool narrow,
+                       std::vector<uint32_t>& slot_of_key, std::vector<uint16_t>& disp,
+                       uint32_t& nb, uint32_t& nslots) {
   const uint64_t K = keys.size();
   nb = (uint32_t)std::max<uint64_t>(1, (K + 2) / 3);
   nslots = (uint32_t)std::max<uint64_t>(1, K + K / 8 + 1);  // ~89% load
-  while (!mphf_try(keys, nb, nslots, disp, slot_of_key)) {
+  while (!mphf_try(keys, nb, nslots, narrow, disp, slot_of_key)) {
     nslots += nslots / 20 + 1;
     nb += nb / 10 + 1;
   }

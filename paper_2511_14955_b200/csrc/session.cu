@@ -276,8 +276,8 @@ static Prefix prepare_prefix(Session& s, const uint64_t* keys, uint64_t K, uint3
     std::vector<uint64_t> hk(K);
     IGB_CUDA(cudaMemcpyAsync(hk.data(), keys, K * 8, cudaMemcpyDeviceToHost, s.stream));
     IGB_CUDA(cudaStreamSynchronize(s.stream));
-    auto owner_of = [](uint64_t key, uint32_t lgno) -> uint32_t {
-      return lgno ? (uint32_t)((key * kOwnerMul) >> (64 - lgno)) : 0u;
+    auto owner_of = [plen](uint64_t key, uint32_t lgno) -> uint32_t {
+      return owner_hash(key, plen, lgno);
     };
     uint32_t lgno = lgno_start;
     std::vector<uint32_t> cnt;
@@ -326,16 +326,16 @@ static Prefix prepare_prefix(Session& s, const uint64_t* keys, uint64_t K, uint3
 static void build_prefix_table(Session& s, Prefix& P) {
   const uint64_t K = P.K;
   const uint32_t lgno = P.rp.lgno;
-  auto owner_of = [](uint64_t key, uint32_t lg) -> uint32_t {
-    return lg ? (uint32_t)((key * kOwnerMul) >> (64 - lg)) : 0u;
-  };
+  const uint32_t plen = P.plen;
+  auto owner_of = [plen](uint64_t key, uint32_t lg) -> uint32_t { return owner_hash(key, plen, lg); };
   const std::vector<uint64_t>& pk = P.pk;
   const std::vector<uint32_t>& ostart = P.ostart;
   // perfect-hash slots; slot value: owner << 6 | index of the prefix in its owner
   std::vector<uint32_t> slot_of_key;
   std::vector<uint16_t> disp;
   uint32_t nb = 0, nslots = 0;
-  build_prefix_mphf(pk, slot_of_key, disp, nb, nslots);
+  const bool narrow = P.plen <= 4;
+  build_prefix_mphf(pk, narrow, slot_of_key, disp, nb, nslots);
   std::vector<uint64_t> slots(nslots, kEmptyKey);
   std::vector<uint32_t> slot_v(nslots, 0xffffffu);
   for (uint64_t pp = 0; pp < K; ++pp) {
@@ -346,7 +346,7 @@ static void build_prefix_table(Session& s, Prefix& P) {
   const bool packed = 8 * P.plen + 24 <= 64 && lgno <= 17;
   if (packed)
     for (size_t i = 0; i < slots.size(); ++i)
-      if (slots[i] != kEmptyKey) slots[i] = (slots[i] << 24) | slot_v[i];
+      if (slots[i] != kEmptyKey) slots[i] = (slots[i] << (narrow ? 32 : 24)) | slot_v[i];
   uint64_t* ds = s.hkeys.as<uint64_t>(slots.size() + 2);
   uint32_t* dpi = s.hidx.as<uint32_t>(slot_v.size() + 2);
   uint16_t* ddisp = s.hpacked.as<uint16_t>(disp.size() + 8);
