@@ -55,12 +55,10 @@ struct RouteParams {
   // owner (ostart[o] .. ostart[o+1]); CHD perfect-hash prefix set
   bool ext = false;
   bool dedup = true;    // scatter drops repeats inside a chunk (optimisation only)
-  bool packed = false;  // slots = (key << 24) | p, else slots = key and pidx[slot] = p
   uint32_t lgno = 0;
   uint32_t nb = 0, nslots = 0;         // perfect-hash buckets / slots
   const uint64_t* slots = nullptr;     // [nslots]
   const uint16_t* disp = nullptr;      // [nb]
-  const uint32_t* pidx = nullptr;      // [nslots] (unpacked only)
   const uint32_t* ostart = nullptr;
   // fused count of the NEXT pass (owner = hash(this pass's gram) >> (64 - next_lgno));
   // -1: not requested

@@ -77,12 +77,13 @@ __device__ __forceinline__ uint64_t gmask() {
 // CHD perfect-hash prefix set (host-built): bucket b = hash1(key) of nb,
 // slot = range(s + d[b] * t) of nslots with (s, t) = hash2(key); every survivor
 // owns exactly one slot.  Keys of <= 4 bytes (NARROW) hash with 32-bit
-// multiplies (bijections of the key) and sit in packed slots as
-// (key << 32) | v; other packed slots
-// hold (key << 24) | v (prefixes of <= 5 bytes); empty = ~0.  Unpacked slots
-// hold the key and v lives in pidx[slot].  A lookup is one u16 and one u64
+// multiplies (bijections of the key).  A slot packs the key with what the
+// scatter needs, by prefix length (layout is a function of the pass):
+//   <= 4 bytes   (key << 32) | v          v = owner << 6 | index in owner
+//      5 bytes   (key << 24) | v
+//   6..7 bytes   (key << 8)  | index      owner recomputed from the key
+// empty = ~0 (an impossible v / index).  A lookup is one u16 and one u64
 // shared-memory load: no probing, no divergence.
-// Returns v = (owner << 6 | index of the prefix in its owner) or 0xffffffff.
 struct MphfHash {
   uint32_t b, s, t;
 };
@@ -109,21 +110,23 @@ __host__ __device__ __forceinline__ uint32_t mphf_place(const MphfHash& h, uint3
   return (uint32_t)(((uint64_t)(h.s + d * h.t) * nslots) >> 32);
 }
 
-template <bool PACKED, bool NARROW>
+template <int PLEN>
 __device__ __forceinline__ uint32_t prefix_lookup_v(const uint64_t* slots, const uint16_t* disp,
-                                                    const uint32_t* pidx, uint32_t nb,
-                                                    uint32_t nslots, uint64_t key) {
-  const MphfHash h = mphf_hash<NARROW>(key, nb);
+                                                    uint32_t nb, uint32_t nslots, uint32_t lgno,
+                                                    uint64_t key) {
+  const MphfHash h = mphf_hash<(PLEN <= 4)>(key, nb);
   const uint32_t sl = mphf_place(h, disp[h.b], nslots);
   const uint64_t e = slots[sl];
-  if constexpr (PACKED && NARROW) {
+  if constexpr (PLEN <= 4) {
     const uint32_t v = (uint32_t)e;
     return ((uint32_t)(e >> 32) == (uint32_t)key && v != 0xffffffffu) ? v : 0xffffffffu;
-  } else if constexpr (PACKED) {
+  } else if constexpr (PLEN == 5) {
     const uint32_t v = (uint32_t)e & 0xffffffu;
     return ((e >> 24) == key && v != 0xffffffu) ? v : 0xffffffffu;
   } else {
-    return e == key ? __ldg(pidx + sl) : 0xffffffffu;
+    const uint32_t idx = (uint32_t)e & 0xffu;
+    return ((e >> 8) == key && idx != 0xffu) ? ((owner_hash(key, PLEN, lgno) << 6) | idx)
+                                             : 0xffffffffu;
   }
 }
 
@@ -177,14 +180,14 @@ __device__ __forceinline__ uint32_t count_owner(const uint32_t (&W)[7], const Ro
 // Scatter pass: (owner << 16 | local) of a gram key, or ~0 (prefix miss).
 // Extension: the slot value is (owner << 6 | index of the prefix inside its
 // owner), so local = value_lo6 * 256 + last byte with no second lookup.
-template <int KIND, int L, bool PACKED>
+template <int KIND, int L>
 __device__ __forceinline__ uint32_t scatter_route(uint64_t key, const RouteParams& rp,
                                                   const uint64_t* slots, const uint16_t* disp) {
   if constexpr (KIND == 0) {
     return dense_route(key, rp);
   } else {
     const uint32_t v =
-        prefix_lookup_v<PACKED, (L - 1 <= 4)>(slots, disp, rp.pidx, rp.nb, rp.nslots, key >> 8);
+        prefix_lookup_v<L - 1>(slots, disp, rp.nb, rp.nslots, rp.lgno, key >> 8);
     if (v == 0xffffffffu) return 0xffffffffu;
     return ((v >> 6) << 16) | ((v & 63u) * 256 + (uint32_t)(key & 0xff));
   }
@@ -254,13 +257,13 @@ constexpr int kScatterThreads = 512;      // default scatter CTA
 constexpr int kScatterThreadsBig = 768;   // smem-staged table: one CTA per SM
 constexpr int kSChunk = kScatterThreads * 16;  // positions per chunk (default CTA)
 
-// TAB: 0 dense (no table), 1 packed table staged in smem, 2 packed table in
-// global memory, 3 unpacked table (key slots + pidx) in global memory.
+// TAB: 0 dense (no table), 1 perfect-hash table staged in smem (768-thread
+// CTA), 4 the same with a 512-thread CTA (smaller staging, bigger tables),
+// 2 table in global memory.
 template <int KIND, int L, int TAB, int NT, int DSLOTS>
 __global__ void __launch_bounds__(NT) k_route_scatter(
     DevCorpus c, RouteView uv, RouteParams rp, const unsigned long long* __restrict__ base,
     uint32_t* __restrict__ actual, uint16_t* __restrict__ entries) {
-  constexpr bool PACKED = TAB != 3;
   extern __shared__ uint4 smem4[];
   char* sp = reinterpret_cast<char*>(smem4);
   uint32_t* staging = reinterpret_cast<uint32_t*>(sp);  // kSChunk x (owner<<16|local)
@@ -282,7 +285,7 @@ __global__ void __launch_bounds__(NT) k_route_scatter(
   using BlockScan = cub::BlockScan<uint32_t, NT>;
   __shared__ typename BlockScan::TempStorage scan_tmp;
   const uint16_t* disp = nullptr;
-  const uint64_t* slots = KIND == 1 ? stage_table<TAB == 1 ? 1 : 2>(rp, s_slots, disp) : nullptr;
+  const uint64_t* slots = KIND == 1 ? stage_table<(TAB == 1 || TAB == 4) ? 1 : 2>(rp, s_slots, disp) : nullptr;
   const bool dedup = rp.dedup;
   const int lane = threadIdx.x & 31;
   for (uint32_t ui = blockIdx.x; ui < uv.nb; ui += gridDim.x) {
@@ -321,7 +324,7 @@ __global__ void __launch_bounds__(NT) k_route_scatter(
         const uint64_t seen = cache[slot];
         const bool fresh = valid && (!dedup || key == ~0ull || seen != key);  // ~0: empty marker
         st_shared_u64_if(fresh, cache + slot, key);
-        uint32_t v = scatter_route<KIND, L, PACKED>(key, rp, slots, disp);
+        uint32_t v = scatter_route<KIND, L>(key, rp, slots, disp);
         v = fresh ? v : 0xffffffffu;
         red_inc_shared_if(v != 0xffffffffu, lhist + (v >> 16));
         if (nextc) {
@@ -517,7 +520,7 @@ template <int KIND, int L, int TAB, typename CT>
 static void route_stage2_t(RouteCtx& x, const DevCorpus& c, const RouteParams& rp, CT* table,
                            int num_sms, cudaStream_t st) {
   const RouteView uv = x.view();
-  const size_t tab = TAB == 1 ? table_bytes(rp) : 0;
+  const size_t tab = (TAB == 1 || TAB == 4) ? table_bytes(rp) : 0;
   const size_t ncnt = (size_t)rp.NO * uv.nb + 1;
   uint32_t* act = x.actual.as<uint32_t>(ncnt);  // TAB 10/11: dense with 1024/768 threads
   unsigned long long* base = x.base.as<unsigned long long>(ncnt);
@@ -534,7 +537,7 @@ static void route_stage2_t(RouteCtx& x, const DevCorpus& c, const RouteParams& r
   {
     constexpr int NT = TAB == 1 || TAB == 11 ? kScatterThreadsBig
                        : (TAB == 10 || TAB == 12) ? 1024 : kScatterThreads;
-    constexpr int DS = TAB == 1 ? 2048 : TAB == 12 ? 8192 : kDedupSlots;
+    constexpr int DS = (TAB == 1 || TAB == 4) ? 2048 : TAB == 12 ? 8192 : kDedupSlots;
     constexpr int KT = TAB >= 10 ? 0 : TAB;  // dense variants carry no table
     const size_t nxt = rp.next_lgno >= 0 ? align16(((size_t)1 << rp.next_lgno) * 4) : 0;
     const size_t smem = (size_t)NT * 16 * 4 + (size_t)DS * 8 + align16((size_t)rp.NO * 8) +
@@ -590,15 +593,18 @@ static void route_stage_l(int stage, RouteCtx& x, const DevCorpus& c, const Rout
     // (measured best of 512/768/1024 threads and 4096/8192 slots)
     route_stage2_t<0, L, 12, CT>(x, c, rp, table, num_sms, st);
   } else {
-    const size_t scatter_fixed = (size_t)kScatterThreadsBig * 64 + 2048 * 8 +
-                                 (size_t)rp.NO * 16 + 256 + 8 * 1024;  // + static smem
-    // the packed table is staged in shared memory when it fits (one 768-thread
-    // CTA per SM: measured 1.2x faster than L1-cached global loads with two
+    auto fixed = [&](size_t nt) {  // + static smem
+      const size_t nxt = rp.next_lgno >= 0 ? align16(((size_t)1 << rp.next_lgno) * 4) : 0;
+      return nt * 64 + 2048 * 8 + (size_t)rp.NO * 16 + 256 + nxt + 8 * 1024;
+    };
+    // the table is staged in shared memory when it fits (one 768-thread CTA
+    // per SM: measured 1.2x faster than L1-cached global loads with two
     // 512-thread CTAs); IG_SCATTER_TABLE_GLOBAL=1 forces the global variant
     static const bool force_global = getenv("IG_SCATTER_TABLE_GLOBAL") != nullptr;
-    if (!rp.packed) route_stage2_t<1, L, 3, CT>(x, c, rp, table, num_sms, st);
-    else if (!force_global && scatter_fixed + table_bytes(rp) <= kMaxOnceSmem)
+    if (!force_global && fixed(kScatterThreadsBig) + table_bytes(rp) <= kMaxOnceSmem)
       route_stage2_t<1, L, 1, CT>(x, c, rp, table, num_sms, st);
+    else if (!force_global && fixed(kScatterThreads) + table_bytes(rp) <= kMaxOnceSmem)
+      route_stage2_t<1, L, 4, CT>(x, c, rp, table, num_sms, st);
     else
       route_stage2_t<1, L, 2, CT>(x, c, rp, table, num_sms, st);
   }

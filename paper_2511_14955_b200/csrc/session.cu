@@ -286,6 +286,10 @@ static Prefix prepare_prefix(Session& s, const uint64_t* keys, uint64_t K, uint3
       uint32_t mx = 0;
       for (uint64_t i = 0; i < K; ++i) mx = std::max(mx, ++cnt[owner_of(hk[i], lgno)]);
       if (mx <= kPrefixesPerOwner) break;
+      // routed entries carry the owner in 16 bits (route_kernels.cu)
+      if (lgno >= 16)
+        throw Error(IG_ECONFIG, "count-once extension pass supports at most ~4M surviving "
+                                "prefixes (k' too large)");
     }
     const uint32_t NO = 1u << lgno;
     std::vector<uint32_t> ostart(NO + 1, 0);
@@ -343,24 +347,22 @@ static void build_prefix_table(Session& s, Prefix& P) {
     slots[slot_of_key[pp]] = pk[pp];
     slot_v[slot_of_key[pp]] = (o << 6) | (uint32_t)(pp - ostart[o]);
   }
-  const bool packed = 8 * P.plen + 24 <= 64 && lgno <= 17;
-  if (packed)
-    for (size_t i = 0; i < slots.size(); ++i)
-      if (slots[i] != kEmptyKey) slots[i] = (slots[i] << (narrow ? 32 : 24)) | slot_v[i];
+  // slot layout by prefix length (route_kernels.cu: prefix_lookup_v)
+  for (size_t i = 0; i < slots.size(); ++i) {
+    if (slots[i] == kEmptyKey) continue;
+    if (P.plen <= 4) slots[i] = (slots[i] << 32) | slot_v[i];
+    else if (P.plen == 5) slots[i] = (slots[i] << 24) | slot_v[i];
+    else slots[i] = (slots[i] << 8) | (slot_v[i] & 63u);
+  }
   uint64_t* ds = s.hkeys.as<uint64_t>(slots.size() + 2);
-  uint32_t* dpi = s.hidx.as<uint32_t>(slot_v.size() + 2);
   uint16_t* ddisp = s.hpacked.as<uint16_t>(disp.size() + 8);
   IGB_CUDA(cudaMemcpyAsync(ds, slots.data(), slots.size() * 8, cudaMemcpyHostToDevice, s.stream));
-  IGB_CUDA(cudaMemcpyAsync(dpi, slot_v.data(), slot_v.size() * 4, cudaMemcpyHostToDevice,
-                           s.stream));
   IGB_CUDA(cudaMemcpyAsync(ddisp, disp.data(), disp.size() * 2, cudaMemcpyHostToDevice, s.stream));
   IGB_CUDA(cudaStreamSynchronize(s.stream));  // host vectors die here
-  P.rp.packed = packed;
   P.rp.nb = nb;
   P.rp.nslots = nslots;
   P.rp.slots = ds;
   P.rp.disp = ddisp;
-  P.rp.pidx = dpi;
 }
 
 // One counting pass.  Returns the device table (tcap entries) and how table
@@ -505,6 +507,15 @@ static void run_t(Session& s, const ig_params& p, ig_result* out) {
   const int32_t fuse_lg = (p.mode == IG_MODE_ONCE && n > 3 && !getenv("IG_NO_FUSED_COUNT"))
                              ? (int32_t)predicted_lgno(kp) : -1;
   CT* table = count_pass<CT>(s, true, n0, p.mode, nullptr, tcap, km, fuse_lg);
+  int32_t next_lg = fuse_lg;
+  // owner bits of a count-once prefix set of K survivors: the width the fused
+  // histogram was built for, unless K came out far shorter (then recount:
+  // thousands of near-empty owners cost more than one count kernel)
+  auto owner_bits = [](int32_t fused, uint64_t K) -> uint32_t {
+    const uint32_t want = predicted_lgno(K);
+    if (fused <= 0) return 0u;
+    return want + 1 < (uint32_t)fused ? want : (uint32_t)fused;
+  };
   IGB_CUDA(cudaGetLastError());
   allreduce(s, table, tcap, sizeof(CT) == 4 ? 0 : 1);
   tm.end(ev);
@@ -532,7 +543,7 @@ static void run_t(Session& s, const ig_params& p, ig_result* out) {
     if (shrt)
       diag += "pass 3 retained " + std::to_string(ns) + " candidates (requested " +
               std::to_string(kp) + ")\n";
-    Prefix P = prepare_prefix(s, sk, ns, 3, p.mode, fuse_lg > 0 ? (uint32_t)fuse_lg : 0u);
+    Prefix P = prepare_prefix(s, sk, ns, 3, p.mode, owner_bits(fuse_lg, ns));
     tm.end(ev);
     rows.push_back(make_row("top-zk 3-grams/trie building", 3, 0, 0, ns, shrt, ev));
 
@@ -542,7 +553,11 @@ static void run_t(Session& s, const ig_params& p, ig_result* out) {
       if (ns == 0) throw Error(IG_ECONFIG, "extension pass needs a trie of depth j-1");
       ev = tm.begin();
       const uint64_t cap = 256 * ns;
-      CT* ct = count_pass<CT>(s, false, j, p.mode, &P, tcap, km, j < n ? fuse_lg : -1);
+      // fused histogram of the next pass's owners, sized for its largest
+      // possible prefix count min(k', 256 * this pass's survivors)
+      next_lg = fuse_lg >= 0 && j < n ? (int32_t)predicted_lgno(std::min<uint64_t>(kp, 256 * ns))
+                                      : -1;
+      CT* ct = count_pass<CT>(s, false, j, p.mode, &P, tcap, km, next_lg);
       IGB_CUDA(cudaGetLastError());
       allreduce(s, ct, tcap, sizeof(CT) == 4 ? 0 : 1);
       tm.end(ev);
@@ -563,7 +578,7 @@ static void run_t(Session& s, const ig_params& p, ig_result* out) {
         s.surv_counts.swap(s.next_counts);
         sk = nk;
         ns = nn;
-        P = prepare_prefix(s, sk, ns, j, p.mode, fuse_lg > 0 ? (uint32_t)fuse_lg : 0u);
+        P = prepare_prefix(s, sk, ns, j, p.mode, owner_bits(next_lg, ns));
         tm.end(ev);
         rows.push_back(make_row("top-zk " + std::to_string(j) + "-grams/trie building", j, 0, 0,
                                 ns, shrt, ev));
