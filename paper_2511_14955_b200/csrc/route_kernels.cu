@@ -268,7 +268,14 @@ __global__ void __launch_bounds__(NT) k_route_scatter(
   char* sp = reinterpret_cast<char*>(smem4);
   uint32_t* staging = reinterpret_cast<uint32_t*>(sp);  // kSChunk x (owner<<16|local)
   sp += (size_t)NT * 16 * 4;
-  uint64_t* cache = reinterpret_cast<uint64_t*>(sp);  // DSLOTS gram keys
+  // dedup cache: DSLOTS * 8 bytes of gram keys.  Grams of <= 4 bytes are
+  // kept as u32 (twice the slots); 5-byte grams as the low 40 - lg bits of a
+  // bijection h = key * odd mod 2^40 whose top lg bits pick the slot (slot +
+  // tag identify the key exactly, and a tag < 2^31 never equals the marker).
+  using CK = std::conditional_t<(L <= 5), uint32_t, uint64_t>;
+  constexpr int kSlots = DSLOTS * (int)(8 / sizeof(CK));
+  constexpr CK kEmpty = (CK)~(CK)0;
+  CK* cache = reinterpret_cast<CK*>(sp);
   sp += (size_t)DSLOTS * 8;
   unsigned long long* res = reinterpret_cast<unsigned long long*>(sp);  // NO
   sp += align16((size_t)rp.NO * 8);
@@ -300,7 +307,7 @@ __global__ void __launch_bounds__(NT) k_route_scatter(
     const int64_t nseg = (hi - first + 15) >> 4;
     // the dedup cache lives for the whole unit: every chunk of a unit belongs to
     // the same sequence, so a gram seen anywhere earlier in it adds nothing
-    for (uint32_t i = threadIdx.x; i < DSLOTS; i += blockDim.x) cache[i] = ~0ull;
+    for (uint32_t i = threadIdx.x; i < kSlots; i += blockDim.x) cache[i] = kEmpty;
     for (int64_t cs = 0; cs < nseg; cs += NT) {
       for (uint32_t i = threadIdx.x; i < rp.NO; i += blockDim.x) lhist[i] = 0;
       __syncthreads();
@@ -318,12 +325,21 @@ __global__ void __launch_bounds__(NT) k_route_scatter(
         const uint64_t key = key8<T>(W) & gmask<L>();
         // a gram already routed from this unit adds nothing (count-once):
         // drop it.  Races only cost a duplicate.
-        constexpr int kLgSlots = DSLOTS == 8192 ? 13 : DSLOTS == 4096 ? 12 : 11;
-        const uint32_t slot =
-            (((uint32_t)key ^ ((uint32_t)(key >> 32) * 0x85EBCA6Bu)) * 0x9E3779B1u) >> (32 - kLgSlots);
-        const uint64_t seen = cache[slot];
-        const bool fresh = valid && (!dedup || key == ~0ull || seen != key);  // ~0: empty marker
-        st_shared_u64_if(fresh, cache + slot, key);
+        constexpr int kLgSlots = kSlots == 16384 ? 14 : kSlots == 8192 ? 13 : kSlots == 4096 ? 12 : 11;
+        uint32_t slot;
+        CK tag;
+        if constexpr (L == 5) {
+          const uint64_t h = (key * 0x9E3779B97F4A7C15ull) & ((1ull << 40) - 1);
+          slot = (uint32_t)(h >> (40 - kLgSlots));
+          tag = (CK)(h & ((1ull << (40 - kLgSlots)) - 1));
+        } else {
+          slot = (((uint32_t)key ^ ((uint32_t)(key >> 32) * 0x85EBCA6Bu)) * 0x9E3779B1u) >> (32 - kLgSlots);
+          tag = (CK)key;
+        }
+        const CK seen = cache[slot];
+        const bool fresh = valid && (!dedup || (L != 5 && tag == kEmpty) || seen != tag);  // kEmpty: marker
+        if constexpr (sizeof(CK) == 8) st_shared_u64_if(fresh, (const uint64_t*)(cache + slot), key);
+        else st_shared_u32_if(fresh, (const uint32_t*)(cache + slot), (uint32_t)tag);
         uint32_t v = scatter_route<KIND, L>(key, rp, slots, disp);
         v = fresh ? v : 0xffffffffu;
         red_inc_shared_if(v != 0xffffffffu, lhist + (v >> 16));
