@@ -443,8 +443,15 @@ def main():
                "d2h_bytes_per_step": int(16 * len(r2.keys)), "ms_per_step": e_ms}
         assert np.array_equal(r2.keys, res.keys) and np.array_equal(r2.counts, res.counts)
         if args.e2e_depth > 1:
-            e2e["pipelined"] = pipelined_e2e(args, ig, torch, sess, corpus, icfg, local, coll,
-                                             bytes_total, world, res)
+            # one more session per run in flight: only when its HBM fits
+            free, total_mem = torch.cuda.mem_get_info()
+            used = total_mem - free
+            if free > 1.1 * used * (args.e2e_depth - 1):
+                e2e["pipelined"] = pipelined_e2e(args, ig, torch, sess, corpus, icfg, local,
+                                                 coll, bytes_total, world, res)
+            else:
+                e2e["pipelined"] = {"skipped": f"{args.e2e_depth} sessions do not fit in HBM "
+                                               f"({used / 2**30:.0f} GiB used per session)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
