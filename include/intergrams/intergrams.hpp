@@ -114,14 +114,28 @@ inline ig_params params_of(const IntergramConfig& cfg) {
 
 }  // namespace detail
 
-// run_intergrams (intergrams.hpp:74-75) on the GPU.
+// run_intergrams (intergrams.hpp:74-75) on the GPU.  A file corpus is read by
+// the library itself (host threads -> pinned slabs -> HBM, line splitting on
+// the GPU); an in-memory corpus is packed into one CSR buffer and copied.
 inline IntergramsResult run_intergrams(const Corpus& corpus, const IntergramConfig& cfg) {
   cfg.validate();
-  const CorpusCSR csr = corpus.materialize();
-  ig_corpus c{csr.data.data(), csr.offsets.data(), csr.offsets.size() - 1, IG_HOST};
   const ig_params p = detail::params_of(cfg);
   ig_result r{};
   char err[1024] = {0};
+  if (!corpus.spec().in_memory.has_value()) {
+    std::vector<std::string> roots;
+    for (const auto& root : corpus.spec().roots) roots.push_back(root.string());
+    std::vector<const char*> ptrs;
+    for (const auto& root : roots) ptrs.push_back(root.c_str());
+    ig_file_corpus spec{ptrs.data(), ptrs.size(), corpus.spec().recurse ? 1 : 0,
+                        corpus.spec().line_mode ? 1 : 0, corpus.spec().chunk_size};
+    detail::raise(ig_topk_ngrams_files(&spec, &p, &r, err, sizeof(err)), err);
+    IntergramsResult out = detail::convert(r);
+    ig_result_free(&r);
+    return out;
+  }
+  const CorpusCSR csr = corpus.materialize();
+  ig_corpus c{csr.data.data(), csr.offsets.data(), csr.offsets.size() - 1, IG_HOST};
   detail::raise(ig_topk_ngrams(&c, &p, &r, err, sizeof(err)), err);
   IntergramsResult out = detail::convert(r);
   ig_result_free(&r);

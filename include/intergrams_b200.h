@@ -184,6 +184,40 @@ IG_API int ig_top_k(const uint64_t* table, uint64_t cap, uint64_t k,
              uint64_t* counts_out, uint64_t* len_out, char* err,
              size_t err_len);
 
+/* ---- corpus ingestion from files (corpus.cpp:13-152) ---------------------
+ * The reference's CorpusSpec: roots are regular files or directories (of
+ * regular files, recursively when `recurse`); all files are taken in path
+ * order; each file gives one sequence, or one per '\n'-terminated line
+ * (`line_mode`; a final unterminated line counts when non-empty), or one per
+ * `chunk_size` bytes (the last one short).  Files are read by host threads
+ * into pinned slabs and copied to HBM as they are read; line splitting runs
+ * on the GPU.  A missing root is IG_ECONFIG, an unreadable file IG_EIO. */
+typedef struct {
+  const char* const* roots;
+  uint64_t num_roots;
+  int32_t recurse;
+  int32_t line_mode;
+  uint64_t chunk_size;
+} ig_file_corpus;
+
+/* run_intergrams(Corpus(spec), cfg) on a file corpus. */
+IG_API int ig_topk_ngrams_files(const ig_file_corpus* spec, const ig_params* params,
+                                ig_result* out, char* err, size_t err_len);
+/* Session variants: load (corpus stays resident), load + run. */
+IG_API int ig_session_load_files(ig_session* s, const ig_file_corpus* spec, char* err,
+                                 size_t err_len);
+IG_API int ig_session_run_files(ig_session* s, const ig_file_corpus* spec,
+                                const ig_params* params, ig_result* out, char* err,
+                                size_t err_len);
+/* The resident corpus of a session, copied back (data / offsets may be NULL;
+ * each is filled only when its capacity suffices). */
+IG_API int ig_session_corpus(ig_session* s, uint8_t* data, uint64_t data_cap, uint64_t* offsets,
+                             uint64_t offsets_cap, uint64_t* num_seqs, uint64_t* total_bytes,
+                             char* err, size_t err_len);
+/* Host-only: the files a spec enumerates (count, total bytes). */
+IG_API int ig_file_corpus_files(const ig_file_corpus* spec, uint64_t* num_files,
+                                uint64_t* total_bytes, char* err, size_t err_len);
+
 /* ---- exact counting paths (sort-based, same sm_100a library) ------------ */
 /* naive_count + naive_topk (proj/src/oracle.cpp:7-47, oracle.hpp:17-27):
  * exact counts of every n-gram, canonical top-k.  A corpus of more than

@@ -131,6 +131,10 @@ def ref() -> C.CDLL:
             C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64, C.c_uint32, C.c_uint32,
             C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.c_char_p,
             C.c_size_t]
+        L.igref_corpus_files.argtypes = [
+            C.POINTER(C.c_char_p), C.c_uint64, C.c_int, C.c_int, C.c_uint64, C.c_void_p,
+            C.c_uint64, C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
+            C.POINTER(C.c_uint64), C.c_char_p, C.c_size_t]
         L.igref_jaccard_tsv.argtypes = [C.c_char_p, C.c_char_p]
         L.igref_jaccard_tsv.restype = C.c_double
         L.igref_report.argtypes = [C.c_char_p, C.c_char_p, C.c_void_p, C.c_uint32, C.c_int,
@@ -393,3 +397,21 @@ def ref_report(algorithm: str, echo: str, rows, jaccard: Optional[float] = None,
                             len(out))
     assert rc == 0, out.value
     return out.value.decode()
+
+
+def ref_corpus_files(roots, recurse=False, line_mode=False, chunk_size=0):
+    """ig_ref::Corpus(CorpusSpec{roots, ...}) -> (rc, data, offsets, num_files, err)."""
+    arr = (C.c_char_p * max(len(roots), 1))(*[os.fsencode(r) for r in roots])
+    m, tot, nf = C.c_uint64(0), C.c_uint64(0), C.c_uint64(0)
+    err = C.create_string_buffer(512)
+    L = ref()
+    rc = L.igref_corpus_files(arr, len(roots), int(recurse), int(line_mode), chunk_size, None, 0,
+                              None, 0, C.byref(m), C.byref(tot), C.byref(nf), err, len(err))
+    if rc != 0:
+        return rc, None, None, 0, err.value.decode()
+    data = np.zeros(max(tot.value, 1), np.uint8)
+    off = np.zeros(m.value + 1, np.uint64)
+    rc = L.igref_corpus_files(arr, len(roots), int(recurse), int(line_mode), chunk_size,
+                              data.ctypes.data, data.size, off.ctypes.data, off.size, C.byref(m),
+                              C.byref(tot), C.byref(nf), err, len(err))
+    return rc, data[:tot.value], off, nf.value, err.value.decode()

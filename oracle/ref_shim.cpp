@@ -13,6 +13,7 @@
 //   featurize        proj/src/metrics.cpp:83-132
 //   jaccard          proj/src/metrics.cpp:16-31
 //   RunReport        proj/src/metrics.cpp:134-200 (to_tsv / to_json)
+//   Corpus(spec)     proj/src/corpus.cpp:13-152 (file enumeration + records)
 // No reference source is copied into this repository.
 #include <chrono>
 #include <cstdint>
@@ -252,6 +253,34 @@ int igref_featurize(const uint8_t* data, const uint64_t* off, uint64_t m,
       entries[i] = (mat.entries[i].first << 32) | mat.entries[i].second;
     *nnz = mat.entries.size();
     *rows = mat.rows;
+  });
+}
+
+// ig_ref::Corpus over files: enumerates roots (recurse / line / chunk) and
+// materialises the records.  data may be NULL (sizes only).  Returns the file
+// count in *num_files.
+int igref_corpus_files(const char* const* roots, uint64_t nroots, int recurse, int line_mode,
+                       uint64_t chunk_size, uint8_t* data, uint64_t cap, uint64_t* offsets,
+                       uint64_t offcap, uint64_t* num_seqs, uint64_t* total, uint64_t* num_files,
+                       char* err, size_t err_len) {
+  return guarded(err, err_len, [&] {
+    CorpusSpec spec;
+    for (uint64_t i = 0; i < nroots; ++i) spec.roots.emplace_back(roots[i]);
+    spec.recurse = recurse != 0;
+    spec.line_mode = line_mode != 0;
+    spec.chunk_size = chunk_size;
+    const Corpus corpus(std::move(spec));
+    uint64_t m = 0, t = 0;
+    if (offsets && offcap) offsets[0] = 0;
+    corpus.for_each([&](const Sequence& s) {
+      if (data && t + s.bytes.size() <= cap) std::memcpy(data + t, s.bytes.data(), s.bytes.size());
+      t += s.bytes.size();
+      ++m;
+      if (offsets && m < offcap) offsets[m] = t;
+    });
+    *num_seqs = m;
+    *total = t;
+    *num_files = corpus.files().size();
   });
 }
 

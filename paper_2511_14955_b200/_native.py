@@ -55,6 +55,11 @@ class ig_matrix(C.Structure):
                 ("row", C.POINTER(C.c_uint64)), ("col", C.POINTER(C.c_uint32))]
 
 
+class ig_file_corpus(C.Structure):
+    _fields_ = [("roots", C.POINTER(C.c_char_p)), ("num_roots", C.c_uint64),
+                ("recurse", C.c_int32), ("line_mode", C.c_int32), ("chunk_size", C.c_uint64)]
+
+
 IG_ORACLE_GUARD = 256 << 20
 
 ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_uint64, C.c_int32, C.c_void_p, C.c_void_p)
@@ -100,6 +105,18 @@ SYMBOLS = [
     ("ig_featurize", C.c_int, [C.POINTER(ig_corpus), C.c_void_p, C.c_uint64, C.c_uint32,
                                C.c_int32, C.POINTER(ig_matrix), C.c_char_p, C.c_size_t]),
     ("ig_matrix_free", None, [C.POINTER(ig_matrix)]),
+    ("ig_topk_ngrams_files", C.c_int, [C.POINTER(ig_file_corpus), C.POINTER(ig_params),
+                                       C.POINTER(ig_result), C.c_char_p, C.c_size_t]),
+    ("ig_session_load_files", C.c_int, [C.c_void_p, C.POINTER(ig_file_corpus), C.c_char_p,
+                                        C.c_size_t]),
+    ("ig_session_run_files", C.c_int, [C.c_void_p, C.POINTER(ig_file_corpus),
+                                       C.POINTER(ig_params), C.POINTER(ig_result), C.c_char_p,
+                                       C.c_size_t]),
+    ("ig_session_corpus", C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64,
+                                    C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.c_char_p,
+                                    C.c_size_t]),
+    ("ig_file_corpus_files", C.c_int, [C.POINTER(ig_file_corpus), C.POINTER(C.c_uint64),
+                                       C.POINTER(C.c_uint64), C.c_char_p, C.c_size_t]),
     ("ig_shard_range", None, [C.c_void_p, C.c_uint64, C.c_int32, C.c_int32,
                               C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     ("ig_version", C.c_char_p, []),

@@ -52,32 +52,25 @@ static uint64_t k_prime(const ig_params& p) {
   return (uint64_t)v;
 }
 
-void load_corpus(Session& s, const ig_corpus& c, bool copy_data) {
-  use_device(s);
-  const uint64_t m = c.num_seqs;
-  std::vector<uint64_t> hoff(m + 1);
-  if (c.location == IG_DEVICE) {
-    IGB_CUDA(cudaMemcpy(hoff.data(), c.offsets, (m + 1) * sizeof(uint64_t),
-                        cudaMemcpyDeviceToHost));
-  } else {
-    memcpy(hoff.data(), c.offsets, (m + 1) * sizeof(uint64_t));
-  }
-  if (hoff[0] != 0) throw Error(IG_ECONFIG, "corpus offsets must start at 0");
-  for (uint64_t i = 0; i < m; ++i)
-    if (hoff[i + 1] < hoff[i]) throw Error(IG_ECONFIG, "corpus offsets must be non-decreasing");
-  if (m >= 0xffffffffull) throw Error(IG_ECONFIG, "too many sequences");
-  const uint64_t total = hoff[m];
+// Allocates the padded corpus buffer for `total` bytes (zero pads) and
+// returns the address of byte 0.
+uint8_t* alloc_corpus(Session& s, uint64_t total) {
   const uint64_t ntiles = (total + kTileBytes - 1) / kTileBytes;
   const size_t alloc = kFrontPad + ntiles * kTileBytes + kBackPad;
   uint8_t* base = s.data.as<uint8_t>(alloc);
   IGB_CUDA(cudaMemsetAsync(base, 0, kFrontPad, s.stream));
   IGB_CUDA(cudaMemsetAsync(base + kFrontPad + total, 0, alloc - kFrontPad - total, s.stream));
-  if (total && copy_data) {
-    IGB_CUDA(cudaMemcpyAsync(base + kFrontPad, c.data, total,
-                             c.location == IG_DEVICE ? cudaMemcpyDeviceToDevice
-                                                     : cudaMemcpyHostToDevice,
-                             s.stream));
-  }
+  return base + kFrontPad;
+}
+
+// Everything derived from the host offsets once the bytes are (or are being)
+// placed at s.data + kFrontPad: device offsets, tile descriptors, the
+// longest-first order and the count-once work units.
+void finish_corpus(Session& s, std::vector<uint64_t>& hoff) {
+  const uint64_t m = hoff.size() - 1;
+  const uint64_t total = hoff[m];
+  const uint64_t ntiles = (total + kTileBytes - 1) / kTileBytes;
+  uint8_t* base = static_cast<uint8_t*>(s.data.p);
   uint64_t* doff = s.off.as<uint64_t>(m + 1);
   IGB_CUDA(cudaMemcpyAsync(doff, hoff.data(), (m + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice,
                            s.stream));
@@ -94,7 +87,7 @@ void load_corpus(Session& s, const ig_corpus& c, bool copy_data) {
   if (m)
     IGB_CUDA(cudaMemcpyAsync(dord, ord.data(), m * sizeof(uint32_t), cudaMemcpyHostToDevice,
                              s.stream));
-  // count-once work units: <= 1 MiB of gram ends of one sequence
+  // count-once work units: <= kUnitBytes of gram ends of one sequence
   std::vector<RouteUnit> units;
   std::vector<uint32_t> ufirst(m + 1, 0);
   for (uint64_t q = 0; q < m; ++q) {
@@ -134,6 +127,36 @@ void load_corpus(Session& s, const ig_corpus& c, bool copy_data) {
   s.dc.total = total;
   s.dc.ntiles = ntiles;
   s.loaded = true;
+}
+
+void check_offsets(const std::vector<uint64_t>& hoff) {
+  const uint64_t m = hoff.size() - 1;
+  if (hoff[0] != 0) throw Error(IG_ECONFIG, "corpus offsets must start at 0");
+  for (uint64_t i = 0; i < m; ++i)
+    if (hoff[i + 1] < hoff[i]) throw Error(IG_ECONFIG, "corpus offsets must be non-decreasing");
+  if (m >= 0xffffffffull) throw Error(IG_ECONFIG, "too many sequences");
+}
+
+void load_corpus(Session& s, const ig_corpus& c, bool copy_data) {
+  use_device(s);
+  const uint64_t m = c.num_seqs;
+  std::vector<uint64_t> hoff(m + 1);
+  if (c.location == IG_DEVICE) {
+    IGB_CUDA(cudaMemcpy(hoff.data(), c.offsets, (m + 1) * sizeof(uint64_t),
+                        cudaMemcpyDeviceToHost));
+  } else {
+    memcpy(hoff.data(), c.offsets, (m + 1) * sizeof(uint64_t));
+  }
+  check_offsets(hoff);
+  const uint64_t total = hoff[m];
+  uint8_t* data = alloc_corpus(s, total);
+  if (total && copy_data) {
+    IGB_CUDA(cudaMemcpyAsync(data, c.data, total,
+                             c.location == IG_DEVICE ? cudaMemcpyDeviceToDevice
+                                                     : cudaMemcpyHostToDevice,
+                             s.stream));
+  }
+  finish_corpus(s, hoff);
 }
 
 void init_select(Session& s) {
@@ -620,7 +643,7 @@ static void run_t(Session& s, const ig_params& p, ig_result* out) {
   s.launches += s.sel.launches - sel_before;
 }
 
-static void run(Session& s, const ig_params& p, ig_result* out) {
+void run(Session& s, const ig_params& p, ig_result* out) {
   validate(p);
   if (!s.loaded) throw Error(IG_ECONFIG, "no corpus loaded");
   use_device(s);

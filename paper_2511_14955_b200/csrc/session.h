@@ -59,7 +59,12 @@ struct Session {
   cudaStream_t copy_stream = nullptr;
   std::vector<cudaEvent_t> events;
 
+  // pinned staging slabs of the file loader (ingest.cu), created on first use
+  void* slabs = nullptr;
+  void (*slabs_free)(void*) = nullptr;
+
   ~Session() {
+    if (slabs && slabs_free) slabs_free(slabs);
     for (auto e : events) cudaEventDestroy(e);
     for (auto e : batch_events) cudaEventDestroy(e);
     if (copy_stream) cudaStreamDestroy(copy_stream);
@@ -141,6 +146,10 @@ inline Row make_row(const std::string& label, uint32_t gl, uint64_t bytes, uint6
 void use_device(Session& s);
 void validate(const ig_params& p);
 void load_corpus(Session& s, const ig_corpus& c, bool copy_data = true);
+uint8_t* alloc_corpus(Session& s, uint64_t total);
+void finish_corpus(Session& s, std::vector<uint64_t>& hoff);
+void check_offsets(const std::vector<uint64_t>& hoff);
+void run(Session& s, const ig_params& p, ig_result* out);
 void init_select(Session& s);
 
 }  // namespace igb

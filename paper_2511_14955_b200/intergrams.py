@@ -19,6 +19,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 from dataclasses import dataclass, field
 from enum import IntEnum
 from typing import Iterable, List, Optional, Sequence, Tuple
@@ -163,6 +164,31 @@ class Corpus:
                            num_seqs=self.num_seqs, location=N.IG_HOST)
 
 
+@dataclass
+class CorpusSpec:
+    """corpus.hpp:30-36: files / directories read by the library straight into
+    HBM (ig_*_files), with the reference's enumeration and record rules."""
+    roots: Sequence[str]
+    recurse: bool = False
+    line_mode: bool = False
+    chunk_size: int = 0
+
+    def _native(self):
+        arr = (C.c_char_p * max(len(self.roots), 1))(*[os.fsencode(r) for r in self.roots])
+        spec = N.ig_file_corpus(roots=arr, num_roots=len(self.roots), recurse=int(self.recurse),
+                                line_mode=int(self.line_mode), chunk_size=int(self.chunk_size))
+        return spec, arr  # keep arr alive with the struct
+
+    def files(self) -> Tuple[int, int]:
+        """(number of files, total bytes) the spec enumerates (host only)."""
+        spec, _keep = self._native()
+        n, b = C.c_uint64(0), C.c_uint64(0)
+        err = C.create_string_buffer(1024)
+        _raise(N.lib().ig_file_corpus_files(C.byref(spec), C.byref(n), C.byref(b), err,
+                                            len(err)), err)
+        return int(n.value), int(b.value)
+
+
 def make_memory_corpus(sequences: Iterable[bytes]) -> Corpus:
     """corpus.hpp:67 — in-memory corpus from a list of byte strings."""
     seqs = [bytes(s) for s in sequences]
@@ -235,8 +261,21 @@ def _result(r: N.ig_result, materialize: bool = True) -> IntergramsResult:
 
 
 def run_intergrams(corpus, cfg: IntergramConfig) -> IntergramsResult:
-    """run_intergrams (intergrams.hpp:74-75) on the GPU."""
+    """run_intergrams (intergrams.hpp:74-75) on the GPU.  A CorpusSpec is read
+    from disk by the library (pinned slabs -> HBM, ig_topk_ngrams_files)."""
     cfg.validate()
+    if isinstance(corpus, CorpusSpec):
+        spec, _keep = corpus._native()
+        err = C.create_string_buffer(1024)
+        out = N.ig_result()
+        params = cfg._params()
+        rc = N.lib().ig_topk_ngrams_files(C.byref(spec), C.byref(params), C.byref(out), err,
+                                          len(err))
+        _raise(rc, err)
+        try:
+            return _result(out)
+        finally:
+            N.lib().ig_result_free(C.byref(out))
     c = as_corpus(corpus)
     lib = N.lib()
     err = C.create_string_buffer(1024)
@@ -515,6 +554,25 @@ class Session:
             return _result(out, materialize)
         finally:
             self._lib.ig_result_free(C.byref(out))
+
+    def load_files(self, spec: CorpusSpec) -> None:
+        """Reads a file corpus straight into this session's HBM."""
+        s, _keep = spec._native()
+        err = C.create_string_buffer(1024)
+        _raise(self._lib.ig_session_load_files(self._h, C.byref(s), err, len(err)), err)
+
+    def corpus(self) -> Tuple[np.ndarray, np.ndarray]:
+        """The resident corpus copied back: (data u8, offsets u64)."""
+        m, tot = C.c_uint64(0), C.c_uint64(0)
+        err = C.create_string_buffer(1024)
+        _raise(self._lib.ig_session_corpus(self._h, None, 0, None, 0, C.byref(m), C.byref(tot),
+                                           err, len(err)), err)
+        data = np.zeros(max(tot.value, 1), np.uint8)
+        off = np.zeros(m.value + 1, np.uint64)
+        _raise(self._lib.ig_session_corpus(self._h, data.ctypes.data, tot.value,
+                                           off.ctypes.data, off.size, C.byref(m), C.byref(tot),
+                                           err, len(err)), err)
+        return data[:tot.value], off
 
     @property
     def launches(self) -> int:
