@@ -31,6 +31,12 @@ for rep in range(3):
     t2 = time.perf_counter()
     print(f"load {len(data) / (t1 - t0) / 1e9:.1f} GB/s ({(t1 - t0) * 1e3:.0f} ms), "
           f"load+run {len(data) / (t2 - t0) / 1e9:.1f} GB/s ({(t2 - t0) * 1e3:.0f} ms)")
+for rep in range(3):
+    t0 = time.perf_counter()
+    r = s.run_files(spec, icfg, materialize=False)
+    t1 = time.perf_counter()
+    print(f"run_files (dense pass overlapped with the load) {len(data) / (t1 - t0) / 1e9:.1f} GB/s "
+          f"({(t1 - t0) * 1e3:.0f} ms)")
 ref = ig.Session(device=0)
 ref.load(ig.Corpus(data, np.ascontiguousarray(off, np.uint64)))
 r2 = ref.run(icfg, materialize=False)

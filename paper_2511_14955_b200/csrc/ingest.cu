@@ -137,84 +137,141 @@ Slabs& slabs_of(Session& s) {
 
 // Copies the concatenation of fl's files to dev[0 .. total) through the
 // pinned slabs: reader threads take slab-sized items in order; item j reuses
-// slab j % kSlabs once item j - kSlabs's copy has completed.
-void stream_files(Session& s, const FileList& fl, uint8_t* dev) {
-  const uint64_t total = fl.start.back();
-  if (total == 0) return;
-  Slabs& sl = slabs_of(s);
-  if (!s.copy_stream) IGB_CUDA(cudaStreamCreateWithFlags(&s.copy_stream, cudaStreamNonBlocking));
-  for (int i = 0; i < kSlabs; ++i) sl.item[i] = -1;
-  const int64_t nitems = (int64_t)((total + kSlabBytes - 1) / kSlabBytes);
-  std::atomic<int64_t> next{0};
-  std::atomic<bool> failed{false};
-  std::exception_ptr first_error;
-  std::mutex err_mu;
-  const int device = s.device;
-  auto worker = [&]() {
+// slab j % kSlabs once item j - kSlabs's copy has completed.  start() returns
+// at once; wait_bytes(e) blocks until every copy of bytes [0, e) has been
+// enqueued on the copy stream; finish() joins the readers, waits for the
+// copies and rethrows the first reader error.
+class FileStreamer {
+ public:
+  FileStreamer(Session& s, const FileList& fl, uint8_t* dev) : s_(s), fl_(fl), dev_(dev) {}
+  ~FileStreamer() {
+    failed_.store(true);
+    sl_cv_notify();
+    join();
+  }
+
+  void start() {
+    total_ = fl_.start.back();
+    if (total_ == 0) return;
+    sl_ = &slabs_of(s_);
+    if (!s_.copy_stream)
+      IGB_CUDA(cudaStreamCreateWithFlags(&s_.copy_stream, cudaStreamNonBlocking));
+    for (int i = 0; i < kSlabs; ++i) sl_->item[i] = -1;
+    nitems_ = (int64_t)((total_ + kSlabBytes - 1) / kSlabBytes);
+    enqueued_.assign((size_t)nitems_, 0);
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const int nthreads = (int)std::min<int64_t>(std::min<unsigned>(hw, 16u), nitems_);
+    for (int i = 0; i < nthreads; ++i) pool_.emplace_back([this] { worker(); });
+  }
+
+  void wait_bytes(uint64_t end) {
+    if (total_ == 0 || end == 0) return;
+    const int64_t need = (int64_t)((std::min(end, total_) + kSlabBytes - 1) / kSlabBytes);
+    std::unique_lock<std::mutex> lk(sl_->mu);
+    sl_->cv.wait(lk, [&] { return failed_.load() || prefix_ >= need; });
+    if (failed_.load()) {
+      lk.unlock();
+      finish();
+    }
+  }
+
+  void finish() {
+    join();
+    if (total_) IGB_CUDA(cudaStreamSynchronize(s_.copy_stream));
+    if (first_error_) std::rethrow_exception(first_error_);
+  }
+
+ private:
+  void sl_cv_notify() {
+    if (sl_) sl_->cv.notify_all();
+  }
+  void join() {
+    for (auto& th : pool_)
+      if (th.joinable()) th.join();
+    pool_.clear();
+  }
+
+  void worker() {
+    Slabs& sl = *sl_;
     int fd = -1;
     size_t fd_file = (size_t)-1;
     try {
-      IGB_CUDA(cudaSetDevice(device));
+      IGB_CUDA(cudaSetDevice(s_.device));
       for (;;) {
-        const int64_t j = next.fetch_add(1);
-        if (j >= nitems || failed.load()) break;
+        const int64_t j = next_.fetch_add(1);
+        if (j >= nitems_ || failed_.load()) break;
         const int b = (int)(j % kSlabs);
         {  // wait until the slab's previous item has been copied out
           std::unique_lock<std::mutex> lk(sl.mu);
-          sl.cv.wait(lk, [&] { return failed.load() || j < kSlabs || sl.item[b] == j - kSlabs; });
-          if (failed.load()) break;
+          sl.cv.wait(lk, [&] { return failed_.load() || j < kSlabs || sl.item[b] == j - kSlabs; });
+          if (failed_.load()) break;
         }
         if (j >= kSlabs) IGB_CUDA(cudaEventSynchronize(sl.done[b]));
         const uint64_t a0 = (uint64_t)j * kSlabBytes;
-        const uint64_t a1 = std::min<uint64_t>(total, a0 + kSlabBytes);
+        const uint64_t a1 = std::min<uint64_t>(total_, a0 + kSlabBytes);
         uint8_t* buf = static_cast<uint8_t*>(sl.host[b]);
-        size_t f = (size_t)(std::upper_bound(fl.start.begin(), fl.start.end(), a0) -
-                            fl.start.begin()) - 1;
+        size_t f = (size_t)(std::upper_bound(fl_.start.begin(), fl_.start.end(), a0) -
+                            fl_.start.begin()) - 1;
         uint64_t x = a0;
         while (x < a1) {
-          while (fl.start[f + 1] <= x) ++f;  // skip empty files
+          while (fl_.start[f + 1] <= x) ++f;  // skip empty files
           if (fd_file != f) {
             if (fd >= 0) ::close(fd);
-            fd = ::open(fl.paths[f].c_str(), O_RDONLY);
-            if (fd < 0) throw Error(IG_EIO, "cannot open file: " + fl.paths[f]);
+            fd = ::open(fl_.paths[f].c_str(), O_RDONLY);
+            if (fd < 0) throw Error(IG_EIO, "cannot open file: " + fl_.paths[f]);
             fd_file = f;
           }
-          const uint64_t want = std::min<uint64_t>(a1, fl.start[f + 1]) - x;
+          const uint64_t want = std::min<uint64_t>(a1, fl_.start[f + 1]) - x;
           uint64_t got = 0;
           while (got < want) {
             const ssize_t r = ::pread(fd, buf + (x - a0) + got, want - got,
-                                      (off_t)(x - fl.start[f] + got));
-            if (r < 0) throw Error(IG_EIO, "read error: " + fl.paths[f]);
-            if (r == 0) throw Error(IG_EIO, "file changed while reading: " + fl.paths[f]);
+                                      (off_t)(x - fl_.start[f] + got));
+            if (r < 0) throw Error(IG_EIO, "read error: " + fl_.paths[f]);
+            if (r == 0) throw Error(IG_EIO, "file changed while reading: " + fl_.paths[f]);
             got += (uint64_t)r;
           }
           x += want;
         }
-        IGB_CUDA(cudaMemcpyAsync(dev + a0, buf, a1 - a0, cudaMemcpyHostToDevice, s.copy_stream));
-        IGB_CUDA(cudaEventRecord(sl.done[b], s.copy_stream));
+        IGB_CUDA(cudaMemcpyAsync(dev_ + a0, buf, a1 - a0, cudaMemcpyHostToDevice, s_.copy_stream));
+        IGB_CUDA(cudaEventRecord(sl.done[b], s_.copy_stream));
         {
           std::lock_guard<std::mutex> lk(sl.mu);
           sl.item[b] = j;
+          enqueued_[(size_t)j] = 1;
+          while (prefix_ < nitems_ && enqueued_[(size_t)prefix_]) ++prefix_;
         }
         sl.cv.notify_all();
       }
     } catch (...) {
       {
-        std::lock_guard<std::mutex> lk(err_mu);
-        if (!first_error) first_error = std::current_exception();
+        std::lock_guard<std::mutex> lk(err_mu_);
+        if (!first_error_) first_error_ = std::current_exception();
       }
-      failed.store(true);
+      failed_.store(true);
       sl.cv.notify_all();
     }
     if (fd >= 0) ::close(fd);
-  };
-  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-  const int nthreads = (int)std::min<int64_t>(std::min<unsigned>(hw, 16u), nitems);
-  std::vector<std::thread> pool;
-  for (int i = 0; i < nthreads; ++i) pool.emplace_back(worker);
-  for (auto& th : pool) th.join();
-  IGB_CUDA(cudaStreamSynchronize(s.copy_stream));
-  if (first_error) std::rethrow_exception(first_error);
+  }
+
+  Session& s_;
+  const FileList& fl_;
+  uint8_t* dev_;
+  Slabs* sl_ = nullptr;
+  uint64_t total_ = 0;
+  int64_t nitems_ = 0;
+  std::atomic<int64_t> next_{0};
+  std::atomic<bool> failed_{false};
+  std::vector<uint8_t> enqueued_;
+  int64_t prefix_ = 0;  // items [0, prefix_) enqueued (under sl_->mu)
+  std::exception_ptr first_error_;
+  std::mutex err_mu_;
+  std::vector<std::thread> pool_;
+};
+
+void stream_files(Session& s, const FileList& fl, uint8_t* dev) {
+  FileStreamer fs(s, fl, dev);
+  fs.start();
+  fs.finish();
 }
 
 struct IsNewline {
@@ -282,6 +339,41 @@ void load_lines(Session& s, const FileList& fl) {
   finish_corpus(s, hoff);  // synchronises the stream; `raw` can go
 }
 
+// Whole-file / chunk records: offsets are known from the sizes, so the dense
+// pass consumes sequence-aligned batches while the readers are still
+// streaming later files (the batch gate waits for a batch's copies to be
+// enqueued, then records its event).  Line records load first, then run.
+void run_files(Session& s, const ig_file_corpus& spec, const ig_params& p, ig_result* out) {
+  use_device(s);
+  const FileList fl = enumerate(spec);
+  if (spec.line_mode) {
+    load_lines(s, fl);
+    run(s, p, out);
+    return;
+  }
+  std::vector<uint64_t> hoff = record_offsets(fl, spec.chunk_size);
+  check_offsets(hoff);
+  uint8_t* data = alloc_corpus(s, fl.start.back());
+  finish_corpus(s, hoff);  // synchronises the stream (pads zeroed)
+  const std::vector<uint64_t> ends = plan_batches(s);
+  FileStreamer fs(s, fl, data);
+  fs.start();
+  s.batch_gate = [&](size_t i) {
+    fs.wait_bytes(ends[i]);
+    IGB_CUDA(cudaEventRecord(s.batches[i].ready, s.copy_stream ? s.copy_stream : s.stream));
+  };
+  try {
+    run(s, p, out);
+  } catch (...) {
+    s.batch_gate = nullptr;
+    s.batches.clear();
+    throw;
+  }
+  s.batch_gate = nullptr;
+  s.batches.clear();
+  fs.finish();
+}
+
 void load_files(Session& s, const ig_file_corpus& spec) {
   use_device(s);
   const FileList fl = enumerate(spec);
@@ -327,8 +419,7 @@ int ig_session_run_files(ig_session* s, const ig_file_corpus* spec, const ig_par
   return guarded(err, err_len, [&] {
     if (!s || !spec || !params || !out) throw Error(IG_ECONFIG, "null argument");
     validate(*params);
-    load_files(*s, *spec);
-    run(*s, *params, out);
+    run_files(*s, *spec, *params, out);
   });
 }
 
@@ -339,8 +430,7 @@ int ig_topk_ngrams_files(const ig_file_corpus* spec, const ig_params* params, ig
     validate(*params);
     ig_session* s = create(params->device, nullptr, nullptr);
     try {
-      load_files(*s, *spec);
-      run(*s, *params, out);
+      run_files(*s, *spec, *params, out);
     } catch (...) {
       delete s;
       throw;

@@ -406,7 +406,9 @@ static CT* count_pass(Session& s, bool dense, uint32_t L, int mode, const Prefix
     if (dense && !s.batches.empty()) {
       // pipelined load: route each batch as soon as its bytes have landed
       rp.next_lgno = next_lgno;
-      for (const auto& b : s.batches) {
+      for (size_t bi = 0; bi < s.batches.size(); ++bi) {
+        const auto& b = s.batches[bi];
+        if (s.batch_gate) s.batch_gate(bi);
         if (b.ready) IGB_CUDA(cudaStreamWaitEvent(s.stream, b.ready, 0));
         s.rc.u0 = b.u0;
         s.rc.u1 = b.u1;
@@ -465,6 +467,7 @@ static CT* count_pass(Session& s, bool dense, uint32_t L, int mode, const Prefix
     waits.push_back(nullptr);
   }
   for (size_t r = 0; r < ranges.size(); ++r) {
+    if (s.batch_gate && dense && !s.batches.empty()) s.batch_gate(r);
     if (waits[r]) IGB_CUDA(cudaStreamWaitEvent(s.stream, waits[r], 0));
     if constexpr (sizeof(CT) == 8) {
       // 64-bit totals: count each < 2^32-byte corpus segment into an
@@ -666,20 +669,15 @@ namespace igb {
 // Host corpus: offsets/units/tiles first, then the bytes in sequence-aligned
 // batches on a copy stream (one event per batch); the dense pass consumes the
 // batches as they land, so most of the H2D hides behind counting.
-static void load_and_run(Session& s, const ig_corpus& c, const ig_params& p, ig_result* out) {
-  validate(p);
-  if (c.location == IG_DEVICE) {
-    load_corpus(s, c, true);
-    run(s, p, out);
-    return;
-  }
-  load_corpus(s, c, false);
+// Sequence-aligned batches of the loaded corpus (>= 256 MiB or 1/8 of it)
+// for a dense pass that consumes the corpus as it lands: fills s.batches
+// (one event each, not yet recorded) and returns each batch's byte end.
+std::vector<uint64_t> plan_batches(Session& s) {
   const uint64_t m = s.dc.m, total = s.dc.total;
-  if (!s.copy_stream) IGB_CUDA(cudaStreamCreateWithFlags(&s.copy_stream, cudaStreamNonBlocking));
   const uint64_t want = std::max<uint64_t>(256ull << 20, (total + 7) / 8);
   s.batches.clear();
-  uint64_t q = 0;
-  uint64_t prev_t1 = 0;
+  std::vector<uint64_t> ends;
+  uint64_t q = 0, prev_t1 = 0;
   size_t nb = 0;
   while (q < m || (m == 0 && nb == 0)) {
     const uint64_t q0 = q;
@@ -692,11 +690,6 @@ static void load_and_run(Session& s, const ig_corpus& c, const ig_params& p, ig_
       IGB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
       s.batch_events.push_back(e);
     }
-    cudaEvent_t ev = s.batch_events[nb];
-    if (b1 > b0)
-      IGB_CUDA(cudaMemcpyAsync(const_cast<uint8_t*>(s.dc.data) + b0, c.data + b0, b1 - b0,
-                               cudaMemcpyHostToDevice, s.copy_stream));
-    IGB_CUDA(cudaEventRecord(ev, s.copy_stream));
     Session::Batch b{};
     b.q0 = (uint32_t)q0;
     b.q1 = (uint32_t)q;
@@ -706,10 +699,35 @@ static void load_and_run(Session& s, const ig_corpus& c, const ig_params& p, ig_
     b.t1 = q >= m ? s.dc.ntiles : std::min<uint64_t>(s.dc.ntiles, b1 / kTileBytes);
     if (b.t1 < b.t0) b.t1 = b.t0;
     prev_t1 = b.t1;
-    b.ready = ev;
+    b.ready = s.batch_events[nb];
     s.batches.push_back(b);
+    ends.push_back(b1);
     ++nb;
     if (m == 0) break;
+  }
+  return ends;
+}
+
+// Host corpus: offsets/units/tiles first, then the bytes in sequence-aligned
+// batches on a copy stream (one event per batch); the dense pass consumes the
+// batches as they land, so most of the H2D hides behind counting.
+static void load_and_run(Session& s, const ig_corpus& c, const ig_params& p, ig_result* out) {
+  validate(p);
+  if (c.location == IG_DEVICE) {
+    load_corpus(s, c, true);
+    run(s, p, out);
+    return;
+  }
+  load_corpus(s, c, false);
+  if (!s.copy_stream) IGB_CUDA(cudaStreamCreateWithFlags(&s.copy_stream, cudaStreamNonBlocking));
+  const std::vector<uint64_t> ends = plan_batches(s);
+  uint64_t b0 = 0;
+  for (size_t i = 0; i < ends.size(); ++i) {
+    if (ends[i] > b0)
+      IGB_CUDA(cudaMemcpyAsync(const_cast<uint8_t*>(s.dc.data) + b0, c.data + b0, ends[i] - b0,
+                               cudaMemcpyHostToDevice, s.copy_stream));
+    IGB_CUDA(cudaEventRecord(s.batches[i].ready, s.copy_stream));
+    b0 = ends[i];
   }
   try {
     run(s, p, out);

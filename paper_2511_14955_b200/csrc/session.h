@@ -8,6 +8,7 @@
 #include <string.h>
 
 #include <cstdio>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -53,6 +54,9 @@ struct Session {
     cudaEvent_t ready;         // copy of the batch's bytes done (null: resident)
   };
   std::vector<Batch> batches;
+  // host gate before batch i is consumed (file loads: waits until the batch's
+  // copies are enqueued, then records its event); empty otherwise
+  std::function<void(size_t)> batch_gate;
   std::vector<cudaEvent_t> batch_events;
   std::vector<uint64_t> hoff;  // host offsets of the loaded corpus
   std::vector<uint32_t> hufirst;
@@ -150,6 +154,7 @@ uint8_t* alloc_corpus(Session& s, uint64_t total);
 void finish_corpus(Session& s, std::vector<uint64_t>& hoff);
 void check_offsets(const std::vector<uint64_t>& hoff);
 void run(Session& s, const ig_params& p, ig_result* out);
+std::vector<uint64_t> plan_batches(Session& s);
 void init_select(Session& s);
 
 }  // namespace igb

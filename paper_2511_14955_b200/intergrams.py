@@ -561,6 +561,24 @@ class Session:
         err = C.create_string_buffer(1024)
         _raise(self._lib.ig_session_load_files(self._h, C.byref(s), err, len(err)), err)
 
+    def run_files(self, spec: CorpusSpec, cfg: IntergramConfig,
+                  materialize: bool = True) -> IntergramsResult:
+        """Reads a file corpus into HBM and runs on it; the dense pass consumes
+        the corpus while later files are still being read (whole-file and
+        chunk records)."""
+        cfg.validate()
+        s, _keep = spec._native()
+        err = C.create_string_buffer(1024)
+        out = N.ig_result()
+        params = cfg._params()
+        rc = self._lib.ig_session_run_files(self._h, C.byref(s), C.byref(params), C.byref(out),
+                                            err, len(err))
+        _raise(rc, err)
+        try:
+            return _result(out, materialize)
+        finally:
+            self._lib.ig_result_free(C.byref(out))
+
     def corpus(self) -> Tuple[np.ndarray, np.ndarray]:
         """The resident corpus copied back: (data u8, offsets u64)."""
         m, tot = C.c_uint64(0), C.c_uint64(0)

@@ -95,3 +95,20 @@ def test_run_over_files_equals_in_memory(gpu_lib, tmp_path, mode):
 def test_missing_root_is_config_error(gpu_lib, tmp_path):
     with pytest.raises(ig.ConfigError):
         ig.run_intergrams(ig.CorpusSpec([str(tmp_path / "missing")]), ig.IntergramConfig(n=3, k=1))
+
+
+@pytest.mark.parametrize("mode", [ig.CountMode.kOnce, ig.CountMode.kAll])
+def test_pipelined_run_files_multi_slab(sess, tmp_path, mode):
+    # run_files overlaps the dense pass with the readers: batches of >= 256 MiB
+    from paper_2511_14955_b200 import synth as S
+    data, off = S.generate(S.scaled(S.CONFIGS["c2"], num_seqs=700), 0, -1)
+    d = tmp_path / "p"
+    d.mkdir()
+    per = (len(data) // 5) // (1 << 20) * (1 << 20)
+    cuts = [0, per, 2 * per, 3 * per, 4 * per, len(data)]
+    for i in range(5):
+        (d / f"x{i}").write_bytes(data[cuts[i]:cuts[i + 1]].tobytes())
+    cfg = ig.IntergramConfig(n=5, k=500, z=1.5, mode=mode)
+    a = sess.run_files(ig.CorpusSpec([str(d)], chunk_size=1 << 20), cfg, materialize=False)
+    b = ig.run_intergrams(ig.Corpus(data, np.ascontiguousarray(off, np.uint64)), cfg)
+    assert np.array_equal(a.keys, b.keys) and np.array_equal(a.counts, b.counts)
