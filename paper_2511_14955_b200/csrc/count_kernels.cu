@@ -1,4 +1,6 @@
-// count_kernels.cu — the counting passes of Intergrams on sm_100a.
+// count_kernels.cu — the count-all counting passes of Intergrams on sm_100a
+// (count-once passes route through route_kernels.cu), tile descriptors and
+// the count-all prefix set.
 //
 // Reference semantics:
 //   dense pass     proj/src/intergrams.cpp:79-100 (= dense_pass.cpp:21-39):
@@ -17,16 +19,9 @@
 //     from the neighbouring lane by shuffle, never from a second HBM read.
 //   * n-gram keys are assembled in registers with funnel shifts / byte perms
 //     at compile-time byte offsets (the gram length is a template parameter).
-//   * count-all: one L2 reduction (RED) per occurrence; duplicate ids within a
-//     warp instruction are merged with MATCH.ANY first so hot grams do not
-//     serialise on one L2 slice.
-//   * count-once: per-sequence dedup in SHARED memory.  The candidate space
-//     is split into G owner slices (G = 16 for the 2^24 dense space); the G
-//     CTAs of a group each keep one slice's bitmap in smem, scan the same
-//     sequence, and handle only the windows they own.  A bit that is already
-//     set is detected with a plain shared load (test before set), so repeated
-//     grams cost no atomic; the first occurrence does one ATOMS.OR and one RED
-//     to the L2-resident count table.
+//   * count-all: one L2 reduction (RED) per occurrence, except for the ids a
+//     CTA's shared-memory hot cache owns (counted with shared atomics and
+//     flushed once), so hot Zipf grams do not serialise on one L2 slice.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -374,153 +369,6 @@ void launch_widen_add(const uint32_t* src, unsigned long long* dst, uint64_t n, 
   k_widen_add<<<blocks, 256, 0, st>>>(src, dst, n4);
 }
 
-// ------------------------------------------------------------------ count-once
-
-constexpr int kOnceThreads = 512;
-constexpr int kOnceWarps = kOnceThreads / 32;
-constexpr int kTileBufWords = 136;  // [2 unused | 2 halo | 128 tile (16-B aligned) | pad]
-
-// Big-endian key of the 8 bytes ending at tile position p (0..511) from the
-// warp's staged tile (word 0..1 = the 8 bytes before the tile).
-__device__ __forceinline__ uint64_t key8_smem(const uint32_t* buf, uint32_t p) {
-  const uint32_t o = p + 9;  // tile byte p lives at buf byte 16 + p; first of the 8 bytes
-  const uint32_t wi = o >> 2, sh = (o & 3) * 8;
-  const uint32_t w0 = buf[wi], w1 = buf[wi + 1], w2 = buf[wi + 2];
-  const uint32_t lo = __funnelshift_r(w0, w1, sh), hi = __funnelshift_r(w1, w2, sh);
-  return ((uint64_t)__byte_perm(lo, 0, 0x0123) << 32) | (uint64_t)__byte_perm(hi, 0, 0x0123);
-}
-
-// One CTA = (group g, owner o); group g takes sequences order[g], order[g+NG],
-// ... (the G CTAs of a group walk the same sequences in the same order, so a
-// sequence is read from HBM once and from L2 by the others).  Per 512-byte
-// tile a warp (1) stages the tile in smem, (2) computes the 16-bit mask of
-// valid gram ends it owns per lane in registers, (3) compacts the owned
-// positions into a warp queue, (4) drains the queue 32 positions at a time
-// with all lanes converged: key -> (prefix lookup) -> bitmap test -> first
-// occurrence: ATOMS.OR + RED.  After each sequence the slice bitmap is cleared.
-template <int KIND, int L, typename CT, int TAB>
-__global__ void __launch_bounds__(kOnceThreads) k_count_once(DevCorpus c, DevPrefixSet ps,
-                                                           const uint64_t* __restrict__ packed,
-                                                           uint32_t G, uint32_t lgG,
-                                                           uint32_t bm_words, uint32_t ngroups,
-                                                           CT* __restrict__ table) {
-  extern __shared__ uint4 smem_raw[];
-  uint32_t* bm = reinterpret_cast<uint32_t*>(smem_raw);
-  uint64_t* s_tab = reinterpret_cast<uint64_t*>(bm + bm_words);
-  const uint32_t tab_words = (TAB == 1) ? ps.S * 2 : 0;
-  uint32_t* tilebuf = bm + bm_words + tab_words;
-  uint16_t* queue = reinterpret_cast<uint16_t*>(tilebuf + kOnceWarps * kTileBufWords);
-
-  const uint32_t o = blockIdx.x % G;
-  const uint32_t g = blockIdx.x / G;
-  const uint32_t gm4 = (G - 1) * 0x01010101u, o4 = o * 0x01010101u;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint32_t* buf = tilebuf + warp * kTileBufWords;
-  uint16_t* q = queue + warp * 512;
-  const uint32_t ostart = (KIND == 1) ? ps.owner_start[o] : 0u;
-
-  for (uint32_t i = threadIdx.x; i < bm_words / 4; i += blockDim.x) smem_raw[i] = make_uint4(0, 0, 0, 0);
-  if constexpr (TAB == 1) {
-    const uint64_t* src = packed + (size_t)o * ps.S;
-    for (uint32_t i = threadIdx.x; i < ps.S; i += blockDim.x) s_tab[i] = src[i];
-  }
-  if (lane == 0) {
-    for (int i = 132; i < kTileBufWords; ++i) buf[i] = 0;
-  }
-  __syncthreads();
-
-  for (uint64_t r = g; r < c.m; r += ngroups) {
-    const uint32_t sq = c.order[r];
-    const int64_t s0 = (int64_t)c.off[sq], s1 = (int64_t)c.off[sq + 1];
-    if (s1 - s0 >= L) {
-      const int64_t first = s0 & ~int64_t(15);
-      const int64_t ntiles = (s1 - first + kTileBytes - 1) / kTileBytes;
-      int64_t t = warp;
-      uint4 v = make_uint4(0, 0, 0, 0);
-      uint2 h = make_uint2(0, 0);
-      if (t < ntiles) {
-        v = __ldcg(reinterpret_cast<const uint4*>(c.data + first + t * kTileBytes + lane * 16));
-        if (lane == 0) h = *reinterpret_cast<const uint2*>(c.data + first + t * kTileBytes - 8);
-      }
-      while (t < ntiles) {
-        const int64_t tn = t + kOnceWarps;
-        uint4 vn = make_uint4(0, 0, 0, 0);
-        uint2 hn = make_uint2(0, 0);
-        if (tn < ntiles) {
-          vn = __ldcg(reinterpret_cast<const uint4*>(c.data + first + tn * kTileBytes + lane * 16));
-          if (lane == 0) hn = *reinterpret_cast<const uint2*>(c.data + first + tn * kTileBytes - 8);
-        }
-        const int64_t b0 = first + t * kTileBytes + lane * 16;
-        Seg s;
-        s.W[2] = v.x;
-        s.W[3] = v.y;
-        s.W[4] = v.z;
-        s.W[5] = v.w;
-        s.W[6] = 0;
-        s.W[0] = __shfl_up_sync(0xffffffffu, v.z, 1);
-        s.W[1] = __shfl_up_sync(0xffffffffu, v.w, 1);
-        if (lane == 0) {
-          s.W[0] = h.x;
-          s.W[1] = h.y;
-          buf[2] = h.x;
-          buf[3] = h.y;
-        }
-        reinterpret_cast<uint4*>(buf + 4)[lane] = v;
-        uint32_t vm = valid_mask_one<L>(b0, s0, s1);
-        if (G > 1) vm &= owner_mask<KIND, L>(s, gm4, o4);
-        // warp exclusive scan of the owned counts -> queue slots
-        const uint32_t cnt = __popc(vm);
-        uint32_t incl = cnt;
-#pragma unroll
-        for (int dd = 1; dd < 32; dd <<= 1) {
-          const uint32_t y = __shfl_up_sync(0xffffffffu, incl, dd);
-          if (lane >= dd) incl += y;
-        }
-        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-        uint32_t pos = incl - cnt;
-        while (vm) {
-          const int T = __ffs(vm) - 1;
-          vm &= vm - 1;
-          q[pos++] = (uint16_t)(lane * 16 + T);
-        }
-        __syncwarp();
-        for (uint32_t i = lane; i < total; i += 32) {
-          const uint32_t p = q[i];
-          const uint64_t key = key8_smem(buf, p) & gram_mask<L>();
-          uint64_t gid;
-          uint32_t local;
-          if constexpr (KIND == 0) {
-            gid = key;
-            local = (uint32_t)(key >> lgG);
-          } else {
-            uint32_t lp;
-            if constexpr (TAB == 1) lp = lookup_packed(s_tab, ps.lgS, ps.ib, key >> 8);
-            else {
-              lp = prefix_lookup(ps.hkeys, ps.hidx, ps.S, ps.lgS, o, key >> 8);
-              if (lp != 0xffffffffu) lp -= ostart;
-            }
-            if (lp == 0xffffffffu) continue;
-            gid = (uint64_t)(ostart + lp) * 256 + (key & 0xff);
-            local = lp * 256 + (uint32_t)(key & 0xff);
-          }
-          const uint32_t bit = 1u << (local & 31);
-          uint32_t* w = bm + (local >> 5);
-          if (!(*(volatile uint32_t*)w & bit)) {
-            if (!(atomicOr(w, bit) & bit)) atomicAdd(table + gid, (CT)1);
-          }
-        }
-        __syncwarp();
-        t = tn;
-        v = vn;
-        h = hn;
-      }
-    }
-    __syncthreads();
-    for (uint32_t i = threadIdx.x; i < bm_words / 4; i += blockDim.x) smem_raw[i] = make_uint4(0, 0, 0, 0);
-    __syncthreads();
-  }
-}
-
 // ------------------------------------------------------------------ launchers
 
 template <int KIND, int L, typename CT>
@@ -546,36 +394,6 @@ static void launch_all_t(const DevCorpus& c, const DevPrefixSet& ps, CT* table, 
   }
 }
 
-template <int KIND, int L, typename CT, int TAB>
-static void launch_once_tt(const DevCorpus& c, const DevPrefixSet& ps, uint32_t G, uint32_t lgG,
-                           uint32_t bm_words, size_t smem, CT* table, int num_sms, cudaStream_t st) {
-  auto kern = k_count_once<KIND, L, CT, TAB>;
-  IGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int per_sm = 0;
-  IGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kOnceThreads, smem));
-  if (per_sm < 1) throw Error(IG_EINTERNAL, "count-once slice does not fit in shared memory");
-  uint64_t ngroups = ((uint64_t)num_sms * per_sm) / G;
-  if (ngroups < 1) ngroups = 1;
-  if (ngroups > c.m) ngroups = c.m;
-  kern<<<(unsigned)(ngroups * G), kOnceThreads, smem, st>>>(c, ps, ps.packed, G, lgG, bm_words,
-                                                            (uint32_t)ngroups, table);
-}
-
-template <int KIND, int L, typename CT>
-static void launch_once_t(const DevCorpus& c, const DevPrefixSet& ps, uint32_t G, uint32_t lgG,
-                          uint64_t slice_bits, CT* table, int num_sms, cudaStream_t st) {
-  if (!c.m) return;
-  const uint32_t bm_words = (uint32_t)((slice_bits + 127) / 128 * 4);  // multiple of 4 words
-  const size_t fixed = (size_t)bm_words * 4 + (size_t)kOnceWarps * (kTileBufWords * 4 + 1024);
-  const size_t tab = (KIND == 1 && ps.packed) ? (size_t)ps.S * 8 : 0;
-  if (tab && fixed + tab <= kMaxOnceSmem) {
-    launch_once_tt<KIND, L, CT, 1>(c, ps, G, lgG, bm_words, fixed + tab, table, num_sms, st);
-  } else {
-    launch_once_tt<KIND, L, CT, (KIND == 1 ? 2 : 0)>(c, ps, G, lgG, bm_words, fixed, table,
-                                                     num_sms, st);
-  }
-}
-
 template <typename CT>
 void launch_count_dense(const DevCorpus& c, uint32_t n0, int mode, CT* table, uint32_t* /*work*/,
                         int num_sms, cudaStream_t st) {
@@ -587,22 +405,18 @@ void launch_count_dense(const DevCorpus& c, uint32_t n0, int mode, CT* table, ui
       default: launch_all_t<0, 3, CT>(c, none, table, num_sms, st); break;
     }
   } else {
-    switch (n0) {
-      case 1: launch_once_t<0, 1, CT>(c, none, 1, 0, 256, table, num_sms, st); break;
-      case 2: launch_once_t<0, 2, CT>(c, none, 1, 0, 65536, table, num_sms, st); break;
-      default: launch_once_t<0, 3, CT>(c, none, 16, 4, 1u << 20, table, num_sms, st); break;
-    }
+    // count-once counts through the route path (route_kernels.cu)
+    throw Error(IG_EINTERNAL, "count_dense kernel is count-all only");
   }
 }
 
 template <typename CT>
 void launch_count_extend(const DevCorpus& c, const DevPrefixSet& ps, uint32_t j, int mode,
                          CT* table, uint32_t* /*work*/, int num_sms, cudaStream_t st) {
-  const uint64_t slice_bits = (uint64_t)ps.max_owner * 256;
-#define IGB_J(J)                                                                        \
-  case J:                                                                               \
-    if (mode == IG_MODE_ALL) launch_all_t<1, J, CT>(c, ps, table, num_sms, st);         \
-    else launch_once_t<1, J, CT>(c, ps, ps.G, ps.lgG, slice_bits, table, num_sms, st);  \
+  if (mode != IG_MODE_ALL) throw Error(IG_EINTERNAL, "count_extend kernel is count-all only");
+#define IGB_J(J)                                             \
+  case J:                                                    \
+    launch_all_t<1, J, CT>(c, ps, table, num_sms, st);       \
     break;
   switch (j) {
     IGB_J(2) IGB_J(3) IGB_J(4) IGB_J(5) IGB_J(6) IGB_J(7) IGB_J(8)

@@ -25,7 +25,6 @@
 
 namespace igb {
 
-static constexpr size_t kOnceSmemBudget = 200 * 1024;  // bytes of bitmap per CTA
 static constexpr uint64_t kUnitBytes = 4ull << 20;     // count-once work unit
 static constexpr uint32_t kPrefixesPerOwner = 64;       // count-once ext: 64*256 ids/owner
 
@@ -167,9 +166,9 @@ void init_select(Session& s) {
   s.sel.scalar = s.sel_scalar.as<unsigned long long>(1);
 }
 
-// Builds the device prefix set for survivors keys[0..K) of length plen.
-static DevPrefixSet build_prefix_set(Session& s, const uint64_t* keys, uint64_t K, uint32_t plen,
-                                     int mode) {
+// Builds the count-all prefix set for survivors keys[0..K) of length plen:
+// one open-addressing slice (load <= 0.5), p = survivor rank.
+static DevPrefixSet build_prefix_set(Session& s, const uint64_t* keys, uint64_t K, uint32_t plen) {
   DevPrefixSet ps;
   ps.K = (uint32_t)K;
   ps.plen = plen;
@@ -177,34 +176,8 @@ static DevPrefixSet build_prefix_set(Session& s, const uint64_t* keys, uint64_t 
   uint32_t* ocnt = s.owner_cnt.as<uint32_t>(16);
   uint32_t* ostart = s.owner_start.as<uint32_t>(17);
   uint32_t* cursor = s.cursor.as<uint32_t>(16);
-  uint32_t G = 1;
+  const uint32_t G = 1;
   std::vector<uint32_t> cnt(16, 0);
-  if (mode == IG_MODE_ONCE) {
-    // owner16 counts, then the smallest G whose largest slice fits in smem
-    IGB_CUDA(cudaMemsetAsync(ocnt, 0, 16 * sizeof(uint32_t), s.stream));
-    launch_prefix_owner(keys, (uint32_t)K, plen, 16, owner, ocnt, s.stream);
-    s.launches++;
-    IGB_CUDA(cudaMemcpyAsync(cnt.data(), ocnt, 16 * sizeof(uint32_t), cudaMemcpyDeviceToHost,
-                             s.stream));
-    IGB_CUDA(cudaStreamSynchronize(s.stream));
-    G = 0;
-    for (uint32_t g = 1; g <= 16; g *= 2) {
-      uint64_t mx = 0;
-      for (uint32_t o = 0; o < g; ++o) {
-        uint64_t c = 0;
-        for (uint32_t q = o; q < 16; q += g) c += cnt[q];
-        mx = std::max(mx, c);
-      }
-      if (mx * 256 / 8 <= kOnceSmemBudget) {
-        G = g;
-        break;
-      }
-    }
-    if (G == 0)
-      throw Error(IG_EINTERNAL,
-                  "count-once prefix slice exceeds shared memory (k' too large for the smem "
-                  "bitmap path)");
-  }
   uint32_t lgG = 0;
   while ((1u << lgG) < G) ++lgG;
   std::vector<uint32_t> gc(G, 0), gs(G + 1, 0);
@@ -342,7 +315,7 @@ static Prefix prepare_prefix(Session& s, const uint64_t* keys, uint64_t K, uint3
     P.pkeys = dpk;
     P.csr = true;
   } else {
-    P.ps = build_prefix_set(s, keys, K, plen, mode);
+    P.ps = build_prefix_set(s, keys, K, plen);
   }
   return P;
 }
