@@ -173,9 +173,9 @@ __host__ __device__ inline uint32_t prefix_owner(uint64_t key, uint32_t plen, ui
 // device agree on it): multiplicative hash (top bits of key * odd constant,
 // in 32-bit arithmetic for prefixes of <= 4 bytes).
 __host__ __device__ inline uint32_t owner_hash(uint64_t pkey, uint32_t plen, uint32_t lgno) {
-  if (!lgno) return 0u;
-  if (plen <= 4) return ((uint32_t)pkey * kOwnerMul32) >> (32 - lgno);
-  return (uint32_t)((pkey * kOwnerMul) >> (64 - lgno));
+  if (plen <= 4)  // a 64-bit shift by 32 (lgno == 0) is defined: owner 0
+    return (uint32_t)((uint64_t)((uint32_t)pkey * kOwnerMul32) >> (32 - lgno));
+  return lgno ? (uint32_t)((pkey * kOwnerMul) >> (64 - lgno)) : 0u;
 }
 
 // Predicated shared-memory operations.  `if (p) atomicAdd(smem, 1)` compiles

@@ -162,10 +162,11 @@ __device__ __forceinline__ uint32_t vmask(int64_t b0, int64_t lo, int64_t hi) {
   return ((1u << b) - 1u) & ~((1u << a) - 1u);
 }
 
-// Dense: (owner << 16 | local) of a dense id via the odd-multiplier permutation.
+// Dense: (owner << 16 | local) of a dense id via the odd-multiplier
+// permutation (dense ids have <= 24 bits, so 32-bit arithmetic is exact).
 __device__ __forceinline__ uint32_t dense_route(uint64_t id, const RouteParams& rp) {
-  const uint64_t idp = (id * rp.mult) & rp.cmask;
-  return ((uint32_t)(idp >> rp.lgl) << 16) | (uint32_t)(idp & ((1u << rp.lgl) - 1));
+  const uint32_t idp = ((uint32_t)id * (uint32_t)rp.mult) & (uint32_t)rp.cmask;
+  return ((idp >> rp.lgl) << 16) | (idp & ((1u << rp.lgl) - 1));
 }
 
 // Count pass owner of the gram ending at T (no prefix lookup: an upper bound
@@ -305,6 +306,7 @@ __global__ void __launch_bounds__(NT) k_route_scatter(
     const int64_t lo = max((int64_t)U.b0, s0 + L - 1), hi = (int64_t)U.b1;
     const int64_t first = (int64_t)U.b0 & ~int64_t(15);
     const int64_t nseg = (hi - first + 15) >> 4;
+    const bool next_in_seq = nextc && hi < (int64_t)c.off[U.q + 1];
     // the dedup cache lives for the whole unit: every chunk of a unit belongs to
     // the same sequence, so a gram seen anywhere earlier in it adds nothing
     for (uint32_t i = threadIdx.x; i < kSlots; i += blockDim.x) cache[i] = kEmpty;
@@ -316,6 +318,9 @@ __global__ void __launch_bounds__(NT) k_route_scatter(
       uint32_t W[7] = {0, 0, 0, 0, 0, 0, 0};
       if (cs + (int64_t)(threadIdx.x & ~31u) < nseg) seg_load(c.data, b0, lane, W);  // warp-uniform
       const uint32_t vm = sgi < nseg ? vmask(b0, lo, hi) : 0u;
+      // the next pass's gram ending at b0+T+1 is in this unit iff T < lim
+      const int64_t lim64 = hi - b0 - 1;
+      const int32_t lim = (int32_t)(lim64 < 0 ? -1 : lim64 > 16 ? 16 : lim64);
       uint32_t r[16];
       static_for<0, 16>([&](auto tc) {
         constexpr int T = decltype(tc)::value;
@@ -332,6 +337,9 @@ __global__ void __launch_bounds__(NT) k_route_scatter(
           const uint64_t h = (key * 0x9E3779B97F4A7C15ull) & ((1ull << 40) - 1);
           slot = (uint32_t)(h >> (40 - kLgSlots));
           tag = (CK)(h & ((1ull << (40 - kLgSlots)) - 1));
+        } else if constexpr (L <= 4) {
+          slot = ((uint32_t)key * 0x9E3779B1u) >> (32 - kLgSlots);
+          tag = (CK)key;
         } else {
           slot = (((uint32_t)key ^ ((uint32_t)(key >> 32) * 0x85EBCA6Bu)) * 0x9E3779B1u) >> (32 - kLgSlots);
           tag = (CK)key;
@@ -348,12 +356,12 @@ __global__ void __launch_bounds__(NT) k_route_scatter(
           // it can be routed only if this gram is a candidate: a lookup hit,
           // or a repeat (counted conservatively: the count is an upper bound)
           const bool cand = valid && (KIND == 0 || v != 0xffffffffu || !fresh);
-          const int64_t nxt_end = b0 + T + 1;
           const uint32_t no = owner_hash(key, L, rp.next_lgno);
-          red_inc_shared_if(cand && nxt_end < hi, nhist + no);
-          if (cand && nxt_end >= hi && nxt_end < (int64_t)c.off[U.q + 1]) {  // first position of unit u+1
+          red_inc_shared_if(cand && T < lim, nhist + no);
+          // a valid position with T >= lim is the unit's last: its successor is
+          // the first position of unit u+1 when that unit is in this sequence
+          if (cand && T >= lim && next_in_seq)
             atomicAdd(rp.next_cnt + (size_t)no * uv.nunits + u + 1, 1u);
-          }
         }
         r[T] = v;
       });
