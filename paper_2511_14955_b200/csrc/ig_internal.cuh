@@ -173,8 +173,12 @@ __host__ __device__ inline uint32_t prefix_owner(uint64_t key, uint32_t plen, ui
 // device agree on it): multiplicative hash (top bits of key * odd constant,
 // in 32-bit arithmetic for prefixes of <= 4 bytes).
 __host__ __device__ inline uint32_t owner_hash(uint64_t pkey, uint32_t plen, uint32_t lgno) {
-  if (plen <= 4)  // a 64-bit shift by 32 (lgno == 0) is defined: owner 0
-    return (uint32_t)((uint64_t)((uint32_t)pkey * kOwnerMul32) >> (32 - lgno));
+#ifdef __CUDA_ARCH__
+  if (plen <= 4)  // clamped funnel shift: a shift by 32 (lgno == 0) gives owner 0
+    return __funnelshift_rc((uint32_t)pkey * kOwnerMul32, 0u, 32 - lgno);
+#else
+  if (plen <= 4) return (uint32_t)((uint64_t)((uint32_t)pkey * kOwnerMul32) >> (32 - lgno));
+#endif
   return lgno ? (uint32_t)((pkey * kOwnerMul) >> (64 - lgno)) : 0u;
 }
 
@@ -184,6 +188,26 @@ __host__ __device__ inline uint32_t owner_hash(uint64_t pkey, uint32_t plen, uin
 #ifdef __CUDACC__
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
+}
+// The same, on 32-bit shared-window addresses (base converted once per
+// kernel: the generic->shared conversion is not free per access).
+__device__ __forceinline__ void red_inc_shared_at(bool p, uint32_t sa) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %0, 0;\n @q red.shared.add.u32 [%1], 1;\n}"
+               :: "r"((uint32_t)p), "r"(sa) : "memory");
+}
+__device__ __forceinline__ uint32_t atom_inc_shared_at(bool p, uint32_t sa) {
+  uint32_t old = 0;
+  asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %1, 0;\n @q atom.shared.add.u32 %0, [%2], 1;\n}"
+               : "+r"(old) : "r"((uint32_t)p), "r"(sa) : "memory");
+  return old;
+}
+__device__ __forceinline__ void st_shared_u32_at(bool p, uint32_t sa, uint32_t v) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %0, 0;\n @q st.shared.u32 [%1], %2;\n}"
+               :: "r"((uint32_t)p), "r"(sa), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_shared_u64_at(bool p, uint32_t sa, uint64_t v) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %0, 0;\n @q st.shared.u64 [%1], %2;\n}"
+               :: "r"((uint32_t)p), "r"(sa), "l"(v) : "memory");
 }
 __device__ __forceinline__ void red_add_shared_if(bool p, const uint32_t* a, uint32_t v) {
   asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %0, 0;\n @q red.shared.add.u32 [%1], %2;\n}"

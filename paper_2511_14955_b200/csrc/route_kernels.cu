@@ -79,8 +79,8 @@ __device__ __forceinline__ uint64_t gmask() {
 // owns exactly one slot.  Keys of <= 4 bytes (NARROW) hash with 32-bit
 // multiplies (bijections of the key).  A slot packs the key with what the
 // scatter needs, by prefix length (layout is a function of the pass):
-//   <= 4 bytes   (key << 32) | v          v = owner << 6 | index in owner
-//      5 bytes   (key << 24) | v
+//   <= 4 bytes   (key << 32) | owner << 16 | index in owner << 8
+//      5 bytes   (key << 24) | v          v = owner << 6 | index in owner
 //   6..7 bytes   (key << 8)  | index      owner recomputed from the key
 // empty = ~0 (an impossible v / index).  A lookup is one u16 and one u64
 // shared-memory load: no probing, no divergence.
@@ -110,6 +110,8 @@ __host__ __device__ __forceinline__ uint32_t mphf_place(const MphfHash& h, uint3
   return (uint32_t)(((uint64_t)(h.s + d * h.t) * nslots) >> 32);
 }
 
+// Returns the route base of a survivor prefix, (owner << 16) | (index in
+// owner << 8), or 0xffffffff when the prefix is not a survivor.
 template <int PLEN>
 __device__ __forceinline__ uint32_t prefix_lookup_v(const uint64_t* slots, const uint16_t* disp,
                                                     uint32_t nb, uint32_t nslots, uint32_t lgno,
@@ -117,15 +119,16 @@ __device__ __forceinline__ uint32_t prefix_lookup_v(const uint64_t* slots, const
   const MphfHash h = mphf_hash<(PLEN <= 4)>(key, nb);
   const uint32_t sl = mphf_place(h, disp[h.b], nslots);
   const uint64_t e = slots[sl];
-  if constexpr (PLEN <= 4) {
+  if constexpr (PLEN <= 4) {  // the base itself is stored
     const uint32_t v = (uint32_t)e;
-    return ((uint32_t)(e >> 32) == (uint32_t)key && v != 0xffffffffu) ? v : 0xffffffffu;
+    return ((uint32_t)(e >> 32) == (uint32_t)key) ? v : 0xffffffffu;  // empty: v = ~0
   } else if constexpr (PLEN == 5) {
     const uint32_t v = (uint32_t)e & 0xffffffu;
-    return ((e >> 24) == key && v != 0xffffffu) ? v : 0xffffffffu;
+    return ((e >> 24) == key && v != 0xffffffu) ? (((v >> 6) << 16) | ((v & 63u) << 8))
+                                                : 0xffffffffu;
   } else {
     const uint32_t idx = (uint32_t)e & 0xffu;
-    return ((e >> 8) == key && idx != 0xffu) ? ((owner_hash(key, PLEN, lgno) << 6) | idx)
+    return ((e >> 8) == key && idx != 0xffu) ? ((owner_hash(key, PLEN, lgno) << 16) | (idx << 8))
                                              : 0xffffffffu;
   }
 }
@@ -179,18 +182,17 @@ __device__ __forceinline__ uint32_t count_owner(const uint32_t (&W)[7], const Ro
 }
 
 // Scatter pass: (owner << 16 | local) of a gram key, or ~0 (prefix miss).
-// Extension: the slot value is (owner << 6 | index of the prefix inside its
-// owner), so local = value_lo6 * 256 + last byte with no second lookup.
+// Extension: the lookup yields (owner << 16 | index of the prefix inside its
+// owner << 8), so the route is that | last byte, with no second lookup.
 template <int KIND, int L>
 __device__ __forceinline__ uint32_t scatter_route(uint64_t key, const RouteParams& rp,
                                                   const uint64_t* slots, const uint16_t* disp) {
   if constexpr (KIND == 0) {
     return dense_route(key, rp);
   } else {
-    const uint32_t v =
+    const uint32_t base =
         prefix_lookup_v<L - 1>(slots, disp, rp.nb, rp.nslots, rp.lgno, key >> 8);
-    if (v == 0xffffffffu) return 0xffffffffu;
-    return ((v >> 6) << 16) | ((v & 63u) * 256 + (uint32_t)(key & 0xff));
+    return base == 0xffffffffu ? base : base | (uint32_t)(key & 0xff);
   }
 }
 
@@ -296,6 +298,8 @@ __global__ void __launch_bounds__(NT) k_route_scatter(
   const uint64_t* slots = KIND == 1 ? stage_table<(TAB == 1 || TAB == 4) ? 1 : 2>(rp, s_slots, disp) : nullptr;
   const bool dedup = rp.dedup;
   const int lane = threadIdx.x & 31;
+  const uint32_t s_cache = smem_u32(cache), s_lhist = smem_u32(lhist), s_nhist = smem_u32(nhist),
+                 s_staging = smem_u32(staging);
   for (uint32_t ui = blockIdx.x; ui < uv.nb; ui += gridDim.x) {
     const uint32_t u = uv.u0 + ui;
     const RouteUnit U = uv.units[u];
@@ -346,18 +350,18 @@ __global__ void __launch_bounds__(NT) k_route_scatter(
         }
         const CK seen = cache[slot];
         const bool fresh = valid && (!dedup || (L != 5 && tag == kEmpty) || seen != tag);  // kEmpty: marker
-        if constexpr (sizeof(CK) == 8) st_shared_u64_if(fresh, (const uint64_t*)(cache + slot), key);
-        else st_shared_u32_if(fresh, (const uint32_t*)(cache + slot), (uint32_t)tag);
+        if constexpr (sizeof(CK) == 8) st_shared_u64_at(fresh, s_cache + slot * 8, key);
+        else st_shared_u32_at(fresh, s_cache + slot * 4, (uint32_t)tag);
         uint32_t v = scatter_route<KIND, L>(key, rp, slots, disp);
         v = fresh ? v : 0xffffffffu;
-        red_inc_shared_if(v != 0xffffffffu, lhist + (v >> 16));
+        red_inc_shared_at(v != 0xffffffffu, s_lhist + (v >> 16) * 4);
         if (nextc) {
           // the next pass's gram ending at b0+T+1 has this gram as its prefix;
           // it can be routed only if this gram is a candidate: a lookup hit,
           // or a repeat (counted conservatively: the count is an upper bound)
           const bool cand = valid && (KIND == 0 || v != 0xffffffffu || !fresh);
           const uint32_t no = owner_hash(key, L, rp.next_lgno);
-          red_inc_shared_if(cand && T < lim, nhist + no);
+          red_inc_shared_at(cand && T < lim, s_nhist + no * 4);
           // a valid position with T >= lim is the unit's last: its successor is
           // the first position of unit u+1 when that unit is in this sequence
           if (cand && T >= lim && next_in_seq)
@@ -388,8 +392,8 @@ __global__ void __launch_bounds__(NT) k_route_scatter(
       static_for<0, 16>([&](auto tc) {
         constexpr int T = decltype(tc)::value;
         const bool h = r[T] != 0xffffffffu;
-        const uint32_t at = atom_add_shared_if(h, lhist + (r[T] >> 16), 1u);
-        st_shared_u32_if(h, staging + at, r[T]);
+        const uint32_t at = atom_inc_shared_at(h, s_lhist + (r[T] >> 16) * 4);
+        st_shared_u32_at(h, s_staging + at * 4, r[T]);
       });
       __syncthreads();
       const uint32_t total = s_total;

@@ -346,7 +346,8 @@ static void build_prefix_table(Session& s, Prefix& P) {
   // slot layout by prefix length (route_kernels.cu: prefix_lookup_v)
   for (size_t i = 0; i < slots.size(); ++i) {
     if (slots[i] == kEmptyKey) continue;
-    if (P.plen <= 4) slots[i] = (slots[i] << 32) | slot_v[i];
+    if (P.plen <= 4)
+      slots[i] = (slots[i] << 32) | ((slot_v[i] >> 6) << 16) | ((slot_v[i] & 63u) << 8);
     else if (P.plen == 5) slots[i] = (slots[i] << 24) | slot_v[i];
     else slots[i] = (slots[i] << 8) | (slot_v[i] & 63u);
   }
