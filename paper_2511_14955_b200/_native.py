@@ -16,7 +16,8 @@ IG_OK, IG_ECONFIG, IG_EIO, IG_EINTERNAL, IG_EINVALID = 0, 2, 3, 4, 5
 IG_MODE_ONCE, IG_MODE_ALL = 0, 1
 IG_HOST, IG_DEVICE = 0, 1
 IG_MAX_N = 8
-KERNEL_FAMILIES = ["route_count", "route_scatter", "route_consume", "count_all", "select"]
+KERNEL_FAMILIES = ["route_count", "route_scatter", "route_consume", "count_all", "select",
+                   "once_short"]
 
 
 class ig_corpus(C.Structure):

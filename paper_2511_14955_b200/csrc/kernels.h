@@ -90,6 +90,15 @@ template <typename CT>
 void route_count_once(int stage, RouteCtx& x, const DevCorpus& c, int kind, uint32_t L,
                       const RouteParams& rp, CT* table, int num_sms, cudaStream_t st);
 
+// Count-once over short sequences (no routing): sw / sc list the sequences
+// of <= kShortWarpLen / <= kShortCtaLen gram ends (a warp / a CTA each).
+constexpr int kShortWarpLen = 512;
+constexpr int kShortCtaLen = 8192;
+template <typename CT>
+void count_once_short(int kind, uint32_t L, const DevCorpus& c, const RouteParams& rp,
+                      const uint32_t* sw, uint32_t nw, const uint32_t* sc, uint32_t nc, CT* table,
+                      int num_sms, cudaStream_t st);
+
 // --- selection (select_kernels.cu)
 struct SelState {
   unsigned long long prefix;   // count digits chosen so far

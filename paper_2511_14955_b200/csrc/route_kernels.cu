@@ -449,6 +449,7 @@ __global__ void __launch_bounds__(kConsumeThreads) k_consume_once(
     const uint64_t q1 = min((uint64_t)uv.q1, q0 + seq_block);
     for (uint64_t q = q0 + warp; q < q1; q += kConsumeWarps) {
       const uint32_t u0 = uv.unit_first[q], u1 = uv.unit_first[q + 1];
+      if (u0 == u1) continue;  // short sequence: counted by k_once_short
       for (uint32_t u = u0; u < u1; ++u) {
         const size_t ix = (size_t)o * uv.nb + (u - uv.u0);
         const uint64_t e0 = base[ix], e1 = e0 + actual[ix];
@@ -488,6 +489,155 @@ __global__ void __launch_bounds__(kConsumeThreads) k_consume_once(
     __syncthreads();
   }
 }
+
+// ------------------------------------------------------------------ 5. short sequences
+
+// Count-once over short sequences (the route path's per-unit and
+// per-(owner, sequence) costs do not amortise over a few hundred bytes): a
+// group of G threads (a warp, or a whole CTA) takes one sequence of <= LMAX
+// gram ends, dedups its candidate table indices exactly in a shared-memory
+// hash set sized to the sequence, and adds 1 per distinct index to the pass
+// table.  Table indices are the route path's (dense: the permuted id;
+// extension: (ostart[owner] + index in owner) * 256 + last byte), so both
+// paths count into one table.
+constexpr int kShortThreads = 512;
+static size_t table_bytes(const RouteParams& rp);
+
+template <int KIND, int L, int TAB, int G, int LMAX, typename CT>
+__global__ void __launch_bounds__(kShortThreads) k_once_short(
+    DevCorpus c, RouteParams rp, const uint32_t* __restrict__ seqs, uint32_t nseqs,
+    CT* __restrict__ table) {
+  extern __shared__ uint4 smem4[];
+  constexpr int NG = kShortThreads / G;  // groups per CTA
+  constexpr int HS = 2 * LMAX;           // hash slots per group (power of two)
+  uint32_t* hs_all = reinterpret_cast<uint32_t*>(smem4);
+  uint32_t* hs = hs_all + (threadIdx.x / G) * HS;
+  uint64_t* s_slots = reinterpret_cast<uint64_t*>(hs_all + NG * HS);
+  const uint16_t* disp = nullptr;
+  const uint64_t* slots = KIND == 1 ? stage_table<TAB>(rp, s_slots, disp) : nullptr;
+  const uint32_t gl = threadIdx.x % G;
+  const uint32_t ngroups = gridDim.x * NG;
+  auto group_sync = [] {
+    if constexpr (G == 32) __syncwarp();
+    else __syncthreads();
+  };
+  for (uint32_t i = blockIdx.x * NG + threadIdx.x / G; i < nseqs; i += ngroups) {
+    const uint32_t q = seqs[i];
+    const uint64_t s0 = c.off[q], s1 = c.off[q + 1];
+    const int64_t npos = (int64_t)(s1 - s0) - (L - 1);  // gram ends (group-uniform)
+    if (npos <= 0) continue;
+    uint32_t lg = 4;
+    while ((1 << lg) < 2 * npos) ++lg;
+    const uint32_t mask = (1u << lg) - 1;
+    for (uint32_t j = gl; j <= mask; j += G) hs[j] = 0xffffffffu;
+    group_sync();
+    // each thread: a contiguous run of gram ends, key rolled byte by byte
+    const uint32_t per = (uint32_t)((npos + G - 1) / G);
+    const int64_t p0 = (int64_t)gl * per;
+    const int64_t p1 = p0 + per < npos ? p0 + per : npos;
+    if (p0 < p1) {
+      const uint8_t* d = c.data + s0;
+      uint64_t key = 0;
+      for (int b = 0; b < L - 1; ++b) key = (key << 8) | d[p0 + b];
+      for (int64_t p = p0; p < p1; ++p) {
+        key = ((key << 8) | d[p + L - 1]) & gmask<L>();
+        uint32_t tidx;
+        if constexpr (KIND == 0) {
+          const uint32_t r = dense_route(key, rp);
+          tidx = ((r >> 16) << rp.lgl) | (r & 0xffffu);
+        } else {
+          const uint32_t base =
+              prefix_lookup_v<L - 1>(slots, disp, rp.nb, rp.nslots, rp.lgno, key >> 8);
+          if (base == 0xffffffffu) continue;
+          tidx = (rp.ostart[base >> 16] + ((base >> 8) & 63u)) * 256u + (uint32_t)(key & 0xff);
+        }
+        uint32_t h = (tidx * 0x9E3779B1u) >> (32 - lg);
+        for (;;) {
+          const uint32_t old = atomicCAS(hs + h, 0xffffffffu, tidx);
+          if (old == 0xffffffffu) {
+            atomicAdd(table + tidx, (CT)1);
+            break;
+          }
+          if (old == tidx) break;
+          h = (h + 1) & mask;
+        }
+      }
+    }
+    group_sync();
+  }
+}
+
+template <int KIND, int L, int TAB, int G, int LMAX, typename CT>
+static void launch_short_t(const DevCorpus& c, const RouteParams& rp, const uint32_t* seqs,
+                           uint32_t n, CT* table, int num_sms, cudaStream_t st) {
+  if (!n) return;
+  constexpr int NG = kShortThreads / G;
+  const size_t smem = (size_t)NG * 2 * LMAX * 4 + (TAB == 1 ? table_bytes(rp) : 0);
+  auto k = k_once_short<KIND, L, TAB, G, LMAX, CT>;
+  IGB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per = 0;
+  IGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, kShortThreads, smem));
+  if (per < 1) throw Error(IG_EINTERNAL, "short-sequence count does not fit in shared memory");
+  const uint64_t want = (n + NG - 1) / NG;
+  const unsigned grid = (unsigned)std::min<uint64_t>(want, (uint64_t)num_sms * per);
+  k<<<grid, kShortThreads, smem, st>>>(c, rp, seqs, n, table);
+}
+
+template <int KIND, int L, typename CT>
+static void launch_short_l(const DevCorpus& c, const RouteParams& rp, const uint32_t* sw,
+                           uint32_t nw, const uint32_t* sc, uint32_t nc, CT* table, int num_sms,
+                           cudaStream_t st) {
+  if constexpr (KIND == 0) {
+    launch_short_t<0, L, 0, 32, kShortWarpLen, CT>(c, rp, sw, nw, table, num_sms, st);
+    launch_short_t<0, L, 0, kShortThreads, kShortCtaLen, CT>(c, rp, sc, nc, table, num_sms, st);
+  } else {
+    // the perfect-hash table in smem next to the hash sets when it fits
+    const bool fits = (size_t)2 * kShortCtaLen * 4 + table_bytes(rp) <= kMaxOnceSmem &&
+                      (size_t)(kShortThreads / 32) * 2 * kShortWarpLen * 4 + table_bytes(rp) <=
+                          kMaxOnceSmem;
+    if (fits) {
+      launch_short_t<1, L, 1, 32, kShortWarpLen, CT>(c, rp, sw, nw, table, num_sms, st);
+      launch_short_t<1, L, 1, kShortThreads, kShortCtaLen, CT>(c, rp, sc, nc, table, num_sms, st);
+    } else {
+      launch_short_t<1, L, 2, 32, kShortWarpLen, CT>(c, rp, sw, nw, table, num_sms, st);
+      launch_short_t<1, L, 2, kShortThreads, kShortCtaLen, CT>(c, rp, sc, nc, table, num_sms, st);
+    }
+  }
+}
+
+template <typename CT>
+void count_once_short(int kind, uint32_t L, const DevCorpus& c, const RouteParams& rp,
+                      const uint32_t* sw, uint32_t nw, const uint32_t* sc, uint32_t nc, CT* table,
+                      int num_sms, cudaStream_t st) {
+  if (!nw && !nc) return;
+  if (kind == 0) {
+    switch (L) {
+      case 1: launch_short_l<0, 1, CT>(c, rp, sw, nw, sc, nc, table, num_sms, st); break;
+      case 2: launch_short_l<0, 2, CT>(c, rp, sw, nw, sc, nc, table, num_sms, st); break;
+      default: launch_short_l<0, 3, CT>(c, rp, sw, nw, sc, nc, table, num_sms, st); break;
+    }
+  } else {
+    switch (L) {
+      case 2: launch_short_l<1, 2, CT>(c, rp, sw, nw, sc, nc, table, num_sms, st); break;
+      case 3: launch_short_l<1, 3, CT>(c, rp, sw, nw, sc, nc, table, num_sms, st); break;
+      case 4: launch_short_l<1, 4, CT>(c, rp, sw, nw, sc, nc, table, num_sms, st); break;
+      case 5: launch_short_l<1, 5, CT>(c, rp, sw, nw, sc, nc, table, num_sms, st); break;
+      case 6: launch_short_l<1, 6, CT>(c, rp, sw, nw, sc, nc, table, num_sms, st); break;
+      case 7: launch_short_l<1, 7, CT>(c, rp, sw, nw, sc, nc, table, num_sms, st); break;
+      case 8: launch_short_l<1, 8, CT>(c, rp, sw, nw, sc, nc, table, num_sms, st); break;
+      default: throw Error(IG_ECONFIG, "gram length above 8 is not supported");
+    }
+  }
+  IGB_CUDA(cudaGetLastError());
+}
+
+template void count_once_short<uint32_t>(int, uint32_t, const DevCorpus&, const RouteParams&,
+                                         const uint32_t*, uint32_t, const uint32_t*, uint32_t,
+                                         uint32_t*, int, cudaStream_t);
+template void count_once_short<unsigned long long>(int, uint32_t, const DevCorpus&,
+                                                   const RouteParams&, const uint32_t*, uint32_t,
+                                                   const uint32_t*, uint32_t,
+                                                   unsigned long long*, int, cudaStream_t);
 
 // ------------------------------------------------------------------ host
 

@@ -86,11 +86,23 @@ void finish_corpus(Session& s, std::vector<uint64_t>& hoff) {
   if (m)
     IGB_CUDA(cudaMemcpyAsync(dord, ord.data(), m * sizeof(uint32_t), cudaMemcpyHostToDevice,
                              s.stream));
-  // count-once work units: <= kUnitBytes of gram ends of one sequence
+  // count-once work units: <= kUnitBytes of gram ends of one long sequence;
+  // short sequences are counted without routing (k_once_short), a warp or a
+  // CTA per sequence
   std::vector<RouteUnit> units;
   std::vector<uint32_t> ufirst(m + 1, 0);
+  std::vector<uint32_t> sw, sc;
   for (uint64_t q = 0; q < m; ++q) {
     ufirst[q] = (uint32_t)units.size();
+    const uint64_t len = hoff[q + 1] - hoff[q];
+    if (len <= (uint64_t)kShortWarpLen) {
+      if (len) sw.push_back((uint32_t)q);
+      continue;
+    }
+    if (len <= (uint64_t)kShortCtaLen) {
+      sc.push_back((uint32_t)q);
+      continue;
+    }
     for (uint64_t b = hoff[q]; b < hoff[q + 1]; b += kUnitBytes) {
       RouteUnit u{};
       u.q = (uint32_t)q;
@@ -107,6 +119,12 @@ void finish_corpus(Session& s, std::vector<uint64_t>& hoff) {
   uint32_t* duf = s.unit_first.as<uint32_t>(m + 1);
   IGB_CUDA(cudaMemcpyAsync(duf, ufirst.data(), (m + 1) * sizeof(uint32_t), cudaMemcpyHostToDevice,
                            s.stream));
+  uint32_t* dsw = s.short_w.as<uint32_t>(sw.size() + 1);
+  uint32_t* dsc = s.short_c.as<uint32_t>(sc.size() + 1);
+  if (!sw.empty())
+    IGB_CUDA(cudaMemcpyAsync(dsw, sw.data(), sw.size() * 4, cudaMemcpyHostToDevice, s.stream));
+  if (!sc.empty())
+    IGB_CUDA(cudaMemcpyAsync(dsc, sc.data(), sc.size() * 4, cudaMemcpyHostToDevice, s.stream));
   s.rc.units = dun;
   s.rc.unit_first = duf;
   s.rc.nunits = (uint32_t)units.size();
@@ -117,6 +135,8 @@ void finish_corpus(Session& s, std::vector<uint64_t>& hoff) {
   IGB_CUDA(cudaStreamSynchronize(s.stream));
   s.hoff.swap(hoff);
   s.hufirst.swap(ufirst);
+  s.h_short_w.swap(sw);
+  s.h_short_c.swap(sc);
   s.batches.clear();
   s.dc.data = base + kFrontPad;
   s.dc.off = doff;
@@ -362,6 +382,26 @@ static void build_prefix_table(Session& s, Prefix& P) {
   P.rp.disp = ddisp;
 }
 
+// Count-once short sequences of [q0, q1) (both classes) into the pass table.
+template <typename CT>
+static void short_pass(Session& s, int kind, uint32_t L, const RouteParams& rp, CT* t, uint32_t q0,
+                       uint32_t q1) {
+  auto range = [&](const std::vector<uint32_t>& v) {
+    const size_t a = std::lower_bound(v.begin(), v.end(), q0) - v.begin();
+    const size_t b = std::lower_bound(v.begin(), v.end(), q1) - v.begin();
+    return std::make_pair(a, b);
+  };
+  const auto w = range(s.h_short_w), c = range(s.h_short_c);
+  if (w.first == w.second && c.first == c.second) return;
+  const size_t ev = s.kt.begin(IG_KF_ONCE_SHORT, s.stream);
+  count_once_short<CT>(kind, L, s.dc, rp, static_cast<const uint32_t*>(s.short_w.p) + w.first,
+                       (uint32_t)(w.second - w.first),
+                       static_cast<const uint32_t*>(s.short_c.p) + c.first,
+                       (uint32_t)(c.second - c.first), t, s.num_sms, s.stream);
+  s.kt.end(ev, s.stream);
+  s.launches += (w.first != w.second) + (c.first != c.second);
+}
+
 // One counting pass.  Returns the device table (tcap entries) and how table
 // indices map to gram keys.
 template <typename CT>
@@ -390,6 +430,7 @@ static CT* count_pass(Session& s, bool dense, uint32_t L, int mode, const Prefix
         s.rc.q1 = b.q1;
         route_count_once<CT>(1, s.rc, s.dc, 0, L, rp, t, s.num_sms, s.stream);
         route_count_once<CT>(2, s.rc, s.dc, 0, L, rp, t, s.num_sms, s.stream);
+        short_pass<CT>(s, 0, L, rp, t, b.q0, b.q1);
       }
       s.rc.u0 = 0;
       s.rc.u1 = s.rc.nunits;
@@ -405,6 +446,7 @@ static CT* count_pass(Session& s, bool dense, uint32_t L, int mode, const Prefix
       }
       rp.next_lgno = next_lgno;
       route_count_once<CT>(2, s.rc, s.dc, dense ? 0 : 1, L, rp, t, s.num_sms, s.stream);
+      short_pass<CT>(s, dense ? 0 : 1, L, rp, t, 0, (uint32_t)s.dc.m);
     }
     s.launches += s.rc.launches - l0;
     km = KeyMap{};
@@ -490,6 +532,7 @@ template <typename CT>
 static void run_t(Session& s, const ig_params& p, ig_result* out) {
   init_select(s);
   s.rc.kt = &s.kt;
+  s.rc.have_next = false;  // fused next-pass counts never outlive a run
   const uint64_t kp = k_prime(p);
   const uint32_t n = p.n;
   const uint32_t n0 = std::min<uint32_t>(n, 3);

@@ -35,6 +35,9 @@ struct Session {
 
   // corpus
   DevBuf data, off, tile, order;
+  // count-once short sequences (route_kernels.cu: k_once_short), by class
+  DevBuf short_w, short_c;
+  std::vector<uint32_t> h_short_w, h_short_c;
   DevCorpus dc;
   bool loaded = false;
 

@@ -128,3 +128,23 @@ def test_top_k_api_equals_oracle(gpu_lib, seed):
     with pytest.raises(ig.ConfigError):
         ig.top_k(t, 0)
     assert ig.top_k(np.zeros(100, np.uint64), 5)[0].size == 0  # test_counting.cpp:144-147
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_once_mixed_short_and_long_sequences(gpu_lib, seed):
+    # count-once splits sequences by length: <= 512 B (a warp each), <= 8 KiB
+    # (a CTA each, both in k_once_short) and longer (route path); all three
+    # classes count into one table and must match the oracle together
+    rng = O.Mt64(4400 + seed)
+    seqs = []
+    for i in range(60):
+        cls = rng() % 3
+        n = (rng() % 513) if cls == 0 else (513 + rng() % 7680) if cls == 1 else (8193 + rng() % 40000)
+        seqs.append(O.random_bytes(rng, n, 3 + seed))
+    d, off = O.csr(seqs)
+    for n, k, z in ((3, 50, 1.5), (5, 200, 1.5), (8, 300, 2.0)):
+        got = ig.run_intergrams(seqs, cfg(n, k, z, ONCE))
+        rc, keys, counts, rows, diag = O.oracle_run(d, off, n, k, z, int(ONCE))
+        assert rc == 0
+        assert [(g.gram, g.count) for g in got.topk] == \
+            [(ig.key_to_gram(int(a), n), int(b)) for a, b in zip(keys, counts)]
