@@ -418,6 +418,13 @@ __global__ void __launch_bounds__(NT) k_route_scatter(
 constexpr int kConsumeThreads = 512;
 constexpr int kConsumeWarps = kConsumeThreads / 32;
 
+// Words of a warp's bitmap / packing region: the bitmap of ipo ids, at least
+// 16 rounds x 32 packed entries, a multiple of 4 words.
+__host__ __device__ inline uint32_t consume_region_words(uint32_t ipo) {
+  const uint32_t w = ((ipo + 31) / 32 + 3) & ~3u;
+  return w < 512u ? 512u : w;
+}
+
 __device__ __forceinline__ void consume_entry(uint32_t local, uint32_t* bm, uint32_t* cnt) {
   const uint32_t bit = 1u << (local & 31);
   uint32_t* w = bm + (local >> 5);
@@ -426,6 +433,50 @@ __device__ __forceinline__ void consume_entry(uint32_t local, uint32_t* bm, uint
   }
 }
 
+// One sequence's runs for owner o through the warp's bitmap (then cleared).
+__device__ __forceinline__ void consume_bitmap(const RouteView& uv, uint32_t o, uint64_t q,
+                                               const unsigned long long* __restrict__ base,
+                                               const uint32_t* __restrict__ actual,
+                                               const uint16_t* __restrict__ entries,
+                                               uint32_t* bm, uint32_t bmw4, uint32_t* cnt,
+                                               int lane) {
+  const uint32_t u0 = uv.unit_first[q], u1 = uv.unit_first[q + 1];
+  for (uint32_t u = u0; u < u1; ++u) {
+    const size_t ix = (size_t)o * uv.nb + (u - uv.u0);
+    const uint64_t e0 = base[ix], e1 = e0 + actual[ix];
+    // uint4-aligned body: 8 entries per lane per load
+    const uint64_t a0 = (e0 + 7) & ~7ull, a1 = e1 & ~7ull;
+    if (a0 >= a1) {
+      for (uint64_t e = e0 + lane; e < e1; e += 32) consume_entry(entries[e], bm, cnt);
+    } else {
+      if (e0 + lane < a0) consume_entry(entries[e0 + lane], bm, cnt);
+      if (a1 + lane < e1) consume_entry(entries[a1 + lane], bm, cnt);
+      const uint4* v4 = reinterpret_cast<const uint4*>(entries + a0);
+      const uint64_t nv = (a1 - a0) >> 3;
+      for (uint64_t i = lane; i < nv; i += 32) {
+        const uint4 v = __ldcs(v4 + i);
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          consume_entry(w[k] & 0xffffu, bm, cnt);
+          consume_entry(w[k] >> 16, bm, cnt);
+        }
+      }
+    }
+  }
+  __syncwarp();
+  for (uint32_t i = lane; i < bmw4 / 4; i += 32) reinterpret_cast<uint4*>(bm)[i] = make_uint4(0, 0, 0, 0);
+  __syncwarp();
+}
+
+// Consume: CTA per (owner, block of sequences).  A warp walks a contiguous
+// range of the block's sequences 16 at a time: lanes fetch the 16 sequences'
+// run metadata in parallel; runs of more than 32 entries (and sequences of
+// several units) go through the warp's bitmap one sequence at a time; short
+// runs are packed whole into rounds of 32 lanes and deduplicated with
+// MATCH.ANY on (run, local) -- no bitmap to set or clear, which is what
+// dominates when sequences are a few KiB.  The bitmap region doubles as the
+// packing buffer (it is zero again afterwards).
 template <typename CT>
 __global__ void __launch_bounds__(kConsumeThreads) k_consume_once(
     RouteView uv, RouteParams rp, uint32_t seq_block, uint32_t nblocks,
@@ -437,7 +488,7 @@ __global__ void __launch_bounds__(kConsumeThreads) k_consume_once(
   uint32_t* cnt = reinterpret_cast<uint32_t*>(smem4);  // u16 pairs
   uint32_t* bms = cnt + cntw;                          // kConsumeWarps x bmw4 words
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint32_t bmw4 = ((ipo + 31) / 32 + 3) & ~3u;
+  const uint32_t bmw4 = consume_region_words(ipo);
   uint32_t* bm = bms + warp * bmw4;
   const uint32_t nitems = rp.NO * nblocks;
   for (uint32_t i = threadIdx.x; i < bmw4 * kConsumeWarps; i += blockDim.x) bms[i] = 0;
@@ -447,34 +498,60 @@ __global__ void __launch_bounds__(kConsumeThreads) k_consume_once(
     __syncthreads();
     const uint64_t q0 = uv.q0 + (uint64_t)b * seq_block;
     const uint64_t q1 = min((uint64_t)uv.q1, q0 + seq_block);
-    for (uint64_t q = q0 + warp; q < q1; q += kConsumeWarps) {
-      const uint32_t u0 = uv.unit_first[q], u1 = uv.unit_first[q + 1];
-      if (u0 == u1) continue;  // short sequence: counted by k_once_short
-      for (uint32_t u = u0; u < u1; ++u) {
-        const size_t ix = (size_t)o * uv.nb + (u - uv.u0);
-        const uint64_t e0 = base[ix], e1 = e0 + actual[ix];
-        // uint4-aligned body: 8 entries per lane per load
-        const uint64_t a0 = (e0 + 7) & ~7ull, a1 = e1 & ~7ull;
-        if (a0 >= a1) {
-          for (uint64_t e = e0 + lane; e < e1; e += 32) consume_entry(entries[e], bm, cnt);
+    const uint64_t per_w = (q1 - q0 + kConsumeWarps - 1) / kConsumeWarps;
+    const uint64_t wq0 = min(q1, q0 + warp * per_w), wq1 = min(q1, wq0 + per_w);
+    for (uint64_t qw = wq0; qw < wq1; qw += 16) {
+      const uint64_t q = qw + (lane & 15);
+      uint64_t e0 = 0;
+      uint32_t len = 0;
+      bool big = false;
+      if (lane < 16 && q < wq1) {
+        const uint32_t ua = uv.unit_first[q], ub = uv.unit_first[q + 1];
+        if (ub == ua + 1) {
+          const size_t ix = (size_t)o * uv.nb + (ua - uv.u0);
+          e0 = base[ix];
+          len = actual[ix];
+          big = len > 32;
         } else {
-          if (e0 + lane < a0) consume_entry(entries[e0 + lane], bm, cnt);
-          if (a1 + lane < e1) consume_entry(entries[a1 + lane], bm, cnt);
-          const uint4* v4 = reinterpret_cast<const uint4*>(entries + a0);
-          const uint64_t nv = (a1 - a0) >> 3;
-          for (uint64_t i = lane; i < nv; i += 32) {
-            const uint4 v = __ldcs(v4 + i);
-            const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              consume_entry(w[k] & 0xffffu, bm, cnt);
-              consume_entry(w[k] >> 16, bm, cnt);
-            }
-          }
+          big = ub > ua + 1;  // zero units: a short sequence (k_once_short)
+        }
+      }
+      uint32_t bigm = __ballot_sync(0xffffffffu, big);
+      while (bigm) {
+        const int l = __ffs(bigm) - 1;
+        bigm &= bigm - 1;
+        consume_bitmap(uv, o, qw + l, base, actual, entries, bm, bmw4, cnt, lane);
+      }
+      // greedy packing of whole short runs into rounds of 32 entries
+      const uint32_t mylen = (lane < 16 && !big) ? len : 0u;
+      uint32_t mypos = 0, round = 0, off = 0;
+      for (int i = 0; i < 16; ++i) {
+        const uint32_t l = __shfl_sync(0xffffffffu, mylen, i);
+        if (l == 0) continue;
+        if (off + l > 32) {
+          ++round;
+          off = 0;
+        }
+        if (lane == i) mypos = round * 32 + off;
+        off += l;
+      }
+      const uint32_t nr = off ? round + 1 : 0;
+      if (!nr) continue;
+      for (uint32_t r = 0; r < nr; ++r) bm[r * 32 + lane] = 0xffffffffu;
+      __syncwarp();
+      for (uint32_t t2 = 0; t2 < mylen; ++t2)
+        bm[mypos + t2] = ((uint32_t)lane << 16) | entries[e0 + t2];
+      __syncwarp();
+      for (uint32_t r = 0; r < nr; ++r) {
+        const uint32_t v = bm[r * 32 + lane];
+        const uint32_t grp = __match_any_sync(0xffffffffu, v);
+        if (v != 0xffffffffu && (__ffs(grp) - 1) == lane) {
+          const uint32_t local = v & 0xffffu;
+          atomicAdd(cnt + (local >> 1), 1u << (16 * (local & 1)));
         }
       }
       __syncwarp();
-      for (uint32_t i = lane; i < bmw4 / 4; i += 32) reinterpret_cast<uint4*>(bm)[i] = make_uint4(0, 0, 0, 0);
+      for (uint32_t r = 0; r < nr; ++r) bm[r * 32 + lane] = 0u;
       __syncwarp();
     }
     __syncthreads();
@@ -733,7 +810,7 @@ static void route_stage2_t(RouteCtx& x, const DevCorpus& c, const RouteParams& r
   }
   {
     const uint32_t ipo = 1u << rp.lgl;
-    const uint32_t bmw4 = ((ipo + 31) / 32 + 3) & ~3u;
+    const uint32_t bmw4 = consume_region_words(ipo);
     const size_t smem = align16((size_t)(ipo + 1) / 2 * 4) + (size_t)kConsumeWarps * bmw4 * 4;
     auto k = k_consume_once<CT>;
     IGB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
