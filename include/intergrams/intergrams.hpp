@@ -15,6 +15,8 @@
 #include "intergrams/common.hpp"
 #include "intergrams/corpus.hpp"
 #include "intergrams/counting.hpp"
+#include "intergrams/pipeline.hpp"
+#include "intergrams/trie.hpp"
 #include "intergrams_b200.h"
 
 namespace intergrams {
@@ -62,6 +64,13 @@ struct IntergramsResult {
 inline size_t candidate_id(size_t prefix_ordinal, unsigned last_byte) {
   assert(last_byte <= 255);
   return prefix_ordinal * 256 + last_byte;
+}
+
+// Gram bytes of an extension-pass candidate id (intergrams.hpp:61-66).
+inline std::string candidate_gram(const TopKList& prefixes, size_t id) {
+  std::string gram = prefixes[id >> 8].gram;
+  gram.push_back(static_cast<char>(id & 0xff));
+  return gram;
 }
 
 namespace detail {
@@ -140,6 +149,34 @@ inline IntergramsResult run_intergrams(const Corpus& corpus, const IntergramConf
   IntergramsResult out = detail::convert(r);
   ig_result_free(&r);
   return out;
+}
+
+// extend_pass (intergrams.hpp:68-72, src/intergrams.cpp:44-66) on the GPU:
+// counts the j-grams whose (j-1)-prefix is in the trie into 256 * trie.size()
+// candidate ids; trie.depth() must equal j-1 (ConfigError otherwise).
+inline CountTable extend_pass(const Corpus& corpus, const PrefixTrie& trie, size_t j,
+                              const CountingOptions& opt, uint64_t* bytes_processed = nullptr,
+                              int device = -1) {
+  std::vector<uint64_t> keys;
+  keys.reserve(trie.size());
+  for (const auto& g : trie.grams()) {
+    if (g.size() > IG_MAX_N) throw ConfigError("gram length above 8 is not supported");
+    uint64_t k = 0;
+    for (unsigned char b : g) k = (k << 8) | b;
+    keys.push_back(k);
+  }
+  CountTable table(256 * trie.size());
+  const CorpusCSR csr = corpus.materialize();
+  ig_corpus c{csr.data.data(), csr.offsets.data(), csr.offsets.size() - 1, IG_HOST};
+  uint64_t bytes = 0;
+  char err[1024] = {0};
+  detail::raise(ig_extend_pass(&c, keys.empty() ? nullptr : keys.data(), keys.size(),
+                               static_cast<uint32_t>(trie.depth()), static_cast<uint32_t>(j),
+                               opt.mode == CountMode::kAll ? IG_MODE_ALL : IG_MODE_ONCE, device,
+                               table.data(), &bytes, err, sizeof(err)),
+                err);
+  if (bytes_processed) *bytes_processed = bytes;
+  return table;
 }
 
 }  // namespace intergrams
