@@ -387,7 +387,11 @@ __global__ void __launch_bounds__(NT) k_route_scatter(
         }
       }
       __syncthreads();
-      for (uint32_t i = threadIdx.x; i < rp.NO; i += blockDim.x) lhist[i] = lbase[i];
+      // res[o] becomes the copy-out delta (global index of staging slot 0 of o)
+      for (uint32_t i = threadIdx.x; i < rp.NO; i += blockDim.x) {
+        lhist[i] = lbase[i];
+        res[i] -= lbase[i];
+      }
       __syncthreads();
       static_for<0, 16>([&](auto tc) {
         constexpr int T = decltype(tc)::value;
@@ -400,10 +404,10 @@ __global__ void __launch_bounds__(NT) k_route_scatter(
       for (uint32_t i = threadIdx.x; i < total; i += blockDim.x) {
         const uint32_t e = staging[i];
         const uint32_t o = e >> 16;
-        entries[res[o] + (i - lbase[o])] = (uint16_t)(e & 0xffffu);
+        entries[res[o] + i] = (uint16_t)(e & 0xffffu);
       }
       __syncthreads();
-      for (uint32_t o = threadIdx.x; o < rp.NO; o += blockDim.x) res[o] += lbase[o + 1] - lbase[o];
+      for (uint32_t o = threadIdx.x; o < rp.NO; o += blockDim.x) res[o] += lbase[o + 1];
     }
     __syncthreads();
     for (uint32_t o = threadIdx.x; o < rp.NO; o += blockDim.x)
