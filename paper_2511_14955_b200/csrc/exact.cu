@@ -44,7 +44,13 @@ constexpr int kXP = 16;             // byte positions per thread
 constexpr int kXChunk = kXT * kXP;  // bytes per CTA
 constexpr uint64_t kBatchBytes = 512ull << 20;
 
-enum EmitKind { kEmitGram = 0, kEmitBucket = 1, kEmitKeptGram = 2, kEmitVocab = 3 };
+enum EmitKind {
+  kEmitGram = 0,       // every gram (naive)
+  kEmitBucket = 1,     // its hash bucket (hash-gramming pass 1)
+  kEmitKeptGram = 2,   // grams of kept buckets (hash-gramming pass 2)
+  kEmitVocab = 3,      // vocabulary hits (featurize)
+  kEmitCandidate = 4   // extension-pass candidate index rank * 256 + last byte
+};
 
 struct EmitSpec {
   const uint8_t* data = nullptr;  // corpus byte g at data[g] (16-aligned, zero padded)
@@ -60,6 +66,7 @@ struct EmitSpec {
   const uint64_t* vkeys = nullptr;  // vocabulary open-addressing table
   const uint32_t* vcols = nullptr;  // column per slot, ~0u = empty
   uint32_t vlg = 0;
+  DevPrefixSet ps;  // kEmitCandidate: open-addressing survivor set (p = rank)
 };
 
 __host__ __device__ inline uint64_t bswap64(uint64_t x) {
@@ -117,6 +124,16 @@ __device__ __forceinline__ uint32_t vocab_col(const EmitSpec& sp, uint64_t key) 
   }
 }
 
+__device__ __forceinline__ uint32_t survivor_rank(const DevPrefixSet& ps, uint64_t key) {
+  uint32_t h = hash_slot(key, ps.lgS);
+  for (;;) {
+    const uint64_t k = ps.hkeys[h];
+    if (k == key) return ps.hidx[h];
+    if (k == kEmptyKey) return 0xffffffffu;
+    h = (h + 1) & (ps.S - 1);
+  }
+}
+
 // Evaluates this thread's 16 positions of chunk `chunk`: bit i of the result
 // is set when position chunk*4096 + tid*16 + i emits val[i] (sequence seq[i]).
 template <int KIND>
@@ -165,6 +182,10 @@ __device__ __forceinline__ uint32_t eval_thread(const EmitSpec& sp, uint64_t chu
           const uint32_t c = vocab_col(sp, key);
           hit = c != 0xffffffffu;
           v = ((uint64_t)s << 32) | c;
+        } else if (KIND == kEmitCandidate) {
+          const uint32_t r = survivor_rank(sp.ps, key >> 8);
+          hit = r != 0xffffffffu;
+          v = (uint64_t)r * 256 + (key & 0xff);
         }
         if (hit) {
           mask |= 1u << i;
@@ -410,6 +431,12 @@ void exact_topk(Session& s, uint64_t U, uint64_t k, std::vector<uint64_t>& keys,
   IGB_CUDA(cudaStreamSynchronize(s.stream));
 }
 
+template <typename CT>
+__global__ void k_put_counts(const uint64_t* keys, const uint64_t* counts, uint64_t n, CT* table) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) table[keys[i]] = (CT)counts[i];
+}
+
 void fill_result(ig_result* out, uint32_t n, const std::vector<uint64_t>& keys,
                  const std::vector<uint64_t>& counts, const std::vector<Row>& rows,
                  StepTimer* tm) {
@@ -451,6 +478,28 @@ void with_session(const ig_corpus* corpus, int32_t device, F&& f) {
 }
 
 }  // namespace
+
+// Count-once extension pass by sorting (the fallback for survivor sets too
+// large for the route path's 16-bit owners): (rank * 256 + last byte,
+// sequence) pairs for every position whose prefix survived, deduplicated per
+// sequence and counted, then written into the pass table (table zeroed by the
+// caller).
+template <typename CT>
+void count_once_exact(Session& s, uint32_t L, const DevPrefixSet& ps, uint64_t cap, CT* table) {
+  EmitSpec sp;
+  sp.n = L;
+  sp.ps = ps;
+  const uint64_t U = exact_count<kEmitCandidate>(s, sp, IG_MODE_ONCE, bits_for(cap ? cap - 1 : 0));
+  if (U == 0) return;
+  k_put_counts<CT><<<grid_of(U), 256, 0, s.stream>>>(
+      static_cast<const uint64_t*>(s.ex.acc_keys.p), static_cast<const uint64_t*>(s.ex.acc_counts.p),
+      U, table);
+  IGB_LAUNCHED(&s);
+}
+template void count_once_exact<uint32_t>(Session&, uint32_t, const DevPrefixSet&, uint64_t,
+                                         uint32_t*);
+template void count_once_exact<unsigned long long>(Session&, uint32_t, const DevPrefixSet&,
+                                                   uint64_t, unsigned long long*);
 
 }  // namespace igb
 

@@ -273,6 +273,7 @@ struct Prefix {
   DevPrefixSet ps;
   RouteParams rp;
   bool csr = false;  // perfect-hash prefix set (count-once)
+  bool exact_once = false;  // count-once by sorting (survivor set too large to route)
   uint64_t K = 0;
   std::vector<uint32_t> rank_of_p;  // count-once: p -> survivor rank
   const uint64_t* pkeys = nullptr;   // count-once: keys by p
@@ -286,6 +287,16 @@ static Prefix prepare_prefix(Session& s, const uint64_t* keys, uint64_t K, uint3
   Prefix P;
   P.K = K;
   if (!K) return P;
+  // count-once with a survivor set too large for 16-bit owners (or forced by
+  // IG_ONCE_EXACT_MIN_K for tests): the open-addressing set + the sort path
+  static const char* force = getenv("IG_ONCE_EXACT_MIN_K");
+  const uint64_t exact_min = force ? strtoull(force, nullptr, 10) : (uint64_t)kPrefixesPerOwner << 15;
+  if (mode == IG_MODE_ONCE && K >= exact_min) {
+    P.ps = build_prefix_set(s, keys, K, plen);
+    P.exact_once = true;
+    P.plen = plen;
+    return P;
+  }
   if (mode == IG_MODE_ONCE) {
     // count-once routing: owners = hash(prefix) with <= 64 prefixes each,
     // prefixes numbered owner by owner (stable by rank), CHD perfect-hash set
@@ -303,9 +314,12 @@ static Prefix prepare_prefix(Session& s, const uint64_t* keys, uint64_t K, uint3
       for (uint64_t i = 0; i < K; ++i) mx = std::max(mx, ++cnt[owner_of(hk[i], lgno)]);
       if (mx <= kPrefixesPerOwner) break;
       // routed entries carry the owner in 16 bits (route_kernels.cu)
-      if (lgno >= 16)
-        throw Error(IG_ECONFIG, "count-once extension pass supports at most ~4M surviving "
-                                "prefixes (k' too large)");
+      if (lgno >= 16) {
+        P.ps = build_prefix_set(s, keys, K, plen);
+        P.exact_once = true;
+        P.plen = plen;
+        return P;
+      }
     }
     const uint32_t NO = 1u << lgno;
     std::vector<uint32_t> ostart(NO + 1, 0);
@@ -407,6 +421,17 @@ static void short_pass(Session& s, int kind, uint32_t L, const RouteParams& rp, 
 template <typename CT>
 static CT* count_pass(Session& s, bool dense, uint32_t L, int mode, const Prefix* P,
                       uint64_t& tcap, KeyMap& km, int32_t next_lgno = -1) {
+  if (mode == IG_MODE_ONCE && !dense && P->exact_once) {
+    tcap = 256 * P->K;
+    CT* t = s.table.as<CT>(tcap);
+    IGB_CUDA(cudaMemsetAsync(t, 0, tcap * sizeof(CT), s.stream));
+    const size_t ev = s.kt.begin(IG_KF_ONCE_SHORT, s.stream);
+    count_once_exact<CT>(s, L, P->ps, tcap, t);
+    s.kt.end(ev, s.stream);
+    km = KeyMap{};
+    km.pkeys = P->ps.pkeys;
+    return t;
+  }
   if (mode == IG_MODE_ONCE) {
     RouteParams rp;
     if (dense) make_route_params(1ull << (8 * L), rp);
@@ -547,8 +572,12 @@ static void run_t(Session& s, const ig_params& p, ig_result* out) {
   size_t ev = tm.begin();
   uint64_t tcap = 0;
   KeyMap km;
-  const int32_t fuse_lg = (p.mode == IG_MODE_ONCE && n > 3 && !getenv("IG_NO_FUSED_COUNT"))
-                             ? (int32_t)predicted_lgno(kp) : -1;
+  // the next pass's owner histogram lives in the scatter's shared memory:
+  // fused only up to 2^13 owners (32 KB)
+  constexpr uint32_t kMaxFusedLg = 13;
+  const int32_t fuse_lg = (p.mode == IG_MODE_ONCE && n > 3 && !getenv("IG_NO_FUSED_COUNT") &&
+                           predicted_lgno(kp) <= kMaxFusedLg)
+                              ? (int32_t)predicted_lgno(kp) : -1;
   CT* table = count_pass<CT>(s, true, n0, p.mode, nullptr, tcap, km, fuse_lg);
   int32_t next_lg = fuse_lg;
   // owner bits of a count-once prefix set of K survivors: the width the fused
@@ -600,6 +629,7 @@ static void run_t(Session& s, const ig_params& p, ig_result* out) {
       // possible prefix count min(k', 256 * this pass's survivors)
       next_lg = fuse_lg >= 0 && j < n ? (int32_t)predicted_lgno(std::min<uint64_t>(kp, 256 * ns))
                                       : -1;
+      if (next_lg > (int32_t)kMaxFusedLg) next_lg = -1;
       CT* ct = count_pass<CT>(s, false, j, p.mode, &P, tcap, km, next_lg);
       IGB_CUDA(cudaGetLastError());
       allreduce(s, ct, tcap, sizeof(CT) == 4 ? 0 : 1);

@@ -158,6 +158,8 @@ void finish_corpus(Session& s, std::vector<uint64_t>& hoff);
 void check_offsets(const std::vector<uint64_t>& hoff);
 void run(Session& s, const ig_params& p, ig_result* out);
 std::vector<uint64_t> plan_batches(Session& s);
+template <typename CT>
+void count_once_exact(Session& s, uint32_t L, const DevPrefixSet& ps, uint64_t cap, CT* table);
 void init_select(Session& s);
 
 }  // namespace igb
