@@ -345,6 +345,30 @@ __global__ void __launch_bounds__(512) k_count_all(DevCorpus c, DevPrefixSet ps,
     if (tag[i] != kNoId && hcnt[i]) atomicAdd(table + tag[i], (CT)hcnt[i]);
 }
 
+// Copies between device memory and mapped pinned host memory with SM loads
+// and stores (zero-copy): the session's small transfers then never queue
+// behind a large DMA (another session's corpus upload) in a copy engine.
+__global__ void k_copy_bytes(uint8_t* __restrict__ dst, const uint8_t* __restrict__ src,
+                             uint64_t n) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t i0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if ((((uintptr_t)dst | (uintptr_t)src) & 15) == 0) {
+    const uint64_t n16 = n / 16;
+    for (uint64_t i = i0; i < n16; i += stride)
+      reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(src)[i];
+    for (uint64_t i = n16 * 16 + i0; i < n; i += stride) dst[i] = src[i];
+  } else {
+    for (uint64_t i = i0; i < n; i += stride) dst[i] = src[i];
+  }
+}
+
+void launch_copy(void* dst, const void* src, uint64_t n, cudaStream_t st) {
+  if (!n) return;
+  const uint64_t blocks = std::min<uint64_t>((n / 16 + 255) / 256 + 1, 1024);
+  k_copy_bytes<<<(unsigned)blocks, 256, 0, st>>>(static_cast<uint8_t*>(dst),
+                                                 static_cast<const uint8_t*>(src), n);
+}
+
 // table64[i] += scratch32[i] (count-all segments of < 2^32 positions).
 __global__ void k_widen_add(const uint32_t* __restrict__ src, unsigned long long* __restrict__ dst,
                             uint64_t n4) {

@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -81,6 +82,43 @@ struct DevBuf {
   T* as(size_t count) { return static_cast<T*>(get(count * sizeof(T))); }
   ~DevBuf() {
     if (p) cudaFree(p);
+  }
+};
+
+// Grow-only mapped pinned host staging.  Every small host<->device transfer
+// of a run goes through it and is moved by a kernel (zero-copy), not a copy
+// engine: a DMA queues behind any large copy already in flight (another
+// session's corpus upload) and would serialise the run with that upload.
+// Chunks are reused after reset() (called when the stream is idle).
+struct PinnedArena {
+  std::vector<std::pair<char*, size_t>> chunks;
+  size_t chunk = 0, used = 0;
+  void* get(size_t n) {
+    n = (n + 15) & ~size_t(15);
+    while (chunk < chunks.size() && used + n > chunks[chunk].second) {
+      ++chunk;
+      used = 0;
+    }
+    if (chunk == chunks.size()) {
+      const size_t sz = std::max<size_t>(n, 16u << 20);
+      void* p = nullptr;
+      IGB_CUDA(cudaHostAlloc(&p, sz, cudaHostAllocMapped));
+      chunks.emplace_back(static_cast<char*>(p), sz);
+      used = 0;
+    }
+    void* r = chunks[chunk].first + used;
+    used += n;
+    return r;
+  }
+  void reset() {
+    chunk = 0;
+    used = 0;
+  }
+  PinnedArena() = default;
+  PinnedArena(const PinnedArena&) = delete;
+  PinnedArena& operator=(const PinnedArena&) = delete;
+  ~PinnedArena() {
+    for (auto& c : chunks) cudaFreeHost(c.first);
   }
 };
 

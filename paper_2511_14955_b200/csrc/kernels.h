@@ -31,6 +31,8 @@ void launch_prefix_insert(const uint64_t* keys, uint32_t K, const uint32_t* owne
                           cudaStream_t st);
 
 void launch_widen_add(const uint32_t* src, unsigned long long* dst, uint64_t n, cudaStream_t st);
+// SM copy to/from mapped pinned host memory (no copy engine)
+void launch_copy(void* dst, const void* src, uint64_t n, cudaStream_t st);
 void launch_pack_prefix(const DevPrefixSet& ps, uint64_t* packed, cudaStream_t st);
 
 // --- count-once route-then-count (route_kernels.cu)
@@ -119,6 +121,15 @@ struct SelectCtx {
   unsigned long long* scalar = nullptr;  // device
   DevBuf tmp_keys, tmp_counts, cub_tmp;
   uint64_t launches = 0;
+  SelState* h_state = nullptr;            // pinned host mirrors (no pageable copies)
+  unsigned long long* h_scalar = nullptr;
+  SelectCtx() = default;
+  SelectCtx(const SelectCtx&) = delete;
+  SelectCtx& operator=(const SelectCtx&) = delete;
+  ~SelectCtx() {
+    if (h_state) cudaFreeHost(h_state);
+    if (h_scalar) cudaFreeHost(h_scalar);
+  }
 };
 
 // Canonical top-k of table[0..cap) (cap % 4 == 0).  Gram key = id, or

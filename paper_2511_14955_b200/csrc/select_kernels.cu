@@ -179,6 +179,8 @@ __global__ void k_invert(const uint64_t* __restrict__ in, uint64_t* __restrict__
 
 static int bits_of(uint64_t v) { return v ? 64 - __builtin_clzll(v) : 0; }
 
+__global__ void k_set_state(SelState* st, SelState v) { *st = v; }
+
 template <typename CT>
 uint64_t select_topk(SelectCtx& x, const CT* table, uint64_t cap, uint64_t k, KeyMap km,
                      int key_bits, uint64_t* out_keys, uint64_t* out_counts) {
@@ -193,14 +195,16 @@ uint64_t select_topk(SelectCtx& x, const CT* table, uint64_t cap, uint64_t k, Ke
 
   SelState init{};
   init.r = k;
-  IGB_CUDA(cudaMemcpyAsync(x.state, &init, sizeof(SelState), cudaMemcpyHostToDevice, s));
+  k_set_state<<<1, 1, 0, s>>>(x.state, init);  // by value: no host copy
+  x.launches++;
   IGB_CUDA(cudaMemsetAsync(x.hist, 0, 256 * sizeof(uint32_t), s));
   IGB_CUDA(cudaMemsetAsync(x.scalar, 0, sizeof(unsigned long long), s));
   k_max<CT><<<blocks, threads, 0, s>>>(table, cap4, x.scalar);
   x.launches++;
-  unsigned long long mx = 0;
-  IGB_CUDA(cudaMemcpyAsync(&mx, x.scalar, sizeof(mx), cudaMemcpyDeviceToHost, s));
+  launch_copy(x.h_scalar, x.scalar, sizeof(unsigned long long), s);  // mapped pinned
+  x.launches++;
   IGB_CUDA(cudaStreamSynchronize(s));
+  const unsigned long long mx = *x.h_scalar;
   if (mx == 0) return 0;  // all-zero table: empty result (counting.cpp:72)
   const int cbits = bits_of(mx);
   const int cpasses = (cbits + 7) / 8;
@@ -211,9 +215,10 @@ uint64_t select_topk(SelectCtx& x, const CT* table, uint64_t cap, uint64_t k, Ke
   }
   k_finish_count_select<<<1, 1, 0, s>>>(x.state);
   x.launches++;
-  SelState hs{};
-  IGB_CUDA(cudaMemcpyAsync(&hs, x.state, sizeof(SelState), cudaMemcpyDeviceToHost, s));
+  launch_copy(x.h_state, x.state, sizeof(SelState), s);
+  x.launches++;
   IGB_CUDA(cudaStreamSynchronize(s));
+  const SelState hs = *x.h_state;
   if (!hs.take_all) {
     const int kpasses = (key_bits + 7) / 8;
     for (int p = kpasses - 1; p >= 0; --p) {

@@ -71,8 +71,8 @@ void finish_corpus(Session& s, std::vector<uint64_t>& hoff) {
   const uint64_t ntiles = (total + kTileBytes - 1) / kTileBytes;
   uint8_t* base = static_cast<uint8_t*>(s.data.p);
   uint64_t* doff = s.off.as<uint64_t>(m + 1);
-  IGB_CUDA(cudaMemcpyAsync(doff, hoff.data(), (m + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice,
-                           s.stream));
+  s.pin.reset();  // the stream is idle between runs and loads
+  h2d(s, doff, hoff.data(), (m + 1) * sizeof(uint64_t));
   uint32_t* dtile = s.tile.as<uint32_t>(ntiles + 1);
   launch_tile_seq(doff, m, ntiles, dtile, s.stream);
   s.launches++;
@@ -84,8 +84,7 @@ void finish_corpus(Session& s, std::vector<uint64_t>& hoff) {
   });
   uint32_t* dord = s.order.as<uint32_t>(m + 1);
   if (m)
-    IGB_CUDA(cudaMemcpyAsync(dord, ord.data(), m * sizeof(uint32_t), cudaMemcpyHostToDevice,
-                             s.stream));
+    h2d(s, dord, ord.data(), m * sizeof(uint32_t));
   // count-once work units: <= kUnitBytes of gram ends of one long sequence;
   // short sequences are counted without routing (k_once_short), a warp or a
   // CTA per sequence
@@ -113,18 +112,16 @@ void finish_corpus(Session& s, std::vector<uint64_t>& hoff) {
   }
   RouteUnit* dun = s.units.as<RouteUnit>(units.size() + 1);
   if (!units.empty())
-    IGB_CUDA(cudaMemcpyAsync(dun, units.data(), units.size() * sizeof(RouteUnit),
-                             cudaMemcpyHostToDevice, s.stream));
+    h2d(s, dun, units.data(), units.size() * sizeof(RouteUnit));
   ufirst[m] = (uint32_t)units.size();
   uint32_t* duf = s.unit_first.as<uint32_t>(m + 1);
-  IGB_CUDA(cudaMemcpyAsync(duf, ufirst.data(), (m + 1) * sizeof(uint32_t), cudaMemcpyHostToDevice,
-                           s.stream));
+  h2d(s, duf, ufirst.data(), (m + 1) * sizeof(uint32_t));
   uint32_t* dsw = s.short_w.as<uint32_t>(sw.size() + 1);
   uint32_t* dsc = s.short_c.as<uint32_t>(sc.size() + 1);
   if (!sw.empty())
-    IGB_CUDA(cudaMemcpyAsync(dsw, sw.data(), sw.size() * 4, cudaMemcpyHostToDevice, s.stream));
+    h2d(s, dsw, sw.data(), sw.size() * 4);
   if (!sc.empty())
-    IGB_CUDA(cudaMemcpyAsync(dsc, sc.data(), sc.size() * 4, cudaMemcpyHostToDevice, s.stream));
+    h2d(s, dsc, sc.data(), sc.size() * 4);
   s.rc.units = dun;
   s.rc.unit_first = duf;
   s.rc.nunits = (uint32_t)units.size();
@@ -184,6 +181,10 @@ void init_select(Session& s) {
   s.sel.state = s.sel_state.as<SelState>(1);
   s.sel.hist = s.sel_hist.as<uint32_t>(256);
   s.sel.scalar = s.sel_scalar.as<unsigned long long>(1);
+  if (!s.sel.h_state) {
+    IGB_CUDA(cudaHostAlloc(&s.sel.h_state, sizeof(SelState), cudaHostAllocMapped));
+    IGB_CUDA(cudaHostAlloc(&s.sel.h_scalar, sizeof(unsigned long long), cudaHostAllocMapped));
+  }
 }
 
 // Builds the count-all prefix set for survivors keys[0..K) of length plen:
@@ -217,8 +218,7 @@ static DevPrefixSet build_prefix_set(Session& s, const uint64_t* keys, uint64_t 
   // recompute owners at width G (owner16 & (G-1) == owner_G)
   launch_prefix_owner(keys, (uint32_t)K, plen, G, owner, ocnt /*scratch*/, s.stream);
   s.launches++;
-  IGB_CUDA(cudaMemcpyAsync(ostart, gs.data(), (G + 1) * sizeof(uint32_t), cudaMemcpyHostToDevice,
-                           s.stream));
+  h2d(s, ostart, gs.data(), (G + 1) * sizeof(uint32_t));
   IGB_CUDA(cudaMemsetAsync(cursor, 0, 16 * sizeof(uint32_t), s.stream));
   uint64_t* hk = s.hkeys.as<uint64_t>((size_t)G * S);
   uint32_t* hi = s.hidx.as<uint32_t>((size_t)G * S);
@@ -301,8 +301,7 @@ static Prefix prepare_prefix(Session& s, const uint64_t* keys, uint64_t K, uint3
     // count-once routing: owners = hash(prefix) with <= 64 prefixes each,
     // prefixes numbered owner by owner (stable by rank), CHD perfect-hash set
     std::vector<uint64_t> hk(K);
-    IGB_CUDA(cudaMemcpyAsync(hk.data(), keys, K * 8, cudaMemcpyDeviceToHost, s.stream));
-    IGB_CUDA(cudaStreamSynchronize(s.stream));
+    d2h(s, hk.data(), keys, K * 8);
     auto owner_of = [plen](uint64_t key, uint32_t lgno) -> uint32_t {
       return owner_hash(key, plen, lgno);
     };
@@ -334,8 +333,8 @@ static Prefix prepare_prefix(Session& s, const uint64_t* keys, uint64_t K, uint3
     }
     uint64_t* dpk = s.pkeys.as<uint64_t>(K + 1);
     uint32_t* dos = s.owner_start.as<uint32_t>(NO + 1);
-    IGB_CUDA(cudaMemcpyAsync(dpk, pk.data(), K * 8, cudaMemcpyHostToDevice, s.stream));
-    IGB_CUDA(cudaMemcpyAsync(dos, ostart.data(), (NO + 1) * 4, cudaMemcpyHostToDevice, s.stream));
+    h2d(s, dpk, pk.data(), K * 8);
+    h2d(s, dos, ostart.data(), (NO + 1) * 4);
     P.pk = std::move(pk);
     P.ostart = std::move(ostart);
     P.plen = plen;
@@ -387,8 +386,8 @@ static void build_prefix_table(Session& s, Prefix& P) {
   }
   uint64_t* ds = s.hkeys.as<uint64_t>(slots.size() + 2);
   uint16_t* ddisp = s.hpacked.as<uint16_t>(disp.size() + 8);
-  IGB_CUDA(cudaMemcpyAsync(ds, slots.data(), slots.size() * 8, cudaMemcpyHostToDevice, s.stream));
-  IGB_CUDA(cudaMemcpyAsync(ddisp, disp.data(), disp.size() * 2, cudaMemcpyHostToDevice, s.stream));
+  h2d(s, ds, slots.data(), slots.size() * 8);
+  h2d(s, ddisp, disp.data(), disp.size() * 2);
   IGB_CUDA(cudaStreamSynchronize(s.stream));  // host vectors die here
   P.rp.nb = nb;
   P.rp.nslots = nslots;
@@ -558,6 +557,8 @@ static void run_t(Session& s, const ig_params& p, ig_result* out) {
   init_select(s);
   s.rc.kt = &s.kt;
   s.rc.have_next = false;  // fused next-pass counts never outlive a run
+  IGB_CUDA(cudaStreamSynchronize(s.stream));
+  s.pin.reset();
   const uint64_t kp = k_prime(p);
   const uint32_t n = p.n;
   const uint32_t n0 = std::min<uint32_t>(n, 3);
@@ -677,10 +678,8 @@ static void run_t(Session& s, const ig_params& p, ig_result* out) {
   if (!out->keys || !out->counts || !out->passes || !out->diagnostics)
     throw Error(IG_EINTERNAL, "host allocation failed");
   if (out_len) {
-    IGB_CUDA(cudaMemcpyAsync(out->keys, out_keys_d, out_len * sizeof(uint64_t),
-                             cudaMemcpyDeviceToHost, s.stream));
-    IGB_CUDA(cudaMemcpyAsync(out->counts, out_counts_d, out_len * sizeof(uint64_t),
-                             cudaMemcpyDeviceToHost, s.stream));
+    d2h(s, out->keys, out_keys_d, out_len * sizeof(uint64_t));
+    d2h(s, out->counts, out_counts_d, out_len * sizeof(uint64_t));
   }
   IGB_CUDA(cudaStreamSynchronize(s.stream));
   for (size_t i = 0; i < rows.size(); ++i) {

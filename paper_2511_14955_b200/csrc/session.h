@@ -50,6 +50,7 @@ struct Session {
   ExactBufs ex;
   RouteCtx rc;
   KernelTimer kt;
+  PinnedArena pin;  // staging of the run's small transfers (reset per run / load)
   // pipelined host load: the dense pass runs batch by batch as the H2D copies land
   struct Batch {
     uint64_t t0, t1;           // count-all tiles whose bytes are all in the batch
@@ -148,6 +149,24 @@ inline Row make_row(const std::string& label, uint32_t gl, uint64_t bytes, uint6
   r.st.retained_short = shrt ? 1 : 0;
   r.ev = ev;
   return r;
+}
+
+// Host->device through the pinned arena (src may be pageable; reusable after
+// the call).  Device->host: staged, synchronised, then copied to dst.
+inline void h2d(Session& s, void* dst, const void* src, size_t n) {
+  if (!n) return;
+  void* p = s.pin.get(n);
+  memcpy(p, src, n);
+  launch_copy(dst, p, n, s.stream);
+  s.launches++;
+}
+inline void d2h(Session& s, void* dst, const void* src, size_t n) {
+  if (!n) return;
+  void* p = s.pin.get(n);
+  launch_copy(p, src, n, s.stream);
+  s.launches++;
+  IGB_CUDA(cudaStreamSynchronize(s.stream));
+  memcpy(dst, p, n);
 }
 
 void use_device(Session& s);
