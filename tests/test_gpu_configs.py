@@ -113,3 +113,36 @@ def test_pipelined_host_load_equals_resident(gpu_lib, name, extra, k):
     s2.close()
     assert r1.topk == r2.topk == r1b.topk
     assert [p.bytes_processed for p in r1.passes] == [p.bytes_processed for p in r2.passes]
+
+
+@pytest.mark.parametrize("name,extra,k", [
+    ("c1", {}, None),                       # full size, the reference's own k
+    ("c2", {"num_seqs": 192}, None),        # 192 MiB, k = 10000
+    ("c3", {"total": 192 << 20}, 20000),
+    ("c4", {"num_seqs": 48}, None),         # 192 MiB, k = 65536
+    ("c5", {"num_seqs": 128}, 100000),
+    pytest.param("c2", {"num_seqs": 1024}, None, marks=pytest.mark.slow),   # 1 GiB
+    pytest.param("c3", {"total": 1 << 30}, None, marks=pytest.mark.slow),   # k = 100000
+    pytest.param("c4", {"num_seqs": 256}, None, marks=pytest.mark.slow),    # 1 GiB
+    pytest.param("c5", {"num_seqs": 1024}, None, marks=pytest.mark.slow),   # k = 1000000
+])
+def test_config_sample_equals_reference(gpu_lib, name, extra, k):
+    """The reference itself (oracle/_ref: proj/src compiled unmodified, all host
+    threads) on the same seeded sample: identical list, counts, order, pass rows
+    and diagnostics."""
+    if not O.ref_available():
+        pytest.skip("reference build unavailable")
+    base = S.CONFIGS[name]
+    cfg = S.scaled(base, **extra)
+    k = k or base.k
+    data, off = S.generate(cfg)
+    r = ig.run_intergrams(ig.Corpus(data, off), ig.IntergramConfig(
+        n=base.n, k=k, z=base.z, mode=ig.CountMode(base.mode)))
+    rc, keys, counts, rows, diag, secs, err = O.ref_run(data, off, base.n, k, base.z, base.mode, 0)
+    assert rc == 0, err
+    assert np.array_equal(r.keys, keys) and np.array_equal(r.counts, counts)
+    assert r.diagnostics == diag
+    got_rows = [{"label": p.label, "gram_len": p.gram_len, "bytes_processed": p.bytes_processed,
+                 "candidate_space": p.candidate_space, "retained": p.retained,
+                 "retained_short": p.retained_short} for p in r.passes]
+    assert got_rows == [{kk: x[kk] for kk in got_rows[0]} for x in rows]
