@@ -26,6 +26,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 
 #include "ig_internal.cuh"
@@ -158,14 +159,29 @@ __device__ __forceinline__ uint32_t prefix_lookup(const uint64_t* __restrict__ h
 
 // Packed prefix-set slice: entry = (key << ib) | local index, kEmptyKey = empty.
 // Returns the local index (p - owner_start) or 0xffffffff.
+// GLOBAL: the slice lives in global memory (read-only path), else in smem.
+template <bool GLOBAL = false>
 __device__ __forceinline__ uint32_t lookup_packed(const uint64_t* tab, uint32_t lgS, uint32_t ib,
                                                   uint64_t key) {
   const uint32_t mask = (1u << lgS) - 1;
   uint32_t h = hash_slot(key, lgS);
   for (;;) {
-    const uint64_t e = tab[h];
+    const uint64_t e = GLOBAL ? __ldg(tab + h) : tab[h];
     if (e == kEmptyKey) return 0xffffffffu;
     if ((e >> ib) == key) return (uint32_t)(e & ((1ull << ib) - 1));
+    h = (h + 1) & mask;
+  }
+}
+
+// The same probe over {key, p} 16-byte slots: one 16-byte load per probe.
+__device__ __forceinline__ uint32_t lookup_wide(const uint64_t* __restrict__ wide, uint32_t lgS,
+                                                uint64_t key) {
+  const uint32_t mask = (1u << lgS) - 1;
+  uint32_t h = hash_slot(key, lgS);
+  for (;;) {
+    const ulonglong2 e = __ldg(reinterpret_cast<const ulonglong2*>(wide) + h);
+    if (e.x == key) return (uint32_t)e.y;
+    if (e.x == kEmptyKey) return 0xffffffffu;
     h = (h + 1) & mask;
   }
 }
@@ -221,6 +237,22 @@ void launch_pack_prefix(const DevPrefixSet& ps, uint64_t* packed, cudaStream_t s
                                                                ps.S, ps.ib, total, packed);
 }
 
+__global__ void k_pack_wide(const uint64_t* __restrict__ hkeys, const uint32_t* __restrict__ hidx,
+                            uint64_t total, uint64_t* __restrict__ wide) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = hkeys[i];
+    reinterpret_cast<ulonglong2*>(wide)[i] =
+        make_ulonglong2(k, k == kEmptyKey ? 0ull : (unsigned long long)hidx[i]);
+  }
+}
+
+void launch_pack_wide(const DevPrefixSet& ps, uint64_t* wide, cudaStream_t st) {
+  const uint64_t total = (uint64_t)ps.G * ps.S;
+  const unsigned blocks = (unsigned)((total + 255) / 256);
+  k_pack_wide<<<blocks < 4096 ? blocks : 4096, 256, 0, st>>>(ps.hkeys, ps.hidx, total, wide);
+}
+
 // Slow path: validity of a segment that crosses sequence boundaries.
 template <int L>
 __device__ __noinline__ uint32_t valid_mask_walk(const uint64_t* __restrict__ off, uint64_t m,
@@ -248,7 +280,9 @@ __device__ __noinline__ uint32_t valid_mask_walk(const uint64_t* __restrict__ of
 // Flat scan of all 512-byte tiles; one count per valid gram end (dense) or per
 // prefix hit (extension).  Each warp keeps the next tile's 128-bit loads in
 // flight while it counts the current one.  TAB: 0 none (dense), 1 prefix set
-// staged in shared memory (packed), 2 prefix set read from global/L2.
+// staged in shared memory (packed), 2 prefix set read from global/L2 (key and
+// index arrays), 3 packed prefix set read from global/L2 (one load per probe),
+// 4 {key, p} 16-byte slots read from global/L2 (one load per probe).
 //
 // Hot grams: a Zipf corpus sends a few percent of all occurrences to single
 // ids, and one L2 address absorbs only ~0.1 G reductions/s.  Every CTA
@@ -273,7 +307,7 @@ __device__ __forceinline__ void count_one(uint32_t id, uint32_t* tag, uint32_t* 
 }
 
 template <int KIND, int L, typename CT, int TAB, bool AGG>
-__global__ void __launch_bounds__(512) k_count_all(DevCorpus c, DevPrefixSet ps,
+__global__ void __launch_bounds__(512, 3) k_count_all(DevCorpus c, DevPrefixSet ps,
                                                    const uint64_t* __restrict__ packed,
                                                    CT* __restrict__ table) {
   extern __shared__ uint64_t s_tab[];
@@ -295,15 +329,29 @@ __global__ void __launch_bounds__(512) k_count_all(DevCorpus c, DevPrefixSet ps,
     uint2 h = make_uint2(0, 0);
     if (lane == 0) h = *reinterpret_cast<const uint2*>(c.data + t * kTileBytes - 8);
     uint32_t d = __ldg(c.tile_seq + t);
+    // hit chaining: this lane's word and the previous segment's word of the
+    // previous pass's hit mask (the prefix of the gram ending at e is the
+    // gram that pass counted ending at e - 1)
+    const bool chain = KIND == 1 && ps.hit_in != nullptr;
+    // mk = this segment's word | the previous segment's word << 16 (lane 0)
+    uint32_t mk = 0xffffffffu;
+    if (chain) {
+      mk = __ldcs(ps.hit_in + t * 32 + lane);
+      mk |= (lane == 0 ? (uint32_t)__ldcs(ps.hit_in + t * 32 - 1) : 0xffffu) << 16;
+    }
     for (;;) {
       const uint64_t tn = t + nwarps;
       uint4 vn = make_uint4(0, 0, 0, 0);
       uint2 hn = make_uint2(0, 0);
-      uint32_t dn = 0;
+      uint32_t dn = 0, mkn = 0xffffffffu;
       if (tn < c.ntiles) {
         vn = __ldcs(reinterpret_cast<const uint4*>(c.data + tn * kTileBytes + lane * 16));
         if (lane == 0) hn = *reinterpret_cast<const uint2*>(c.data + tn * kTileBytes - 8);
         dn = __ldg(c.tile_seq + tn);
+        if (chain) {
+          mkn = __ldcs(ps.hit_in + tn * 32 + lane);
+          mkn |= (lane == 0 ? (uint32_t)__ldcs(ps.hit_in + tn * 32 - 1) : 0xffffu) << 16;
+        }
       }
       Seg s;
       s.W[2] = v.x;
@@ -318,7 +366,12 @@ __global__ void __launch_bounds__(512) k_count_all(DevCorpus c, DevPrefixSet ps,
         s.W[1] = h.y;
       }
       const int64_t b0 = (int64_t)t * kTileBytes + lane * 16;
-      const uint32_t vm = (d >> 31) ? 0xffffu : valid_mask_walk<L>(c.off, c.m, c.total, d & 0x7fffffffu, b0);
+      uint32_t vm = (d >> 31) ? 0xffffu : valid_mask_walk<L>(c.off, c.m, c.total, d & 0x7fffffffu, b0);
+      if (chain) {
+        const uint32_t up = __shfl_up_sync(0xffffffffu, mk, 1);
+        vm &= (mk << 1) | (((lane == 0 ? mk >> 16 : up) >> 15) & 1u);
+      }
+      uint32_t hm = 0;  // this pass's hits (extension passes)
       static_for<0, 16>([&](auto tc) {
         constexpr int T = decltype(tc)::value;
         if ((vm >> T) & 1u) {
@@ -328,16 +381,23 @@ __global__ void __launch_bounds__(512) k_count_all(DevCorpus c, DevPrefixSet ps,
           } else {
             uint32_t p;
             if constexpr (TAB == 1) p = lookup_packed(s_tab, ps.lgS, ps.ib, key >> 8);
+            else if constexpr (TAB == 3) p = lookup_packed<true>(packed, ps.lgS, ps.ib, key >> 8);
+            else if constexpr (TAB == 4) p = lookup_wide(packed, ps.lgS, key >> 8);
             else p = prefix_lookup(ps.hkeys, ps.hidx, ps.S, ps.lgS, 0, key >> 8);
-            if (p != 0xffffffffu) count_one<CT>(p * 256 + (uint32_t)(key & 0xff), tag, hcnt, table);
+            if (p != 0xffffffffu) {
+              count_one<CT>(p * 256 + (uint32_t)(key & 0xff), tag, hcnt, table);
+              hm |= 1u << T;
+            }
           }
         }
       });
+      if (KIND == 1 && ps.hit_out != nullptr) __stcs(ps.hit_out + t * 32 + lane, (uint16_t)hm);
       if (tn >= c.ntiles) break;
       t = tn;
       v = vn;
       h = hn;
       d = dn;
+      mk = mkn;
     }
   }
   __syncthreads();
@@ -413,7 +473,12 @@ static void launch_all_t(const DevCorpus& c, const DevPrefixSet& ps, CT* table, 
   if constexpr (KIND == 0) {
     go(k_count_all<0, L, CT, 0, false>, 0, nullptr);
   } else {
+    // key and index packed in one 8-byte slot: one load per probe (staged in
+    // smem when small); otherwise the key and index arrays (two loads on a hit)
+    static const bool no_packed = getenv("IG_NO_PACKED_GLOBAL") != nullptr;
     if (ps.packed && (size_t)ps.S * 8 <= 64 * 1024) go(k_count_all<1, L, CT, 1, false>, ps.S * 8, ps.packed);
+    else if (ps.packed && !no_packed) go(k_count_all<1, L, CT, 3, false>, 0, ps.packed);
+    else if (ps.wide && !no_packed) go(k_count_all<1, L, CT, 4, false>, 0, ps.wide);
     else go(k_count_all<1, L, CT, 2, false>, 0, nullptr);
   }
 }

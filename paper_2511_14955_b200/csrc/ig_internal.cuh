@@ -193,6 +193,12 @@ struct DevPrefixSet {
   uint32_t max_owner = 0;  // largest owner slice size
   uint32_t ib = 0;         // local-index bits of a packed entry
   const uint64_t* packed = nullptr;  // [G*S] (key << ib) | local, or null
+  const uint64_t* wide = nullptr;    // [2*S] {key, p} slots (G == 1), or null
+  // count-all hit chaining: one u16 per 16-byte segment
+  // (index = tile * 32 + lane), bit T = the gram ending at byte 16*index + T
+  // was counted by the pass that wrote it.  hit_in[-1] is readable (zero).
+  const uint16_t* hit_in = nullptr;  // previous extension pass's hits, or null
+  uint16_t* hit_out = nullptr;       // this pass's hits (read by the next pass), or null
 };
 
 __host__ __device__ inline uint32_t hash_slot(uint64_t key, uint32_t lgS) {

@@ -34,6 +34,8 @@ void launch_widen_add(const uint32_t* src, unsigned long long* dst, uint64_t n, 
 // SM copy to/from mapped pinned host memory (no copy engine)
 void launch_copy(void* dst, const void* src, uint64_t n, cudaStream_t st);
 void launch_pack_prefix(const DevPrefixSet& ps, uint64_t* packed, cudaStream_t st);
+// {key, index} 16-byte slots (prefixes too long for the packed 8-byte slot)
+void launch_pack_wide(const DevPrefixSet& ps, uint64_t* wide, cudaStream_t st);
 
 // --- count-once route-then-count (route_kernels.cu)
 struct RouteUnit {  // <= 1 MiB of gram ends of one sequence: byte range [b0, b1)

@@ -246,6 +246,11 @@ static DevPrefixSet build_prefix_set(Session& s, const uint64_t* keys, uint64_t 
     ps.packed = pk2;
     launch_pack_prefix(ps, pk2, s.stream);
     s.launches++;
+  } else if (G == 1) {
+    uint64_t* w = s.hpacked.as<uint64_t>((size_t)2 * S);
+    ps.wide = w;
+    launch_pack_wide(ps, w, s.stream);
+    s.launches++;
   }
   return ps;
 }
@@ -620,10 +625,32 @@ static void run_t(Session& s, const ig_params& p, ig_result* out) {
     tm.end(ev);
     rows.push_back(make_row("top-zk 3-grams/trie building", 3, 0, 0, ns, shrt, ev));
 
+    // count-all hit chaining: a j-gram can be a candidate
+    // only where its (j-1)-byte prefix was counted by pass j-1 one byte
+    // earlier, so each pass records its hits and the next probes only those
+    uint16_t* hmask[2] = {nullptr, nullptr};
+    if (p.mode == IG_MODE_ALL && n >= 5 && !getenv("IG_NO_HIT_CHAIN")) {
+      const size_t words = (size_t)s.dc.ntiles * 32 + 32;
+      size_t fr = 0, tot = 0;
+      IGB_CUDA(cudaMemGetInfo(&fr, &tot));
+      const size_t have = s.hitmask[0].bytes + s.hitmask[1].bytes;
+      if (have >= 4 * words || fr + have > 4 * words + (1ull << 30)) {
+        for (int b = 0; b < 2; ++b) {
+          uint16_t* w = s.hitmask[b].as<uint16_t>(words);
+          IGB_CUDA(cudaMemsetAsync(w, 0, 32 * sizeof(uint16_t), s.stream));
+          hmask[b] = w + 32;
+        }
+      }
+    }
+
     for (uint32_t j = 4; j <= n; ++j) {
       // an empty survivor list is a depth-0 trie (trie.cpp:23) and the
       // extension pass rejects it (intergrams.cpp:46-48)
       if (ns == 0) throw Error(IG_ECONFIG, "extension pass needs a trie of depth j-1");
+      if (hmask[0]) {
+        P.ps.hit_in = j >= 5 ? hmask[(j - 1) & 1] : nullptr;
+        P.ps.hit_out = j < n ? hmask[j & 1] : nullptr;
+      }
       ev = tm.begin();
       const uint64_t cap = 256 * ns;
       // fused histogram of the next pass's owners, sized for its largest
