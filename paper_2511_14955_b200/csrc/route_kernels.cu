@@ -740,6 +740,21 @@ static void scan_u32_to_u64(RouteCtx& x, const uint32_t* cnt, unsigned long long
   IGB_CUDA(cub::DeviceScan::ExclusiveSum(tmp, need, in, base, (int64_t)n, st));
 }
 
+// Folds a fused owner histogram built at 2^d times this pass's owner count:
+// owner_hash keeps the top bits of one hash, so owner o at the narrower width
+// covers owners [o << d, (o + 1) << d) of the wider one.
+__global__ void k_fold_counts(const uint32_t* __restrict__ wide, uint32_t d, uint32_t NO,
+                              uint32_t nunits, uint32_t* __restrict__ cnt) {
+  const uint64_t n = (uint64_t)NO * nunits;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t o = i / nunits, u = i - o * nunits;
+    uint32_t sum = 0;
+    for (uint32_t w = 0; w < (1u << d); ++w) sum += wide[((o << d) + w) * nunits + u];
+    cnt[i] = sum;
+  }
+}
+
 // Stage 1: count kernel + owner-major scan (needs only the owner function).
 template <int KIND, int L>
 static void route_stage1_t(RouteCtx& x, const DevCorpus& c, const RouteParams& rp, int num_sms,
@@ -754,6 +769,24 @@ static void route_stage1_t(RouteCtx& x, const DevCorpus& c, const RouteParams& r
     x.have_next = false;
     uint32_t* cnt = x.cnt.as<uint32_t>(ncnt);
     scan_u32_to_u64(x, cnt, base, ncnt, st);
+    return;
+  }
+  if (KIND == 1 && x.have_next && x.next_lgno > (int32_t)rp.lgno && uv.u0 == 0 &&
+      uv.nb == x.nunits) {
+    // the survivors came out fewer than the fused width was sized for (a
+    // small alphabet): fold the fused histogram instead of recounting
+    uint32_t* cnt = x.cnt.as<uint32_t>(ncnt);
+    const uint64_t n = (uint64_t)rp.NO * uv.nb;
+    const unsigned grid = (unsigned)std::min<uint64_t>((n + 255) / 256, 4096);
+    IGB_CUDA(cudaMemsetAsync(cnt + ncnt - 1, 0, 4, st));
+    if (n) {
+      k_fold_counts<<<grid, 256, 0, st>>>(x.cnt_next.as<uint32_t>(1), x.next_lgno - rp.lgno,
+                                          rp.NO, uv.nb, cnt);
+      x.launches++;
+    }
+    x.have_next = false;
+    scan_u32_to_u64(x, cnt, base, ncnt, st);
+    IGB_CUDA(cudaGetLastError());
     return;
   }
   x.have_next = false;
