@@ -22,6 +22,7 @@
 //   * count-all: one L2 reduction (RED) per occurrence, except for the ids a
 //     CTA's shared-memory hot cache owns (counted with shared atomics and
 //     flushed once), so hot Zipf grams do not serialise on one L2 slice.
+#include <cub/cub.cuh>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -186,6 +187,14 @@ __device__ __forceinline__ uint32_t lookup_wide(const uint64_t* __restrict__ wid
   }
 }
 
+// 3-byte prefix p in the rank bitmap: one 16-byte load, no probing.
+__device__ __forceinline__ uint32_t lookup_rank(const uint64_t* __restrict__ rankbits,
+                                                uint32_t pre) {
+  const ulonglong2 e = __ldg(reinterpret_cast<const ulonglong2*>(rankbits) + (pre >> 6));
+  const uint64_t bit = 1ull << (pre & 63);
+  return (e.x & bit) ? (uint32_t)e.y + (uint32_t)__popcll(e.x & (bit - 1)) : 0xffffffffu;
+}
+
 // ------------------------------------------------------------------ tiles
 
 // tile_desc[t]: bit 31 = "fast" (the 512-byte tile lies inside one sequence
@@ -253,6 +262,52 @@ void launch_pack_wide(const DevPrefixSet& ps, uint64_t* wide, cudaStream_t st) {
   k_pack_wide<<<blocks < 4096 ? blocks : 4096, 256, 0, st>>>(ps.hkeys, ps.hidx, total, wide);
 }
 
+constexpr uint32_t kRankWords = 1u << 18;  // 2^24 prefixes / 64
+
+__global__ void k_rank_set(const uint64_t* __restrict__ keys, uint32_t K,
+                           unsigned long long* __restrict__ rankbits) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < K; i += gridDim.x * blockDim.x) {
+    const uint32_t pre = (uint32_t)keys[i];
+    atomicOr(rankbits + 2 * (pre >> 6), 1ull << (pre & 63));
+  }
+}
+
+// One CTA: rank[w] = set bits in words [0, w).
+__global__ void __launch_bounds__(1024) k_rank_scan(uint64_t* __restrict__ rankbits) {
+  using BlockScan = cub::BlockScan<uint32_t, 1024>;
+  __shared__ typename BlockScan::TempStorage tmp;
+  constexpr uint32_t per = kRankWords / 1024;
+  const uint32_t w0 = threadIdx.x * per;
+  uint32_t sum = 0;
+  for (uint32_t w = 0; w < per; ++w) sum += (uint32_t)__popcll(rankbits[2 * (w0 + w)]);
+  uint32_t ex;
+  BlockScan(tmp).ExclusiveSum(sum, ex);
+  for (uint32_t w = 0; w < per; ++w) {
+    rankbits[2 * (w0 + w) + 1] = ex;
+    ex += (uint32_t)__popcll(rankbits[2 * (w0 + w)]);
+  }
+}
+
+__global__ void k_rank_fill(const uint64_t* __restrict__ keys, uint32_t K,
+                            const uint64_t* __restrict__ rankbits, uint64_t* __restrict__ pkeys,
+                            uint32_t* __restrict__ rank_of_p) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < K; i += gridDim.x * blockDim.x) {
+    const uint64_t key = keys[i];
+    const uint32_t p = lookup_rank(rankbits, (uint32_t)key);
+    pkeys[p] = key;
+    rank_of_p[p] = i;
+  }
+}
+
+void launch_rank_prefix(const uint64_t* keys, uint32_t K, uint64_t* rankbits, uint64_t* pkeys,
+                        uint32_t* rank_of_p, cudaStream_t st) {
+  IGB_CUDA(cudaMemsetAsync(rankbits, 0, (size_t)2 * kRankWords * 8, st));
+  const unsigned blocks = std::max(1u, std::min(4096u, (K + 255) / 256));
+  k_rank_set<<<blocks, 256, 0, st>>>(keys, K, reinterpret_cast<unsigned long long*>(rankbits));
+  k_rank_scan<<<1, 1024, 0, st>>>(rankbits);
+  k_rank_fill<<<blocks, 256, 0, st>>>(keys, K, rankbits, pkeys, rank_of_p);
+}
+
 // Slow path: validity of a segment that crosses sequence boundaries.
 template <int L>
 __device__ __noinline__ uint32_t valid_mask_walk(const uint64_t* __restrict__ off, uint64_t m,
@@ -282,7 +337,8 @@ __device__ __noinline__ uint32_t valid_mask_walk(const uint64_t* __restrict__ of
 // flight while it counts the current one.  TAB: 0 none (dense), 1 prefix set
 // staged in shared memory (packed), 2 prefix set read from global/L2 (key and
 // index arrays), 3 packed prefix set read from global/L2 (one load per probe),
-// 4 {key, p} 16-byte slots read from global/L2 (one load per probe).
+// 4 {key, p} 16-byte slots read from global/L2 (one load per probe), 5 rank
+// bitmap of 3-byte prefixes (one 16-byte load, L2-resident 4 MiB).
 //
 // Hot grams: a Zipf corpus sends a few percent of all occurrences to single
 // ids, and one L2 address absorbs only ~0.1 G reductions/s.  Every CTA
@@ -383,6 +439,7 @@ __global__ void __launch_bounds__(512, 3) k_count_all(DevCorpus c, DevPrefixSet 
             if constexpr (TAB == 1) p = lookup_packed(s_tab, ps.lgS, ps.ib, key >> 8);
             else if constexpr (TAB == 3) p = lookup_packed<true>(packed, ps.lgS, ps.ib, key >> 8);
             else if constexpr (TAB == 4) p = lookup_wide(packed, ps.lgS, key >> 8);
+            else if constexpr (TAB == 5) p = lookup_rank(packed, (uint32_t)(key >> 8));
             else p = prefix_lookup(ps.hkeys, ps.hidx, ps.S, ps.lgS, 0, key >> 8);
             if (p != 0xffffffffu) {
               count_one<CT>(p * 256 + (uint32_t)(key & 0xff), tag, hcnt, table);
@@ -476,6 +533,12 @@ static void launch_all_t(const DevCorpus& c, const DevPrefixSet& ps, CT* table, 
     // key and index packed in one 8-byte slot: one load per probe (staged in
     // smem when small); otherwise the key and index arrays (two loads on a hit)
     static const bool no_packed = getenv("IG_NO_PACKED_GLOBAL") != nullptr;
+    if constexpr (L == 4) {
+      if (ps.rankbits && !no_packed) {
+        go(k_count_all<1, L, CT, 5, false>, 0, ps.rankbits);
+        return;
+      }
+    }
     if (ps.packed && (size_t)ps.S * 8 <= 64 * 1024) go(k_count_all<1, L, CT, 1, false>, ps.S * 8, ps.packed);
     else if (ps.packed && !no_packed) go(k_count_all<1, L, CT, 3, false>, 0, ps.packed);
     else if (ps.wide && !no_packed) go(k_count_all<1, L, CT, 4, false>, 0, ps.wide);

@@ -194,6 +194,9 @@ struct DevPrefixSet {
   uint32_t ib = 0;         // local-index bits of a packed entry
   const uint64_t* packed = nullptr;  // [G*S] (key << ib) | local, or null
   const uint64_t* wide = nullptr;    // [2*S] {key, p} slots (G == 1), or null
+  // 3-byte prefixes (the first extension pass): {bits, rank} pairs over the
+  // 2^24 prefix space, p = rank of the prefix in key order (pkeys sorted), or null
+  const uint64_t* rankbits = nullptr;  // [2 * 2^18]
   // count-all hit chaining: one u16 per 16-byte segment
   // (index = tile * 32 + lane), bit T = the gram ending at byte 16*index + T
   // was counted by the pass that wrote it.  hit_in[-1] is readable (zero).

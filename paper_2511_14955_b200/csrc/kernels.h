@@ -36,6 +36,10 @@ void launch_copy(void* dst, const void* src, uint64_t n, cudaStream_t st);
 void launch_pack_prefix(const DevPrefixSet& ps, uint64_t* packed, cudaStream_t st);
 // {key, index} 16-byte slots (prefixes too long for the packed 8-byte slot)
 void launch_pack_wide(const DevPrefixSet& ps, uint64_t* wide, cudaStream_t st);
+// Rank bitmap of K distinct 3-byte prefixes (rankbits: 2^19 u64, {bits, rank}
+// pairs): p = rank in key order; writes pkeys[p] = key, rank_of_p[p] = i.
+void launch_rank_prefix(const uint64_t* keys, uint32_t K, uint64_t* rankbits, uint64_t* pkeys,
+                        uint32_t* rank_of_p, cudaStream_t st);
 
 // --- count-once route-then-count (route_kernels.cu)
 struct RouteUnit {  // <= 1 MiB of gram ends of one sequence: byte range [b0, b1)

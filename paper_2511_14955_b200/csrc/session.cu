@@ -189,10 +189,23 @@ void init_select(Session& s) {
 
 // Builds the count-all prefix set for survivors keys[0..K) of length plen:
 // one open-addressing slice (load <= 0.5), p = survivor rank.
-static DevPrefixSet build_prefix_set(Session& s, const uint64_t* keys, uint64_t K, uint32_t plen) {
+static DevPrefixSet build_prefix_set(Session& s, const uint64_t* keys, uint64_t K, uint32_t plen,
+                                     bool dense_rank = false) {
   DevPrefixSet ps;
   ps.K = (uint32_t)K;
   ps.plen = plen;
+  if (dense_rank && plen == 3 && K > 4096 && !getenv("IG_NO_RANK_BITMAP")) {
+    // 3-byte prefixes too many for the shared-memory set: a rank bitmap over
+    // the whole 2^24 prefix space (4 MiB, L2-resident), p = rank in key order
+    uint64_t* rb = s.rankbits.as<uint64_t>((size_t)2 << 18);
+    uint64_t* pk = s.pkeys.as<uint64_t>(K + 1);
+    uint32_t* rp = s.rank_of_p.as<uint32_t>(K + 1);
+    launch_rank_prefix(keys, (uint32_t)K, rb, pk, rp, s.stream);
+    s.launches += 3;
+    ps.pkeys = pk;
+    ps.rankbits = rb;
+    return ps;
+  }
   uint32_t* owner = s.owner.as<uint32_t>(K + 1);
   uint32_t* ocnt = s.owner_cnt.as<uint32_t>(16);
   uint32_t* ostart = s.owner_start.as<uint32_t>(17);
@@ -353,7 +366,7 @@ static Prefix prepare_prefix(Session& s, const uint64_t* keys, uint64_t K, uint3
     P.pkeys = dpk;
     P.csr = true;
   } else {
-    P.ps = build_prefix_set(s, keys, K, plen);
+    P.ps = build_prefix_set(s, keys, K, plen, /*dense_rank=*/true);
   }
   return P;
 }

@@ -43,6 +43,7 @@ struct Session {
 
   // pass buffers
   DevBuf table, work, scratch32;
+  DevBuf rankbits;    // count-all 3-byte prefix rank bitmap
   DevBuf hitmask[2];  // count-all hit chaining (ping-pong by pass parity)
   DevBuf surv_keys, surv_counts, next_keys, next_counts;
   DevBuf pkeys, hkeys, hidx, hpacked, owner, owner_cnt, owner_start, cursor, rank_of_p;
