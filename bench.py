@@ -68,12 +68,28 @@ REASON_BITS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_pow
 
 
 class ClockSampler:
+    """SM clock and throttle reasons sampled DURING the timed region: NVML
+    polled from a thread every ~2 ms (short regions such as c1's still get
+    samples), else nvidia-smi -lms 100."""
+
     def __init__(self, index: int):
         self.index = index
         self.samples = []
         self.proc = None
+        self.stop = threading.Event()
+        self.t = None
 
     def __enter__(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self._nvml_sample(pynvml, h)  # fails here, not in the thread, without NVML
+            self.t = threading.Thread(target=self._poll, args=(pynvml, h), daemon=True)
+            self.t.start()
+            return self
+        except Exception:
+            pass
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index),
@@ -86,6 +102,21 @@ class ClockSampler:
             self.proc = None
         return self
 
+    def _nvml_sample(self, pynvml, h):
+        sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+        mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+        return sm, mx, rs
+
+    def _poll(self, pynvml, h):
+        while not self.stop.is_set():
+            try:
+                s = self._nvml_sample(pynvml, h)
+                self.samples.append((float(s[0]), float(s[1]), int(s[2])))
+            except Exception:
+                return
+            self.stop.wait(0.002)
+
     def _read(self):
         for line in self.proc.stdout:
             parts = [x.strip() for x in line.split(",")]
@@ -96,12 +127,15 @@ class ClockSampler:
                     pass
 
     def __exit__(self, *exc):
+        self.stop.set()
         if self.proc:
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=2)
             except Exception:
                 self.proc.kill()
+        elif self.t:
+            self.t.join(timeout=2)
 
     def summary(self):
         if not self.samples:

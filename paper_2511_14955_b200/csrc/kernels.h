@@ -107,6 +107,20 @@ void count_once_short(int kind, uint32_t L, const DevCorpus& c, const RouteParam
                       const uint32_t* sw, uint32_t nw, const uint32_t* sc, uint32_t nc, CT* table,
                       int num_sms, cudaStream_t st);
 
+// Count-once over a small alphabet (A <= 16 bytes): one CTA per long
+// sequence, a shared-memory bitmap over the K * A candidates that can occur
+// (DESIGN.md §3.2d).  Adds into table (p * 256 + byte layout).
+size_t direct_smem(const RouteParams& rp, uint64_t nbits);
+template <typename CT>
+void count_once_direct(const DevCorpus& c, uint32_t L, const RouteParams& rp,
+                       const uint32_t* seqs, uint32_t nseqs, const uint8_t* arank,
+                       const uint8_t* alpha, uint32_t A, uint64_t K, uint32_t* compact, CT* table,
+                       int num_sms, cudaStream_t st);
+// 256-bit mask of the bytes in the nonzero entries of a dense n0-gram table.
+template <typename CT>
+void alphabet_mask(const CT* table, uint64_t cap, uint64_t minv, uint64_t cmask, uint32_t n0,
+                   uint32_t* mask, int num_sms, cudaStream_t st);
+
 // --- selection (select_kernels.cu)
 struct SelState {
   unsigned long long prefix;   // count digits chosen so far

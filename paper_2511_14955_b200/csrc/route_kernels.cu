@@ -720,6 +720,115 @@ template void count_once_short<unsigned long long>(int, uint32_t, const DevCorpu
                                                    const uint32_t*, uint32_t,
                                                    unsigned long long*, int, cudaStream_t);
 
+// ------------------------------------------------------------------ direct
+
+// Count-once over a small alphabet.  When the corpus uses
+// A <= 16 distinct bytes, an extension pass has at most K' * A candidates
+// that can occur (prefix ordinal p, rank r of the last byte in the alphabet).
+// When that fits a shared-memory bitmap, a CTA takes one whole sequence at a
+// time: every position's candidate bit is set (test first, then an atomic OR),
+// and at the end of the sequence each set bit adds 1 to compact[p * A + r]
+// and is cleared.  No routing, no dedup cache, no consume pass.
+constexpr int kDirectThreads = 1024;
+
+template <int L>
+__global__ void __launch_bounds__(kDirectThreads, 1) k_once_direct(
+    DevCorpus c, RouteParams rp, const uint32_t* __restrict__ seqs, uint32_t nseqs,
+    const uint8_t* __restrict__ arank, uint32_t A, uint32_t nwords,
+    uint32_t* __restrict__ compact) {
+  extern __shared__ uint4 smem4[];
+  char* sp = reinterpret_cast<char*>(smem4);
+  uint32_t* bm = reinterpret_cast<uint32_t*>(sp);
+  sp += align16((size_t)nwords * 4);
+  uint32_t* s_ostart = reinterpret_cast<uint32_t*>(sp);
+  sp += align16((size_t)rp.NO * 4);
+  uint8_t* s_arank = reinterpret_cast<uint8_t*>(sp);
+  sp += 256;
+  uint64_t* s_slots = reinterpret_cast<uint64_t*>(sp);
+  for (uint32_t i = threadIdx.x; i < nwords; i += blockDim.x) bm[i] = 0;
+  for (uint32_t i = threadIdx.x; i < rp.NO; i += blockDim.x) s_ostart[i] = rp.ostart[i];
+  for (uint32_t i = threadIdx.x; i < 256; i += blockDim.x) s_arank[i] = arank[i];
+  const uint16_t* disp = nullptr;
+  const uint64_t* slots = stage_table<1>(rp, s_slots, disp);  // ends with a barrier
+  const int lane = threadIdx.x & 31;
+  for (uint32_t qi = blockIdx.x; qi < nseqs; qi += gridDim.x) {
+    const uint32_t q = seqs[qi];
+    const int64_t s0 = (int64_t)c.off[q], s1 = (int64_t)c.off[q + 1];
+    const int64_t lo = s0 + L - 1, hi = s1;
+    const int64_t first = s0 & ~int64_t(15);
+    const int64_t nseg = (hi - first + 15) >> 4;
+    const int64_t nseg_r = (nseg + 31) & ~int64_t(31);  // whole warps (seg_load shuffles)
+    for (int64_t sgi = threadIdx.x; sgi < nseg_r; sgi += blockDim.x) {
+      const int64_t b0 = first + sgi * 16;
+      uint32_t W[7];
+      seg_load(c.data, b0, lane, W);
+      const uint32_t vm = sgi < nseg ? vmask(b0, lo, hi) : 0u;
+      static_for<0, 16>([&](auto tc) {
+        constexpr int T = decltype(tc)::value;
+        if ((vm >> T) & 1u) {
+          const uint64_t key = key8<T>(W) & gmask<L>();
+          const uint32_t v = scatter_route<1, L>(key, rp, slots, disp);
+          if (v != 0xffffffffu) {
+            const uint32_t id = (s_ostart[v >> 16] + ((v >> 8) & 0xffu)) * A + s_arank[v & 0xffu];
+            uint32_t* w = bm + (id >> 5);
+            const uint32_t bit = 1u << (id & 31);
+            if (!(*(volatile uint32_t*)w & bit)) atomicOr(w, bit);
+          }
+        }
+      });
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < nwords; i += blockDim.x) {
+      uint32_t x = bm[i];
+      if (x) {
+        bm[i] = 0;
+        do {
+          atomicAdd(compact + i * 32 + (__ffs(x) - 1), 1u);
+          x &= x - 1;
+        } while (x);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// table[p * 256 + alpha[r]] += compact[p * A + r]
+template <typename CT>
+__global__ void k_expand_compact(const uint32_t* __restrict__ compact, uint64_t n, uint32_t A,
+                                 const uint8_t* __restrict__ alpha, CT* __restrict__ table) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t v = compact[i];
+    if (v) {
+      const uint64_t p = i / A, r = i - p * A;
+      table[p * 256 + alpha[r]] += (CT)v;
+    }
+  }
+}
+
+// Byte alphabet of a corpus from its dense count-once n0-gram table: every
+// byte that can end an extension-pass gram lies in some counted n0-gram.
+// index -> key = (index * minv) & cmask (the dense route permutation).
+template <typename CT>
+__global__ void k_alphabet(const CT* __restrict__ table, uint64_t cap, uint64_t minv,
+                           uint64_t cmask, uint32_t n0, uint32_t* __restrict__ mask) {
+  __shared__ uint32_t sm[8];
+  if (threadIdx.x < 8) sm[threadIdx.x] = 0;
+  __syncthreads();
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < cap;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    if (table[i]) {
+      const uint64_t key = minv ? ((i * minv) & cmask) : i;
+      for (uint32_t b = 0; b < n0; ++b) {
+        const uint32_t by = (uint32_t)(key >> (8 * b)) & 0xffu;
+        if (!(sm[by >> 5] & (1u << (by & 31)))) atomicOr(sm + (by >> 5), 1u << (by & 31));
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < 8 && sm[threadIdx.x]) atomicOr(mask + threadIdx.x, sm[threadIdx.x]);
+}
+
 // ------------------------------------------------------------------ host
 
 static size_t table_bytes(const RouteParams& rp) {
@@ -1005,6 +1114,64 @@ void build_prefix_mphf(const std::vector<uint64_t>& keys, bool narrow,
 }
 
 // Host: the permuted id space of a candidate space of `cap` ids.
+size_t direct_smem(const RouteParams& rp, uint64_t nbits) {
+  return align16((nbits + 31) / 32 * 4) + align16((size_t)rp.NO * 4) + 256 + table_bytes(rp);
+}
+
+template <typename CT>
+void alphabet_mask(const CT* table, uint64_t cap, uint64_t minv, uint64_t cmask, uint32_t n0,
+                   uint32_t* mask, int num_sms, cudaStream_t st) {
+  IGB_CUDA(cudaMemsetAsync(mask, 0, 8 * sizeof(uint32_t), st));
+  const unsigned grid = (unsigned)std::min<uint64_t>((cap + 255) / 256, (uint64_t)num_sms * 8);
+  k_alphabet<CT><<<grid ? grid : 1, 256, 0, st>>>(table, cap, minv, cmask, n0, mask);
+  IGB_CUDA(cudaGetLastError());
+}
+
+template <typename CT>
+void count_once_direct(const DevCorpus& c, uint32_t L, const RouteParams& rp,
+                       const uint32_t* seqs, uint32_t nseqs, const uint8_t* arank,
+                       const uint8_t* alpha, uint32_t A, uint64_t K, uint32_t* compact, CT* table,
+                       int num_sms, cudaStream_t st) {
+  const uint64_t nbits = K * A;
+  const uint32_t nwords = (uint32_t)((nbits + 31) / 32);
+  IGB_CUDA(cudaMemsetAsync(compact, 0, nbits * 4, st));
+  if (nseqs) {
+    const size_t smem = direct_smem(rp, nbits);
+    auto go = [&](auto k) {
+      IGB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      const unsigned grid = (unsigned)std::min<uint64_t>(nseqs, (uint64_t)num_sms);
+      k<<<grid, kDirectThreads, smem, st>>>(c, rp, seqs, nseqs, arank, A, nwords, compact);
+    };
+    switch (L) {
+      case 2: go(k_once_direct<2>); break;
+      case 3: go(k_once_direct<3>); break;
+      case 4: go(k_once_direct<4>); break;
+      case 5: go(k_once_direct<5>); break;
+      case 6: go(k_once_direct<6>); break;
+      case 7: go(k_once_direct<7>); break;
+      case 8: go(k_once_direct<8>); break;
+      default: throw Error(IG_ECONFIG, "gram length above 8 is not supported");
+    }
+  }
+  const unsigned g2 = (unsigned)std::min<uint64_t>((nbits + 255) / 256, (uint64_t)num_sms * 8);
+  k_expand_compact<CT><<<g2 ? g2 : 1, 256, 0, st>>>(compact, nbits, A, alpha, table);
+  IGB_CUDA(cudaGetLastError());
+}
+
+template void alphabet_mask<uint32_t>(const uint32_t*, uint64_t, uint64_t, uint64_t, uint32_t,
+                                      uint32_t*, int, cudaStream_t);
+template void alphabet_mask<unsigned long long>(const unsigned long long*, uint64_t, uint64_t,
+                                                uint64_t, uint32_t, uint32_t*, int, cudaStream_t);
+template void count_once_direct<uint32_t>(const DevCorpus&, uint32_t, const RouteParams&,
+                                          const uint32_t*, uint32_t, const uint8_t*,
+                                          const uint8_t*, uint32_t, uint64_t, uint32_t*,
+                                          uint32_t*, int, cudaStream_t);
+template void count_once_direct<unsigned long long>(const DevCorpus&, uint32_t,
+                                                    const RouteParams&, const uint32_t*, uint32_t,
+                                                    const uint8_t*, const uint8_t*, uint32_t,
+                                                    uint64_t, uint32_t*, unsigned long long*, int,
+                                                    cudaStream_t);
+
 void make_route_params(uint64_t cap, RouteParams& rp) {
   uint32_t lgc = 0;
   while ((1ull << lgc) < cap) ++lgc;

@@ -88,6 +88,9 @@ void finish_corpus(Session& s, std::vector<uint64_t>& hoff) {
   // count-once work units: <= kUnitBytes of gram ends of one long sequence;
   // short sequences are counted without routing (k_once_short), a warp or a
   // CTA per sequence
+  uint32_t n_long = 0;
+  for (uint64_t q = 0; q < m; ++q) n_long += hoff[q + 1] - hoff[q] > (uint64_t)kShortCtaLen;
+  s.n_long = n_long;
   std::vector<RouteUnit> units;
   std::vector<uint32_t> ufirst(m + 1, 0);
   std::vector<uint32_t> sw, sc;
@@ -298,6 +301,7 @@ struct Prefix {
   std::vector<uint64_t> pk;          // count-once: host keys by p
   std::vector<uint32_t> ostart;      // count-once: host owner ranges
   uint32_t plen = 0;
+  bool table_built = false;  // count-once: build_prefix_table already ran
 };
 
 static Prefix prepare_prefix(Session& s, const uint64_t* keys, uint64_t K, uint32_t plen,
@@ -449,6 +453,33 @@ static CT* count_pass(Session& s, bool dense, uint32_t L, int mode, const Prefix
     km.pkeys = P->ps.pkeys;
     return t;
   }
+  if (mode == IG_MODE_ONCE && !dense && s.alpha_n <= 16 && !getenv("IG_NO_DIRECT")) {
+    // small alphabet: K' * A candidates in a shared-memory bitmap per sequence
+    const uint64_t nbits = P->K * s.alpha_n;
+    const size_t est = (nbits + 31) / 32 * 4 + (size_t)P->rp.NO * 4 + 256 + 12 * P->K + 1024;
+    if (nbits <= (1ull << 20) && est <= kMaxOnceSmem) {
+      build_prefix_table(s, *const_cast<Prefix*>(P));
+      if (direct_smem(P->rp, nbits) <= kMaxOnceSmem) {
+        tcap = 256 * P->K;
+        CT* t = s.table.as<CT>(tcap);
+        IGB_CUDA(cudaMemsetAsync(t, 0, tcap * sizeof(CT), s.stream));
+        s.rc.have_next = false;  // no fused histogram for the pass after this one
+        short_pass<CT>(s, 1, L, P->rp, t, 0, (uint32_t)s.dc.m);
+        const uint8_t* ab = static_cast<const uint8_t*>(s.alpha_dev.p) + 32;
+        const size_t ev = s.kt.begin(IG_KF_ROUTE_SCATTER, s.stream);
+        count_once_direct<CT>(s.dc, L, P->rp, static_cast<const uint32_t*>(s.order.p), s.n_long,
+                              ab, ab + 256, s.alpha_n, P->K, s.compact.as<uint32_t>(nbits + 1),
+                              t, s.num_sms, s.stream);
+        s.kt.end(ev, s.stream);
+        s.launches += (s.n_long ? 1 : 0) + 1;
+        km = KeyMap{};
+        km.pkeys = P->pkeys;
+        return t;
+      }
+      // did not fit after all: the route path (its table build is done)
+      const_cast<Prefix*>(P)->table_built = true;
+    }
+  }
   if (mode == IG_MODE_ONCE) {
     RouteParams rp;
     if (dense) make_route_params(1ull << (8 * L), rp);
@@ -481,7 +512,7 @@ static CT* count_pass(Session& s, bool dense, uint32_t L, int mode, const Prefix
     } else {
       route_count_once<CT>(1, s.rc, s.dc, dense ? 0 : 1, L, rp, t, s.num_sms, s.stream);
       if (!dense) {  // the host table build overlaps the count kernel
-        build_prefix_table(s, *const_cast<Prefix*>(P));
+        if (!P->table_built) build_prefix_table(s, *const_cast<Prefix*>(P));
         const bool dd = rp.dedup;
         rp = P->rp;
         rp.dedup = dd;
@@ -609,6 +640,28 @@ static void run_t(Session& s, const ig_params& p, ig_result* out) {
   };
   IGB_CUDA(cudaGetLastError());
   allreduce(s, table, tcap, sizeof(CT) == 4 ? 0 : 1);
+  s.alpha_n = 256;
+  if (p.mode == IG_MODE_ONCE && n > 3) {
+    // the byte alphabet, from the (global) dense table: a small one lets the
+    // extension passes count candidates in a per-sequence bitmap
+    uint8_t* ad = s.alpha_dev.as<uint8_t>(32 + 512);
+    alphabet_mask<CT>(table, tcap, km.minv, km.cmask, n0, reinterpret_cast<uint32_t*>(ad),
+                      s.num_sms, s.stream);
+    s.launches++;
+    uint32_t mask[8];
+    d2h(s, mask, ad, sizeof(mask));
+    uint8_t tab[512];
+    memset(tab, 0, sizeof(tab));
+    uint32_t A = 0;
+    for (uint32_t b = 0; b < 256; ++b)
+      if (mask[b >> 5] >> (b & 31) & 1u) {
+        tab[b] = (uint8_t)std::min<uint32_t>(A, 255);  // arank
+        if (A < 256) tab[256 + A] = (uint8_t)b;       // alpha
+        ++A;
+      }
+    s.alpha_n = std::max<uint32_t>(A, 1);
+    if (s.alpha_n <= 16) h2d(s, ad + 32, tab, sizeof(tab));
+  }
   tm.end(ev);
   rows.push_back(make_row(std::to_string(n0) + "-gram pass", n0, total_bytes, dcap, 0, false, ev));
 

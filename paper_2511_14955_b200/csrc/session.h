@@ -38,6 +38,11 @@ struct Session {
   // count-once short sequences (route_kernels.cu: k_once_short), by class
   DevBuf short_w, short_c;
   std::vector<uint32_t> h_short_w, h_short_c;
+  uint32_t n_long = 0;  // sequences of > kShortCtaLen bytes: order[0 .. n_long)
+  // byte alphabet of the current run (count-once small-alphabet passes)
+  DevBuf alpha_dev;      // u32 mask[8] | u8 arank[256] | u8 alpha[256]
+  DevBuf compact;        // u32 [K' * A] direct-pass counts
+  uint32_t alpha_n = 256;
   DevCorpus dc;
   bool loaded = false;
 
