@@ -284,8 +284,9 @@ __global__ void __launch_bounds__(NT) k_route_scatter(
   sp += align16((size_t)rp.NO * 8);
   uint32_t* lhist = reinterpret_cast<uint32_t*>(sp);  // NO
   sp += align16((size_t)rp.NO * 4);
-  uint32_t* lbase = reinterpret_cast<uint32_t*>(sp);  // NO + 1
-  sp += align16((size_t)(rp.NO + 1) * 4);
+  // copy-out delta of each owner: global index of its staging slot 0
+  unsigned long long* delta = reinterpret_cast<unsigned long long*>(sp);  // NO
+  sp += align16((size_t)rp.NO * 8);
   const bool nextc = rp.next_lgno >= 0;
   const uint32_t nno = nextc ? (1u << rp.next_lgno) : 0u;
   uint32_t* nhist = reinterpret_cast<uint32_t*>(sp);  // next pass's owner histogram
@@ -314,8 +315,11 @@ __global__ void __launch_bounds__(NT) k_route_scatter(
     // the dedup cache lives for the whole unit: every chunk of a unit belongs to
     // the same sequence, so a gram seen anywhere earlier in it adds nothing
     for (uint32_t i = threadIdx.x; i < kSlots; i += blockDim.x) cache[i] = kEmpty;
+    for (uint32_t i = threadIdx.x; i < rp.NO; i += blockDim.x) lhist[i] = 0;
+    // four barriers per chunk: the scan phase also turns counts into bases,
+    // copy-out deltas and advanced cursors (each owner belongs to one
+    // thread), and the copy-out phase zeroes the histogram for the next chunk
     for (int64_t cs = 0; cs < nseg; cs += NT) {
-      for (uint32_t i = threadIdx.x; i < rp.NO; i += blockDim.x) lhist[i] = 0;
       __syncthreads();
       const int64_t sgi = cs + threadIdx.x;
       const int64_t b0 = first + sgi * 16;
@@ -370,7 +374,7 @@ __global__ void __launch_bounds__(NT) k_route_scatter(
         r[T] = v;
       });
       __syncthreads();
-      {  // exclusive scan lhist -> lbase; each thread owns a contiguous run of owners
+      {  // exclusive scan of lhist; each thread owns a contiguous run of owners
         const uint32_t per = (rp.NO + NT - 1) / NT;
         const uint32_t a = threadIdx.x * per, e = min(rp.NO, a + per);
         uint32_t sum = 0;
@@ -378,19 +382,13 @@ __global__ void __launch_bounds__(NT) k_route_scatter(
         uint32_t ex, tot;
         BlockScan(scan_tmp).ExclusiveSum(sum, ex, tot);
         for (uint32_t o = a; o < e; ++o) {
-          lbase[o] = ex;
-          ex += lhist[o];
+          const uint32_t cnt = lhist[o];
+          lhist[o] = ex;               // placement cursor (staging base of o)
+          delta[o] = res[o] - ex;      // staging slot i of o -> entries[delta + i]
+          res[o] += cnt;               // o's global cursor after this chunk
+          ex += cnt;
         }
-        if (threadIdx.x == 0) {
-          lbase[rp.NO] = tot;
-          s_total = tot;
-        }
-      }
-      __syncthreads();
-      // res[o] becomes the copy-out delta (global index of staging slot 0 of o)
-      for (uint32_t i = threadIdx.x; i < rp.NO; i += blockDim.x) {
-        lhist[i] = lbase[i];
-        res[i] -= lbase[i];
+        if (threadIdx.x == 0) s_total = tot;
       }
       __syncthreads();
       static_for<0, 16>([&](auto tc) {
@@ -404,10 +402,9 @@ __global__ void __launch_bounds__(NT) k_route_scatter(
       for (uint32_t i = threadIdx.x; i < total; i += blockDim.x) {
         const uint32_t e = staging[i];
         const uint32_t o = e >> 16;
-        entries[res[o] + i] = (uint16_t)(e & 0xffffu);
+        entries[delta[o] + i] = (uint16_t)(e & 0xffffu);
       }
-      __syncthreads();
-      for (uint32_t o = threadIdx.x; o < rp.NO; o += blockDim.x) res[o] += lbase[o + 1];
+      for (uint32_t i = threadIdx.x; i < rp.NO; i += blockDim.x) lhist[i] = 0;
     }
     __syncthreads();
     for (uint32_t o = threadIdx.x; o < rp.NO; o += blockDim.x)
@@ -942,7 +939,7 @@ static void route_stage2_t(RouteCtx& x, const DevCorpus& c, const RouteParams& r
     constexpr int KT = TAB >= 10 ? 0 : TAB;  // dense variants carry no table
     const size_t nxt = rp.next_lgno >= 0 ? align16(((size_t)1 << rp.next_lgno) * 4) : 0;
     const size_t smem = (size_t)NT * 16 * 4 + (size_t)DS * 8 + align16((size_t)rp.NO * 8) +
-                        align16((size_t)rp.NO * 4) + align16((size_t)(rp.NO + 1) * 4) + nxt + tab;
+                        align16((size_t)rp.NO * 4) + align16((size_t)rp.NO * 8) + nxt + tab;
     auto k = k_route_scatter<KIND, L, KT, NT, DS>;
     IGB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per = 0;
@@ -996,7 +993,7 @@ static void route_stage_l(int stage, RouteCtx& x, const DevCorpus& c, const Rout
   } else {
     auto fixed = [&](size_t nt) {  // + static smem
       const size_t nxt = rp.next_lgno >= 0 ? align16(((size_t)1 << rp.next_lgno) * 4) : 0;
-      return nt * 64 + 2048 * 8 + (size_t)rp.NO * 16 + 256 + nxt + 8 * 1024;
+      return nt * 64 + 2048 * 8 + (size_t)rp.NO * 20 + 256 + nxt + 8 * 1024;
     };
     // the table is staged in shared memory when it fits (one 768-thread CTA
     // per SM: measured 1.2x faster than L1-cached global loads with two
