@@ -12,6 +12,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <chrono>
 #include <type_traits>
 #include <cmath>
 #include <cstdio>
@@ -379,6 +380,18 @@ static Prefix prepare_prefix(Session& s, const uint64_t* keys, uint64_t K, uint3
 // while the pass's count kernel (which needs only the owner function) is in
 // flight.
 static void build_prefix_table(Session& s, Prefix& P) {
+  static const bool trace = getenv("IG_TRACE_BUILD") != nullptr;
+  const auto t0 = std::chrono::steady_clock::now();
+  struct Tr {
+    bool on;
+    std::chrono::steady_clock::time_point t0;
+    uint64_t K;
+    ~Tr() {
+      if (on)
+        fprintf(stderr, "[ig] prefix table build: K=%llu %.3f ms\n", (unsigned long long)K,
+                std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+    }
+  } tr{trace, t0, P.K};
   const uint64_t K = P.K;
   const uint32_t lgno = P.rp.lgno;
   const uint32_t plen = P.plen;
