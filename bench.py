@@ -160,12 +160,15 @@ def make_collective(rank, world, bytes_total, seqs_total):
 
     from paper_2511_14955_b200 import _native as N
 
+    calls = [0]
+
     class _CAI:
         def __init__(self, ptr, n, typestr):
             self.__cuda_array_interface__ = {"data": (ptr, False), "shape": (n,),
                                              "typestr": typestr, "version": 3, "strides": None}
 
     def _allreduce(buf, count, dtype, stream, user):
+        calls[0] += 1
         try:
             # sum of unsigned counters == sum of the same bits as signed ints (mod 2^w)
             t = torch.as_tensor(_CAI(buf, count, "<i4" if dtype == 0 else "<i8"), device="cuda")
@@ -179,6 +182,7 @@ def make_collective(rank, world, bytes_total, seqs_total):
     cb = N.ALLREDUCE_FN(_allreduce)
     coll = N.ig_collective(rank=rank, world=world, bytes_total=bytes_total,
                            seqs_total=seqs_total, allreduce=cb, user=None)
+    coll.calls = calls  # python-side counter (the ctypes struct keeps a reference)
     return coll, cb
 
 
@@ -346,7 +350,10 @@ def main():
     from paper_2511_14955_b200 import intergrams as ig
 
     torch.cuda.set_device(local)
-    if world > 1:
+    # IG_BENCH_FORCE_COLLECTIVE=1 (tests): a 1-rank NCCL group with the
+    # collective hook installed, to exercise the N>1 plumbing on one GPU
+    force_coll = os.environ.get("IG_BENCH_FORCE_COLLECTIVE") == "1"
+    if world > 1 or force_coll:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     # ---- this rank's shard: weak scaling, sequences [rank*m, (rank+1)*m)
@@ -376,8 +383,10 @@ def main():
 
     stream = torch.cuda.Stream()
     coll, _cb = (None, None)
-    if world > 1:
-        coll, _cb = make_collective(rank, world, bytes_total, seqs_total)
+    if world > 1 or force_coll:
+        # forced on one rank: the library skips the hook at world 1, so it is
+        # told 2; the 1-rank NCCL all-reduce is the identity
+        coll, _cb = make_collective(rank, max(world, 2), bytes_total, seqs_total)
     sess = ig.Session(device=local, stream=stream.cuda_stream, collective=coll)
     corpus = ig.Corpus(data, off_np)
     sess.load(corpus)
@@ -515,6 +524,8 @@ def main():
             "step_breakdown_ms": step_breakdown,
             "kernel_breakdown": kernel_breakdown,
             "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches,
+            "collective": None if coll is None else
+            {"backend": "nccl", "world": world, "allreduce_calls": coll.calls[0]},
             "clocks": clk.summary(),
             "result_digest": hashlib.sha256(
                 ig.topk_to_tsv(ig.run_result_topk(res, cfg.n)).encode()).hexdigest()[:16],
@@ -522,7 +533,7 @@ def main():
         }
         print(json.dumps(line), flush=True)
     sess.close()
-    if world > 1:
+    if world > 1 or force_coll:
         dist.destroy_process_group()
     return 0
 
