@@ -510,6 +510,61 @@ void launch_widen_add(const uint32_t* src, unsigned long long* dst, uint64_t n, 
   k_widen_add<<<blocks, 256, 0, st>>>(src, dst, n4);
 }
 
+// Narrowed all-reduce of a u64 table: the largest entry, the
+// u64 -> u32 narrowing and the widening back (n % 4 == 0).
+__global__ void k_max_u64(const unsigned long long* __restrict__ t, uint64_t n,
+                          unsigned long long* __restrict__ out) {
+  unsigned long long m = 0;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    m = max(m, t[i]);
+  for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
+}
+
+__global__ void k_narrow_u64(const unsigned long long* __restrict__ src, uint32_t* __restrict__ dst,
+                             uint64_t n4) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n4;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const ulonglong2 a = reinterpret_cast<const ulonglong2*>(src)[2 * i];
+    const ulonglong2 b = reinterpret_cast<const ulonglong2*>(src)[2 * i + 1];
+    reinterpret_cast<uint4*>(dst)[i] =
+        make_uint4((uint32_t)a.x, (uint32_t)a.y, (uint32_t)b.x, (uint32_t)b.y);
+  }
+}
+
+__global__ void k_widen_set(const uint32_t* __restrict__ src, unsigned long long* __restrict__ dst,
+                            uint64_t n4) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n4;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint4 v = reinterpret_cast<const uint4*>(src)[i];
+    reinterpret_cast<ulonglong2*>(dst)[2 * i] = make_ulonglong2(v.x, v.y);
+    reinterpret_cast<ulonglong2*>(dst)[2 * i + 1] = make_ulonglong2(v.z, v.w);
+  }
+}
+
+void launch_max_u64(const unsigned long long* t, uint64_t n, unsigned long long* out,
+                    cudaStream_t st) {
+  IGB_CUDA(cudaMemsetAsync(out, 0, sizeof(*out), st));
+  if (!n) return;
+  const unsigned blocks = (unsigned)std::min<uint64_t>((n + 255) / 256, 148 * 8);
+  k_max_u64<<<blocks, 256, 0, st>>>(t, n, out);
+}
+
+void launch_narrow_u64(const unsigned long long* src, uint32_t* dst, uint64_t n, cudaStream_t st) {
+  const uint64_t n4 = n / 4;
+  if (!n4) return;
+  const unsigned blocks = (unsigned)std::min<uint64_t>((n4 + 255) / 256, 148 * 16);
+  k_narrow_u64<<<blocks, 256, 0, st>>>(src, dst, n4);
+}
+
+void launch_widen_set(const uint32_t* src, unsigned long long* dst, uint64_t n, cudaStream_t st) {
+  const uint64_t n4 = n / 4;
+  if (!n4) return;
+  const unsigned blocks = (unsigned)std::min<uint64_t>((n4 + 255) / 256, 148 * 16);
+  k_widen_set<<<blocks, 256, 0, st>>>(src, dst, n4);
+}
+
 // ------------------------------------------------------------------ launchers
 
 template <int KIND, int L, typename CT>

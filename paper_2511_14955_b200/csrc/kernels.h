@@ -31,6 +31,11 @@ void launch_prefix_insert(const uint64_t* keys, uint32_t K, const uint32_t* owne
                           cudaStream_t st);
 
 void launch_widen_add(const uint32_t* src, unsigned long long* dst, uint64_t n, cudaStream_t st);
+// narrowed all-reduce of u64 tables (n % 4 == 0)
+void launch_max_u64(const unsigned long long* t, uint64_t n, unsigned long long* out,
+                    cudaStream_t st);
+void launch_narrow_u64(const unsigned long long* src, uint32_t* dst, uint64_t n, cudaStream_t st);
+void launch_widen_set(const uint32_t* src, unsigned long long* dst, uint64_t n, cudaStream_t st);
 // SM copy to/from mapped pinned host memory (no copy engine)
 void launch_copy(void* dst, const void* src, uint64_t n, cudaStream_t st);
 void launch_pack_prefix(const DevPrefixSet& ps, uint64_t* packed, cudaStream_t st);

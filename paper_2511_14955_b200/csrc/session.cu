@@ -279,6 +279,36 @@ static void allreduce(Session& s, void* buf, uint64_t count, int dtype) {
   if (rc != 0) throw Error(IG_EINTERNAL, "allreduce callback failed");
 }
 
+// A pass table summed over the ranks.  A u64 table goes through the
+// collective as u32 when that is provably exact: the sum of the per-rank
+// maxima (itself all-reduced, one u64) bounds every summed entry, so below
+// 2^32 no entry can overflow.  Halves the bytes of count-all tables whose
+// totals only might reach 2^32 (c5: 3 GB per pass -> 1.5 GB).
+template <typename CT>
+static void allreduce_table(Session& s, CT* t, uint64_t n) {
+  if (!s.has_coll || s.coll.world <= 1) return;
+  if constexpr (sizeof(CT) == 8) {
+    static const bool no_narrow = getenv("IG_NO_NARROW_ALLREDUCE") != nullptr;
+    if (!no_narrow && n && n % 4 == 0) {
+      unsigned long long* mx = reinterpret_cast<unsigned long long*>(s.work.as<uint32_t>(64));
+      launch_max_u64(t, n, mx, s.stream);
+      s.launches++;
+      allreduce(s, mx, 1, 1);
+      unsigned long long bound = 0;
+      d2h(s, &bound, mx, sizeof(bound));
+      if (bound < (1ull << 32)) {
+        uint32_t* nar = s.scratch32.as<uint32_t>(n);
+        launch_narrow_u64(t, nar, n, s.stream);
+        allreduce(s, nar, n, 0);
+        launch_widen_set(nar, t, n, s.stream);
+        s.launches += 2;
+        return;
+      }
+    }
+  }
+  allreduce(s, t, n, sizeof(CT) == 4 ? 0 : 1);
+}
+
 // Owner-hash width the count-once extension passes use for k' survivors: ~40
 // prefixes per owner on average (at most kPrefixesPerOwner after the check in
 // prepare_prefix).  Known before the survivors are, so the previous pass's
@@ -652,7 +682,7 @@ static void run_t(Session& s, const ig_params& p, ig_result* out) {
     return want + 1 < (uint32_t)fused ? want : (uint32_t)fused;
   };
   IGB_CUDA(cudaGetLastError());
-  allreduce(s, table, tcap, sizeof(CT) == 4 ? 0 : 1);
+  allreduce_table<CT>(s, table, tcap);
   s.alpha_n = 256;
   if (p.mode == IG_MODE_ONCE && n > 3) {
     // the byte alphabet, from the (global) dense table: a small one lets the
@@ -739,7 +769,7 @@ static void run_t(Session& s, const ig_params& p, ig_result* out) {
       if (next_lg > (int32_t)kMaxFusedLg) next_lg = -1;
       CT* ct = count_pass<CT>(s, false, j, p.mode, &P, tcap, km, next_lg);
       IGB_CUDA(cudaGetLastError());
-      allreduce(s, ct, tcap, sizeof(CT) == 4 ? 0 : 1);
+      allreduce_table<CT>(s, ct, tcap);
       tm.end(ev);
       rows.push_back(
           make_row(std::to_string(j) + "-gram pass", j, total_bytes, cap, 0, false, ev));

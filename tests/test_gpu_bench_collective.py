@@ -36,13 +36,15 @@ def _bench(config, extra_env, torchrun):
     return json.loads(out.stdout.strip().splitlines()[-1])
 
 
-@pytest.mark.parametrize("config", ["c2", "c3"])  # count-once u32 tables / count-all u64 (c3 totals 16 GiB)
-def test_bench_collective_hook_equals_single(gpu_lib, config):
+# c2: count-once u32 tables, one all-reduce per pass.  c3: count-all with a
+# 16 GiB total, u64 tables: a u64 bound, then the table narrowed to u32.
+@pytest.mark.parametrize("config,calls_per_pass", [("c2", 1), ("c3", 2)])
+def test_bench_collective_hook_equals_single(gpu_lib, config, calls_per_pass):
     plain = _bench(config, {}, torchrun=False)
     coll = _bench(config, {"IG_BENCH_FORCE_COLLECTIVE": "1"}, torchrun=True)
     assert plain["collective"] is None
     assert coll["collective"]["backend"] == "nccl"
-    # one all-reduce per counting pass, every run (3 warm-up + 1 timed)
+    # every counting pass of every run (3 warm-up + 1 timed)
     passes = max(coll["config"]["n"], 3) - 2
-    assert coll["collective"]["allreduce_calls"] == 4 * passes
+    assert coll["collective"]["allreduce_calls"] == 4 * passes * calls_per_pass
     assert coll["result_digest"] == plain["result_digest"]

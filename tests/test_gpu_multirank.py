@@ -23,6 +23,7 @@ class HostAllreduce:
         self.bar = threading.Barrier(world)
         self.bufs = {}
         self.calls = 0
+        self.dtypes = []
 
     def make(self, rank):
         def cb(buf, count, dtype, stream, user):
@@ -44,6 +45,7 @@ class HostAllreduce:
                 torch.cuda.synchronize()
                 if rank == 0:
                     self.calls += 1
+                    self.dtypes.append((int(dtype), int(count)))
                 return 0
             except Exception as e:  # noqa: BLE001
                 print("allreduce failed", repr(e))
@@ -83,3 +85,41 @@ def test_two_ranks_equal_one(gpu_lib, name, n, k, mode):
         assert results[r].topk == single.topk
         assert [p.bytes_processed for p in results[r].passes] == \
                [p.bytes_processed for p in single.passes]
+
+
+def test_two_ranks_u64_tables_narrowed(gpu_lib):
+    """Count-all with a total that might reach 2^32 (bytes_total 8 GiB): the
+    tables are u64, and each pass's all-reduce goes through the hook as one
+    u64 bound (sum of the per-rank maxima) followed by the table as u32."""
+    cfg = S.scaled(S.CONFIGS["c5"], num_seqs=16, seq_len=65536)
+    data, off = S.generate(cfg)
+    icfg = ig.IntergramConfig(n=6, k=300, z=1.5, mode=ig.CountMode.kAll)
+    single = ig.run_intergrams(ig.Corpus(data, off), icfg)
+    ar = HostAllreduce(2)
+    results = [None, None]
+    cbs = [ar.make(r) for r in range(2)]
+
+    def rank_main(r):
+        a, b = ig.shard_range(off, r, 2)
+        ld = data[int(off[a]):int(off[b])]
+        loff = (off[a:b + 1] - off[a]).astype(np.uint64)
+        coll = N.ig_collective(rank=r, world=2, bytes_total=8 << 30,
+                               seqs_total=int(off.size - 1), allreduce=cbs[r], user=None)
+        sess = ig.Session(device=0, collective=coll)
+        sess.load(ig.Corpus(ld, loff))
+        results[r] = sess.run(icfg)
+        sess.close()
+
+    ts = [threading.Thread(target=rank_main, args=(r,)) for r in range(2)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=300)
+    passes = 6 - 2
+    assert ar.calls == 2 * passes
+    assert [d for d, _ in ar.dtypes] == [1, 0] * passes  # bound (u64), then the table (u32)
+    assert all(c == 1 for d, c in ar.dtypes if d == 1)
+    for r in range(2):
+        assert results[r] is not None
+        assert np.array_equal(results[r].keys, single.keys)
+        assert np.array_equal(results[r].counts, single.counts)
