@@ -110,7 +110,10 @@ typedef struct {
  * library shards nothing itself: each rank passes its own whole-sequence
  * shard (see ig_shard_range) and the library calls allreduce once per
  * counting pass on the device count table (sum, in place, on `stream`).
- * dtype: 0 = u32, 1 = u64.  bytes_total / seqs_total are the GLOBAL corpus
+ * A u64 table is preceded by a one-element u64 call (the sum of the ranks'
+ * largest entries); when that sum is below 2^32 the table itself follows as
+ * u32 (exact, half the bytes).  Every rank makes the same calls in the same
+ * order.  dtype: 0 = u32, 1 = u64.  bytes_total / seqs_total are the GLOBAL corpus
  * totals (they choose the counter width identically on every rank and are
  * what PassResult::bytes_processed reports). */
 typedef struct {
