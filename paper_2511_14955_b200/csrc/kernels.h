@@ -84,6 +84,7 @@ struct RouteCtx {
   const uint32_t* unit_first = nullptr;
   uint32_t nunits = 0;
   DevBuf cnt, actual, base, entries, cub_tmp, cnt_next;
+  DevBuf consume_order;  // consume: owners heaviest first + the work counter
   uint64_t launches = 0;
   KernelTimer* kt = nullptr;
   bool have_next = false;   // cnt_next holds the next pass's counts (fused in the scatter)

@@ -482,7 +482,8 @@ template <typename CT>
 __global__ void __launch_bounds__(kConsumeThreads) k_consume_once(
     RouteView uv, RouteParams rp, uint32_t seq_block, uint32_t nblocks,
     const unsigned long long* __restrict__ base, const uint32_t* __restrict__ actual,
-    const uint16_t* __restrict__ entries, CT* __restrict__ table) {
+    const uint16_t* __restrict__ entries, CT* __restrict__ table,
+    const uint32_t* __restrict__ owner_order, uint32_t* __restrict__ work) {
   extern __shared__ uint4 smem4[];
   const uint32_t ipo = 1u << rp.lgl;                   // ids per owner
   const uint32_t cntw = (uint32_t)(align16((size_t)(ipo + 1) / 2 * 4) / 4);
@@ -493,8 +494,15 @@ __global__ void __launch_bounds__(kConsumeThreads) k_consume_once(
   uint32_t* bm = bms + warp * bmw4;
   const uint32_t nitems = rp.NO * nblocks;
   for (uint32_t i = threadIdx.x; i < bmw4 * kConsumeWarps; i += blockDim.x) bms[i] = 0;
-  for (uint32_t item = blockIdx.x; item < nitems; item += gridDim.x) {
-    const uint32_t o = item / nblocks, b = item % nblocks;
+  // items are claimed dynamically, owners heaviest first (Zipf corpora route
+  // most entries to a few owners; a static split leaves SMs idle at the end)
+  __shared__ uint32_t s_item;
+  for (;;) {
+    if (threadIdx.x == 0) s_item = atomicAdd(work, 1u);
+    __syncthreads();
+    const uint32_t item = s_item;
+    if (item >= nitems) break;
+    const uint32_t o = owner_order[item / nblocks], b = item % nblocks;
     for (uint32_t i = threadIdx.x; i < cntw; i += blockDim.x) cnt[i] = 0;
     __syncthreads();
     const uint64_t q0 = uv.q0 + (uint64_t)b * seq_block;
@@ -716,6 +724,48 @@ template void count_once_short<unsigned long long>(int, uint32_t, const DevCorpu
                                                    const RouteParams&, const uint32_t*, uint32_t,
                                                    const uint32_t*, uint32_t,
                                                    unsigned long long*, int, cudaStream_t);
+
+// Routed entries per owner (one CTA per owner row of `actual`).
+__global__ void k_owner_totals(const uint32_t* __restrict__ actual, uint32_t nb,
+                               uint32_t* __restrict__ tot) {
+  uint64_t t = 0;
+  const uint32_t* row = actual + (size_t)blockIdx.x * nb;
+  for (uint32_t u = threadIdx.x; u < nb; u += blockDim.x) t += row[u];
+  for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  __shared__ uint64_t ws[32];
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = t;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint64_t s = 0;
+    for (uint32_t w = 0; w < blockDim.x / 32; ++w) s += ws[w];
+    tot[blockIdx.x] = (uint32_t)(s < 0xfffffffeull ? s : 0xfffffffeull);
+  }
+}
+
+// Owners heaviest first (one CTA, block radix sort on ~total).  work[0] = 0
+// (the item counter).
+constexpr int kOrderThreads = 1024, kOrderItems = 8;  // <= 8192 owners
+__global__ void __launch_bounds__(kOrderThreads) k_owner_order(const uint32_t* __restrict__ tot,
+                                                                uint32_t NO,
+                                                                uint32_t* __restrict__ order,
+                                                                uint32_t* __restrict__ work) {
+  using Sort = cub::BlockRadixSort<uint32_t, kOrderThreads, kOrderItems, uint32_t>;
+  __shared__ typename Sort::TempStorage tmp;
+  uint32_t keys[kOrderItems], vals[kOrderItems];
+#pragma unroll
+  for (int i = 0; i < kOrderItems; ++i) {
+    const uint32_t o = threadIdx.x * kOrderItems + i;
+    keys[i] = o < NO ? ~tot[o] : 0xffffffffu;
+    vals[i] = o;
+  }
+  Sort(tmp).Sort(keys, vals);
+#pragma unroll
+  for (int i = 0; i < kOrderItems; ++i) {
+    const uint32_t r = threadIdx.x * kOrderItems + i;
+    if (r < NO) order[r] = vals[i];
+  }
+  if (threadIdx.x == 0) work[0] = 0;
+}
 
 // ------------------------------------------------------------------ direct
 
@@ -962,7 +1012,9 @@ static void route_stage2_t(RouteCtx& x, const DevCorpus& c, const RouteParams& r
     if (per < 1) throw Error(IG_EINTERNAL, "route consume does not fit in shared memory");
     const uint64_t slots = (uint64_t)num_sms * per;
     const uint64_t mq = uv.q1 - uv.q0;
-    uint64_t nblocks = (slots * 4 + rp.NO - 1) / rp.NO;
+    static const char* cg = getenv("IG_CONSUME_GRAIN");
+    const uint64_t grain = cg ? std::max<uint64_t>(1, strtoull(cg, nullptr, 10)) : 8;
+    uint64_t nblocks = (slots * grain + rp.NO - 1) / rp.NO;
     if (nblocks > mq) nblocks = mq;
     if (nblocks < 1) nblocks = 1;
     uint64_t sb = (mq + nblocks - 1) / nblocks;
@@ -972,9 +1024,26 @@ static void route_stage2_t(RouteCtx& x, const DevCorpus& c, const RouteParams& r
     if (nblocks < 1) nblocks = 1;
     const uint64_t nitems = (uint64_t)rp.NO * nblocks;
     const unsigned grid = (unsigned)std::min<uint64_t>(nitems, slots);
+    uint32_t* ord = x.consume_order.as<uint32_t>(2 * (size_t)rp.NO + 8);
+    uint32_t* work = ord + rp.NO + 4;
+    uint32_t* tot = work + 4;
     const size_t ev = x.kt ? x.kt->begin(IG_KF_ROUTE_CONSUME, st) : 0;
+    static const bool no_order = getenv("IG_CONSUME_NO_ORDER") != nullptr;
+    if (!no_order && rp.NO <= (uint32_t)(kOrderThreads * kOrderItems)) {
+      k_owner_totals<<<rp.NO, 256, 0, st>>>(act, uv.nb, tot);
+      k_owner_order<<<1, kOrderThreads, 0, st>>>(tot, rp.NO, ord, work);
+      x.launches++;
+    } else {  // identity order
+      std::vector<uint32_t> id(rp.NO + 1);
+      for (uint32_t o = 0; o < rp.NO; ++o) id[o] = o;
+      id[rp.NO] = 0;
+      IGB_CUDA(cudaMemcpyAsync(ord, id.data(), rp.NO * 4, cudaMemcpyHostToDevice, st));
+      IGB_CUDA(cudaMemsetAsync(work, 0, 4, st));
+      IGB_CUDA(cudaStreamSynchronize(st));
+    }
+    x.launches++;
     k<<<grid, kConsumeThreads, smem, st>>>(uv, rp, (uint32_t)sb, (uint32_t)nblocks, base, act,
-                                            ent, table);
+                                            ent, table, ord, work);
     if (x.kt) x.kt->end(ev, st);
     x.launches++;
   }
