@@ -839,6 +839,83 @@ __global__ void __launch_bounds__(kDirectThreads, 1) k_once_direct(
   }
 }
 
+// The same with the prefix looked up in a direct table (alphabet of <= 16
+// bytes, `bits` per rank, bits * (L - 1) <= 16): the 24 window bytes of a lane
+// are translated to ranks once, the rank-packed prefix rolls from position to
+// position, and lut[prefix] is the ordinal p (0xffff: not a survivor).
+template <int L>
+__global__ void __launch_bounds__(1024, 1) k_once_direct_lut(
+    DevCorpus c, const uint16_t* __restrict__ lut, uint32_t lut_n, uint32_t bits,
+    const uint32_t* __restrict__ seqs, uint32_t nseqs, const uint8_t* __restrict__ arank,
+    uint32_t A, uint32_t nwords, uint32_t* __restrict__ compact) {
+  extern __shared__ uint4 smem4[];
+  char* sp = reinterpret_cast<char*>(smem4);
+  uint32_t* bm = reinterpret_cast<uint32_t*>(sp);
+  sp += align16((size_t)nwords * 4);
+  uint8_t* s_arank = reinterpret_cast<uint8_t*>(sp);
+  sp += 256;
+  uint16_t* s_lut = reinterpret_cast<uint16_t*>(sp);
+  for (uint32_t i = threadIdx.x; i < nwords; i += blockDim.x) bm[i] = 0;
+  for (uint32_t i = threadIdx.x; i < 256; i += blockDim.x) s_arank[i] = arank[i];
+  for (uint32_t i = threadIdx.x; i < lut_n; i += blockDim.x) s_lut[i] = lut[i];
+  __syncthreads();
+  constexpr int PL = L - 1;
+  const uint32_t pmask = (1u << (bits * PL)) - 1u;
+  const int lane = threadIdx.x & 31;
+  for (uint32_t qi = blockIdx.x; qi < nseqs; qi += gridDim.x) {
+    const uint32_t q = seqs[qi];
+    const int64_t s0 = (int64_t)c.off[q], s1 = (int64_t)c.off[q + 1];
+    const int64_t lo = s0 + L - 1, hi = s1;
+    const int64_t first = s0 & ~int64_t(15);
+    const int64_t nseg = (hi - first + 15) >> 4;
+    const int64_t nseg_r = (nseg + 31) & ~int64_t(31);
+    for (int64_t sgi = threadIdx.x; sgi < nseg_r; sgi += blockDim.x) {
+      const int64_t b0 = first + sgi * 16;
+      uint32_t W[7];
+      seg_load(c.data, b0, lane, W);
+      const uint32_t vm = sgi < nseg ? vmask(b0, lo, hi) : 0u;
+      // ranks of window bytes 0..23 (bytes 8 + T are the segment's)
+      uint32_t R[3] = {0u, 0u, 0u};
+      static_for<0, 24>([&](auto kc) {
+        constexpr int K = decltype(kc)::value;
+        const uint32_t by = (W[K >> 2] >> (8 * (K & 3))) & 0xffu;
+        R[K >> 3] |= (uint32_t)s_arank[by] << (4 * (K & 7));
+      });
+      auto rk = [&](auto kc) -> uint32_t {
+        constexpr int K = decltype(kc)::value;
+        return (R[K >> 3] >> (4 * (K & 7))) & 0xfu;
+      };
+      uint32_t pre = 0;  // prefix of the gram ending at T = 0: bytes 9-L .. 7
+      static_for<9 - L, 8>([&](auto kc) { pre = (pre << bits) | rk(kc); });
+      static_for<0, 16>([&](auto tc) {
+        constexpr int T = decltype(tc)::value;
+        if ((vm >> T) & 1u) {
+          const uint32_t p = s_lut[pre & pmask];
+          if (p != 0xffffu) {
+            const uint32_t id = p * A + rk(std::integral_constant<int, 8 + T>{});
+            uint32_t* w = bm + (id >> 5);
+            const uint32_t bit = 1u << (id & 31);
+            if (!(*(volatile uint32_t*)w & bit)) atomicOr(w, bit);
+          }
+        }
+        pre = (pre << bits) | rk(std::integral_constant<int, 8 + T>{});
+      });
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < nwords; i += blockDim.x) {
+      uint32_t x = bm[i];
+      if (x) {
+        bm[i] = 0;
+        do {
+          atomicAdd(compact + i * 32 + (__ffs(x) - 1), 1u);
+          x &= x - 1;
+        } while (x);
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // table[p * 256 + alpha[r]] += compact[p * A + r]
 template <typename CT>
 __global__ void k_expand_compact(const uint32_t* __restrict__ compact, uint64_t n, uint32_t A,
@@ -1197,11 +1274,27 @@ template <typename CT>
 void count_once_direct(const DevCorpus& c, uint32_t L, const RouteParams& rp,
                        const uint32_t* seqs, uint32_t nseqs, const uint8_t* arank,
                        const uint8_t* alpha, uint32_t A, uint64_t K, uint32_t* compact, CT* table,
-                       int num_sms, cudaStream_t st) {
+                       int num_sms, cudaStream_t st, const uint16_t* lut, uint32_t lut_n,
+                       uint32_t bits) {
   const uint64_t nbits = K * A;
   const uint32_t nwords = (uint32_t)((nbits + 31) / 32);
   IGB_CUDA(cudaMemsetAsync(compact, 0, nbits * 4, st));
-  if (nseqs) {
+  if (nseqs && lut) {
+    const size_t smem = align16((size_t)nwords * 4) + 256 + (size_t)lut_n * 2;
+    auto go = [&](auto k) {
+      IGB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      const unsigned grid = (unsigned)std::min<uint64_t>(nseqs, (uint64_t)num_sms);
+      k<<<grid, 1024, smem, st>>>(c, lut, lut_n, bits, seqs, nseqs, arank, A, nwords, compact);
+    };
+    switch (L) {
+      case 4: go(k_once_direct_lut<4>); break;
+      case 5: go(k_once_direct_lut<5>); break;
+      case 6: go(k_once_direct_lut<6>); break;
+      case 7: go(k_once_direct_lut<7>); break;
+      case 8: go(k_once_direct_lut<8>); break;
+      default: throw Error(IG_EINTERNAL, "direct lookup table needs 4 <= j <= 8");
+    }
+  } else if (nseqs) {
     const size_t smem = direct_smem(rp, nbits);
     auto go = [&](auto k) {
       IGB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -1231,12 +1324,14 @@ template void alphabet_mask<unsigned long long>(const unsigned long long*, uint6
 template void count_once_direct<uint32_t>(const DevCorpus&, uint32_t, const RouteParams&,
                                           const uint32_t*, uint32_t, const uint8_t*,
                                           const uint8_t*, uint32_t, uint64_t, uint32_t*,
-                                          uint32_t*, int, cudaStream_t);
+                                          uint32_t*, int, cudaStream_t, const uint16_t*, uint32_t,
+                                          uint32_t);
 template void count_once_direct<unsigned long long>(const DevCorpus&, uint32_t,
                                                     const RouteParams&, const uint32_t*, uint32_t,
                                                     const uint8_t*, const uint8_t*, uint32_t,
                                                     uint64_t, uint32_t*, unsigned long long*, int,
-                                                    cudaStream_t);
+                                                    cudaStream_t, const uint16_t*, uint32_t,
+                                                    uint32_t);
 
 void make_route_params(uint64_t cap, RouteParams& rp) {
   uint32_t lgc = 0;

@@ -500,6 +500,42 @@ static CT* count_pass(Session& s, bool dense, uint32_t L, int mode, const Prefix
     // small alphabet: K' * A candidates in a shared-memory bitmap per sequence
     const uint64_t nbits = P->K * s.alpha_n;
     const size_t est = (nbits + 31) / 32 * 4 + (size_t)P->rp.NO * 4 + 256 + 12 * P->K + 1024;
+    // prefixes as rank-packed indices into a direct table when they fit 16 bits
+    uint32_t bits = 1;
+    while ((1u << bits) < s.alpha_n) ++bits;
+    const uint32_t plen = L - 1;
+    const uint64_t lut_n = bits * plen <= 16 ? (1ull << (bits * plen)) : 0;
+    const bool lut_ok = lut_n && P->K < 0xffff && L >= 4 && !getenv("IG_NO_DIRECT_LUT") &&
+                        (nbits + 31) / 32 * 4 + 256 + lut_n * 2 + 1024 <= kMaxOnceSmem;
+    if (nbits <= (1ull << 20) && lut_ok) {
+      std::vector<uint16_t> lut(lut_n, 0xffff);
+      for (uint64_t pp = 0; pp < P->K; ++pp) {
+        uint32_t ci = 0;
+        for (uint32_t i = 0; i < plen; ++i)
+          ci = (ci << bits) | s.h_arank[(P->pk[pp] >> (8 * (plen - 1 - i))) & 0xffu];
+        lut[ci] = (uint16_t)pp;
+      }
+      uint16_t* dl = s.lut.as<uint16_t>(lut_n);
+      h2d(s, dl, lut.data(), lut_n * 2);
+      tcap = 256 * P->K;
+      CT* t = s.table.as<CT>(tcap);
+      IGB_CUDA(cudaMemsetAsync(t, 0, tcap * sizeof(CT), s.stream));
+      s.rc.have_next = false;
+      if (!s.h_short_w.empty() || !s.h_short_c.empty()) {  // short sequences: route table
+        build_prefix_table(s, *const_cast<Prefix*>(P));
+        short_pass<CT>(s, 1, L, P->rp, t, 0, (uint32_t)s.dc.m);
+      }
+      const uint8_t* ab = static_cast<const uint8_t*>(s.alpha_dev.p) + 32;
+      const size_t ev = s.kt.begin(IG_KF_ROUTE_SCATTER, s.stream);
+      count_once_direct<CT>(s.dc, L, P->rp, static_cast<const uint32_t*>(s.order.p), s.n_long,
+                            ab, ab + 256, s.alpha_n, P->K, s.compact.as<uint32_t>(nbits + 1), t,
+                            s.num_sms, s.stream, dl, (uint32_t)lut_n, bits);
+      s.kt.end(ev, s.stream);
+      s.launches += (s.n_long ? 1 : 0) + 1;
+      km = KeyMap{};
+      km.pkeys = P->pkeys;
+      return t;
+    }
     if (nbits <= (1ull << 20) && est <= kMaxOnceSmem) {
       build_prefix_table(s, *const_cast<Prefix*>(P));
       if (direct_smem(P->rp, nbits) <= kMaxOnceSmem) {
@@ -704,6 +740,7 @@ static void run_t(Session& s, const ig_params& p, ig_result* out) {
       }
     s.alpha_n = std::max<uint32_t>(A, 1);
     if (s.alpha_n <= 16) h2d(s, ad + 32, tab, sizeof(tab));
+    s.h_arank.assign(tab, tab + 256);
   }
   tm.end(ev);
   rows.push_back(make_row(std::to_string(n0) + "-gram pass", n0, total_bytes, dcap, 0, false, ev));
