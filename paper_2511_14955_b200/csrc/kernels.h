@@ -122,7 +122,13 @@ void count_once_direct(const DevCorpus& c, uint32_t L, const RouteParams& rp,
                        const uint32_t* seqs, uint32_t nseqs, const uint8_t* arank,
                        const uint8_t* alpha, uint32_t A, uint64_t K, uint32_t* compact, CT* table,
                        int num_sms, cudaStream_t st, const uint16_t* lut = nullptr,
-                       uint32_t lut_n = 0, uint32_t bits = 0);
+                       uint32_t lut_n = 0, uint32_t bits = 0, bool expand = true);
+// 256-bit mask of the bytes of a corpus.
+void byte_presence(const uint8_t* data, uint64_t n, uint32_t* mask, int num_sms, cudaStream_t st);
+// Dense small-alphabet counts (A^3, mixed radix) added into the permuted dense table.
+template <typename CT>
+void expand_dense(const uint32_t* compact, uint32_t A, const uint8_t* alpha, uint64_t mult,
+                  uint64_t cmask, CT* table, cudaStream_t st);
 // 256-bit mask of the bytes in the nonzero entries of a dense n0-gram table.
 template <typename CT>
 void alphabet_mask(const CT* table, uint64_t cap, uint64_t minv, uint64_t cmask, uint32_t n0,

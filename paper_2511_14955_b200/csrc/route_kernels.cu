@@ -930,6 +930,61 @@ __global__ void k_expand_compact(const uint32_t* __restrict__ compact, uint64_t 
   }
 }
 
+// Bytes present in the corpus (256-bit mask): 16-byte loads, flags in smem.
+__global__ void k_byte_presence(const uint8_t* __restrict__ data, uint64_t n,
+                                uint32_t* __restrict__ mask) {
+  __shared__ uint32_t sm[8];
+  if (threadIdx.x < 8) sm[threadIdx.x] = 0;
+  __syncthreads();
+  uint32_t local[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  const uint64_t n16 = n / 16;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n16;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint4 v = __ldcs(reinterpret_cast<const uint4*>(data) + i);
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const uint32_t by = (w[k >> 2] >> (8 * (k & 3))) & 0xffu;
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if ((by >> 5) == (uint32_t)q) local[q] |= 1u << (by & 31);
+    }
+  }
+  for (uint64_t i = n16 * 16 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t by = data[i];
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if ((by >> 5) == (uint32_t)q) local[q] |= 1u << (by & 31);
+  }
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    uint32_t x = local[q];
+    for (int o = 16; o; o >>= 1) x |= __shfl_xor_sync(0xffffffffu, x, o);
+    if ((threadIdx.x & 31) == 0 && x) atomicOr(sm + q, x);
+  }
+  __syncthreads();
+  if (threadIdx.x < 8 && sm[threadIdx.x]) atomicOr(mask + threadIdx.x, sm[threadIdx.x]);
+}
+
+// Dense count-once over a small alphabet: compact[(r0 * A + r1) * A + r2]
+// counts the 3-gram alpha[r0] alpha[r1] alpha[r2]; added into the dense
+// table at its route permutation (index = key * mult & cmask).
+template <typename CT>
+__global__ void k_expand_dense(const uint32_t* __restrict__ compact, uint32_t A,
+                               const uint8_t* __restrict__ alpha, uint64_t mult, uint64_t cmask,
+                               CT* __restrict__ table) {
+  const uint32_t n = A * A * A;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint32_t v = compact[i];
+    if (v) {
+      const uint32_t r2 = i % A, r1 = (i / A) % A, r0 = i / (A * A);
+      const uint64_t key = ((uint64_t)alpha[r0] << 16) | ((uint64_t)alpha[r1] << 8) | alpha[r2];
+      table[(key * mult) & cmask] += (CT)v;
+    }
+  }
+}
+
 // Byte alphabet of a corpus from its dense count-once n0-gram table: every
 // byte that can end an extension-pass gram lies in some counted n0-gram.
 // index -> key = (index * minv) & cmask (the dense route permutation).
@@ -1275,7 +1330,7 @@ void count_once_direct(const DevCorpus& c, uint32_t L, const RouteParams& rp,
                        const uint32_t* seqs, uint32_t nseqs, const uint8_t* arank,
                        const uint8_t* alpha, uint32_t A, uint64_t K, uint32_t* compact, CT* table,
                        int num_sms, cudaStream_t st, const uint16_t* lut, uint32_t lut_n,
-                       uint32_t bits) {
+                       uint32_t bits, bool expand) {
   const uint64_t nbits = K * A;
   const uint32_t nwords = (uint32_t)((nbits + 31) / 32);
   IGB_CUDA(cudaMemsetAsync(compact, 0, nbits * 4, st));
@@ -1287,12 +1342,13 @@ void count_once_direct(const DevCorpus& c, uint32_t L, const RouteParams& rp,
       k<<<grid, 1024, smem, st>>>(c, lut, lut_n, bits, seqs, nseqs, arank, A, nwords, compact);
     };
     switch (L) {
+      case 3: go(k_once_direct_lut<3>); break;
       case 4: go(k_once_direct_lut<4>); break;
       case 5: go(k_once_direct_lut<5>); break;
       case 6: go(k_once_direct_lut<6>); break;
       case 7: go(k_once_direct_lut<7>); break;
       case 8: go(k_once_direct_lut<8>); break;
-      default: throw Error(IG_EINTERNAL, "direct lookup table needs 4 <= j <= 8");
+      default: throw Error(IG_EINTERNAL, "direct lookup table needs 3 <= j <= 8");
     }
   } else if (nseqs) {
     const size_t smem = direct_smem(rp, nbits);
@@ -1312,10 +1368,32 @@ void count_once_direct(const DevCorpus& c, uint32_t L, const RouteParams& rp,
       default: throw Error(IG_ECONFIG, "gram length above 8 is not supported");
     }
   }
+  if (!expand) return;
   const unsigned g2 = (unsigned)std::min<uint64_t>((nbits + 255) / 256, (uint64_t)num_sms * 8);
   k_expand_compact<CT><<<g2 ? g2 : 1, 256, 0, st>>>(compact, nbits, A, alpha, table);
   IGB_CUDA(cudaGetLastError());
 }
+
+void byte_presence(const uint8_t* data, uint64_t n, uint32_t* mask, int num_sms,
+                   cudaStream_t st) {
+  IGB_CUDA(cudaMemsetAsync(mask, 0, 8 * sizeof(uint32_t), st));
+  if (!n) return;
+  const unsigned grid =
+      (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n / 16 + 255) / 256, (uint64_t)num_sms * 8));
+  k_byte_presence<<<grid, 256, 0, st>>>(data, n, mask);
+  IGB_CUDA(cudaGetLastError());
+}
+
+template <typename CT>
+void expand_dense(const uint32_t* compact, uint32_t A, const uint8_t* alpha, uint64_t mult,
+                  uint64_t cmask, CT* table, cudaStream_t st) {
+  k_expand_dense<CT><<<16, 256, 0, st>>>(compact, A, alpha, mult, cmask, table);
+  IGB_CUDA(cudaGetLastError());
+}
+template void expand_dense<uint32_t>(const uint32_t*, uint32_t, const uint8_t*, uint64_t, uint64_t,
+                                     uint32_t*, cudaStream_t);
+template void expand_dense<unsigned long long>(const uint32_t*, uint32_t, const uint8_t*, uint64_t,
+                                               uint64_t, unsigned long long*, cudaStream_t);
 
 template void alphabet_mask<uint32_t>(const uint32_t*, uint64_t, uint64_t, uint64_t, uint32_t,
                                       uint32_t*, int, cudaStream_t);
@@ -1325,13 +1403,13 @@ template void count_once_direct<uint32_t>(const DevCorpus&, uint32_t, const Rout
                                           const uint32_t*, uint32_t, const uint8_t*,
                                           const uint8_t*, uint32_t, uint64_t, uint32_t*,
                                           uint32_t*, int, cudaStream_t, const uint16_t*, uint32_t,
-                                          uint32_t);
+                                          uint32_t, bool);
 template void count_once_direct<unsigned long long>(const DevCorpus&, uint32_t,
                                                     const RouteParams&, const uint32_t*, uint32_t,
                                                     const uint8_t*, const uint8_t*, uint32_t,
                                                     uint64_t, uint32_t*, unsigned long long*, int,
                                                     cudaStream_t, const uint16_t*, uint32_t,
-                                                    uint32_t);
+                                                    uint32_t, bool);
 
 void make_route_params(uint64_t cap, RouteParams& rp) {
   uint32_t lgc = 0;

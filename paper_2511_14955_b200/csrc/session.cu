@@ -92,6 +92,7 @@ void finish_corpus(Session& s, std::vector<uint64_t>& hoff) {
   uint32_t n_long = 0;
   for (uint64_t q = 0; q < m; ++q) n_long += hoff[q + 1] - hoff[q] > (uint64_t)kShortCtaLen;
   s.n_long = n_long;
+  s.corpus_alpha = -1;  // measured lazily by the first count-once run
   std::vector<RouteUnit> units;
   std::vector<uint32_t> ufirst(m + 1, 0);
   std::vector<uint32_t> sw, sc;
@@ -557,6 +558,59 @@ static CT* count_pass(Session& s, bool dense, uint32_t L, int mode, const Prefix
       }
       // did not fit after all: the route path (its table build is done)
       const_cast<Prefix*>(P)->table_built = true;
+    }
+  }
+  if (mode == IG_MODE_ONCE && dense && L == 3 && s.batches.empty() && !getenv("IG_NO_DIRECT")) {
+    // resident corpus over <= 16 distinct bytes: the dense pass counts the
+    // A^3 possible 3-grams in a per-sequence bitmap too
+    if (s.corpus_alpha < 0) {
+      uint8_t* ad = s.calpha_dev.as<uint8_t>(32 + 512);
+      byte_presence(s.dc.data, s.dc.total, reinterpret_cast<uint32_t*>(ad), s.num_sms, s.stream);
+      s.launches++;
+      uint32_t mask[8];
+      d2h(s, mask, ad, sizeof(mask));
+      uint8_t tab[512];
+      memset(tab, 0, sizeof(tab));
+      uint32_t A = 0;
+      for (uint32_t b = 0; b < 256; ++b)
+        if (mask[b >> 5] >> (b & 31) & 1u) {
+          tab[b] = (uint8_t)std::min<uint32_t>(A, 255);
+          if (A < 256) tab[256 + A] = (uint8_t)b;
+          ++A;
+        }
+      s.corpus_alpha = (int32_t)A;
+      if (A >= 1 && A <= 16) h2d(s, ad + 32, tab, sizeof(tab));
+    }
+    const uint32_t A = (uint32_t)s.corpus_alpha;
+    if (A >= 1 && A <= 16) {
+      RouteParams rp;
+      make_route_params(1ull << 24, rp);
+      uint32_t bits = 1;
+      while ((1u << bits) < A) ++bits;
+      const uint32_t lut_n = 1u << (2 * bits);
+      std::vector<uint16_t> lut(lut_n, 0xffff);
+      for (uint32_t r0 = 0; r0 < A; ++r0)
+        for (uint32_t r1 = 0; r1 < A; ++r1) lut[(r0 << bits) | r1] = (uint16_t)(r0 * A + r1);
+      uint16_t* dl = s.lut.as<uint16_t>(lut_n);
+      h2d(s, dl, lut.data(), (size_t)lut_n * 2);
+      tcap = 1ull << rp.lgc;
+      CT* t = s.table.as<CT>(tcap);
+      IGB_CUDA(cudaMemsetAsync(t, 0, tcap * sizeof(CT), s.stream));
+      s.rc.have_next = false;
+      short_pass<CT>(s, 0, L, rp, t, 0, (uint32_t)s.dc.m);
+      const uint8_t* ab = static_cast<const uint8_t*>(s.calpha_dev.p) + 32;
+      uint32_t* cmp = s.compact.as<uint32_t>((size_t)A * A * A + 1);
+      const size_t ev = s.kt.begin(IG_KF_ROUTE_SCATTER, s.stream);
+      count_once_direct<CT>(s.dc, 3, rp, static_cast<const uint32_t*>(s.order.p), s.n_long, ab,
+                            ab + 256, A, (uint64_t)A * A, cmp, t, s.num_sms, s.stream, dl, lut_n,
+                            bits, /*expand=*/false);
+      expand_dense<CT>(cmp, A, ab + 256, rp.mult, rp.cmask, t, s.stream);
+      s.kt.end(ev, s.stream);
+      s.launches += (s.n_long ? 1 : 0) + 1;
+      km = KeyMap{};
+      km.minv = rp.minv;
+      km.cmask = rp.cmask;
+      return t;
     }
   }
   if (mode == IG_MODE_ONCE) {

@@ -42,21 +42,37 @@ def oracle(name, n, k):
 
 
 @pytest.mark.parametrize("name", ["acgt", "mixed", "hex16"])
-@pytest.mark.parametrize("n,k", [(8, 65536), (6, 300), (5, 20)])
-@pytest.mark.parametrize("direct", [True, False])
-def test_once_small_alphabet_equals_oracle(gpu_lib, name, n, k, direct):
+@pytest.mark.parametrize("n,k", [(8, 65536), (6, 300), (5, 20), (3, 50)])
+@pytest.mark.parametrize("path", ["direct", "direct-chd", "route", "resident"])
+def test_once_small_alphabet_equals_oracle(gpu_lib, name, n, k, path):
+    # direct: the one-shot call (pipelined load: extension passes direct, dense
+    # pass routed); direct-chd: the CHD lookup instead of the rank table;
+    # route: no direct path; resident: Session.load + run, where the dense
+    # pass is direct too (the corpus alphabet is known)
     data, off = corpus(name)
     rc, keys, counts, rows, diag = oracle(name, n, k)
     assert rc == 0
-    old = os.environ.pop("IG_NO_DIRECT", None)
+    env = {"direct-chd": {"IG_NO_DIRECT_LUT": "1"}, "route": {"IG_NO_DIRECT": "1"}}.get(path, {})
+    old = {v: os.environ.get(v) for v in ("IG_NO_DIRECT", "IG_NO_DIRECT_LUT")}
     try:
-        if not direct:
-            os.environ["IG_NO_DIRECT"] = "1"
-        r = ig.run_intergrams(ig.Corpus(data, off), ig.IntergramConfig(n=n, k=k, z=1.5, mode=ONCE))
+        for v in old:
+            os.environ.pop(v, None)
+        os.environ.update(env)
+        icfg = ig.IntergramConfig(n=n, k=k, z=1.5, mode=ONCE)
+        if path == "resident":
+            sess = ig.Session(device=0)
+            sess.load(ig.Corpus(data, off))
+            r = sess.run(icfg)
+            r2 = sess.run(icfg)  # the corpus alphabet is measured once per load
+            sess.close()
+            assert np.array_equal(r2.keys, keys) and np.array_equal(r2.counts, counts)
+        else:
+            r = ig.run_intergrams(ig.Corpus(data, off), icfg)
     finally:
-        os.environ.pop("IG_NO_DIRECT", None)
-        if old is not None:
-            os.environ["IG_NO_DIRECT"] = old
+        for v, x in old.items():
+            os.environ.pop(v, None)
+            if x is not None:
+                os.environ[v] = x
     assert np.array_equal(r.keys, keys) and np.array_equal(r.counts, counts)
     assert r.diagnostics == diag
     assert [p.retained for p in r.passes] == [q["retained"] for q in rows]
