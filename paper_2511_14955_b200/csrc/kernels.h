@@ -123,7 +123,8 @@ void count_once_direct(const DevCorpus& c, uint32_t L, const RouteParams& rp,
                        const uint8_t* alpha, uint32_t A, uint64_t K, uint32_t* compact, CT* table,
                        int num_sms, cudaStream_t st, const uint16_t* lut = nullptr,
                        uint32_t lut_n = 0, uint32_t bits = 0, bool expand = true);
-// 256-bit mask of the bytes of a corpus.
+// 256-bit mask of the bytes of a corpus (mask[0..7]); mask[8] = 1 when the
+// scan stopped early at more than 16 distinct bytes (the mask is then partial).
 void byte_presence(const uint8_t* data, uint64_t n, uint32_t* mask, int num_sms, cudaStream_t st);
 // Dense small-alphabet counts (A^3, mixed radix) added into the permuted dense table.
 template <typename CT>

@@ -938,8 +938,18 @@ __global__ void k_byte_presence(const uint8_t* __restrict__ data, uint64_t n,
   __syncthreads();
   uint32_t local[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   const uint64_t n16 = n / 16;
+  // only "at most 16 distinct bytes" matters to the caller: every 64 steps a
+  // warp checks its bytes so far and the global verdict (mask[8] = 1: more)
+  uint32_t step = 0;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n16;
        i += (uint64_t)gridDim.x * blockDim.x) {
+    if ((++step & 63) == 0) {
+      uint32_t c = 0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) c += __popc(__reduce_or_sync(__activemask(), local[q]));
+      if (c > 16) atomicExch(mask + 8, 1u);
+      if (*(volatile uint32_t*)(mask + 8)) break;
+    }
     const uint4 v = __ldcs(reinterpret_cast<const uint4*>(data) + i);
     const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
@@ -1376,7 +1386,7 @@ void count_once_direct(const DevCorpus& c, uint32_t L, const RouteParams& rp,
 
 void byte_presence(const uint8_t* data, uint64_t n, uint32_t* mask, int num_sms,
                    cudaStream_t st) {
-  IGB_CUDA(cudaMemsetAsync(mask, 0, 8 * sizeof(uint32_t), st));
+  IGB_CUDA(cudaMemsetAsync(mask, 0, 9 * sizeof(uint32_t), st));
   if (!n) return;
   const unsigned grid =
       (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n / 16 + 255) / 256, (uint64_t)num_sms * 8));

@@ -564,10 +564,10 @@ static CT* count_pass(Session& s, bool dense, uint32_t L, int mode, const Prefix
     // resident corpus over <= 16 distinct bytes: the dense pass counts the
     // A^3 possible 3-grams in a per-sequence bitmap too
     if (s.corpus_alpha < 0) {
-      uint8_t* ad = s.calpha_dev.as<uint8_t>(32 + 512);
+      uint8_t* ad = s.calpha_dev.as<uint8_t>(48 + 512);  // mask[9] | pad | arank | alpha
       byte_presence(s.dc.data, s.dc.total, reinterpret_cast<uint32_t*>(ad), s.num_sms, s.stream);
       s.launches++;
-      uint32_t mask[8];
+      uint32_t mask[9];
       d2h(s, mask, ad, sizeof(mask));
       uint8_t tab[512];
       memset(tab, 0, sizeof(tab));
@@ -578,8 +578,8 @@ static CT* count_pass(Session& s, bool dense, uint32_t L, int mode, const Prefix
           if (A < 256) tab[256 + A] = (uint8_t)b;
           ++A;
         }
-      s.corpus_alpha = (int32_t)A;
-      if (A >= 1 && A <= 16) h2d(s, ad + 32, tab, sizeof(tab));
+      s.corpus_alpha = mask[8] ? 257 : (int32_t)A;
+      if (!mask[8] && A >= 1 && A <= 16) h2d(s, ad + 48, tab, sizeof(tab));
     }
     const uint32_t A = (uint32_t)s.corpus_alpha;
     if (A >= 1 && A <= 16) {
@@ -598,7 +598,7 @@ static CT* count_pass(Session& s, bool dense, uint32_t L, int mode, const Prefix
       IGB_CUDA(cudaMemsetAsync(t, 0, tcap * sizeof(CT), s.stream));
       s.rc.have_next = false;
       short_pass<CT>(s, 0, L, rp, t, 0, (uint32_t)s.dc.m);
-      const uint8_t* ab = static_cast<const uint8_t*>(s.calpha_dev.p) + 32;
+      const uint8_t* ab = static_cast<const uint8_t*>(s.calpha_dev.p) + 48;
       uint32_t* cmp = s.compact.as<uint32_t>((size_t)A * A * A + 1);
       const size_t ev = s.kt.begin(IG_KF_ROUTE_SCATTER, s.stream);
       count_once_direct<CT>(s.dc, 3, rp, static_cast<const uint32_t*>(s.order.p), s.n_long, ab,

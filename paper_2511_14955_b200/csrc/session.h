@@ -45,7 +45,7 @@ struct Session {
   uint32_t alpha_n = 256;
   std::vector<uint8_t> h_arank;  // byte -> rank in the alphabet (host)
   int32_t corpus_alpha = -1;      // bytes present in the resident corpus (-1: not measured)
-  DevBuf calpha_dev;              // u32 mask[8] | u8 arank[256] | u8 alpha[256] of the corpus
+  DevBuf calpha_dev;              // u32 mask[9] | pad | u8 arank[256] | u8 alpha[256] (offset 48)
   DevBuf lut;            // u16 [2^(bits*(j-1))] rank-packed prefix -> p
   DevCorpus dc;
   bool loaded = false;
