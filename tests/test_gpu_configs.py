@@ -95,9 +95,12 @@ def test_more_than_2_32_routed_positions_doubling(gpu_lib):
 
 @pytest.mark.parametrize("name,extra,k", [("c2", {"num_seqs": 600, "seq_len": 1 << 20}, 1000),
                                           ("c1", {}, 1024),
-                                          ("c3", {"total": 700 << 20}, 2000)])
+                                          ("c3", {"total": 700 << 20}, 2000),
+                                          ("c4", {"num_seqs": 48}, 65536)])
 def test_pipelined_host_load_equals_resident(gpu_lib, name, extra, k):
-    # ig_session_run_host (batched H2D under the dense pass) == load + run
+    # ig_session_run_host (batched H2D under the dense pass) == load + run.
+    # c4 (4 bytes): the resident run counts its dense pass with the
+    # small-alphabet kernel, the pipelined one routes it
     base = S.CONFIGS[name]
     cfg = S.scaled(base, **extra)
     data, off = S.generate(cfg)
