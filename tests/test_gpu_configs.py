@@ -93,6 +93,28 @@ def test_more_than_2_32_routed_positions_doubling(gpu_lib):
     sess.close()
 
 
+@pytest.mark.slow
+def test_count_all_past_2_32_positions_doubling(gpu_lib):
+    # Count-all over two identical halves totalling > 2^32 bytes: u64 tables,
+    # several < 4 GiB count launches per pass, hit masks across launch
+    # boundaries, the rank bitmap.  Every count doubles and the list stays.
+    cfg = S.scaled(S.CONFIGS["c5"], num_seqs=2100)
+    data, off = S.generate(cfg)
+    half = ig.Corpus(data, off)
+    off2 = np.concatenate([off, off[1:] + off[-1]]).astype(np.uint64)
+    doubled = ig.Corpus(np.concatenate([data, data]), off2)
+    assert int(off2[-1]) > (1 << 32)
+    icfg = ig.IntergramConfig(n=8, k=20000, z=1.5, mode=ig.CountMode.kAll)
+    sess = ig.Session(device=0)
+    sess.load(half)
+    r1 = sess.run(icfg, materialize=False)
+    sess.load(doubled)
+    r2 = sess.run(icfg, materialize=False)
+    sess.close()
+    assert np.array_equal(r2.keys, r1.keys)
+    assert np.array_equal(r2.counts, 2 * r1.counts)
+
+
 @pytest.mark.parametrize("name,extra,k", [("c2", {"num_seqs": 600, "seq_len": 1 << 20}, 1000),
                                           ("c1", {}, 1024),
                                           ("c3", {"total": 700 << 20}, 2000),
