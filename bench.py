@@ -436,7 +436,7 @@ def main():
     # per launch: algorithmic bytes per launch = corpus bytes.
     peak, peak_src = peaks()
     counting = {f: v for f, v in kstats.items()
-                if f in ("route_count", "route_scatter", "count_all") and v[1] > 0}
+                if f in ("route_count", "route_scatter", "count_all", "once_direct") and v[1] > 0}
     dom, (dom_ms, dom_n) = max(counting.items(), key=lambda kv: kv[1][0])
     # count-all splits a pass into < 4 GiB segment launches: normalise to the
     # corpus passes the family covered (one corpus read per counting pass)

@@ -160,6 +160,7 @@ IG_API uint64_t ig_session_launches(const ig_session* s);
 #define IG_KF_COUNT_ALL 3     /* count-all counting kernels               */
 #define IG_KF_SELECT 4        /* canonical top-k selection (all kernels)  */
 #define IG_KF_ONCE_SHORT 5    /* count-once: short sequences, no routing  */
+#define IG_KF_ONCE_DIRECT 6   /* count-once: small-alphabet bitmap passes */
 IG_API void ig_session_set_profiling(ig_session* s, int32_t on);
 IG_API int ig_session_kernel_stats(ig_session* s, double* ms, uint64_t* launches, int32_t n,
                                    int32_t reset);

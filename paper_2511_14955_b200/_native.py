@@ -17,7 +17,7 @@ IG_MODE_ONCE, IG_MODE_ALL = 0, 1
 IG_HOST, IG_DEVICE = 0, 1
 IG_MAX_N = 8
 KERNEL_FAMILIES = ["route_count", "route_scatter", "route_consume", "count_all", "select",
-                   "once_short"]
+                   "once_short", "once_direct"]
 
 
 class ig_corpus(C.Structure):

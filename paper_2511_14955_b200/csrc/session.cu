@@ -527,7 +527,7 @@ static CT* count_pass(Session& s, bool dense, uint32_t L, int mode, const Prefix
         short_pass<CT>(s, 1, L, P->rp, t, 0, (uint32_t)s.dc.m);
       }
       const uint8_t* ab = static_cast<const uint8_t*>(s.alpha_dev.p) + 32;
-      const size_t ev = s.kt.begin(IG_KF_ROUTE_SCATTER, s.stream);
+      const size_t ev = s.kt.begin(IG_KF_ONCE_DIRECT, s.stream);
       count_once_direct<CT>(s.dc, L, P->rp, static_cast<const uint32_t*>(s.order.p), s.n_long,
                             ab, ab + 256, s.alpha_n, P->K, s.compact.as<uint32_t>(nbits + 1), t,
                             s.num_sms, s.stream, dl, (uint32_t)lut_n, bits);
@@ -546,7 +546,7 @@ static CT* count_pass(Session& s, bool dense, uint32_t L, int mode, const Prefix
         s.rc.have_next = false;  // no fused histogram for the pass after this one
         short_pass<CT>(s, 1, L, P->rp, t, 0, (uint32_t)s.dc.m);
         const uint8_t* ab = static_cast<const uint8_t*>(s.alpha_dev.p) + 32;
-        const size_t ev = s.kt.begin(IG_KF_ROUTE_SCATTER, s.stream);
+        const size_t ev = s.kt.begin(IG_KF_ONCE_DIRECT, s.stream);
         count_once_direct<CT>(s.dc, L, P->rp, static_cast<const uint32_t*>(s.order.p), s.n_long,
                               ab, ab + 256, s.alpha_n, P->K, s.compact.as<uint32_t>(nbits + 1),
                               t, s.num_sms, s.stream);
@@ -600,7 +600,7 @@ static CT* count_pass(Session& s, bool dense, uint32_t L, int mode, const Prefix
       short_pass<CT>(s, 0, L, rp, t, 0, (uint32_t)s.dc.m);
       const uint8_t* ab = static_cast<const uint8_t*>(s.calpha_dev.p) + 48;
       uint32_t* cmp = s.compact.as<uint32_t>((size_t)A * A * A + 1);
-      const size_t ev = s.kt.begin(IG_KF_ROUTE_SCATTER, s.stream);
+      const size_t ev = s.kt.begin(IG_KF_ONCE_DIRECT, s.stream);
       count_once_direct<CT>(s.dc, 3, rp, static_cast<const uint32_t*>(s.order.p), s.n_long, ab,
                             ab + 256, A, (uint64_t)A * A, cmp, t, s.num_sms, s.stream, dl, lut_n,
                             bits, /*expand=*/false);
