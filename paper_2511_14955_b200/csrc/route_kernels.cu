@@ -1279,30 +1279,58 @@ static bool mphf_try(const std::vector<uint64_t>& keys, uint32_t nb, uint32_t ns
   for (uint32_t b = 0; b < nb; ++b) ++szoff[maxsz - (boff[b + 1] - boff[b]) + 1];
   for (uint32_t z = 0; z <= maxsz; ++z) szoff[z + 1] += szoff[z];
   for (uint32_t b = 0; b < nb; ++b) order[szoff[maxsz - (boff[b + 1] - boff[b])]++] = b;
-  std::vector<uint8_t> used(nslots, 0);
+  // occupancy bitset (fits L1); a bucket's hashes gathered once, contiguous
+  std::vector<uint64_t> used((nslots + 63) / 64, 0);
   disp.assign(nb, 0);
   slot_of_key.assign(K, 0);
-  uint32_t cand[64];
+  uint32_t cand[64], bs[64], bt[64];
   for (uint32_t b : order) {
     const uint32_t a0 = boff[b], n = boff[b + 1] - a0;
     if (n == 0) break;
     if (n > 64) return false;
+    for (uint32_t t = 0; t < n; ++t) {
+      bs[t] = ks[idx[a0 + t]];
+      bt[t] = kt[idx[a0 + t]];
+    }
+    auto place = [&](uint32_t t, uint32_t d) {
+      return (uint32_t)(((uint64_t)(bs[t] + d * bt[t]) * nslots) >> 32);
+    };
+    auto is_used = [&](uint32_t sl) { return (uint32_t)(used[sl >> 6] >> (sl & 63)) & 1u; };
+    if (n <= 2) {  // most buckets: branch-free tests, one mispredict per bucket
+      uint32_t d = 0;
+      if (n == 1) {
+        while (d < 65536 && is_used(place(0, d))) ++d;
+      } else {
+        for (; d < 65536; ++d) {
+          const uint32_t s0 = place(0, d), s1 = place(1, d);
+          if (!(is_used(s0) | is_used(s1) | (uint32_t)(s0 == s1))) break;
+        }
+      }
+      if (d >= 65536) return false;
+      disp[b] = (uint16_t)d;
+      for (uint32_t t = 0; t < n; ++t) {
+        const uint32_t sl = place(t, d);
+        used[sl >> 6] |= 1ull << (sl & 63);
+        slot_of_key[idx[a0 + t]] = sl;
+      }
+      continue;
+    }
     bool ok = false;
     for (uint32_t d = 0; d < 65536 && !ok; ++d) {
-      ok = true;
-      for (uint32_t t = 0; t < n && ok; ++t) {
-        const uint32_t i = idx[a0 + t];
-        const uint32_t sl = mphf_place(MphfHash{kb[i], ks[i], kt[i]}, d, nslots);
-        if (used[sl]) ok = false;
-        for (uint32_t u = 0; u < t && ok; ++u)
-          if (cand[u] == sl) ok = false;
-        cand[t] = sl;
+      // every test of a trial, then one branch (the loop trip counts repeat)
+      uint32_t bad = 0;
+      for (uint32_t t = 0; t < n; ++t) {
+        cand[t] = place(t, d);
+        bad |= is_used(cand[t]);
       }
+      for (uint32_t t = 1; t < n; ++t)
+        for (uint32_t u = 0; u < t; ++u) bad |= (uint32_t)(cand[u] == cand[t]);
+      ok = !bad;
       if (ok) disp[b] = (uint16_t)d;
     }
     if (!ok) return false;
     for (uint32_t t = 0; t < n; ++t) {
-      used[cand[t]] = 1;
+      used[cand[t] >> 6] |= 1ull << (cand[t] & 63);
       slot_of_key[idx[a0 + t]] = cand[t];
     }
   }
