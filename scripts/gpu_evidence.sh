@@ -1,7 +1,7 @@
 # Round evidence on one B200: GPU suite, smoke, every config's bench line, the
 # c2 launch list, and full ncu captures of the dominant kernels.
 #   bash scripts/gpu_evidence.sh TAG
-TAG=${1:-r11}
+TAG=${1:-r12}
 set -x
 nvidia-smi -L
 timeout 3000 python -m pytest tests -m gpu -q -x 2>&1 | tail -5 > gpurun_out/${TAG}_pytest_gpu.txt
