@@ -6,16 +6,21 @@ input GB/s per top-k n-gram run, and % of the HBM roofline).
 
 A step is one full run_intergrams (every counting pass, every top-k' selection
 and prefix-set build, the final top-k list copied to the host) over the
-config's synthetic corpus.  N=1 runs BASELINE configs[1] (c2: 4096 x 1 MiB
-Zipf-token corpus, n=6, k=10000, count-once).  For N>1 (torchrun, one process
-per GPU) every rank holds its own 4096-sequence shard of the same generator
-(weak scaling) and the per-pass count tables are summed with NCCL all-reduce.
+config's synthetic corpus.  The default workload is BASELINE configs[2] (c3:
+16 GiB lognormal-length Zipf-token corpus, n=8, k=100000, count-all), the
+config the metric's 1/2/4/8-GPU figure is quoted on; it fits one B200.  For
+N>1 (one process per GPU; `--gpus N` without torchrun re-launches itself
+under torch.distributed.run) the fixed corpus is sharded by whole sequences,
+balanced by bytes (strong scaling), and each pass's count table is summed
+with an NCCL all-reduce.
 
 `value` is device-timed with CUDA events on the library's stream with the corpus
 resident in HBM; `e2e` is the same metric through the public session API with
 the corpus in pinned host memory, the H2D copy and the result D2H inside the
 timed region.  `--impl reference` times the reference CPU implementation
-(compiled from its own sources into oracle/_ref) on a bounded sample.
+(compiled from its own sources into oracle/_ref) on the same config: each
+timed step is one complete run over a bounded sample of whole sequences, the
+samples spread evenly over the corpus.
 """
 from __future__ import annotations
 
@@ -188,6 +193,33 @@ def make_collective(rank, world, bytes_total, seqs_total):
 
 # ------------------------------------------------------------------ reference arm
 
+def ref_samples(cfg, nsamples, sample_bytes):
+    """Whole-sequence samples of cfg spread over the corpus: sample i starts at
+    the first sequence at or after byte i*total/nsamples and takes sequences
+    until it holds >= sample_bytes (at least one)."""
+    from paper_2511_14955_b200 import synth as S
+    off = S.offsets(cfg)
+    m, total = off.size - 1, int(off[-1])
+    out = []
+    for i in range(nsamples):
+        q = int(np.searchsorted(off, i * total // nsamples, side="left"))
+        q = min(q, m - 1)
+        e = int(np.searchsorted(off, int(off[q]) + sample_bytes, side="left"))
+        e = max(q + 1, min(e, m))
+        out.append((q, e - q))
+    return out
+
+
+def ref_plan(args, cfg):
+    """(timed steps, bytes per step) of the reference arm: --ref-bytes of the
+    corpus in total, at most --steps samples of >= --ref-min-step bytes each."""
+    from paper_2511_14955_b200 import synth as S
+    total = int(S.offsets(cfg)[-1])
+    budget = min(args.ref_bytes, total)
+    steps = max(1, min(args.steps, budget // args.ref_min_step))
+    return steps, budget // steps
+
+
 def run_reference(args, cfg, rank, world):
     from oracle import oracle as O
     from paper_2511_14955_b200 import synth as S
@@ -201,26 +233,33 @@ def run_reference(args, cfg, rank, world):
     except Exception as e:  # noqa: BLE001
         print(json.dumps({"impl": "reference", "unavailable": f"reference build missing: {e}"}))
         return 0
-    sample_seqs = args.ref_sample
-    data, off = S.generate(cfg, 0, sample_seqs)
-    nbytes = int(off[-1])
-    times = []
-    for i in range(args.warmup + args.steps):
-        rc, keys, counts, rows, diag, secs, err = O.ref_run(data, off, cfg.n, cfg.k, cfg.z,
-                                                            cfg.mode, 0)
+    steps, per = ref_plan(args, cfg)
+    # warm-up: complete runs on a small sample (pages in the library and the
+    # allocator); the timed steps are the spread samples
+    wdata, woff = S.generate(cfg, 0, 1)
+    wdata, woff = wdata[:1 << 20], np.minimum(woff, 1 << 20).astype(np.uint64)
+    for _ in range(args.warmup):
+        O.ref_run(wdata, woff, cfg.n, cfg.k, cfg.z, cfg.mode, 0)
+    nbytes = 0
+    secs = 0.0
+    for q, cnt in ref_samples(cfg, steps, per):
+        data, off = S.generate(cfg, q, cnt)
+        rc, keys, counts, rows, diag, t, err = O.ref_run(data, off, cfg.n, cfg.k, cfg.z,
+                                                         cfg.mode, 0)
         if rc != 0:
             print(json.dumps({"impl": "reference", "unavailable": f"reference failed: {err}"}))
             return 0
-        if i >= args.warmup:
-            times.append(secs)
-    t = sum(times) / len(times)
-    v = nbytes / t / 1e9
-    sample = f"first {sample_seqs} of {cfg.num_seqs or 'all'} sequences ({nbytes} B) of {cfg.name}"
+        nbytes += int(off[-1])
+        secs += t
+        del data
+    v = nbytes / secs / 1e9
+    sample = (f"{steps} complete runs, each over ~{per / 2**30:.2f} GiB of whole sequences "
+              f"spread evenly over the {cfg.name} corpus ({nbytes} B in total), "
+              f"n={cfg.n} k={cfg.k} z={cfg.z} {'once' if cfg.mode == 0 else 'all'}")
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
-            "data": "synthetic (seeded generator, csrc/synth.c)",
-            "config": config_dict(cfg, world),
+            "steps": steps, "warmup": args.warmup, "ms_per_step": secs / steps * 1e3,
+            "higher_is_better": True, "scaling": scaling_of(cfg, args), "vs_baseline": None,
+            "dtype": "u8", "data": DATA, "config": config_dict(cfg, world),
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": kind,
                              "sample": sample},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -228,18 +267,32 @@ def run_reference(args, cfg, rank, world):
     return 0
 
 
+DATA = "synthetic (seeded generator csrc/synth.c; BASELINE shapes)"
+
+
+def scaling_of(cfg, args):
+    return "weak" if args.weak else "strong"
+
+
 def config_dict(cfg, world):
+    """The workload (identical on both arms)."""
+    from paper_2511_14955_b200 import synth as S
+    off = S.offsets(cfg)
     return {"workload": f"{cfg.name}: {cfg.describe()}", "n": cfg.n, "k": cfg.k, "z": cfg.z,
-            "mode": "once" if cfg.mode == 0 else "all",
-            "corpus_bytes_per_gpu": None, "parallelism": f"dp{world} (whole-sequence shards)",
+            "mode": "once" if cfg.mode == 0 else "all", "corpus_bytes": int(off[-1]),
+            "sequences": int(off.size - 1), "counting_passes": max(cfg.n, 3) - 2,
+            "parallelism": f"dp{world} (whole-sequence shards balanced by bytes)",
             "l2": "inputs larger than L2 (corpus >> 126 MB), no flush needed"}
 
 
-def cpu_baseline(cfg, sample_seqs):
-    """The reference CPU path (oracle/_ref) timed on this host, bounded sample."""
+def cpu_baseline(args, cfg):
+    """The reference CPU path (oracle/_ref) timed on this host: one complete
+    run over the first spread sample of the reference arm."""
     from oracle import oracle as O
     from paper_2511_14955_b200 import synth as S
-    data, off = S.generate(cfg, 0, sample_seqs)
+    steps, per = ref_plan(args, cfg)
+    q, cnt = ref_samples(cfg, steps, per)[0]
+    data, off = S.generate(cfg, q, cnt)
     nbytes = int(off[-1])
     try:
         L = O.ref()
@@ -256,8 +309,9 @@ def cpu_baseline(cfg, sample_seqs):
         secs = time.perf_counter() - t0
         kind, cores = "port", 1
     return {"value": nbytes / secs / 1e9, "unit": UNIT, "cores": cores, "kind": kind,
-            "sample": f"first {sample_seqs} sequences ({nbytes} B) of {cfg.name}, "
-                      f"n={cfg.n} k={cfg.k} z={cfg.z} {'once' if cfg.mode == 0 else 'all'}"}
+            "sample": f"one complete run over sequences [{q}, {q + cnt}) ({nbytes} B) of "
+                      f"{cfg.name}, n={cfg.n} k={cfg.k} z={cfg.z} "
+                      f"{'once' if cfg.mode == 0 else 'all'}"}
 
 
 # ------------------------------------------------------------------ our arm
@@ -318,15 +372,33 @@ def pipelined_e2e(args, ig, torch, sess, corpus, icfg, local, coll, bytes_total,
             "runs": runs, "ms_per_run": ms}
 
 
+def relaunch_distributed(n):
+    """`--gpus N` without a torchrun environment: re-run this command as N
+    ranks under torch.distributed.run (one process per GPU, 127.0.0.1)."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={n}", "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.abspath(__file__)] + sys.argv[1:]
+    log("relaunching as", n, "ranks:", " ".join(cmd[1:6]))
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c2")
+    ap.add_argument("--config", default="c3")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--ref-sample", type=int, default=256,
-                    help="sequences of the config the CPU reference is timed on")
+    ap.add_argument("--ref-bytes", type=int, default=1 << 30,
+                    help="corpus bytes the CPU reference processes over its timed steps")
+    ap.add_argument("--ref-min-step", type=int, default=256 << 20,
+                    help="smallest reference sample per timed step (bytes)")
+    ap.add_argument("--weak", action="store_true",
+                    help="weak scaling: every rank holds a full-size shard of the generator")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-depth", type=int, default=2,
@@ -340,6 +412,17 @@ def main():
     from paper_2511_14955_b200 import synth as S
     cfg = S.CONFIGS[args.config]
     rank, world, local = dist_env()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        if args.impl == "ours":
+            import torch
+            have = torch.cuda.device_count()
+            if have < args.gpus:
+                log(f"--gpus {args.gpus} needs {args.gpus} visible GPUs, found {have}")
+                return 2
+        return relaunch_distributed(args.gpus)
+    if "WORLD_SIZE" in os.environ and args.gpus != world:
+        log(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+        return 2
 
     if args.impl == "reference":
         return run_reference(args, cfg, rank, world)
@@ -356,30 +439,38 @@ def main():
     if world > 1 or force_coll:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
-    # ---- this rank's shard: weak scaling, sequences [rank*m, (rank+1)*m)
+    # ---- this rank's shard.  Strong scaling (default): the config's fixed
+    # corpus, whole sequences balanced by bytes.  Weak (--weak): every rank
+    # holds `per` sequences of an N-times larger corpus of the same generator.
     off_all = S.offsets(cfg)
     m_all = off_all.size - 1
-    per = args.seqs or m_all
-    if cfg.kind == S.K_LOGNORMAL or world == 1:
-        # one corpus sharded by bytes (lognormal lengths), or the whole config at N=1
-        first, count = 0, per
-        if world > 1:
-            first, last = ig.shard_range(off_all, rank, world)
-            count = last - first
-        gen_cfg = cfg
-    else:
+    if args.weak and cfg.kind != S.K_LOGNORMAL and world > 1:
+        per = args.seqs or m_all
         gen_cfg = S.scaled(cfg, num_seqs=per * world)
         first, count = rank * per, per
+    else:
+        gen_cfg = cfg
+        if args.seqs:
+            gen_cfg = S.scaled(cfg, num_seqs=args.seqs) if cfg.kind != S.K_LOGNORMAL else cfg
+        off_g = S.offsets(gen_cfg)
+        first, last = ig.shard_range(off_g, rank, world) if world > 1 else (0, off_g.size - 1)
+        if args.seqs and cfg.kind == S.K_LOGNORMAL and world == 1:
+            last = min(last, args.seqs)
+        count = last - first
+    off_gen = S.offsets(gen_cfg)
     t0 = time.time()
-    nbytes = int(S.offsets(gen_cfg)[first + count] - S.offsets(gen_cfg)[first])
-    host = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    nbytes = int(off_gen[first + count] - off_gen[first])
+    host = torch.empty(max(nbytes, 1), dtype=torch.uint8, pin_memory=True)
     data, off = S.generate(gen_cfg, first, count, out=host.numpy())
     log(f"rank {rank}: generated {nbytes / 2**30:.2f} GiB ({count} seqs) in {time.time() - t0:.1f}s")
     off_np = np.ascontiguousarray(off, np.uint64)
-    bytes_total = nbytes * world if cfg.kind != S.K_LOGNORMAL else int(off_all[-1])
-    if world > 1 and cfg.kind == S.K_LOGNORMAL:
-        bytes_total = int(off_all[-1])
-    seqs_total = count * world if cfg.kind != S.K_LOGNORMAL else m_all
+    # totals over all ranks (count-table widths and the metric's bytes)
+    if args.weak and world > 1 and cfg.kind != S.K_LOGNORMAL:
+        bytes_total, seqs_total = nbytes * world, count * world
+    elif world > 1:
+        bytes_total, seqs_total = int(off_gen[-1]), int(off_gen.size - 1)
+    else:
+        bytes_total, seqs_total = nbytes, count
 
     stream = torch.cuda.Stream()
     coll, _cb = (None, None)
@@ -485,7 +576,11 @@ def main():
                "h2d_bytes_per_step": int(nbytes + off_np.nbytes),
                "d2h_bytes_per_step": int(16 * len(r2.keys)), "ms_per_step": e_ms}
         assert np.array_equal(r2.keys, res.keys) and np.array_equal(r2.counts, res.counts)
-        if args.e2e_depth > 1:
+        if args.e2e_depth > 1 and world > 1:
+            # in-flight sessions on separate host threads would issue their
+            # all-reduces on the one default group in a rank-dependent order
+            e2e["pipelined"] = {"skipped": "single-rank only (one NCCL group per process)"}
+        elif args.e2e_depth > 1:
             # one more session per run in flight: only when its HBM fits
             free, total_mem = torch.cuda.mem_get_info()
             used = total_mem - free
@@ -498,19 +593,21 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(cfg, args.ref_sample)
+        cpu = cpu_baseline(args, cfg)
 
     if rank == 0:
         passes_alg = max(cfg.n, 3) - 2
-        cd = config_dict(cfg, world)
-        cd["corpus_bytes_per_gpu"] = nbytes
-        cd["sequences_per_gpu"] = count
-        cd["counting_passes"] = passes_alg
+        cd = config_dict(gen_cfg, world)
+        if args.weak and world > 1:
+            cd["workload"] += f" (weak scaling: {count} sequences per rank)"
+        elif world == 1 and (gen_cfg is not cfg or count != off_gen.size - 1):
+            cd["workload"] += f" (reduced: {count} sequences, {nbytes} B)"
+            cd["corpus_bytes"], cd["sequences"] = nbytes, count
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
-            "data": "synthetic (seeded generator csrc/synth.c; BASELINE shapes)",
+            "higher_is_better": True, "scaling": scaling_of(cfg, args), "vs_baseline": None,
+            "dtype": "u8", "data": DATA,
             "config": cd,
             "hbm_roofline_frac_full_run": (bytes_total * passes_alg / (ms * 1e-3) / 1e9)
             / (world * peak),

@@ -2,22 +2,24 @@
 // (corpus.hpp:23-67; enumeration semantics of src/corpus.cpp:40-152): regular
 // files gathered from all roots and sorted lexicographically by path, then
 // records in file order — whole file, '\n'-separated lines, or fixed-size
-// chunks — or an in-memory list.  Header-only.
+// chunks — or an in-memory list.  File enumeration and record walking are the
+// library's (ingest.cu, over the C ABI); this header only adapts them to the
+// reference's class.
 //
 // GPU extension: materialize() packs the enumeration into one CSR buffer
 // (bytes + offsets) — the layout the C-ABI uploads to HBM.
 #pragma once
 
-#include <algorithm>
 #include <cstdint>
+#include <exception>
 #include <filesystem>
-#include <fstream>
 #include <functional>
 #include <optional>
 #include <string>
 #include <vector>
 
 #include "intergrams/common.hpp"
+#include "intergrams_b200.h"
 
 namespace intergrams {
 
@@ -48,48 +50,58 @@ struct CorpusCSR {
 
 class Corpus {
  public:
+  // File corpora: the library enumerates the roots (ig_file_corpus_list —
+  // the reference's rules, ingest.cu) once here; records are read by the
+  // library on each walk (ig_file_corpus_records).
   explicit Corpus(CorpusSpec spec) : spec_(std::move(spec)) {
-    namespace fs = std::filesystem;
     if (spec_.in_memory.has_value()) return;
-    if (spec_.roots.empty()) throw ConfigError("corpus spec has no roots and no in-memory data");
-    for (const auto& root : spec_.roots) {
-      std::error_code ec;
-      if (fs::is_regular_file(root, ec)) {
-        files_.push_back(root);
-      } else if (fs::is_directory(root, ec)) {
-        if (spec_.recurse) {
-          for (fs::recursive_directory_iterator it(root, ec), end; it != end; it.increment(ec)) {
-            if (ec) throw IoError("cannot traverse directory: " + root.string());
-            if (it->is_regular_file()) files_.push_back(it->path());
-          }
-        } else {
-          for (fs::directory_iterator it(root, ec), end; it != end; it.increment(ec)) {
-            if (ec) throw IoError("cannot traverse directory: " + root.string());
-            if (it->is_regular_file()) files_.push_back(it->path());
-          }
-        }
-      } else {
-        throw ConfigError("corpus root does not exist: " + root.string());
-      }
-    }
-    std::sort(files_.begin(), files_.end(),
-              [](const fs::path& a, const fs::path& b) { return a.native() < b.native(); });
-    files_.erase(std::unique(files_.begin(), files_.end()), files_.end());
+    with_spec([&](const ig_file_corpus& fc) {
+      struct Ctx {
+        std::vector<std::filesystem::path>* out;
+      } ctx{&files_};
+      const ig_file_fn fn = [](const char* path, uint64_t, void* user) -> int {
+        static_cast<Ctx*>(user)->out->emplace_back(path);
+        return 0;
+      };
+      char err[512] = {0};
+      rethrow(ig_file_corpus_list(&fc, fn, &ctx, err, sizeof(err)), err, nullptr);
+    });
   }
 
   // Visits every sequence in enumeration order.
   void for_each(const std::function<void(const Sequence&)>& fn) const {
-    uint64_t next_id = 0;
     if (spec_.in_memory.has_value()) {
       Sequence seq;
+      uint64_t id = 0;
       for (const auto& bytes : *spec_.in_memory) {
-        seq.id = next_id++;
+        seq.id = id++;
         seq.bytes = bytes;
         fn(seq);
       }
       return;
     }
-    for (const auto& path : files_) walk_file(path, next_id, fn);
+    with_spec([&](const ig_file_corpus& fc) {
+      struct Ctx {
+        const std::function<void(const Sequence&)>* fn;
+        Sequence seq;
+        std::exception_ptr ex;
+      } ctx{&fn, {}, nullptr};
+      const ig_record_fn rec = [](uint64_t id, const uint8_t* p, uint64_t n, void* user) -> int {
+        Ctx& c = *static_cast<Ctx*>(user);
+        try {
+          c.seq.id = id;
+          c.seq.bytes.assign(reinterpret_cast<const char*>(p), n);
+          (*c.fn)(c.seq);
+          return 0;
+        } catch (...) {
+          c.ex = std::current_exception();  // rethrown on the caller's side
+          return 1;
+        }
+      };
+      char err[512] = {0};
+      const int rc = ig_file_corpus_records(&fc, rec, &ctx, err, sizeof(err));
+      rethrow(rc, err, ctx.ex);
+    });
   }
 
   CorpusStats stats(size_t n) const {
@@ -117,64 +129,28 @@ class Corpus {
   const CorpusSpec& spec() const { return spec_; }
 
  private:
-  void walk_file(const std::filesystem::path& path, uint64_t& next_id,
-                 const std::function<void(const Sequence&)>& fn) const {
-    constexpr size_t kBlock = 1 << 20;
-    std::ifstream in(path, std::ios::binary);
-    if (!in) throw IoError("cannot open file: " + path.string());
-    Sequence seq;
-    std::string block(kBlock, '\0');
-    if (spec_.line_mode) {
-      std::string carry;
-      for (;;) {
-        in.read(block.data(), static_cast<std::streamsize>(block.size()));
-        const size_t got = static_cast<size_t>(in.gcount());
-        if (in.bad()) throw IoError("read error: " + path.string());
-        size_t start = 0;
-        for (size_t i = 0; i < got; ++i) {
-          if (block[i] == '\n') {
-            seq.id = next_id++;
-            seq.bytes = std::move(carry);
-            seq.bytes.append(block, start, i - start);
-            carry.clear();
-            fn(seq);
-            start = i + 1;
-          }
-        }
-        carry.append(block, start, got - start);
-        if (got < block.size()) break;
-      }
-      if (!carry.empty()) {
-        seq.id = next_id++;
-        seq.bytes = std::move(carry);
-        fn(seq);
-      }
-    } else if (spec_.chunk_size > 0) {
-      for (;;) {
-        std::string chunk(spec_.chunk_size, '\0');
-        in.read(chunk.data(), static_cast<std::streamsize>(spec_.chunk_size));
-        const size_t got = static_cast<size_t>(in.gcount());
-        if (in.bad()) throw IoError("read error: " + path.string());
-        if (got == 0) break;
-        chunk.resize(got);
-        seq.id = next_id++;
-        seq.bytes = std::move(chunk);
-        fn(seq);
-        if (got < spec_.chunk_size) break;
-      }
-    } else {
-      std::string data;
-      for (;;) {
-        in.read(block.data(), static_cast<std::streamsize>(block.size()));
-        const size_t got = static_cast<size_t>(in.gcount());
-        if (in.bad()) throw IoError("read error: " + path.string());
-        data.append(block, 0, got);
-        if (got < block.size()) break;
-      }
-      seq.id = next_id++;
-      seq.bytes = std::move(data);
-      fn(seq);
-    }
+  // The spec as the C ABI's ig_file_corpus (roots as C strings).
+  template <typename F>
+  void with_spec(F&& f) const {
+    std::vector<std::string> roots;
+    for (const auto& r : spec_.roots) roots.push_back(r.string());
+    std::vector<const char*> ptrs;
+    for (const auto& r : roots) ptrs.push_back(r.c_str());
+    ig_file_corpus fc{};
+    fc.roots = ptrs.data();
+    fc.num_roots = ptrs.size();
+    fc.recurse = spec_.recurse ? 1 : 0;
+    fc.line_mode = spec_.line_mode ? 1 : 0;
+    fc.chunk_size = spec_.chunk_size;
+    f(fc);
+  }
+
+  static void rethrow(int rc, const char* err, std::exception_ptr ex) {
+    if (ex) std::rethrow_exception(ex);
+    if (rc == IG_OK) return;
+    if (rc == IG_ECONFIG) throw ConfigError(err);
+    if (rc == IG_EIO) throw IoError(err);
+    throw DeviceError(err);
   }
 
   CorpusSpec spec_;

@@ -50,6 +50,7 @@ extern "C" {
 #define IG_EIO 3
 #define IG_EINTERNAL 4
 #define IG_EINVALID 5
+#define IG_ECALLBACK 6 /* a caller callback asked to stop (its own exception is rethrown by the C++ layer) */
 
 /* CountMode (counting.hpp:19). */
 #define IG_MODE_ONCE 0
@@ -219,6 +220,17 @@ IG_API int ig_session_run_files(ig_session* s, const ig_file_corpus* spec,
 IG_API int ig_session_corpus(ig_session* s, uint8_t* data, uint64_t data_cap, uint64_t* offsets,
                              uint64_t offsets_cap, uint64_t* num_seqs, uint64_t* total_bytes,
                              char* err, size_t err_len);
+/* Host-only: the spec's files in enumeration order, one callback each
+ * (path, size); a nonzero return stops the walk with IG_ECALLBACK. */
+typedef int (*ig_file_fn)(const char* path, uint64_t size, void* user);
+IG_API int ig_file_corpus_list(const ig_file_corpus* spec, ig_file_fn fn, void* user, char* err,
+                               size_t err_len);
+/* Host-only: every record of the spec in enumeration order (Corpus::for_each,
+ * corpus.hpp:51), as (id, bytes, len) views valid during the callback; a
+ * nonzero return stops the walk with IG_ECALLBACK. */
+typedef int (*ig_record_fn)(uint64_t id, const uint8_t* bytes, uint64_t len, void* user);
+IG_API int ig_file_corpus_records(const ig_file_corpus* spec, ig_record_fn fn, void* user,
+                                  char* err, size_t err_len);
 /* Host-only: the files a spec enumerates (count, total bytes). */
 IG_API int ig_file_corpus_files(const ig_file_corpus* spec, uint64_t* num_files,
                                 uint64_t* total_bytes, char* err, size_t err_len);

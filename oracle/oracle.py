@@ -258,8 +258,46 @@ def ref_run(data: np.ndarray, off: np.ndarray, n: int, k: int, z: float, mode: i
                                 grams.ctypes.data, counts.ctypes.data, C.byref(ln), passes, 32,
                                 C.byref(np_), diag, len(diag), C.byref(secs), err, len(err))
     m = ln.value
-    keys = np.array([int.from_bytes(grams[i * n:(i + 1) * n].tobytes(), "big") for i in range(m)],
-                    dtype=np.uint64)
+    g = grams[:m * n].reshape(m, n) if m else np.zeros((0, n), np.uint8)
+    keys = np.zeros(m, np.uint64)
+    for i in range(n):
+        keys = (keys << np.uint64(8)) | g[:, i].astype(np.uint64)
+    rows = [dict(label=passes[i].label.decode(), gram_len=passes[i].gram_len,
+                 seconds=passes[i].seconds, bytes_processed=passes[i].bytes_processed,
+                 candidate_space=passes[i].candidate_space, retained=passes[i].retained,
+                 retained_short=bool(passes[i].retained_short)) for i in range(np_.value)]
+    return (rc, keys, counts[:m], rows, [d for d in diag.value.decode().split("\n") if d],
+            secs.value, err.value.decode())
+
+
+def ref_run_file(path: str, chunk_size: int, n: int, k: int, z: float, mode: int,
+                 workers: int = 0):
+    """ig_ref::run_intergrams over a file corpus (one root; chunk_size records,
+    or whole-file records when 0) -> the same tuple as ref_run."""
+    L = ref()
+    if not hasattr(L, "_file_bound"):
+        L.igref_run_intergrams_file.argtypes = [
+            C.c_char_p, C.c_uint64, C.c_uint32, C.c_uint64, C.c_double, C.c_int, C.c_uint32,
+            C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p, C.c_char_p,
+            C.c_size_t, C.c_void_p, C.c_char_p, C.c_size_t]
+        L._file_bound = True
+    grams = np.zeros(max(k * n, 1), np.uint8)
+    counts = np.zeros(k, np.uint64)
+    ln = C.c_uint64(0)
+    passes = (igref_pass * 32)()
+    np_ = C.c_uint32(0)
+    diag = C.create_string_buffer(4096)
+    err = C.create_string_buffer(512)
+    secs = C.c_double(0)
+    rc = L.igref_run_intergrams_file(path.encode(), chunk_size, n, k, z, mode, workers,
+                                     grams.ctypes.data, counts.ctypes.data, C.byref(ln), passes,
+                                     32, C.byref(np_), diag, len(diag), C.byref(secs), err,
+                                     len(err))
+    m = ln.value
+    g = grams[:m * n].reshape(m, n) if m else np.zeros((0, n), np.uint8)
+    keys = np.zeros(m, np.uint64)
+    for i in range(n):
+        keys = (keys << np.uint64(8)) | g[:, i].astype(np.uint64)
     rows = [dict(label=passes[i].label.decode(), gram_len=passes[i].gram_len,
                  seconds=passes[i].seconds, bytes_processed=passes[i].bytes_processed,
                  candidate_space=passes[i].candidate_space, retained=passes[i].retained,
@@ -298,8 +336,10 @@ def ref_naive(data, off, n: int, mode: int, k: int):
                                 grams.ctypes.data, counts.ctypes.data, C.byref(ln), err, len(err))
     assert rc == 0, err.value
     m = ln.value
-    keys = np.array([int.from_bytes(grams[i * n:(i + 1) * n].tobytes(), "big") for i in range(m)],
-                    dtype=np.uint64)
+    g = grams[:m * n].reshape(m, n) if m else np.zeros((0, n), np.uint8)
+    keys = np.zeros(m, np.uint64)
+    for i in range(n):
+        keys = (keys << np.uint64(8)) | g[:, i].astype(np.uint64)
     return keys, counts[:m]
 
 
@@ -352,8 +392,10 @@ def ref_hashgram(data, off, n: int, k: int, mode: int, buckets: int, seed: int,
                               seed, workers, int(trie), grams.ctypes.data, counts.ctypes.data,
                               C.byref(ln), passes, 8, C.byref(np_), err, len(err))
     m = ln.value
-    keys = np.array([int.from_bytes(grams[i * n:(i + 1) * n].tobytes(), "big") for i in range(m)],
-                    dtype=np.uint64)
+    g = grams[:m * n].reshape(m, n) if m else np.zeros((0, n), np.uint8)
+    keys = np.zeros(m, np.uint64)
+    for i in range(n):
+        keys = (keys << np.uint64(8)) | g[:, i].astype(np.uint64)
     rows = [dict(label=passes[i].label.decode(), gram_len=passes[i].gram_len,
                  seconds=passes[i].seconds, bytes_processed=passes[i].bytes_processed,
                  candidate_space=passes[i].candidate_space, retained=passes[i].retained,

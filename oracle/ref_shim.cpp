@@ -92,8 +92,48 @@ unsigned igref_hardware_concurrency() {
   return hw == 0 ? 1 : hw;
 }
 
-// Runs ig_ref::run_intergrams. grams: k*n bytes (gram i at i*n). seconds:
-// wall time of run_intergrams alone (corpus materialisation excluded).
+// ig_ref::run_intergrams over an already-built corpus: grams k*n bytes (gram
+// i at i*n); seconds = wall time of run_intergrams alone.
+static void run_on(const Corpus& corpus, uint32_t n, uint64_t k, double z, int mode,
+                   uint32_t workers, uint8_t* grams, uint64_t* counts, uint64_t* out_len,
+                   igref_pass* passes, uint32_t max_passes, uint32_t* num_passes, char* diag,
+                   size_t diag_len, double* seconds) {
+  IntergramConfig cfg;
+  cfg.n = n;
+  cfg.k = k;
+  cfg.z = z;
+  cfg.mode = to_mode(mode);
+  cfg.workers = workers ? workers : igref_hardware_concurrency();
+  const auto t0 = std::chrono::steady_clock::now();
+  const IntergramsResult r = run_intergrams(corpus, cfg);
+  const auto t1 = std::chrono::steady_clock::now();
+  if (seconds) *seconds = std::chrono::duration<double>(t1 - t0).count();
+  *out_len = r.topk.size();
+  for (size_t i = 0; i < r.topk.size(); ++i) {
+    std::memcpy(grams + i * n, r.topk[i].gram.data(), n);
+    counts[i] = r.topk[i].count;
+  }
+  uint32_t np = 0;
+  for (const auto& p : r.passes) {
+    if (np >= max_passes) break;
+    igref_pass& o = passes[np++];
+    std::memset(&o, 0, sizeof(o));
+    std::strncpy(o.label, p.label.c_str(), sizeof(o.label) - 1);
+    o.gram_len = static_cast<uint32_t>(p.gram_len);
+    o.seconds = p.seconds;
+    o.bytes_processed = p.bytes_processed;
+    o.candidate_space = p.candidate_space;
+    o.retained = p.retained;
+    o.retained_short = p.retained_short;
+  }
+  *num_passes = np;
+  std::string d;
+  for (const auto& s : r.diagnostics) d += s + "\n";
+  if (diag && diag_len) put_err(diag, diag_len, d.c_str());
+}
+
+// Runs ig_ref::run_intergrams on an in-memory corpus (CSR data/off; the
+// corpus materialisation is excluded from *seconds).
 int igref_run_intergrams(const uint8_t* data, const uint64_t* off, uint64_t m,
                          uint32_t n, uint64_t k, double z, int mode,
                          uint32_t workers, uint8_t* grams, uint64_t* counts,
@@ -103,42 +143,30 @@ int igref_run_intergrams(const uint8_t* data, const uint64_t* off, uint64_t m,
                          size_t err_len) {
   return guarded(err, err_len, [&] {
     const Corpus corpus = make_corpus(data, off, m);
-    IntergramConfig cfg;
-    cfg.n = n;
-    cfg.k = k;
-    cfg.z = z;
-    cfg.mode = to_mode(mode);
-    cfg.workers = workers ? workers : igref_hardware_concurrency();
-    const auto t0 = std::chrono::steady_clock::now();
-    const IntergramsResult r = run_intergrams(corpus, cfg);
-    const auto t1 = std::chrono::steady_clock::now();
-    if (seconds) *seconds = std::chrono::duration<double>(t1 - t0).count();
-    *out_len = r.topk.size();
-    for (size_t i = 0; i < r.topk.size(); ++i) {
-      std::memcpy(grams + i * n, r.topk[i].gram.data(), n);
-      counts[i] = r.topk[i].count;
-    }
-    uint32_t np = 0;
-    for (const auto& p : r.passes) {
-      if (np >= max_passes) break;
-      igref_pass& o = passes[np++];
-      std::memset(&o, 0, sizeof(o));
-      std::strncpy(o.label, p.label.c_str(), sizeof(o.label) - 1);
-      o.gram_len = static_cast<uint32_t>(p.gram_len);
-      o.seconds = p.seconds;
-      o.bytes_processed = p.bytes_processed;
-      o.candidate_space = p.candidate_space;
-      o.retained = p.retained;
-      o.retained_short = p.retained_short;
-    }
-    *num_passes = np;
-    std::string d;
-    for (const auto& s : r.diagnostics) d += s + "\n";
-    if (diag && diag_len) put_err(diag, diag_len, d.c_str());
+    run_on(corpus, n, k, z, mode, workers, grams, counts, out_len, passes, max_passes,
+           num_passes, diag, diag_len, seconds);
   });
 }
 
-// ig_ref::count_dense into table (256^n u64).
+// The same over a file corpus (CorpusSpec: one root, whole-file records or
+// fixed chunk_size records, corpus.cpp:55-119): equal-length configs read as
+// one flat file with chunk_size = the sequence length reproduce the
+// sequence boundaries exactly without a second in-memory copy.
+int igref_run_intergrams_file(const char* root, uint64_t chunk_size, uint32_t n, uint64_t k,
+                              double z, int mode, uint32_t workers, uint8_t* grams,
+                              uint64_t* counts, uint64_t* out_len, igref_pass* passes,
+                              uint32_t max_passes, uint32_t* num_passes, char* diag,
+                              size_t diag_len, double* seconds, char* err, size_t err_len) {
+  return guarded(err, err_len, [&] {
+    CorpusSpec spec;
+    spec.roots.emplace_back(root);
+    spec.chunk_size = chunk_size;
+    const Corpus corpus(std::move(spec));
+    run_on(corpus, n, k, z, mode, workers, grams, counts, out_len, passes, max_passes,
+           num_passes, diag, diag_len, seconds);
+  });
+}
+
 int igref_count_dense(const uint8_t* data, const uint64_t* off, uint64_t m,
                       uint32_t n, int mode, uint32_t workers, uint64_t* table,
                       char* err, size_t err_len) {

@@ -63,6 +63,8 @@ class ig_file_corpus(C.Structure):
 
 IG_ORACLE_GUARD = 256 << 20
 
+FILE_FN = C.CFUNCTYPE(C.c_int, C.c_char_p, C.c_uint64, C.c_void_p)
+RECORD_FN = C.CFUNCTYPE(C.c_int, C.c_uint64, C.c_void_p, C.c_uint64, C.c_void_p)
 ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_uint64, C.c_int32, C.c_void_p, C.c_void_p)
 
 
@@ -116,6 +118,10 @@ SYMBOLS = [
     ("ig_session_corpus", C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64,
                                     C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.c_char_p,
                                     C.c_size_t]),
+    ("ig_file_corpus_list", C.c_int, [C.POINTER(ig_file_corpus), FILE_FN, C.c_void_p,
+                                      C.c_char_p, C.c_size_t]),
+    ("ig_file_corpus_records", C.c_int, [C.POINTER(ig_file_corpus), RECORD_FN, C.c_void_p,
+                                         C.c_char_p, C.c_size_t]),
     ("ig_file_corpus_files", C.c_int, [C.POINTER(ig_file_corpus), C.POINTER(C.c_uint64),
                                        C.POINTER(C.c_uint64), C.c_char_p, C.c_size_t]),
     ("ig_shard_range", None, [C.c_void_p, C.c_uint64, C.c_int32, C.c_int32,

@@ -378,8 +378,8 @@ __global__ void __launch_bounds__(512, 3) k_count_all(DevCorpus c, DevPrefixSet 
   }
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  uint64_t t = c.tile0 + ((blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5);
+  const uint64_t nwarps = (((uint64_t)gridDim.x * blockDim.x) >> 5) * c.tstride;
+  uint64_t t = c.tile0 + ((blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5) * c.tstride;
   if (t < c.ntiles) {
     uint4 v = __ldcs(reinterpret_cast<const uint4*>(c.data + t * kTileBytes + lane * 16));
     uint2 h = make_uint2(0, 0);
@@ -572,7 +572,7 @@ static void launch_all_t(const DevCorpus& c, const DevPrefixSet& ps, CT* table, 
                          cudaStream_t st) {
   if (c.ntiles <= c.tile0) return;
   const int threads = 512;
-  const uint64_t want = ((c.ntiles - c.tile0) * 32 + threads - 1) / threads;
+  const uint64_t want = ((c.ntiles - c.tile0 + c.tstride - 1) / c.tstride * 32 + threads - 1) / threads;
   auto go = [&](auto kern, size_t smem, const uint64_t* pk) {
     IGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per = 0;
@@ -645,6 +645,39 @@ template void launch_count_extend<unsigned long long>(const DevCorpus&, const De
 
 // ------------------------------------------------------------------ prefix set build
 
+// Survivor keys in ascending key order with their selection ranks (count-all
+// prefix numbering p = rank in key order: deterministic on every GPU, and the
+// slices of a hot-gram sweep are then contiguous p ranges).
+__global__ void k_iota(uint32_t* __restrict__ v, uint32_t n) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    v[i] = i;
+}
+
+void sort_keys_by_value(const uint64_t* keys, uint32_t K, uint32_t key_bits, uint64_t* out_keys,
+                        uint32_t* out_ranks, uint32_t* tmp_ranks, DevBuf& tmp, cudaStream_t st) {
+  if (!K) return;
+  k_iota<<<std::min(4096u, (K + 255) / 256), 256, 0, st>>>(tmp_ranks, K);
+  size_t bytes = 0;
+  IGB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys, out_keys, tmp_ranks, out_ranks,
+                                           (int)K, 0, (int)key_bits, st));
+  void* t = tmp.get(bytes);
+  IGB_CUDA(cub::DeviceRadixSort::SortPairs(t, bytes, keys, out_keys, tmp_ranks, out_ranks, (int)K,
+                                           0, (int)key_bits, st));
+}
+
+// bounds[s] = pkeys[K * s / S] (s in 1..S-1), bounds[0] = 0, bounds[S] = ~0.
+__global__ void k_slice_bounds(const uint64_t* __restrict__ pkeys, uint32_t K, uint32_t S,
+                               uint64_t* __restrict__ bounds) {
+  const uint32_t s = threadIdx.x;
+  if (s > S) return;
+  bounds[s] = s == 0 ? 0ull : (s == S ? ~0ull : pkeys[(uint64_t)K * s / S]);
+}
+
+void launch_slice_bounds(const uint64_t* pkeys, uint32_t K, uint32_t S, uint64_t* bounds,
+                         cudaStream_t st) {
+  k_slice_bounds<<<1, 32, 0, st>>>(pkeys, K, S, bounds);
+}
+
 // Pass 1: owner of every survivor key and per-owner sizes.
 __global__ void k_prefix_owner(const uint64_t* __restrict__ keys, uint32_t K, uint32_t plen,
                                uint32_t G, uint32_t* __restrict__ owner,
@@ -665,7 +698,7 @@ __global__ void k_prefix_insert(const uint64_t* __restrict__ keys, uint32_t K,
                                 uint32_t* __restrict__ cursor, uint32_t S, uint32_t lgS,
                                 uint64_t* __restrict__ hkeys, uint32_t* __restrict__ hidx,
                                 uint64_t* __restrict__ pkeys, uint32_t* __restrict__ rank_of_p,
-                                bool S_single) {
+                                bool S_single, const uint32_t* __restrict__ ranks) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < K; i += gridDim.x * blockDim.x) {
     const uint32_t o = owner[i];
     // single slice (count-all): p = rank, identical on every rank of a
@@ -673,7 +706,7 @@ __global__ void k_prefix_insert(const uint64_t* __restrict__ keys, uint32_t K,
     const uint32_t p = S_single ? i : owner_start[o] + atomicAdd(cursor + o, 1u);
     const uint64_t key = keys[i];
     pkeys[p] = key;
-    rank_of_p[p] = i;
+    rank_of_p[p] = ranks ? ranks[i] : i;
     unsigned long long* kk = reinterpret_cast<unsigned long long*>(hkeys + (size_t)o * S);
     uint32_t h = hash_slot(key, lgS);
     for (;;) {
@@ -699,12 +732,12 @@ void launch_prefix_owner(const uint64_t* keys, uint32_t K, uint32_t plen, uint32
 void launch_prefix_insert(const uint64_t* keys, uint32_t K, const uint32_t* owner,
                           const uint32_t* owner_start, uint32_t* cursor, uint32_t S, uint32_t lgS,
                           uint64_t* hkeys, uint32_t* hidx, uint64_t* pkeys, uint32_t* rank_of_p,
-                          cudaStream_t st) {
+                          cudaStream_t st, const uint32_t* ranks) {
   if (!K) return;
   const unsigned blocks = (K + 255) / 256;
   k_prefix_insert<<<blocks < 4096 ? blocks : 4096, 256, 0, st>>>(
       keys, K, owner, owner_start, cursor, S, lgS, hkeys, hidx, pkeys, rank_of_p,
-      owner_start == nullptr);
+      owner_start == nullptr, ranks);
 }
 
 }  // namespace igb

@@ -1,0 +1,461 @@
+// hot_kernels.cu — count-all passes with sampled hot-gram tables in shared
+// memory.
+//
+// Reference semantics are those of count_kernels.cu (count-all:
+// pipeline.hpp:106-113, counts[id] += 1 per occurrence; extension pass:
+// proj/src/intergrams.cpp:44-66, id = p * 256 + last byte when the (j-1)-byte
+// prefix is survivor p).  Only the way the additions reach the table changes:
+//
+//   1. sample  — 1/64 of the 512-byte tiles (t % 64 == 0) are counted by the
+//                plain kernel into a scratch table (thrown away after step 2;
+//                the sweeps count every tile, sampled ones included).
+//   2. select  — per slice of the table's id range, the ids with the largest
+//                sample counts become that slice's hot set (a semi-log
+//                histogram picks a threshold; at most 2 candidates per slot).
+//   3. build   — each slice's hot grams go into NB two-way buckets, the two
+//                hottest keys of a bucket winning it (64-bit atomicMax on
+//                (count << 32 | id)).  An empty slot holds a key whose own
+//                bucket is a different one, so no query can ever match it.
+//   4. sweep   — every tile, once per slice: the CTA keeps its slice's
+//                bucket keys (16 B per bucket, one LDS.128 per lookup) and
+//                u32 counters in shared memory.  A gram found there is one
+//                shared-memory atomic — for an extension pass a hot gram's
+//                prefix is known to be a survivor, so the L2 prefix probe is
+//                skipped too.  Every other gram takes the plain path (prefix
+//                probe + one RED to L2).  A slice is a contiguous id range,
+//                so the REDs of one sweep touch 1/S of the table (kept under
+//                the L2 knee).  CTAs flush their counters with one RED per
+//                nonzero slot when they retire.
+//
+// Which grams are hot changes nothing but speed: every occurrence is counted
+// exactly once, in shared memory or in L2, and the final table is the same
+// integer table as the plain kernel's (tests/test_gpu_count_all_paths.py runs
+// both against the oracle).
+#include <cub/cub.cuh>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <cstdlib>
+
+#include "ig_internal.cuh"
+#include "kernels.h"
+
+namespace igb {
+
+constexpr uint64_t kHotMul = 0xA24BAED4963EE407ull;  // bucket hash (odd)
+constexpr int kHotBins = 128;                        // semi-log count bins
+
+__host__ __device__ __forceinline__ uint32_t hot_bucket(uint64_t key, uint32_t lgnb) {
+  return (uint32_t)((key * kHotMul) >> (64 - lgnb));
+}
+
+// Semi-log bin of a count c >= 1: 2 * floor(log2 c) + the next bit.
+__device__ __forceinline__ uint32_t hot_bin(uint64_t c) {
+  const uint32_t bl = 63 - __clzll(c);
+  const uint32_t nx = bl ? (uint32_t)((c >> (bl - 1)) & 1) : 0;
+  return 2 * bl + nx;
+}
+
+struct HotKeyFn {
+  const uint64_t* pkeys;  // nullptr: key = id (dense pass)
+  __device__ __forceinline__ uint64_t operator()(uint64_t id) const {
+    return pkeys ? ((__ldg(pkeys + (id >> 8)) << 8) | (id & 255)) : id;
+  }
+};
+
+__device__ __forceinline__ uint32_t slice_of(uint64_t id, const HotSliceIds& sl) {
+  uint32_t s = 0;
+#pragma unroll
+  for (int i = 1; i < kMaxHotSlices; ++i)
+    if (i < (int)sl.S && id >= sl.lo[i]) s = i;
+  return s;
+}
+
+// ---------------------------------------------------------------- select
+
+template <typename CT>
+__global__ void k_hot_hist(const CT* __restrict__ t, uint64_t cap, HotSliceIds sl,
+                           uint32_t* __restrict__ hist) {
+  __shared__ uint32_t h[kMaxHotSlices * kHotBins];
+  for (int i = threadIdx.x; i < kMaxHotSlices * kHotBins; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < cap;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t c = t[i];
+    if (c) atomicAdd(&h[slice_of(i, sl) * kHotBins + hot_bin(c)], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kMaxHotSlices * kHotBins; i += blockDim.x)
+    if (h[i]) atomicAdd(&hist[i], h[i]);
+}
+
+// One thread per slice: the lowest bin whose cumulative (from the top) stays
+// within `cap` candidates, except that the top bin is always taken.
+__global__ void k_hot_thresh(const uint32_t* __restrict__ hist, uint32_t S, uint32_t cap,
+                             uint32_t* __restrict__ thr) {
+  const uint32_t s = threadIdx.x;
+  if (s >= S) return;
+  uint64_t cum = 0;
+  uint32_t b = kHotBins;
+  while (b > 0) {
+    const uint32_t n = hist[s * kHotBins + b - 1];
+    if (n && cum + n > cap && cum) break;
+    cum += n;
+    --b;
+    if (cum >= cap) break;
+  }
+  thr[s] = b;
+}
+
+template <typename CT>
+__global__ void k_hot_collect(const CT* __restrict__ t, uint64_t cap, HotSliceIds sl,
+                              const uint32_t* __restrict__ thr, uint32_t ccap,
+                              uint32_t* __restrict__ ncand, unsigned long long* __restrict__ cand) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < cap;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t c = t[i];
+    if (!c) continue;
+    const uint32_t s = slice_of(i, sl);
+    if (hot_bin(c) < thr[s]) continue;
+    const uint32_t pos = atomicAdd(&ncand[s], 1u);
+    if (pos < ccap)
+      cand[(uint64_t)s * ccap + pos] =
+          ((unsigned long long)min(c, (uint64_t)0xffffffffu) << 32) | (uint32_t)i;
+  }
+}
+
+// Pass w (0, 1): slot w of each bucket takes the best candidate not already
+// in slot 0.
+__global__ void k_hot_best(const unsigned long long* __restrict__ cand,
+                           const uint32_t* __restrict__ ncand, uint32_t S, uint32_t ccap,
+                           HotKeyFn kf, uint32_t lgnb, int way,
+                           unsigned long long* __restrict__ best) {
+  const uint32_t nb = 1u << lgnb;
+  for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < (uint64_t)S * ccap;
+       g += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t s = (uint32_t)(g / ccap), i = (uint32_t)(g % ccap);
+    if (i >= min(ncand[s], ccap)) continue;
+    const unsigned long long v = cand[g];
+    const uint32_t b = hot_bucket(kf(v & 0xffffffffu), lgnb);
+    unsigned long long* bk = best + ((uint64_t)s * nb + b) * 2;
+    if (way == 1 && bk[0] == v) continue;
+    atomicMax(bk + way, v);
+  }
+}
+
+__global__ void k_hot_fill(const unsigned long long* __restrict__ best, uint32_t S, HotKeyFn kf,
+                           uint32_t lgnb, uint64_t* __restrict__ keys, uint32_t* __restrict__ ids) {
+  const uint32_t nb = 1u << lgnb;
+  for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < (uint64_t)S * nb * 2;
+       g += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t b = (uint32_t)((g >> 1) & (nb - 1));
+    const unsigned long long v = best[g];
+    if (v) {
+      keys[g] = kf(v & 0xffffffffu);
+      ids[g] = (uint32_t)v;
+    } else {
+      // a key this bucket can never be asked for
+      uint64_t k = ~0ull;
+      for (uint64_t c = 0; hot_bucket(k, lgnb) == b; ++c) k = c;
+      keys[g] = k;
+      ids[g] = 0xffffffffu;
+    }
+  }
+}
+
+template <typename CT>
+void build_hot_set(const CT* table, uint64_t cap, const HotSliceIds& sl, const uint64_t* pkeys,
+                   uint32_t lgnb, HotSet& hs, DevBuf& work, int num_sms, cudaStream_t st) {
+  const uint32_t S = sl.S, nb = 1u << lgnb;
+  const uint32_t ccap = 2 * nb * 2;  // candidates per slice: twice the slots
+  // work layout: hist | thr | ncand | cand | best
+  const size_t o_hist = 0, n_hist = (size_t)kMaxHotSlices * kHotBins * 4;
+  const size_t o_thr = o_hist + n_hist, o_nc = o_thr + 64, o_cand = o_nc + 64;
+  const size_t o_best = o_cand + (size_t)S * ccap * 8;
+  const size_t need = o_best + (size_t)S * nb * 2 * 8;
+  char* w = static_cast<char*>(work.get(need));
+  uint32_t* hist = reinterpret_cast<uint32_t*>(w + o_hist);
+  uint32_t* thr = reinterpret_cast<uint32_t*>(w + o_thr);
+  uint32_t* nc = reinterpret_cast<uint32_t*>(w + o_nc);
+  auto* cand = reinterpret_cast<unsigned long long*>(w + o_cand);
+  auto* best = reinterpret_cast<unsigned long long*>(w + o_best);
+  IGB_CUDA(cudaMemsetAsync(w, 0, o_cand, st));
+  IGB_CUDA(cudaMemsetAsync(best, 0, (size_t)S * nb * 2 * 8, st));
+  const unsigned gb = (unsigned)std::min<uint64_t>((cap + 255) / 256, (uint64_t)num_sms * 8);
+  k_hot_hist<CT><<<gb ? gb : 1, 256, 0, st>>>(table, cap, sl, hist);
+  k_hot_thresh<<<1, 32, 0, st>>>(hist, S, ccap / 2, thr);
+  k_hot_collect<CT><<<gb ? gb : 1, 256, 0, st>>>(table, cap, sl, thr, ccap, nc, cand);
+  const HotKeyFn kf{pkeys};
+  const unsigned cb = (unsigned)std::min<uint64_t>(((uint64_t)S * ccap + 255) / 256, 4096);
+  k_hot_best<<<cb, 256, 0, st>>>(cand, nc, S, ccap, kf, lgnb, 0, best);
+  k_hot_best<<<cb, 256, 0, st>>>(cand, nc, S, ccap, kf, lgnb, 1, best);
+  const unsigned fb = (unsigned)std::min<uint64_t>(((uint64_t)S * nb * 2 + 255) / 256, 4096);
+  k_hot_fill<<<fb, 256, 0, st>>>(best, S, kf, lgnb, hs.keys, hs.ids);
+  hs.S = S;
+  hs.lgnb = lgnb;
+}
+
+template void build_hot_set<uint32_t>(const uint32_t*, uint64_t, const HotSliceIds&,
+                                      const uint64_t*, uint32_t, HotSet&, DevBuf&, int,
+                                      cudaStream_t);
+template void build_hot_set<unsigned long long>(const unsigned long long*, uint64_t,
+                                                const HotSliceIds&, const uint64_t*, uint32_t,
+                                                HotSet&, DevBuf&, int, cudaStream_t);
+
+// ---------------------------------------------------------------- sweep
+
+// The 8 bytes before a lane's 16-byte segment + the segment (count_kernels.cu Seg).
+struct HSeg {
+  uint32_t W[7];
+};
+
+template <int T>
+__device__ __forceinline__ uint64_t hkey8_at(const HSeg& s) {
+  constexpr int o = T + 1;
+  constexpr int wi = o / 4, sh = 8 * (o % 4);
+  uint32_t lo, hi;
+  if constexpr (sh == 0) {
+    lo = s.W[wi];
+    hi = s.W[wi + 1];
+  } else {
+    lo = __funnelshift_r(s.W[wi], s.W[wi + 1], sh);
+    hi = __funnelshift_r(s.W[wi + 1], s.W[wi + 2], sh);
+  }
+  return ((uint64_t)__byte_perm(lo, 0, 0x0123) << 32) | (uint64_t)__byte_perm(hi, 0, 0x0123);
+}
+
+template <int L>
+__device__ __forceinline__ uint64_t hgram_mask() {
+  if constexpr (L >= 8) return ~0ull;
+  else return (1ull << (8 * L)) - 1;
+}
+
+template <int B, int E, typename F>
+__device__ __forceinline__ void hstatic_for(F&& f) {
+  if constexpr (B < E) {
+    f(std::integral_constant<int, B>{});
+    hstatic_for<B + 1, E>(f);
+  }
+}
+
+// Validity of a segment that crosses sequence boundaries (count_kernels.cu).
+template <int L>
+__device__ __noinline__ uint32_t hvalid_walk(const uint64_t* __restrict__ off, uint64_t m,
+                                             uint64_t total, uint64_t q, int64_t b0) {
+  if (b0 >= (int64_t)total) return 0;
+  int64_t s0 = (int64_t)off[q], s1 = (int64_t)off[q + 1];
+  while (s1 <= b0 && q + 1 < m) {
+    ++q;
+    s0 = s1;
+    s1 = (int64_t)off[q + 1];
+  }
+  uint32_t vm = 0;
+  for (;;) {
+    const int64_t lo = s0 + L - 1;
+    int64_t a = lo - b0, b = s1 - b0;
+    if (a < 0) a = 0;
+    if (b > 16) b = 16;
+    if (a < b) vm |= ((1u << b) - 1u) & ~((1u << a) - 1u);
+    if (s1 >= b0 + 16 || q + 1 >= m) break;
+    ++q;
+    s0 = s1;
+    s1 = (int64_t)off[q + 1];
+  }
+  return vm;
+}
+
+__device__ __forceinline__ uint32_t hlookup_rank(const uint64_t* __restrict__ rankbits,
+                                                 uint32_t pre) {
+  const ulonglong2 e = __ldg(reinterpret_cast<const ulonglong2*>(rankbits) + (pre >> 6));
+  const uint64_t bit = 1ull << (pre & 63);
+  return (e.x & bit) ? (uint32_t)e.y + (uint32_t)__popcll(e.x & (bit - 1)) : 0xffffffffu;
+}
+
+__device__ __forceinline__ uint32_t hlookup_packed(const uint64_t* __restrict__ tab, uint32_t lgS,
+                                                   uint32_t ib, uint64_t key) {
+  const uint32_t mask = (1u << lgS) - 1;
+  uint32_t h = hash_slot(key, lgS);
+  for (;;) {
+    const uint64_t e = __ldg(tab + h);
+    if (e == kEmptyKey) return 0xffffffffu;
+    if ((e >> ib) == key) return (uint32_t)(e & ((1ull << ib) - 1));
+    h = (h + 1) & mask;
+  }
+}
+
+__device__ __forceinline__ uint32_t hlookup_wide(const uint64_t* __restrict__ wide, uint32_t lgS,
+                                                 uint64_t key) {
+  const uint32_t mask = (1u << lgS) - 1;
+  uint32_t h = hash_slot(key, lgS);
+  for (;;) {
+    const ulonglong2 e = __ldg(reinterpret_cast<const ulonglong2*>(wide) + h);
+    if (e.x == key) return (uint32_t)e.y;
+    if (e.x == kEmptyKey) return 0xffffffffu;
+    h = (h + 1) & mask;
+  }
+}
+
+// KIND 0: dense pass (gram = id).  KIND 1: extension pass; TAB 3 packed
+// global prefix set, 4 {key, p} slots, 5 rank bitmap of 3-byte prefixes.
+// CT: pass table (hot flushes); CC: cold REDs (CT itself, or a u32
+// per-segment scratch when CT is u64).
+template <int KIND, int L, int TAB, typename CT, typename CC>
+__global__ void __launch_bounds__(1024, 1)
+    k_count_hot(DevCorpus c, DevPrefixSet ps, const uint64_t* __restrict__ ptab, HotSweep hw,
+                CT* __restrict__ table, CC* __restrict__ cold) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const uint32_t nb = 1u << hw.lgnb;
+  ulonglong2* skeys = reinterpret_cast<ulonglong2*>(smem_raw);
+  uint32_t* scnt = reinterpret_cast<uint32_t*>(smem_raw + (size_t)nb * 16);
+  {
+    const ulonglong2* gk = reinterpret_cast<const ulonglong2*>(hw.keys);
+    for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) skeys[i] = gk[i];
+    for (uint32_t i = threadIdx.x; i < 2 * nb; i += blockDim.x) scnt[i] = 0;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const uint64_t lo = hw.bounds[0], hi = hw.bounds[1];  // this slice's key range
+  const bool chain = KIND == 1 && ps.hit_in != nullptr;
+  uint64_t t = c.tile0 + ((blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5);
+  if (t < c.ntiles) {
+    // the next tile's loads stay in flight while the current one is counted
+    uint4 v = __ldcs(reinterpret_cast<const uint4*>(c.data + t * kTileBytes + lane * 16));
+    uint2 h = make_uint2(0, 0);
+    if (lane == 0) h = *reinterpret_cast<const uint2*>(c.data + t * kTileBytes - 8);
+    uint32_t d = __ldg(c.tile_seq + t);
+    uint32_t mk = 0xffffffffu;
+    if (chain) {
+      mk = __ldcs(ps.hit_in + t * 32 + lane);
+      mk |= (lane == 0 ? (uint32_t)__ldcs(ps.hit_in + t * 32 - 1) : 0xffffu) << 16;
+    }
+    for (;;) {
+      const uint64_t tn = t + nwarps;
+      uint4 vn = make_uint4(0, 0, 0, 0);
+      uint2 hn = make_uint2(0, 0);
+      uint32_t dn = 0, mkn = 0xffffffffu;
+      if (tn < c.ntiles) {
+        vn = __ldcs(reinterpret_cast<const uint4*>(c.data + tn * kTileBytes + lane * 16));
+        if (lane == 0) hn = *reinterpret_cast<const uint2*>(c.data + tn * kTileBytes - 8);
+        dn = __ldg(c.tile_seq + tn);
+        if (chain) {
+          mkn = __ldcs(ps.hit_in + tn * 32 + lane);
+          mkn |= (lane == 0 ? (uint32_t)__ldcs(ps.hit_in + tn * 32 - 1) : 0xffffu) << 16;
+        }
+      }
+      HSeg s;
+      s.W[2] = v.x;
+      s.W[3] = v.y;
+      s.W[4] = v.z;
+      s.W[5] = v.w;
+      s.W[6] = 0;
+      s.W[0] = __shfl_up_sync(0xffffffffu, v.z, 1);
+      s.W[1] = __shfl_up_sync(0xffffffffu, v.w, 1);
+      if (lane == 0) {
+        s.W[0] = h.x;
+        s.W[1] = h.y;
+      }
+      const int64_t b0 = (int64_t)t * kTileBytes + lane * 16;
+      uint32_t vm = (d >> 31) ? 0xffffu : hvalid_walk<L>(c.off, c.m, c.total, d & 0x7fffffffu, b0);
+      if (chain) {
+        const uint32_t up = __shfl_up_sync(0xffffffffu, mk, 1);
+        vm &= (mk << 1) | (((lane == 0 ? mk >> 16 : up) >> 15) & 1u);
+      }
+      uint32_t hm = 0;
+      hstatic_for<0, 16>([&](auto tc) {
+        constexpr int T = decltype(tc)::value;
+        if ((vm >> T) & 1u) {
+          const uint64_t key = hkey8_at<T>(s) & hgram_mask<L>();
+          const uint64_t sk = KIND == 1 ? key >> 8 : key;
+          if (sk >= lo && sk < hi) {
+            const uint32_t b = hot_bucket(key, hw.lgnb);
+            const ulonglong2 e = skeys[b];
+            const uint32_t slot = e.x == key ? 2 * b : (e.y == key ? 2 * b + 1 : 0xffffffffu);
+            if (slot != 0xffffffffu) {
+              atomicAdd(scnt + slot, 1u);
+              hm |= 1u << T;
+            } else if constexpr (KIND == 0) {
+              atomicAdd(cold + key, (CC)1);
+            } else {
+              uint32_t p;
+              if constexpr (TAB == 3) p = hlookup_packed(ptab, ps.lgS, ps.ib, key >> 8);
+              else if constexpr (TAB == 4) p = hlookup_wide(ptab, ps.lgS, key >> 8);
+              else p = hlookup_rank(ptab, (uint32_t)(key >> 8));
+              if (p != 0xffffffffu) {
+                atomicAdd(cold + ((uint64_t)p * 256 + (uint32_t)(key & 0xff)), (CC)1);
+                hm |= 1u << T;
+              }
+            }
+          }
+        }
+      });
+      if (KIND == 1 && ps.hit_out != nullptr) {
+        uint16_t* w = ps.hit_out + t * 32 + lane;
+        if (hw.first) __stcs(w, (uint16_t)hm);  // slice 0 writes every word
+        else if (hm) *w = (uint16_t)(*w | hm);  // later slices add their bits
+      }
+      if (tn >= c.ntiles) break;
+      t = tn;
+      v = vn;
+      h = hn;
+      d = dn;
+      mk = mkn;
+    }
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < 2 * nb; i += blockDim.x) {
+    const uint32_t n = scnt[i];
+    if (n) atomicAdd(table + hw.ids[i], (CT)n);
+  }
+}
+
+size_t hot_smem(uint32_t lgnb) { return ((size_t)1 << lgnb) * 24; }
+
+template <typename CT, typename CC>
+void launch_count_hot(const DevCorpus& c, const DevPrefixSet& ps, bool dense, uint32_t L,
+                      const HotSweep& hw, CT* table, CC* cold, int num_sms, cudaStream_t st) {
+  if (c.ntiles <= c.tile0) return;
+  const size_t smem = hot_smem(hw.lgnb);
+  const int threads = 1024;
+  auto go = [&](auto kern, const uint64_t* ptab) {
+    IGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per = 0;
+    IGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, threads, smem));
+    const uint64_t want = ((c.ntiles - c.tile0) * 32 + threads - 1) / threads;
+    const uint64_t capb = (uint64_t)num_sms * (per > 0 ? per : 1);
+    const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min(want, capb));
+    kern<<<blocks, threads, smem, st>>>(c, ps, ptab, hw, table, cold);
+  };
+  if (dense) {
+    switch (L) {
+      case 1: go(k_count_hot<0, 1, 0, CT, CC>, nullptr); break;
+      case 2: go(k_count_hot<0, 2, 0, CT, CC>, nullptr); break;
+      default: go(k_count_hot<0, 3, 0, CT, CC>, nullptr); break;
+    }
+    return;
+  }
+#define IGB_HOT_J(J)                                                             \
+  case J:                                                                        \
+    if (J == 4 && ps.rankbits) go(k_count_hot<1, J, 5, CT, CC>, ps.rankbits);    \
+    else if (ps.packed) go(k_count_hot<1, J, 3, CT, CC>, ps.packed);             \
+    else go(k_count_hot<1, J, 4, CT, CC>, ps.wide);                              \
+    break;
+  switch (L) {
+    IGB_HOT_J(2) IGB_HOT_J(3) IGB_HOT_J(4) IGB_HOT_J(5) IGB_HOT_J(6) IGB_HOT_J(7) IGB_HOT_J(8)
+    default: throw Error(IG_ECONFIG, "gram length above 8 is not supported");
+  }
+#undef IGB_HOT_J
+}
+
+template void launch_count_hot<uint32_t, uint32_t>(const DevCorpus&, const DevPrefixSet&, bool,
+                                                   uint32_t, const HotSweep&, uint32_t*,
+                                                   uint32_t*, int, cudaStream_t);
+template void launch_count_hot<unsigned long long, uint32_t>(
+    const DevCorpus&, const DevPrefixSet&, bool, uint32_t, const HotSweep&, unsigned long long*,
+    uint32_t*, int, cudaStream_t);
+template void launch_count_hot<unsigned long long, unsigned long long>(
+    const DevCorpus&, const DevPrefixSet&, bool, uint32_t, const HotSweep&, unsigned long long*,
+    unsigned long long*, int, cudaStream_t);
+
+}  // namespace igb

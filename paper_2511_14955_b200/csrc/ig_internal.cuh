@@ -177,6 +177,7 @@ struct DevCorpus {
   uint64_t total = 0;      // bytes
   uint64_t ntiles = 0;     // tiles [tile0, ntiles) are counted by count-all kernels
   uint64_t tile0 = 0;
+  uint32_t tstride = 1;    // count-all: visit tiles tile0, tile0 + tstride, ... (sampling)
 };
 
 // Device prefix set for an extension pass.

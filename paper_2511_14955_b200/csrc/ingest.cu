@@ -16,6 +16,7 @@
 // positions, from which the host derives the sequence offsets.
 #include <cub/cub.cuh>
 #include <fcntl.h>
+#include <sys/mman.h>
 #include <sys/stat.h>
 #include <unistd.h>
 
@@ -404,6 +405,68 @@ int ig_file_corpus_files(const ig_file_corpus* spec, uint64_t* num_files, uint64
     const FileList fl = enumerate(*spec);
     if (num_files) *num_files = fl.paths.size();
     if (total_bytes) *total_bytes = fl.start.back();
+  });
+}
+
+int ig_file_corpus_list(const ig_file_corpus* spec, ig_file_fn fn, void* user, char* err,
+                        size_t err_len) {
+  return guarded(err, err_len, [&] {
+    if (!spec || !fn) throw Error(IG_ECONFIG, "null corpus spec or callback");
+    const FileList fl = enumerate(*spec);
+    for (size_t f = 0; f < fl.paths.size(); ++f)
+      if (fn(fl.paths[f].c_str(), fl.start[f + 1] - fl.start[f], user) != 0)
+        throw Error(IG_ECALLBACK, "file callback stopped the enumeration");
+  });
+}
+
+int ig_file_corpus_records(const ig_file_corpus* spec, ig_record_fn fn, void* user, char* err,
+                           size_t err_len) {
+  return guarded(err, err_len, [&] {
+    if (!spec || !fn) throw Error(IG_ECONFIG, "null corpus spec or callback");
+    const FileList fl = enumerate(*spec);
+    uint64_t id = 0;
+    auto emit = [&](const uint8_t* p, uint64_t n) {
+      if (fn(id++, p, n, user) != 0) throw Error(IG_ECALLBACK, "record callback stopped the walk");
+    };
+    for (size_t f = 0; f < fl.paths.size(); ++f) {
+      const uint64_t size = fl.start[f + 1] - fl.start[f];
+      // the file mapped read-only; records are views into the mapping
+      const uint8_t* base = nullptr;
+      void* map = nullptr;
+      int fd = ::open(fl.paths[f].c_str(), O_RDONLY);
+      if (fd < 0) throw Error(IG_EIO, "cannot open file: " + fl.paths[f]);
+      if (size) {
+        map = ::mmap(nullptr, size, PROT_READ, MAP_PRIVATE, fd, 0);
+        if (map == MAP_FAILED) {
+          ::close(fd);
+          throw Error(IG_EIO, "read error: " + fl.paths[f]);
+        }
+        ::madvise(map, size, MADV_SEQUENTIAL);
+        base = static_cast<const uint8_t*>(map);
+      }
+      ::close(fd);
+      struct Unmap {
+        void* p;
+        uint64_t n;
+        ~Unmap() {
+          if (p) ::munmap(p, n);
+        }
+      } um{map, size};
+      if (spec->line_mode) {
+        uint64_t a = 0;
+        while (a < size) {
+          const void* nl = memchr(base + a, '\n', size - a);
+          const uint64_t e = nl ? (uint64_t)(static_cast<const uint8_t*>(nl) - base) : size;
+          if (nl || e > a) emit(base + a, e - a);
+          a = e + 1;
+        }
+      } else if (spec->chunk_size) {
+        for (uint64_t a = 0; a < size; a += spec->chunk_size)
+          emit(base + a, std::min<uint64_t>(spec->chunk_size, size - a));
+      } else {
+        emit(base, size);
+      }
+    }
   });
 }
 

@@ -28,7 +28,13 @@ void launch_prefix_owner(const uint64_t* keys, uint32_t K, uint32_t plen, uint32
 void launch_prefix_insert(const uint64_t* keys, uint32_t K, const uint32_t* owner,
                           const uint32_t* owner_start, uint32_t* cursor, uint32_t S, uint32_t lgS,
                           uint64_t* hkeys, uint32_t* hidx, uint64_t* pkeys, uint32_t* rank_of_p,
-                          cudaStream_t st);
+                          cudaStream_t st, const uint32_t* ranks = nullptr);
+// keys[0..K) ascending (key_bits significant bits) with their input indices
+void sort_keys_by_value(const uint64_t* keys, uint32_t K, uint32_t key_bits, uint64_t* out_keys,
+                        uint32_t* out_ranks, uint32_t* tmp_ranks, DevBuf& tmp, cudaStream_t st);
+// bounds[0..S]: 0, pkeys[K*s/S] for 0 < s < S, ~0
+void launch_slice_bounds(const uint64_t* pkeys, uint32_t K, uint32_t S, uint64_t* bounds,
+                         cudaStream_t st);
 
 void launch_widen_add(const uint32_t* src, unsigned long long* dst, uint64_t n, cudaStream_t st);
 // narrowed all-reduce of u64 tables (n % 4 == 0)
@@ -45,6 +51,41 @@ void launch_pack_wide(const DevPrefixSet& ps, uint64_t* wide, cudaStream_t st);
 // pairs): p = rank in key order; writes pkeys[p] = key, rank_of_p[p] = i.
 void launch_rank_prefix(const uint64_t* keys, uint32_t K, uint64_t* rankbits, uint64_t* pkeys,
                         uint32_t* rank_of_p, cudaStream_t st);
+
+// --- count-all with sampled hot-gram tables (hot_kernels.cu)
+constexpr uint32_t kHotSampleStride = 64;  // sample tiles: t % 64 == 0
+constexpr int kMaxHotSlices = 8;
+// Slices of a pass table's id range: slice s = ids [lo[s], lo[s+1]).
+struct HotSliceIds {
+  uint32_t S = 1;
+  uint64_t lo[kMaxHotSlices] = {};
+};
+// Per slice: 2^lgnb two-way buckets of gram keys and their table ids.
+struct HotSet {
+  uint32_t S = 1, lgnb = 0;
+  uint64_t* keys = nullptr;  // [S][2 << lgnb]
+  uint32_t* ids = nullptr;   // [S][2 << lgnb] (~0u: empty slot)
+};
+// One sweep (one slice): its bucket keys/ids, the slice's key range
+// bounds[0] <= key < bounds[1] (the prefix key for extension passes, the
+// gram for the dense pass), and whether this is the first slice (it writes
+// every hit-mask word; later ones OR).
+struct HotSweep {
+  const uint64_t* keys = nullptr;
+  const uint32_t* ids = nullptr;
+  uint32_t lgnb = 0;
+  const uint64_t* bounds = nullptr;  // device, 2 values
+  bool first = true;
+};
+size_t hot_smem(uint32_t lgnb);
+// Hot set of each slice from the (sample) counts in table[0, cap).  pkeys:
+// gram key of id = (pkeys[id >> 8] << 8) | (id & 255), or null (key = id).
+template <typename CT>
+void build_hot_set(const CT* table, uint64_t cap, const HotSliceIds& sl, const uint64_t* pkeys,
+                   uint32_t lgnb, HotSet& hs, DevBuf& work, int num_sms, cudaStream_t st);
+template <typename CT, typename CC>
+void launch_count_hot(const DevCorpus& c, const DevPrefixSet& ps, bool dense, uint32_t L,
+                      const HotSweep& hw, CT* table, CC* cold, int num_sms, cudaStream_t st);
 
 // --- count-once route-then-count (route_kernels.cu)
 struct RouteUnit {  // <= 1 MiB of gram ends of one sequence: byte range [b0, b1)

@@ -243,8 +243,14 @@ static DevPrefixSet build_prefix_set(Session& s, const uint64_t* keys, uint64_t 
   uint64_t* pk = s.pkeys.as<uint64_t>(K + 1);
   uint32_t* rp = s.rank_of_p.as<uint32_t>(K + 1);
   IGB_CUDA(cudaMemsetAsync(hk, 0xff, (size_t)G * S * sizeof(uint64_t), s.stream));
-  launch_prefix_insert(keys, (uint32_t)K, owner, G == 1 ? nullptr : ostart, cursor, S, lgS, hk, hi,
-                       pk, rp, s.stream);
+  // p = rank in key order (deterministic on every GPU; hot-gram slices of
+  // the pass table are then contiguous p ranges)
+  uint64_t* sk = s.sort_keys.as<uint64_t>(K + 1);
+  uint32_t* sr = s.sort_vals.as<uint32_t>(2 * K + 2);
+  sort_keys_by_value(keys, (uint32_t)K, 8 * plen, sk, sr, sr + K + 1, s.sort_tmp, s.stream);
+  s.launches += 2;
+  launch_prefix_insert(sk, (uint32_t)K, owner, G == 1 ? nullptr : ostart, cursor, S, lgS, hk, hi,
+                       pk, rp, s.stream, sr);
   s.launches++;
   ps.pkeys = pk;
   ps.hkeys = hk;
@@ -481,6 +487,114 @@ static void short_pass(Session& s, int kind, uint32_t L, const RouteParams& rp, 
   s.launches += (w.first != w.second) + (c.first != c.second);
 }
 
+// ---- count-all with sampled hot-gram tables
+static constexpr uint64_t kHotMinTiles = 1ull << 16;  // 32 MiB: below, the plain kernel
+
+static uint64_t env_u64(const char* name, uint64_t dflt) {
+  const char* v = getenv(name);
+  return v ? strtoull(v, nullptr, 10) : dflt;
+}
+
+// Tiles per count-all segment of a u64 table (< 2^32 positions each, so the
+// u32 scratch cannot wrap).  IG_SEG_TILES shrinks it for tests.
+static uint64_t seg_tiles() {
+  return std::max<uint64_t>(1, env_u64("IG_SEG_TILES", 0xF0000000ull / kTileBytes));
+}
+
+static bool hot_path_ok(Session& s, bool dense, const Prefix* P) {
+  if (getenv("IG_NO_HOT") || s.dc.ntiles < env_u64("IG_HOT_MIN_TILES", kHotMinTiles)) return false;
+  if (dense) return true;
+  const DevPrefixSet& ps = P->ps;
+  if (ps.packed && (size_t)ps.S * 8 <= 64 * 1024) return false;  // smem-staged: plain kernel
+  return ps.rankbits || ps.packed || ps.wide;
+}
+
+
+template <typename CT>
+static void count_all_hot(Session& s, bool dense, uint32_t L, const Prefix* P, CT* t,
+                          uint64_t tcap) {
+  // slices: the cold REDs of one sweep touch <= IG_HOT_SLICE_MB of table
+  const uint64_t slice_mb = env_u64("IG_HOT_SLICE_MB", 4096);
+  const uint32_t lgnb = (uint32_t)std::max<uint64_t>(6, std::min<uint64_t>(13, env_u64("IG_HOT_LGNB", 13)));
+  const uint64_t cold_bytes = tcap * 4;
+  uint32_t S = 1;
+  while (S < (uint32_t)kMaxHotSlices && cold_bytes > (uint64_t)S * slice_mb * (1ull << 20)) S *= 2;
+  if (getenv("IG_HOT_SLICES"))
+    S = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(kMaxHotSlices, env_u64("IG_HOT_SLICES", 1)));
+  const uint64_t K = dense ? 0 : P->K;
+  if (!dense && S > K) S = 1;
+  HotSliceIds sl;
+  sl.S = S;
+  uint64_t* bounds = s.hot_bounds.as<uint64_t>(kMaxHotSlices + 2);
+  if (dense) {
+    std::vector<uint64_t> b(S + 1);
+    for (uint32_t i = 0; i < S; ++i) b[i] = sl.lo[i] = tcap * i / S;
+    b[S] = ~0ull;
+    h2d(s, bounds, b.data(), (S + 1) * 8);
+  } else {
+    for (uint32_t i = 0; i < S; ++i) sl.lo[i] = 256 * (K * i / S);
+    launch_slice_bounds(P->ps.pkeys, (uint32_t)K, S, bounds, s.stream);
+    s.launches++;
+  }
+  // 1. sample: tiles t % 64 == 0, plain kernel, into a u32 scratch (< 2^32
+  // positions: 1/64 of the corpus); the sweeps below count every tile
+  uint32_t* sample = s.scratch32.as<uint32_t>(tcap);
+  IGB_CUDA(cudaMemsetAsync(sample, 0, tcap * 4, s.stream));
+  {
+    DevCorpus dc = s.dc;
+    dc.tile0 = 0;
+    dc.tstride = kHotSampleStride;
+    DevPrefixSet sps = dense ? DevPrefixSet{} : P->ps;
+    sps.hit_out = nullptr;  // the sweeps write this pass's hit masks
+    const size_t ev = s.kt.begin(IG_KF_COUNT_ALL, s.stream);
+    uint32_t* work = s.work.as<uint32_t>(64);
+    if (dense) launch_count_dense<uint32_t>(dc, L, IG_MODE_ALL, sample, work, s.num_sms, s.stream);
+    else launch_count_extend<uint32_t>(dc, sps, L, IG_MODE_ALL, sample, work, s.num_sms, s.stream);
+    s.kt.end(ev, s.stream);
+    s.launches++;
+  }
+  // 2-3. hot sets of every slice from the sample counts
+  HotSet hs;
+  const size_t slots = (size_t)S * (2u << lgnb);
+  hs.keys = s.hot_keys.as<uint64_t>(slots);
+  hs.ids = s.hot_ids.as<uint32_t>(slots);
+  build_hot_set<uint32_t>(sample, tcap, sl, dense ? nullptr : P->ps.pkeys, lgnb, hs, s.hot_work,
+                          s.num_sms, s.stream);
+  s.launches += 6;
+  // 4. sweeps: per < 2^32-position segment when the table is u64 (cold REDs
+  // into a u32 scratch, widened after the segment), once per slice
+  const DevPrefixSet& ps = dense ? DevPrefixSet{} : P->ps;
+  auto sweep = [&](const DevCorpus& dc, auto* cold) {
+    for (uint32_t i = 0; i < S; ++i) {
+      HotSweep hw;
+      hw.keys = hs.keys + (size_t)i * (2u << lgnb);
+      hw.ids = hs.ids + (size_t)i * (2u << lgnb);
+      hw.lgnb = lgnb;
+      hw.bounds = bounds + i;
+      hw.first = i == 0;
+      const size_t ev = s.kt.begin(IG_KF_COUNT_ALL, s.stream);
+      launch_count_hot(dc, ps, dense, L, hw, t, cold, s.num_sms, s.stream);
+      s.kt.end(ev, s.stream);
+      s.launches++;
+    }
+  };
+  if constexpr (sizeof(CT) == 8) {
+    uint32_t* scratch = s.scratch32.as<uint32_t>(tcap);
+    const uint64_t seg = seg_tiles();
+    for (uint64_t t0 = 0; t0 < s.dc.ntiles; t0 += seg) {
+      DevCorpus dc = s.dc;
+      dc.tile0 = t0;
+      dc.ntiles = std::min<uint64_t>(s.dc.ntiles, t0 + seg);
+      IGB_CUDA(cudaMemsetAsync(scratch, 0, tcap * 4, s.stream));
+      sweep(dc, scratch);
+      launch_widen_add(scratch, t, tcap, s.stream);
+      s.launches++;
+    }
+  } else {
+    sweep(s.dc, t);
+  }
+}
+
 // One counting pass.  Returns the device table (tcap entries) and how table
 // indices map to gram keys.
 template <typename CT>
@@ -668,6 +782,12 @@ static CT* count_pass(Session& s, bool dense, uint32_t L, int mode, const Prefix
   tcap = dense ? (1ull << (8 * L)) : 256 * P->K;
   CT* t = s.table.as<CT>(tcap);
   IGB_CUDA(cudaMemsetAsync(t, 0, tcap * sizeof(CT), s.stream));
+  if (!(dense && !s.batches.empty()) && hot_path_ok(s, dense, P)) {
+    count_all_hot<CT>(s, dense, L, P, t, tcap);
+    km = KeyMap{};
+    if (!dense) km.pkeys = P->ps.pkeys;
+    return t;
+  }
   auto launch = [&](const DevCorpus& dc, auto* tab) {
     using T = std::remove_pointer_t<decltype(tab)>;
     const size_t ev = s.kt.begin(IG_KF_COUNT_ALL, s.stream);
@@ -695,11 +815,11 @@ static CT* count_pass(Session& s, bool dense, uint32_t L, int mode, const Prefix
       // 64-bit totals: count each < 2^32-byte corpus segment into an
       // L2-friendly u32 scratch table, then widen-accumulate into the u64 table
       uint32_t* scratch = s.scratch32.as<uint32_t>(tcap);
-      const uint64_t seg_tiles = (0xF0000000ull / kTileBytes);
-      for (uint64_t t0 = ranges[r].first; t0 < ranges[r].second; t0 += seg_tiles) {
+      const uint64_t seg = seg_tiles();
+      for (uint64_t t0 = ranges[r].first; t0 < ranges[r].second; t0 += seg) {
         DevCorpus dc = s.dc;
         dc.tile0 = t0;
-        dc.ntiles = std::min<uint64_t>(ranges[r].second, t0 + seg_tiles);
+        dc.ntiles = std::min<uint64_t>(ranges[r].second, t0 + seg);
         IGB_CUDA(cudaMemsetAsync(scratch, 0, tcap * 4, s.stream));
         launch(dc, scratch);
         launch_widen_add(scratch, t, tcap, s.stream);
@@ -729,6 +849,7 @@ static uint64_t timed_select(Session& s, const CT* table, uint64_t cap, uint64_t
 // Count-table dtype: u32 whenever no count can reach 2^32 (count-once counts
 // are <= m; count-all counts are <= the corpus bytes), else u64.
 static bool use_u32(Session& s, int mode) {
+  if (getenv("IG_FORCE_U64")) return false;  // tests: the u64 / segment paths on small corpora
   const uint64_t bytes = s.has_coll ? s.coll.bytes_total : s.dc.total;
   const uint64_t seqs = s.has_coll ? s.coll.seqs_total : s.dc.m;
   return mode == IG_MODE_ONCE ? seqs < 0xffffffffull : bytes < 0xffffffffull;

@@ -53,6 +53,8 @@ struct Session {
   // pass buffers
   DevBuf table, work, scratch32;
   DevBuf rankbits;    // count-all 3-byte prefix rank bitmap
+  DevBuf hot_keys, hot_ids, hot_work, hot_bounds;  // count-all hot-gram tables (§3.2e)
+  DevBuf sort_keys, sort_vals, sort_tmp;           // count-all survivors in key order
   DevBuf hitmask[2];  // count-all hit chaining (ping-pong by pass parity)
   DevBuf surv_keys, surv_counts, next_keys, next_counts;
   DevBuf pkeys, hkeys, hidx, hpacked, owner, owner_cnt, owner_start, cursor, rank_of_p;

@@ -119,3 +119,15 @@ def scaled(cfg: Config, num_seqs: int = None, seq_len: int = None, total: int = 
     if total is not None:
         kw["total"] = total
     return replace(cfg, **kw)
+
+
+def fingerprint(data: np.ndarray, off: np.ndarray) -> str:
+    """Cheap corpus fingerprint (sha256 over the offsets and the first 64 bytes
+    of every 1 MiB block) pinning the generator output behind a golden."""
+    import hashlib
+    h = hashlib.sha256(np.ascontiguousarray(off, np.uint64).tobytes())
+    n = int(data.size)
+    if n:
+        idx = (np.arange(0, n, 1 << 20, dtype=np.int64)[:, None] + np.arange(64)[None, :])
+        h.update(np.asarray(data)[np.minimum(idx, n - 1)].tobytes())
+    return h.hexdigest()[:16]

@@ -53,28 +53,61 @@ def oracle(name, k):
     return O.oracle_run(data, off, 8, k, 1.5, int(ALL))
 
 
-@pytest.mark.parametrize("name", ["c5", "c3", "mixed"])
-@pytest.mark.parametrize("k", [40, 5000])  # K' = 60 (shared memory) / 7500 (global, rank bitmap)
-@pytest.mark.parametrize("toggles", [(), ("IG_NO_HIT_CHAIN",), ("IG_NO_RANK_BITMAP",),
-                                     ("IG_NO_HIT_CHAIN", "IG_NO_RANK_BITMAP")])
-def test_count_all_paths_equal_oracle(gpu_lib, name, k, toggles):
-    data, off = corpus(name)
-    rc, keys, counts, rows, diag = oracle(name, k)
-    assert rc == 0
-    saved = {t: os.environ.get(t) for t in toggles}
+# hot-gram sweeps engage from 32 MiB corpora; these force
+# them on the small test corpora, with tiny bucket tables (collisions,
+# empty-slot keys), several slices (hit masks OR-ed across sweeps), and u64
+# tables counted per segment into a u32 scratch (IG_SEG_TILES: many segments)
+HOT = {"IG_HOT_MIN_TILES": "0"}
+HOT_SMALL = {**HOT, "IG_HOT_LGNB": "6", "IG_HOT_SLICES": "4"}
+HOT_U64 = {**HOT, "IG_HOT_SLICES": "2", "IG_FORCE_U64": "1", "IG_SEG_TILES": "1000"}
+TOGGLES = [{}, {"IG_NO_HIT_CHAIN": "1"}, {"IG_NO_RANK_BITMAP": "1"},
+           {"IG_NO_HIT_CHAIN": "1", "IG_NO_RANK_BITMAP": "1"},
+           HOT, HOT_SMALL, HOT_U64, {**HOT_SMALL, "IG_NO_HIT_CHAIN": "1"},
+           {**HOT, "IG_NO_RANK_BITMAP": "1", "IG_HOT_SLICES": "3"},
+           {"IG_FORCE_U64": "1", "IG_SEG_TILES": "777", "IG_NO_HOT": "1"}]
+
+
+def run_with_env(env, fn):
+    saved = {t: os.environ.get(t) for t in env}
     try:
-        for t in toggles:
-            os.environ[t] = "1"
-        r = ig.run_intergrams(ig.Corpus(data, off), ig.IntergramConfig(n=8, k=k, z=1.5, mode=ALL))
+        os.environ.update(env)
+        return fn()
     finally:
         for t, v in saved.items():
             if v is None:
                 os.environ.pop(t, None)
             else:
                 os.environ[t] = v
+
+
+def _id(d):
+    return "-".join(f"{k}={v}" for k, v in d.items()) or "default"
+
+
+@pytest.mark.parametrize("name", ["c5", "c3", "mixed"])
+@pytest.mark.parametrize("k", [40, 5000])  # K' = 60 (shared memory) / 7500 (global, rank bitmap)
+@pytest.mark.parametrize("toggles", TOGGLES, ids=_id)
+def test_count_all_paths_equal_oracle(gpu_lib, name, k, toggles):
+    data, off = corpus(name)
+    rc, keys, counts, rows, diag = oracle(name, k)
+    assert rc == 0
+    r = run_with_env(toggles, lambda: ig.run_intergrams(
+        ig.Corpus(data, off), ig.IntergramConfig(n=8, k=k, z=1.5, mode=ALL)))
     assert np.array_equal(r.keys, keys) and np.array_equal(r.counts, counts)
     assert r.diagnostics == diag
     assert [p.retained for p in r.passes] == [q["retained"] for q in rows]
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 5])
+@pytest.mark.parametrize("toggles", [HOT, HOT_SMALL, HOT_U64], ids=_id)
+def test_hot_sweeps_short_grams_equal_oracle(gpu_lib, n, toggles):
+    # the dense pass alone (n <= 3) and one extension pass (n = 4, 5)
+    data, off = corpus("mixed")
+    rc, keys, counts, rows, diag = O.oracle_run(data, off, n, 3000, 1.5, int(ALL))
+    assert rc == 0
+    r = run_with_env(toggles, lambda: ig.run_intergrams(
+        ig.Corpus(data, off), ig.IntergramConfig(n=n, k=3000, z=1.5, mode=ALL)))
+    assert np.array_equal(r.keys, keys) and np.array_equal(r.counts, counts)
 
 
 def test_extend_pass_rank_bitmap_layout(gpu_lib):
