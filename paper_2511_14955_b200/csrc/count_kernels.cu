@@ -503,10 +503,11 @@ __global__ void k_widen_add(const uint32_t* __restrict__ src, unsigned long long
   }
 }
 
-void launch_widen_add(const uint32_t* src, unsigned long long* dst, uint64_t n, cudaStream_t st) {
+void launch_widen_add(const uint32_t* src, unsigned long long* dst, uint64_t n, int num_sms,
+                      cudaStream_t st) {
   const uint64_t n4 = n / 4;  // table capacities are multiples of 256
   if (!n4) return;
-  const unsigned blocks = (unsigned)std::min<uint64_t>((n4 + 255) / 256, 148 * 16);
+  const unsigned blocks = (unsigned)std::min<uint64_t>((n4 + 255) / 256, (uint64_t)num_sms * 16);
   k_widen_add<<<blocks, 256, 0, st>>>(src, dst, n4);
 }
 
@@ -544,24 +545,26 @@ __global__ void k_widen_set(const uint32_t* __restrict__ src, unsigned long long
 }
 
 void launch_max_u64(const unsigned long long* t, uint64_t n, unsigned long long* out,
-                    cudaStream_t st) {
+                    int num_sms, cudaStream_t st) {
   IGB_CUDA(cudaMemsetAsync(out, 0, sizeof(*out), st));
   if (!n) return;
-  const unsigned blocks = (unsigned)std::min<uint64_t>((n + 255) / 256, 148 * 8);
+  const unsigned blocks = (unsigned)std::min<uint64_t>((n + 255) / 256, (uint64_t)num_sms * 8);
   k_max_u64<<<blocks, 256, 0, st>>>(t, n, out);
 }
 
-void launch_narrow_u64(const unsigned long long* src, uint32_t* dst, uint64_t n, cudaStream_t st) {
+void launch_narrow_u64(const unsigned long long* src, uint32_t* dst, uint64_t n, int num_sms,
+                      cudaStream_t st) {
   const uint64_t n4 = n / 4;
   if (!n4) return;
-  const unsigned blocks = (unsigned)std::min<uint64_t>((n4 + 255) / 256, 148 * 16);
+  const unsigned blocks = (unsigned)std::min<uint64_t>((n4 + 255) / 256, (uint64_t)num_sms * 16);
   k_narrow_u64<<<blocks, 256, 0, st>>>(src, dst, n4);
 }
 
-void launch_widen_set(const uint32_t* src, unsigned long long* dst, uint64_t n, cudaStream_t st) {
+void launch_widen_set(const uint32_t* src, unsigned long long* dst, uint64_t n, int num_sms,
+                      cudaStream_t st) {
   const uint64_t n4 = n / 4;
   if (!n4) return;
-  const unsigned blocks = (unsigned)std::min<uint64_t>((n4 + 255) / 256, 148 * 16);
+  const unsigned blocks = (unsigned)std::min<uint64_t>((n4 + 255) / 256, (uint64_t)num_sms * 16);
   k_widen_set<<<blocks, 256, 0, st>>>(src, dst, n4);
 }
 

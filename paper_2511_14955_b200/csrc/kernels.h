@@ -36,12 +36,15 @@ void sort_keys_by_value(const uint64_t* keys, uint32_t K, uint32_t key_bits, uin
 void launch_slice_bounds(const uint64_t* pkeys, uint32_t K, uint32_t S, uint64_t* bounds,
                          cudaStream_t st);
 
-void launch_widen_add(const uint32_t* src, unsigned long long* dst, uint64_t n, cudaStream_t st);
+void launch_widen_add(const uint32_t* src, unsigned long long* dst, uint64_t n, int num_sms,
+                      cudaStream_t st);
 // narrowed all-reduce of u64 tables (n % 4 == 0)
 void launch_max_u64(const unsigned long long* t, uint64_t n, unsigned long long* out,
-                    cudaStream_t st);
-void launch_narrow_u64(const unsigned long long* src, uint32_t* dst, uint64_t n, cudaStream_t st);
-void launch_widen_set(const uint32_t* src, unsigned long long* dst, uint64_t n, cudaStream_t st);
+                    int num_sms, cudaStream_t st);
+void launch_narrow_u64(const unsigned long long* src, uint32_t* dst, uint64_t n, int num_sms,
+                       cudaStream_t st);
+void launch_widen_set(const uint32_t* src, unsigned long long* dst, uint64_t n, int num_sms,
+                      cudaStream_t st);
 // SM copy to/from mapped pinned host memory (no copy engine)
 void launch_copy(void* dst, const void* src, uint64_t n, cudaStream_t st);
 void launch_pack_prefix(const DevPrefixSet& ps, uint64_t* packed, cudaStream_t st);
@@ -158,9 +161,23 @@ void count_once_short(int kind, uint32_t L, const DevCorpus& c, const RouteParam
 // sequence, a shared-memory bitmap over the K * A candidates that can occur
 // (DESIGN.md §3.2d).  Adds into table (p * 256 + byte layout).
 size_t direct_smem(const RouteParams& rp, uint64_t nbits);
+// Work item of the small-alphabet kernels: byte range `part` of `nparts`
+// equal ranges of long sequence q.  A split sequence (nparts > 1) ORs each
+// part's bitmap into global slot `slot`; the last part to finish counts the
+// union once (so a corpus of a few long sequences still fills every SM).
+struct DirectItem {
+  uint32_t q, part, nparts, slot;
+};
+struct DirectWork {
+  const DirectItem* items = nullptr;
+  uint32_t nitems = 0;
+  uint32_t nsplit = 0;       // split sequences (global bitmap slots)
+  uint32_t* gbm = nullptr;   // [nsplit * nwords] bitmaps, zeroed per launch
+  uint32_t* done = nullptr;  // [nsplit] finished parts, zeroed per launch
+};
 template <typename CT>
 void count_once_direct(const DevCorpus& c, uint32_t L, const RouteParams& rp,
-                       const uint32_t* seqs, uint32_t nseqs, const uint8_t* arank,
+                       const DirectWork& w, const uint8_t* arank,
                        const uint8_t* alpha, uint32_t A, uint64_t K, uint32_t* compact, CT* table,
                        int num_sms, cudaStream_t st, const uint16_t* lut = nullptr,
                        uint32_t lut_n = 0, uint32_t bits = 0, bool expand = true);

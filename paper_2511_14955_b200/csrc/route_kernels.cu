@@ -745,6 +745,15 @@ __global__ void k_owner_totals(const uint32_t* __restrict__ actual, uint32_t nb,
 // Owners heaviest first (one CTA, block radix sort on ~total).  work[0] = 0
 // (the item counter).
 constexpr int kOrderThreads = 1024, kOrderItems = 8;  // <= 8192 owners
+// Owners in index order (the consume fallback for > kOrderThreads *
+// kOrderItems owners or IG_CONSUME_NO_ORDER) and a zeroed item counter.
+__global__ void k_identity_order(uint32_t* __restrict__ ord, uint32_t n,
+                                 uint32_t* __restrict__ work) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) ord[i] = i;
+  if (i == 0) work[0] = 0;
+}
+
 __global__ void __launch_bounds__(kOrderThreads) k_owner_order(const uint32_t* __restrict__ tot,
                                                                 uint32_t NO,
                                                                 uint32_t* __restrict__ order,
@@ -776,13 +785,74 @@ __global__ void __launch_bounds__(kOrderThreads) k_owner_order(const uint32_t* _
 // time: every position's candidate bit is set (test first, then an atomic OR),
 // and at the end of the sequence each set bit adds 1 to compact[p * A + r]
 // and is cleared.  No routing, no dedup cache, no consume pass.
+// Gram ends [lo, hi) of a direct work item: part `part` of `nparts` equal
+// byte ranges of sequence q (the first part starts at the sequence's first
+// complete gram).
+__device__ __forceinline__ void direct_part(const DevCorpus& c, const DirectItem& it, uint32_t L,
+                                            int64_t& lo, int64_t& hi) {
+  const int64_t s0 = (int64_t)c.off[it.q], s1 = (int64_t)c.off[it.q + 1];
+  const int64_t len = s1 - s0;
+  const int64_t a = s0 + (int64_t)((__int128)len * it.part / it.nparts);
+  hi = s0 + (int64_t)((__int128)len * (it.part + 1) / it.nparts);
+  lo = a > s0 + (int64_t)L - 1 ? a : s0 + (int64_t)L - 1;
+  if (lo > hi) lo = hi;
+}
+
+// End of a work item: every set bit of the CTA bitmap counts one sequence.
+// A part of a split sequence ORs its bits into the sequence's global bitmap
+// instead; the last of its parts to arrive (threadfence-reduction order)
+// counts the union and leaves the slot zeroed.
+__device__ __forceinline__ void direct_flush(uint32_t* bm, uint32_t nwords, const DirectItem& it,
+                                             const DirectWork& w, uint32_t* compact,
+                                             uint32_t* s_last) {
+  __syncthreads();
+  if (it.nparts == 1) {
+    for (uint32_t i = threadIdx.x; i < nwords; i += blockDim.x) {
+      uint32_t x = bm[i];
+      if (x) {
+        bm[i] = 0;
+        do {
+          atomicAdd(compact + i * 32 + (__ffs(x) - 1), 1u);
+          x &= x - 1;
+        } while (x);
+      }
+    }
+  } else {
+    uint32_t* g = w.gbm + (size_t)it.slot * nwords;
+    for (uint32_t i = threadIdx.x; i < nwords; i += blockDim.x) {
+      const uint32_t x = bm[i];
+      if (x) {
+        bm[i] = 0;
+        atomicOr(g + i, x);
+      }
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) *s_last = atomicAdd(w.done + it.slot, 1u) == it.nparts - 1;
+    __syncthreads();
+    if (*s_last) {
+      __threadfence();
+      for (uint32_t i = threadIdx.x; i < nwords; i += blockDim.x) {
+        uint32_t x = __ldcg(g + i);
+        if (x) {
+          g[i] = 0;
+          do {
+            atomicAdd(compact + i * 32 + (__ffs(x) - 1), 1u);
+            x &= x - 1;
+          } while (x);
+        }
+      }
+    }
+  }
+  __syncthreads();
+}
+
 constexpr int kDirectThreads = 1024;
 
 template <int L>
 __global__ void __launch_bounds__(kDirectThreads, 1) k_once_direct(
-    DevCorpus c, RouteParams rp, const uint32_t* __restrict__ seqs, uint32_t nseqs,
-    const uint8_t* __restrict__ arank, uint32_t A, uint32_t nwords,
-    uint32_t* __restrict__ compact) {
+    DevCorpus c, RouteParams rp, DirectWork w, const uint8_t* __restrict__ arank, uint32_t A,
+    uint32_t nwords, uint32_t* __restrict__ compact) {
   extern __shared__ uint4 smem4[];
   char* sp = reinterpret_cast<char*>(smem4);
   uint32_t* bm = reinterpret_cast<uint32_t*>(sp);
@@ -798,11 +868,12 @@ __global__ void __launch_bounds__(kDirectThreads, 1) k_once_direct(
   const uint16_t* disp = nullptr;
   const uint64_t* slots = stage_table<1>(rp, s_slots, disp);  // ends with a barrier
   const int lane = threadIdx.x & 31;
-  for (uint32_t qi = blockIdx.x; qi < nseqs; qi += gridDim.x) {
-    const uint32_t q = seqs[qi];
-    const int64_t s0 = (int64_t)c.off[q], s1 = (int64_t)c.off[q + 1];
-    const int64_t lo = s0 + L - 1, hi = s1;
-    const int64_t first = s0 & ~int64_t(15);
+  __shared__ uint32_t s_last;
+  for (uint32_t qi = blockIdx.x; qi < w.nitems; qi += gridDim.x) {
+    const DirectItem it = w.items[qi];
+    int64_t lo, hi;
+    direct_part(c, it, L, lo, hi);
+    const int64_t first = (lo - (L - 1)) & ~int64_t(15);
     const int64_t nseg = (hi - first + 15) >> 4;
     const int64_t nseg_r = (nseg + 31) & ~int64_t(31);  // whole warps (seg_load shuffles)
     for (int64_t sgi = threadIdx.x; sgi < nseg_r; sgi += blockDim.x) {
@@ -824,18 +895,7 @@ __global__ void __launch_bounds__(kDirectThreads, 1) k_once_direct(
         }
       });
     }
-    __syncthreads();
-    for (uint32_t i = threadIdx.x; i < nwords; i += blockDim.x) {
-      uint32_t x = bm[i];
-      if (x) {
-        bm[i] = 0;
-        do {
-          atomicAdd(compact + i * 32 + (__ffs(x) - 1), 1u);
-          x &= x - 1;
-        } while (x);
-      }
-    }
-    __syncthreads();
+    direct_flush(bm, nwords, it, w, compact, &s_last);
   }
 }
 
@@ -845,9 +905,9 @@ __global__ void __launch_bounds__(kDirectThreads, 1) k_once_direct(
 // position, and lut[prefix] is the ordinal p (0xffff: not a survivor).
 template <int L>
 __global__ void __launch_bounds__(1024, 1) k_once_direct_lut(
-    DevCorpus c, const uint16_t* __restrict__ lut, uint32_t lut_n, uint32_t bits,
-    const uint32_t* __restrict__ seqs, uint32_t nseqs, const uint8_t* __restrict__ arank,
-    uint32_t A, uint32_t nwords, uint32_t* __restrict__ compact) {
+    DevCorpus c, const uint16_t* __restrict__ lut, uint32_t lut_n, uint32_t bits, DirectWork w,
+    const uint8_t* __restrict__ arank, uint32_t A, uint32_t nwords,
+    uint32_t* __restrict__ compact) {
   extern __shared__ uint4 smem4[];
   char* sp = reinterpret_cast<char*>(smem4);
   uint32_t* bm = reinterpret_cast<uint32_t*>(sp);
@@ -862,11 +922,12 @@ __global__ void __launch_bounds__(1024, 1) k_once_direct_lut(
   constexpr int PL = L - 1;
   const uint32_t pmask = (1u << (bits * PL)) - 1u;
   const int lane = threadIdx.x & 31;
-  for (uint32_t qi = blockIdx.x; qi < nseqs; qi += gridDim.x) {
-    const uint32_t q = seqs[qi];
-    const int64_t s0 = (int64_t)c.off[q], s1 = (int64_t)c.off[q + 1];
-    const int64_t lo = s0 + L - 1, hi = s1;
-    const int64_t first = s0 & ~int64_t(15);
+  __shared__ uint32_t s_last;
+  for (uint32_t qi = blockIdx.x; qi < w.nitems; qi += gridDim.x) {
+    const DirectItem it = w.items[qi];
+    int64_t lo, hi;
+    direct_part(c, it, L, lo, hi);
+    const int64_t first = (lo - (L - 1)) & ~int64_t(15);
     const int64_t nseg = (hi - first + 15) >> 4;
     const int64_t nseg_r = (nseg + 31) & ~int64_t(31);
     for (int64_t sgi = threadIdx.x; sgi < nseg_r; sgi += blockDim.x) {
@@ -901,18 +962,7 @@ __global__ void __launch_bounds__(1024, 1) k_once_direct_lut(
         pre = (pre << bits) | rk(std::integral_constant<int, 8 + T>{});
       });
     }
-    __syncthreads();
-    for (uint32_t i = threadIdx.x; i < nwords; i += blockDim.x) {
-      uint32_t x = bm[i];
-      if (x) {
-        bm[i] = 0;
-        do {
-          atomicAdd(compact + i * 32 + (__ffs(x) - 1), 1u);
-          x &= x - 1;
-        } while (x);
-      }
-    }
-    __syncthreads();
+    direct_flush(bm, nwords, it, w, compact, &s_last);
   }
 }
 
@@ -1175,13 +1225,8 @@ static void route_stage2_t(RouteCtx& x, const DevCorpus& c, const RouteParams& r
       k_owner_totals<<<rp.NO, 256, 0, st>>>(act, uv.nb, tot);
       k_owner_order<<<1, kOrderThreads, 0, st>>>(tot, rp.NO, ord, work);
       x.launches++;
-    } else {  // identity order
-      std::vector<uint32_t> id(rp.NO + 1);
-      for (uint32_t o = 0; o < rp.NO; ++o) id[o] = o;
-      id[rp.NO] = 0;
-      IGB_CUDA(cudaMemcpyAsync(ord, id.data(), rp.NO * 4, cudaMemcpyHostToDevice, st));
-      IGB_CUDA(cudaMemsetAsync(work, 0, 4, st));
-      IGB_CUDA(cudaStreamSynchronize(st));
+    } else {  // identity order, written on the stream (no host stall)
+      k_identity_order<<<(rp.NO + 255) / 256, 256, 0, st>>>(ord, rp.NO, work);
     }
     x.launches++;
     k<<<grid, kConsumeThreads, smem, st>>>(uv, rp, (uint32_t)sb, (uint32_t)nblocks, base, act,
@@ -1365,19 +1410,24 @@ void alphabet_mask(const CT* table, uint64_t cap, uint64_t minv, uint64_t cmask,
 
 template <typename CT>
 void count_once_direct(const DevCorpus& c, uint32_t L, const RouteParams& rp,
-                       const uint32_t* seqs, uint32_t nseqs, const uint8_t* arank,
+                       const DirectWork& w, const uint8_t* arank,
                        const uint8_t* alpha, uint32_t A, uint64_t K, uint32_t* compact, CT* table,
                        int num_sms, cudaStream_t st, const uint16_t* lut, uint32_t lut_n,
                        uint32_t bits, bool expand) {
   const uint64_t nbits = K * A;
   const uint32_t nwords = (uint32_t)((nbits + 31) / 32);
   IGB_CUDA(cudaMemsetAsync(compact, 0, nbits * 4, st));
+  if (w.nsplit) {
+    IGB_CUDA(cudaMemsetAsync(w.gbm, 0, (size_t)w.nsplit * nwords * 4, st));
+    IGB_CUDA(cudaMemsetAsync(w.done, 0, (size_t)w.nsplit * 4, st));
+  }
+  const uint32_t nseqs = w.nitems;
   if (nseqs && lut) {
     const size_t smem = align16((size_t)nwords * 4) + 256 + (size_t)lut_n * 2;
     auto go = [&](auto k) {
       IGB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       const unsigned grid = (unsigned)std::min<uint64_t>(nseqs, (uint64_t)num_sms);
-      k<<<grid, 1024, smem, st>>>(c, lut, lut_n, bits, seqs, nseqs, arank, A, nwords, compact);
+      k<<<grid, 1024, smem, st>>>(c, lut, lut_n, bits, w, arank, A, nwords, compact);
     };
     switch (L) {
       case 3: go(k_once_direct_lut<3>); break;
@@ -1393,7 +1443,7 @@ void count_once_direct(const DevCorpus& c, uint32_t L, const RouteParams& rp,
     auto go = [&](auto k) {
       IGB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       const unsigned grid = (unsigned)std::min<uint64_t>(nseqs, (uint64_t)num_sms);
-      k<<<grid, kDirectThreads, smem, st>>>(c, rp, seqs, nseqs, arank, A, nwords, compact);
+      k<<<grid, kDirectThreads, smem, st>>>(c, rp, w, arank, A, nwords, compact);
     };
     switch (L) {
       case 2: go(k_once_direct<2>); break;
@@ -1438,12 +1488,12 @@ template void alphabet_mask<uint32_t>(const uint32_t*, uint64_t, uint64_t, uint6
 template void alphabet_mask<unsigned long long>(const unsigned long long*, uint64_t, uint64_t,
                                                 uint64_t, uint32_t, uint32_t*, int, cudaStream_t);
 template void count_once_direct<uint32_t>(const DevCorpus&, uint32_t, const RouteParams&,
-                                          const uint32_t*, uint32_t, const uint8_t*,
+                                          const DirectWork&, const uint8_t*,
                                           const uint8_t*, uint32_t, uint64_t, uint32_t*,
                                           uint32_t*, int, cudaStream_t, const uint16_t*, uint32_t,
                                           uint32_t, bool);
 template void count_once_direct<unsigned long long>(const DevCorpus&, uint32_t,
-                                                    const RouteParams&, const uint32_t*, uint32_t,
+                                                    const RouteParams&, const DirectWork&,
                                                     const uint8_t*, const uint8_t*, uint32_t,
                                                     uint64_t, uint32_t*, unsigned long long*, int,
                                                     cudaStream_t, const uint16_t*, uint32_t,

@@ -186,6 +186,10 @@ uint64_t select_topk(SelectCtx& x, const CT* table, uint64_t cap, uint64_t k, Ke
                      int key_bits, uint64_t* out_keys, uint64_t* out_counts) {
   cudaStream_t s = x.stream;
   const uint64_t cap4 = cap / 4;  // cap is a multiple of 4
+  // u32 digit histograms and CUB's int item counts bound the table
+  if (cap >= 0x7fffffffull)
+    throw Error(IG_ECONFIG, "count table of " + std::to_string(cap) +
+                                " entries exceeds the selection's 2^31 - 1 limit");
   const KeyFn kf{km.pkeys, km.minv, km.cmask};
   const int threads = 512;
   unsigned blocks = (unsigned)((cap4 + threads - 1) / threads);

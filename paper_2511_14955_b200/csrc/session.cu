@@ -47,8 +47,9 @@ void validate(const ig_params& p) {
 
 static uint64_t k_prime(const ig_params& p) {
   // k_prime(), intergrams.hpp:29-31: ceil(z * k)
+  // (the reference's size_t cast; saturated where that cast is undefined)
   const double v = std::ceil(p.z * (double)p.k);
-  if (v >= 4.0e9) return 4000000000ull;  // survivors are bounded by the table anyway
+  if (v >= 18446744073709551615.0) return ~0ull;
   return (uint64_t)v;
 }
 
@@ -92,6 +93,33 @@ void finish_corpus(Session& s, std::vector<uint64_t>& hoff) {
   uint32_t n_long = 0;
   for (uint64_t q = 0; q < m; ++q) n_long += hoff[q + 1] - hoff[q] > (uint64_t)kShortCtaLen;
   s.n_long = n_long;
+  // small-alphabet work items: long sequences, the longest
+  // cut into parts of ~1/(4 * SMs) of the long bytes (>= 1 MiB) so a corpus
+  // of a few long sequences (a genome per chromosome) still fills every SM
+  {
+    uint64_t long_bytes = 0;
+    for (uint32_t i = 0; i < n_long; ++i) long_bytes += hoff[ord[i] + 1] - hoff[ord[i]];
+    const char* sb = getenv("IG_DIRECT_SPLIT_BYTES");  // tests: force splits
+    const uint64_t target = sb ? std::max<uint64_t>(1024, strtoull(sb, nullptr, 10))
+                               : std::max<uint64_t>(1ull << 20, long_bytes / (4ull * s.num_sms));
+    std::vector<DirectItem> items;
+    uint32_t nsplit = 0;
+    for (uint32_t i = 0; i < n_long; ++i) {
+      const uint64_t len = hoff[ord[i] + 1] - hoff[ord[i]];
+      const uint32_t np = len > 2 * target
+                              ? (uint32_t)std::min<uint64_t>((len + target - 1) / target, 1u << 16)
+                              : 1u;
+      const uint32_t slot = np > 1 ? nsplit++ : 0u;
+      for (uint32_t p = 0; p < np; ++p) items.push_back(DirectItem{ord[i], p, np, slot});
+    }
+    std::stable_sort(items.begin(), items.end(), [&](const DirectItem& a, const DirectItem& b) {
+      return (hoff[a.q + 1] - hoff[a.q]) / a.nparts > (hoff[b.q + 1] - hoff[b.q]) / b.nparts;
+    });
+    DirectItem* di = s.direct_items.as<DirectItem>(items.size() + 1);
+    if (!items.empty()) h2d(s, di, items.data(), items.size() * sizeof(DirectItem));
+    s.n_direct_items = (uint32_t)items.size();
+    s.n_direct_split = nsplit;
+  }
   s.corpus_alpha = -1;  // measured lazily by the first count-once run
   std::vector<RouteUnit> units;
   std::vector<uint32_t> ufirst(m + 1, 0);
@@ -298,16 +326,16 @@ static void allreduce_table(Session& s, CT* t, uint64_t n) {
     static const bool no_narrow = getenv("IG_NO_NARROW_ALLREDUCE") != nullptr;
     if (!no_narrow && n && n % 4 == 0) {
       unsigned long long* mx = reinterpret_cast<unsigned long long*>(s.work.as<uint32_t>(64));
-      launch_max_u64(t, n, mx, s.stream);
+      launch_max_u64(t, n, mx, s.num_sms, s.stream);
       s.launches++;
       allreduce(s, mx, 1, 1);
       unsigned long long bound = 0;
       d2h(s, &bound, mx, sizeof(bound));
       if (bound < (1ull << 32)) {
         uint32_t* nar = s.scratch32.as<uint32_t>(n);
-        launch_narrow_u64(t, nar, n, s.stream);
+        launch_narrow_u64(t, nar, n, s.num_sms, s.stream);
         allreduce(s, nar, n, 0);
-        launch_widen_set(nar, t, n, s.stream);
+        launch_widen_set(nar, t, n, s.num_sms, s.stream);
         s.launches += 2;
         return;
       }
@@ -322,7 +350,7 @@ static void allreduce_table(Session& s, CT* t, uint64_t n) {
 // scatter can histogram the next pass's owners (fused count).
 static uint32_t predicted_lgno(uint64_t kp) {
   uint32_t lg = 0;
-  while ((kp + (1ull << lg) - 1) / (1ull << lg) > 40) ++lg;
+  while (lg < 63 && (kp >> lg) + ((kp & ((1ull << lg) - 1)) != 0) > 40) ++lg;
   return lg;
 }
 
@@ -587,12 +615,26 @@ static void count_all_hot(Session& s, bool dense, uint32_t L, const Prefix* P, C
       dc.ntiles = std::min<uint64_t>(s.dc.ntiles, t0 + seg);
       IGB_CUDA(cudaMemsetAsync(scratch, 0, tcap * 4, s.stream));
       sweep(dc, scratch);
-      launch_widen_add(scratch, t, tcap, s.stream);
+      launch_widen_add(scratch, t, tcap, s.num_sms, s.stream);
       s.launches++;
     }
   } else {
     sweep(s.dc, t);
   }
+}
+
+// The small-alphabet kernels' work for a candidate space of nbits bits.
+static DirectWork direct_work(Session& s, uint64_t nbits) {
+  DirectWork w;
+  w.items = static_cast<const DirectItem*>(s.direct_items.p);
+  w.nitems = s.n_direct_items;
+  w.nsplit = s.n_direct_split;
+  if (w.nsplit) {
+    const size_t nwords = (nbits + 31) / 32;
+    w.gbm = s.direct_gbm.as<uint32_t>((size_t)w.nsplit * (nwords + 1));
+    w.done = w.gbm + (size_t)w.nsplit * nwords;
+  }
+  return w;
 }
 
 // One counting pass.  Returns the device table (tcap entries) and how table
@@ -642,9 +684,9 @@ static CT* count_pass(Session& s, bool dense, uint32_t L, int mode, const Prefix
       }
       const uint8_t* ab = static_cast<const uint8_t*>(s.alpha_dev.p) + 32;
       const size_t ev = s.kt.begin(IG_KF_ONCE_DIRECT, s.stream);
-      count_once_direct<CT>(s.dc, L, P->rp, static_cast<const uint32_t*>(s.order.p), s.n_long,
-                            ab, ab + 256, s.alpha_n, P->K, s.compact.as<uint32_t>(nbits + 1), t,
-                            s.num_sms, s.stream, dl, (uint32_t)lut_n, bits);
+      count_once_direct<CT>(s.dc, L, P->rp, direct_work(s, nbits), ab, ab + 256, s.alpha_n,
+                            P->K, s.compact.as<uint32_t>(nbits + 1), t, s.num_sms, s.stream, dl,
+                            (uint32_t)lut_n, bits);
       s.kt.end(ev, s.stream);
       s.launches += (s.n_long ? 1 : 0) + 1;
       km = KeyMap{};
@@ -661,9 +703,9 @@ static CT* count_pass(Session& s, bool dense, uint32_t L, int mode, const Prefix
         short_pass<CT>(s, 1, L, P->rp, t, 0, (uint32_t)s.dc.m);
         const uint8_t* ab = static_cast<const uint8_t*>(s.alpha_dev.p) + 32;
         const size_t ev = s.kt.begin(IG_KF_ONCE_DIRECT, s.stream);
-        count_once_direct<CT>(s.dc, L, P->rp, static_cast<const uint32_t*>(s.order.p), s.n_long,
-                              ab, ab + 256, s.alpha_n, P->K, s.compact.as<uint32_t>(nbits + 1),
-                              t, s.num_sms, s.stream);
+        count_once_direct<CT>(s.dc, L, P->rp, direct_work(s, nbits), ab, ab + 256,
+                              s.alpha_n, P->K, s.compact.as<uint32_t>(nbits + 1), t, s.num_sms,
+                              s.stream);
         s.kt.end(ev, s.stream);
         s.launches += (s.n_long ? 1 : 0) + 1;
         km = KeyMap{};
@@ -715,7 +757,7 @@ static CT* count_pass(Session& s, bool dense, uint32_t L, int mode, const Prefix
       const uint8_t* ab = static_cast<const uint8_t*>(s.calpha_dev.p) + 48;
       uint32_t* cmp = s.compact.as<uint32_t>((size_t)A * A * A + 1);
       const size_t ev = s.kt.begin(IG_KF_ONCE_DIRECT, s.stream);
-      count_once_direct<CT>(s.dc, 3, rp, static_cast<const uint32_t*>(s.order.p), s.n_long, ab,
+      count_once_direct<CT>(s.dc, 3, rp, direct_work(s, (uint64_t)A * A * A), ab,
                             ab + 256, A, (uint64_t)A * A, cmp, t, s.num_sms, s.stream, dl, lut_n,
                             bits, /*expand=*/false);
       expand_dense<CT>(cmp, A, ab + 256, rp.mult, rp.cmask, t, s.stream);
@@ -822,7 +864,7 @@ static CT* count_pass(Session& s, bool dense, uint32_t L, int mode, const Prefix
         dc.ntiles = std::min<uint64_t>(ranges[r].second, t0 + seg);
         IGB_CUDA(cudaMemsetAsync(scratch, 0, tcap * 4, s.stream));
         launch(dc, scratch);
-        launch_widen_add(scratch, t, tcap, s.stream);
+        launch_widen_add(scratch, t, tcap, s.num_sms, s.stream);
         s.launches++;
       }
     } else {

@@ -39,6 +39,8 @@ struct Session {
   DevBuf short_w, short_c;
   std::vector<uint32_t> h_short_w, h_short_c;
   uint32_t n_long = 0;  // sequences of > kShortCtaLen bytes: order[0 .. n_long)
+  DevBuf direct_items, direct_gbm;  // small-alphabet work items (DirectItem), split bitmaps
+  uint32_t n_direct_items = 0, n_direct_split = 0;
   // byte alphabet of the current run (count-once small-alphabet passes)
   DevBuf alpha_dev;      // u32 mask[8] | u8 arank[256] | u8 alpha[256]
   DevBuf compact;        // u32 [K' * A] direct-pass counts

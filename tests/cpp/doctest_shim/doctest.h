@@ -89,12 +89,23 @@ struct Subcase {
 };
 
 inline int run_all(int argc, char** argv) {
-  const char* filter = nullptr;
-  for (int i = 1; i < argc; ++i)
+  const char* filter = nullptr;  // substring of the test name
+  const char* exact = nullptr;   // the whole test name
+  std::set<std::string> excluded;  // -ntc=<whole name>: skip
+  for (int i = 1; i < argc; ++i) {
     if (!std::strncmp(argv[i], "-tc=", 4)) filter = argv[i] + 4;
+    if (!std::strncmp(argv[i], "-tce=", 5)) exact = argv[i] + 5;
+    if (!std::strncmp(argv[i], "-ntc=", 5)) excluded.insert(argv[i] + 5);
+    if (!std::strcmp(argv[i], "-ltc")) {  // list test cases: "file\tname"
+      for (const TestCase& tc : registry()) std::printf("%s\t%s\n", tc.file, tc.name);
+      return 0;
+    }
+  }
   long cases = 0, failed_cases = 0, checks = 0, failures = 0;
   for (const TestCase& tc : registry()) {
     if (filter && !std::strstr(tc.name, filter)) continue;
+    if (exact && std::strcmp(tc.name, exact)) continue;
+    if (excluded.count(tc.name)) continue;
     ++cases;
     State& s = st();
     s = State{};

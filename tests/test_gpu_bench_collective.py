@@ -36,12 +36,14 @@ def _bench(config, extra_env, torchrun):
     return json.loads(out.stdout.strip().splitlines()[-1])
 
 
-# c2: count-once u32 tables, one all-reduce per pass.  c3: count-all with a
-# 16 GiB total, u64 tables: a u64 bound, then the table narrowed to u32.
+# c2: count-once u32 tables, one all-reduce per pass.  c3 (24 sequences,
+# u64 tables forced as for a > 4 GiB corpus): a u64 bound, then the table
+# narrowed to u32.
 @pytest.mark.parametrize("config,calls_per_pass", [("c2", 1), ("c3", 2)])
 def test_bench_collective_hook_equals_single(gpu_lib, config, calls_per_pass):
-    plain = _bench(config, {}, torchrun=False)
-    coll = _bench(config, {"IG_BENCH_FORCE_COLLECTIVE": "1"}, torchrun=True)
+    env = {"IG_FORCE_U64": "1"} if calls_per_pass == 2 else {}
+    plain = _bench(config, env, torchrun=False)
+    coll = _bench(config, dict(env, IG_BENCH_FORCE_COLLECTIVE="1"), torchrun=True)
     assert plain["collective"] is None
     assert coll["collective"]["backend"] == "nccl"
     # every counting pass of every run (3 warm-up + 1 timed)

@@ -76,3 +76,41 @@ def test_once_small_alphabet_equals_oracle(gpu_lib, name, n, k, path):
     assert np.array_equal(r.keys, keys) and np.array_equal(r.counts, counts)
     assert r.diagnostics == diag
     assert [p.retained for p in r.passes] == [q["retained"] for q in rows]
+
+
+@functools.lru_cache(maxsize=None)
+def few_long(nseq):
+    """nseq long sequences (a genome read one chromosome per sequence):
+    the direct path splits each into parts counted by different CTAs, whose
+    bitmaps are OR-ed per sequence before counting (DirectItem)."""
+    return S.generate(S.scaled(S.CONFIGS["c4"], num_seqs=nseq, seq_len=3 << 20))
+
+
+@pytest.mark.parametrize("nseq", [1, 3])
+@pytest.mark.parametrize("split", [None, "65536", "1000"])
+def test_once_direct_few_long_sequences_split(gpu_lib, nseq, split):
+    # split None: the default plan (>= 1 MiB parts of the 3 MiB sequences);
+    # 65536 / 1000: forced small parts (many parts per sequence, part ends
+    # inside a 16-byte segment)
+    data, off = few_long(nseq)
+    rc, keys, counts, rows, diag = O.oracle_run(data, off, 8, 4096, 1.5, int(ONCE))
+    assert rc == 0
+    old = os.environ.get("IG_DIRECT_SPLIT_BYTES")
+    try:
+        if split:
+            os.environ["IG_DIRECT_SPLIT_BYTES"] = split
+        for resident in (False, True):
+            icfg = ig.IntergramConfig(n=8, k=4096, z=1.5, mode=ONCE)
+            if resident:
+                sess = ig.Session(device=0)
+                sess.load(ig.Corpus(data, off))
+                r = sess.run(icfg)
+                sess.close()
+            else:
+                r = ig.run_intergrams(ig.Corpus(data, off), icfg)
+            assert np.array_equal(r.keys, keys) and np.array_equal(r.counts, counts)
+            assert [p.retained for p in r.passes] == [q["retained"] for q in rows]
+    finally:
+        os.environ.pop("IG_DIRECT_SPLIT_BYTES", None)
+        if old is not None:
+            os.environ["IG_DIRECT_SPLIT_BYTES"] = old
