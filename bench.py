@@ -404,6 +404,9 @@ def main():
     ap.add_argument("--e2e-depth", type=int, default=2,
                     help="runs in flight for e2e.pipelined (1 disables it)")
     ap.add_argument("--seqs", type=int, default=0, help="override sequences per GPU")
+    ap.add_argument("--collective", default="lib", choices=["lib", "torch"],
+                    help="N>1 table all-reduce: the library's own NCCL communicator "
+                         "(ig_session_create_nccl) or a torch.distributed hook")
     ap.add_argument("--profile-run", action="store_true",
                     help="load, run once, exit (for ncu captures; prints nothing)")
     args = ap.parse_args()
@@ -473,12 +476,23 @@ def main():
         bytes_total, seqs_total = nbytes, count
 
     stream = torch.cuda.Stream()
-    coll, _cb = (None, None)
-    if world > 1 or force_coll:
+    coll, _cb, nccl = None, None, None
+    if (world > 1 or force_coll) and args.collective == "lib":
+        # the library's own communicator: rank 0's NCCL id goes to every rank
+        # over the torch group; forced on one rank, the library runs the
+        # collective at world 1 too (a 1-rank all-reduce is the identity)
+        if force_coll:
+            os.environ["IG_COLLECTIVE_AT_WORLD1"] = "1"
+        box = [ig.nccl_unique_id() if rank == 0 else None]
+        if world > 1:
+            dist.broadcast_object_list(box, src=0)
+        nccl = {"rank": rank, "world": world, "id": box[0], "bytes_total": bytes_total,
+                "seqs_total": seqs_total}
+    elif world > 1 or force_coll:
         # forced on one rank: the library skips the hook at world 1, so it is
         # told 2; the 1-rank NCCL all-reduce is the identity
         coll, _cb = make_collective(rank, max(world, 2), bytes_total, seqs_total)
-    sess = ig.Session(device=local, stream=stream.cuda_stream, collective=coll)
+    sess = ig.Session(device=local, stream=stream.cuda_stream, collective=coll, nccl=nccl)
     corpus = ig.Corpus(data, off_np)
     sess.load(corpus)
     icfg = ig.IntergramConfig(n=cfg.n, k=cfg.k, z=cfg.z, mode=ig.CountMode(cfg.mode))
@@ -621,8 +635,11 @@ def main():
             "step_breakdown_ms": step_breakdown,
             "kernel_breakdown": kernel_breakdown,
             "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches,
-            "collective": None if coll is None else
-            {"backend": "nccl", "world": world, "allreduce_calls": coll.calls[0]},
+            "collective": ({"backend": "nccl", "owner": "library (ig_session_create_nccl)",
+                            "world": world} if nccl is not None else
+                           None if coll is None else
+                           {"backend": "nccl", "owner": "torch.distributed hook",
+                            "world": world, "allreduce_calls": coll.calls[0]}),
             "clocks": clk.summary(),
             "result_digest": hashlib.sha256(
                 ig.topk_to_tsv(ig.run_result_topk(res, cfg.n)).encode()).hexdigest()[:16],

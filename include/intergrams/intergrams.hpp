@@ -9,6 +9,7 @@
 #include <cassert>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -31,6 +32,26 @@ struct IntergramConfig {
   size_t flush_batch_size = 8;                          // validated only
   bool frequency_ordered_trie = true;                   // no effect on results
   int device = -1;                                      // CUDA ordinal (-1: current)
+  // Several GPUs of this process (the reference's data parallelism,
+  // pipeline.hpp:101-199, on GPUs): whole-sequence shards balanced by bytes,
+  // one NCCL all-reduce per pass (ig_topk_ngrams_multi).  Empty: `device`
+  // alone, unless IG_DEVICES="0,1,..." names them (for unmodified callers).
+  std::vector<int> devices;
+
+  std::vector<int> device_list() const {
+    if (!devices.empty()) return devices;
+    std::vector<int> v;
+    if (const char* e = std::getenv("IG_DEVICES")) {
+      for (const char* p = e; *p;) {
+        char* end = nullptr;
+        const long d = std::strtol(p, &end, 10);
+        if (end == p) break;
+        v.push_back(static_cast<int>(d));
+        p = *end ? end + 1 : end;
+      }
+    }
+    return v;
+  }
 
   size_t k_prime() const { return static_cast<size_t>(std::ceil(z * static_cast<double>(k))); }
   void validate() const {
@@ -125,12 +146,25 @@ inline ig_params params_of(const IntergramConfig& cfg) {
 
 // run_intergrams (intergrams.hpp:74-75) on the GPU.  A file corpus is read by
 // the library itself (host threads -> pinned slabs -> HBM, line splitting on
-// the GPU); an in-memory corpus is packed into one CSR buffer and copied.
+// the GPU); an in-memory corpus is gathered sequence by sequence the same way.
 inline IntergramsResult run_intergrams(const Corpus& corpus, const IntergramConfig& cfg) {
   cfg.validate();
-  const ig_params p = detail::params_of(cfg);
+  ig_params p = detail::params_of(cfg);
   ig_result r{};
   char err[1024] = {0};
+  const std::vector<int> devs = cfg.device_list();
+  if (devs.size() == 1) p.device = devs[0];
+  if (devs.size() > 1) {  // sharded over several GPUs: one contiguous host corpus
+    const CorpusCSR csr = corpus.materialize();
+    ig_corpus c{csr.data.data(), csr.offsets.data(), csr.offsets.size() - 1, IG_HOST};
+    std::vector<int32_t> d(devs.begin(), devs.end());
+    detail::raise(ig_topk_ngrams_multi(&c, d.data(), static_cast<int32_t>(d.size()), &p, &r, err,
+                                       sizeof(err)),
+                  err);
+    IntergramsResult out = detail::convert(r);
+    ig_result_free(&r);
+    return out;
+  }
   if (!corpus.spec().in_memory.has_value()) {
     std::vector<std::string> roots;
     for (const auto& root : corpus.spec().roots) roots.push_back(root.string());
@@ -143,9 +177,18 @@ inline IntergramsResult run_intergrams(const Corpus& corpus, const IntergramConf
     ig_result_free(&r);
     return out;
   }
-  const CorpusCSR csr = corpus.materialize();
-  ig_corpus c{csr.data.data(), csr.offsets.data(), csr.offsets.size() - 1, IG_HOST};
-  detail::raise(ig_topk_ngrams(&c, &p, &r, err, sizeof(err)), err);
+  // in-memory: the sequences are gathered in place (no packed copy) by the
+  // library's host threads into pinned slabs that stream under the dense pass
+  const std::vector<std::string>& seqs = *corpus.spec().in_memory;
+  std::vector<const uint8_t*> ptrs(seqs.size());
+  std::vector<uint64_t> lens(seqs.size());
+  for (size_t q = 0; q < seqs.size(); ++q) {
+    ptrs[q] = reinterpret_cast<const uint8_t*>(seqs[q].data());
+    lens[q] = seqs[q].size();
+  }
+  detail::raise(ig_topk_ngrams_seqs(ptrs.data(), lens.data(), seqs.size(), &p, &r, err,
+                                    sizeof(err)),
+                err);
   IntergramsResult out = detail::convert(r);
   ig_result_free(&r);
   return out;

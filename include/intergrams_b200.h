@@ -131,6 +131,15 @@ typedef struct {
 IG_API int ig_topk_ngrams(const ig_corpus* corpus, const ig_params* params,
                    ig_result* out, char* err, size_t err_len);
 IG_API void ig_result_free(ig_result* r);
+/* run_intergrams over the reference's in-memory Corpus (a list of sequences,
+ * corpus.hpp:60-62 / make_memory_corpus) without packing it first: sequence
+ * q is seqs[q][0 .. lens[q]) in ordinary host memory.  Host threads gather
+ * the bytes into pinned slabs that stream to HBM under the dense pass.  A
+ * host ig_corpus that is not page-locked takes the same path in
+ * ig_topk_ngrams / ig_session_run_host. */
+IG_API int ig_topk_ngrams_seqs(const uint8_t* const* seqs, const uint64_t* lens,
+                               uint64_t num_seqs, const ig_params* params, ig_result* out,
+                               char* err, size_t err_len);
 
 /* ---- session API: corpus resident in HBM across runs ---------------------
  * ig_session_create binds a device and (optionally) a collective.  load
@@ -149,6 +158,28 @@ IG_API int ig_session_run(ig_session* s, const ig_params* params, ig_result* out
  * corpus stays resident afterwards, as after ig_session_load). */
 IG_API int ig_session_run_host(ig_session* s, const ig_corpus* corpus, const ig_params* params,
                                ig_result* out, char* err, size_t err_len);
+/* ---- multi-GPU with the library's own NCCL communicators --------------
+ * The reference's data parallelism (pipeline.hpp:101-199: whole sequences per
+ * worker, per-pass tables merged into one) on GPUs: each device counts a
+ * byte-balanced shard of whole sequences (ig_shard_range) and every pass
+ * table is summed in place by one NCCL all-reduce; selection then runs
+ * identically everywhere.  NCCL (libnccl.so.2) is loaded at first use.
+ *
+ * One process per GPU: rank 0 calls ig_nccl_unique_id and the caller moves
+ * the 128 bytes to every rank; each rank then creates its session with
+ * ig_session_create_nccl (ncclCommInitRank; collective over all ranks),
+ * loads its shard and runs.  bytes_total / seqs_total are the whole
+ * corpus's (count-table widths).  One process, several GPUs:
+ * ig_topk_ngrams_multi shards a host corpus over `devices`
+ * (ncclCommInitAll, one host thread per device) and returns the list. */
+IG_API int ig_nccl_unique_id(uint8_t id_out[128], char* err, size_t err_len);
+IG_API int ig_session_create_nccl(int32_t device, void* cuda_stream, int32_t rank, int32_t world,
+                                  const uint8_t id[128], uint64_t bytes_total,
+                                  uint64_t seqs_total, ig_session** out, char* err,
+                                  size_t err_len);
+IG_API int ig_topk_ngrams_multi(const ig_corpus* corpus, const int32_t* devices, int32_t ndev,
+                                const ig_params* params, ig_result* out, char* err,
+                                size_t err_len);
 /* Kernel launches issued by the session so far (for launch accounting). */
 IG_API uint64_t ig_session_launches(const ig_session* s);
 

@@ -79,6 +79,9 @@ SYMBOLS = [
     ("ig_topk_ngrams", C.c_int, [C.POINTER(ig_corpus), C.POINTER(ig_params),
                                  C.POINTER(ig_result), C.c_char_p, C.c_size_t]),
     ("ig_result_free", None, [C.POINTER(ig_result)]),
+    ("ig_topk_ngrams_seqs", C.c_int, [C.POINTER(C.c_void_p), C.POINTER(C.c_uint64), C.c_uint64,
+                                      C.POINTER(ig_params), C.POINTER(ig_result), C.c_char_p,
+                                      C.c_size_t]),
     ("ig_session_create", C.c_int, [C.c_int32, C.c_void_p, C.POINTER(ig_collective),
                                     C.POINTER(C.c_void_p), C.c_char_p, C.c_size_t]),
     ("ig_session_load", C.c_int, [C.c_void_p, C.POINTER(ig_corpus), C.c_char_p, C.c_size_t]),
@@ -87,6 +90,13 @@ SYMBOLS = [
     ("ig_session_run_host", C.c_int, [C.c_void_p, C.POINTER(ig_corpus), C.POINTER(ig_params),
                                       C.POINTER(ig_result), C.c_char_p, C.c_size_t]),
     ("ig_session_launches", C.c_uint64, [C.c_void_p]),
+    ("ig_nccl_unique_id", C.c_int, [C.c_char_p, C.c_char_p, C.c_size_t]),
+    ("ig_session_create_nccl", C.c_int, [C.c_int32, C.c_void_p, C.c_int32, C.c_int32,
+                                         C.c_char_p, C.c_uint64, C.c_uint64,
+                                         C.POINTER(C.c_void_p), C.c_char_p, C.c_size_t]),
+    ("ig_topk_ngrams_multi", C.c_int, [C.POINTER(ig_corpus), C.POINTER(C.c_int32), C.c_int32,
+                                       C.POINTER(ig_params), C.POINTER(ig_result), C.c_char_p,
+                                       C.c_size_t]),
     ("ig_session_set_profiling", None, [C.c_void_p, C.c_int32]),
     ("ig_session_kernel_stats", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32,
                                           C.c_int32]),

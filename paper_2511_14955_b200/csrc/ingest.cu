@@ -136,15 +136,27 @@ Slabs& slabs_of(Session& s) {
   return *static_cast<Slabs*>(s.slabs);
 }
 
-// Copies the concatenation of fl's files to dev[0 .. total) through the
-// pinned slabs: reader threads take slab-sized items in order; item j reuses
-// slab j % kSlabs once item j - kSlabs's copy has completed.  start() returns
-// at once; wait_bytes(e) blocks until every copy of bytes [0, e) has been
+// Where the streamed bytes come from: the concatenation of files, or host
+// memory that is not page-locked (one contiguous buffer, or one pointer per
+// sequence — the reference's in-memory Corpus without a packed copy).
+struct HostSource {
+  const FileList* files = nullptr;
+  const uint8_t* mem = nullptr;
+  const uint8_t* const* seqs = nullptr;
+  const uint64_t* seq_start = nullptr;  // [m + 1] byte offset of each sequence
+  uint64_t m = 0;
+  uint64_t total = 0;
+};
+
+// Copies the source's bytes to dev[0 .. total) through the pinned slabs:
+// reader threads take slab-sized items in order; item j reuses slab
+// j % kSlabs once item j - kSlabs's copy has completed.  start() returns at
+// once; wait_bytes(e) blocks until every copy of bytes [0, e) has been
 // enqueued on the copy stream; finish() joins the readers, waits for the
 // copies and rethrows the first reader error.
 class FileStreamer {
  public:
-  FileStreamer(Session& s, const FileList& fl, uint8_t* dev) : s_(s), fl_(fl), dev_(dev) {}
+  FileStreamer(Session& s, const HostSource& src, uint8_t* dev) : s_(s), src_(src), dev_(dev) {}
   ~FileStreamer() {
     failed_.store(true);
     sl_cv_notify();
@@ -152,7 +164,7 @@ class FileStreamer {
   }
 
   void start() {
-    total_ = fl_.start.back();
+    total_ = src_.total;
     if (total_ == 0) return;
     sl_ = &slabs_of(s_);
     if (!s_.copy_stream)
@@ -211,27 +223,41 @@ class FileStreamer {
         const uint64_t a0 = (uint64_t)j * kSlabBytes;
         const uint64_t a1 = std::min<uint64_t>(total_, a0 + kSlabBytes);
         uint8_t* buf = static_cast<uint8_t*>(sl.host[b]);
-        size_t f = (size_t)(std::upper_bound(fl_.start.begin(), fl_.start.end(), a0) -
-                            fl_.start.begin()) - 1;
-        uint64_t x = a0;
-        while (x < a1) {
-          while (fl_.start[f + 1] <= x) ++f;  // skip empty files
-          if (fd_file != f) {
-            if (fd >= 0) ::close(fd);
-            fd = ::open(fl_.paths[f].c_str(), O_RDONLY);
-            if (fd < 0) throw Error(IG_EIO, "cannot open file: " + fl_.paths[f]);
-            fd_file = f;
+        if (src_.mem) {
+          memcpy(buf, src_.mem + a0, a1 - a0);
+        } else if (src_.seqs) {
+          const uint64_t* st = src_.seq_start;
+          size_t q = (size_t)(std::upper_bound(st, st + src_.m + 1, a0) - st) - 1;
+          for (uint64_t x = a0; x < a1;) {
+            while (st[q + 1] <= x) ++q;  // skip empty sequences
+            const uint64_t e = std::min<uint64_t>(a1, st[q + 1]);
+            memcpy(buf + (x - a0), src_.seqs[q] + (x - st[q]), e - x);
+            x = e;
           }
-          const uint64_t want = std::min<uint64_t>(a1, fl_.start[f + 1]) - x;
-          uint64_t got = 0;
-          while (got < want) {
-            const ssize_t r = ::pread(fd, buf + (x - a0) + got, want - got,
-                                      (off_t)(x - fl_.start[f] + got));
-            if (r < 0) throw Error(IG_EIO, "read error: " + fl_.paths[f]);
-            if (r == 0) throw Error(IG_EIO, "file changed while reading: " + fl_.paths[f]);
-            got += (uint64_t)r;
+        } else {
+          const FileList& fl = *src_.files;
+          size_t f = (size_t)(std::upper_bound(fl.start.begin(), fl.start.end(), a0) -
+                              fl.start.begin()) - 1;
+          uint64_t x = a0;
+          while (x < a1) {
+            while (fl.start[f + 1] <= x) ++f;  // skip empty files
+            if (fd_file != f) {
+              if (fd >= 0) ::close(fd);
+              fd = ::open(fl.paths[f].c_str(), O_RDONLY);
+              if (fd < 0) throw Error(IG_EIO, "cannot open file: " + fl.paths[f]);
+              fd_file = f;
+            }
+            const uint64_t want = std::min<uint64_t>(a1, fl.start[f + 1]) - x;
+            uint64_t got = 0;
+            while (got < want) {
+              const ssize_t r = ::pread(fd, buf + (x - a0) + got, want - got,
+                                        (off_t)(x - fl.start[f] + got));
+              if (r < 0) throw Error(IG_EIO, "read error: " + fl.paths[f]);
+              if (r == 0) throw Error(IG_EIO, "file changed while reading: " + fl.paths[f]);
+              got += (uint64_t)r;
+            }
+            x += want;
           }
-          x += want;
         }
         IGB_CUDA(cudaMemcpyAsync(dev_ + a0, buf, a1 - a0, cudaMemcpyHostToDevice, s_.copy_stream));
         IGB_CUDA(cudaEventRecord(sl.done[b], s_.copy_stream));
@@ -255,7 +281,7 @@ class FileStreamer {
   }
 
   Session& s_;
-  const FileList& fl_;
+  const HostSource& src_;
   uint8_t* dev_;
   Slabs* sl_ = nullptr;
   uint64_t total_ = 0;
@@ -269,8 +295,16 @@ class FileStreamer {
   std::vector<std::thread> pool_;
 };
 
+HostSource file_source(const FileList& fl) {
+  HostSource src;
+  src.files = &fl;
+  src.total = fl.start.back();
+  return src;
+}
+
 void stream_files(Session& s, const FileList& fl, uint8_t* dev) {
-  FileStreamer fs(s, fl, dev);
+  const HostSource src = file_source(fl);
+  FileStreamer fs(s, src, dev);
   fs.start();
   fs.finish();
 }
@@ -344,6 +378,9 @@ void load_lines(Session& s, const FileList& fl) {
 // pass consumes sequence-aligned batches while the readers are still
 // streaming later files (the batch gate waits for a batch's copies to be
 // enqueued, then records its event).  Line records load first, then run.
+void run_streamed(Session& s, const HostSource& src, std::vector<uint64_t>& hoff,
+                  const ig_params& p, ig_result* out);
+
 void run_files(Session& s, const ig_file_corpus& spec, const ig_params& p, ig_result* out) {
   use_device(s);
   const FileList fl = enumerate(spec);
@@ -353,11 +390,20 @@ void run_files(Session& s, const ig_file_corpus& spec, const ig_params& p, ig_re
     return;
   }
   std::vector<uint64_t> hoff = record_offsets(fl, spec.chunk_size);
+  const HostSource src = file_source(fl);
+  run_streamed(s, src, hoff, p, out);
+}
+
+// A run whose corpus bytes stream from `src` through the pinned slabs while
+// the dense pass consumes sequence-aligned batches as they land (the batch
+// gate waits for a batch's copies to be enqueued, then records its event).
+void run_streamed(Session& s, const HostSource& src, std::vector<uint64_t>& hoff,
+                  const ig_params& p, ig_result* out) {
   check_offsets(hoff);
-  uint8_t* data = alloc_corpus(s, fl.start.back());
+  uint8_t* data = alloc_corpus(s, src.total);
   finish_corpus(s, hoff);  // synchronises the stream (pads zeroed)
   const std::vector<uint64_t> ends = plan_batches(s);
-  FileStreamer fs(s, fl, data);
+  FileStreamer fs(s, src, data);
   fs.start();
   s.batch_gate = [&](size_t i) {
     fs.wait_bytes(ends[i]);
@@ -391,6 +437,22 @@ void load_files(Session& s, const ig_file_corpus& spec) {
 }
 
 }  // namespace
+
+// Host corpus that is not page-locked (a contiguous buffer `mem`, or one
+// pointer per sequence `seqs`): streamed through the pinned slabs by host
+// threads, under the dense pass.
+void run_host_streamed(Session& s, const uint8_t* mem, const uint8_t* const* seqs,
+                       std::vector<uint64_t>& hoff, const ig_params& p, ig_result* out) {
+  use_device(s);
+  const std::vector<uint64_t> starts = hoff;  // finish_corpus takes hoff
+  HostSource src;
+  src.mem = mem;
+  src.seqs = seqs;
+  src.seq_start = starts.data();
+  src.m = starts.size() - 1;
+  src.total = starts.back();
+  run_streamed(s, src, hoff, p, out);
+}
 
 }  // namespace igb
 

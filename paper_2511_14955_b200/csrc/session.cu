@@ -307,8 +307,15 @@ static DevPrefixSet build_prefix_set(Session& s, const uint64_t* keys, uint64_t 
   return ps;
 }
 
+// A collective at world 1 is skipped, except under IG_COLLECTIVE_AT_WORLD1
+// (tests: the whole collective plumbing on a one-GPU box).
+static bool coll_active(const Session& s) {
+  static const bool at1 = getenv("IG_COLLECTIVE_AT_WORLD1") != nullptr;
+  return s.has_coll && (s.coll.world > 1 || at1);
+}
+
 static void allreduce(Session& s, void* buf, uint64_t count, int dtype) {
-  if (!s.has_coll || s.coll.world <= 1) return;
+  if (!coll_active(s)) return;
   if (!s.coll.allreduce) throw Error(IG_EINTERNAL, "collective has no allreduce");
   const int rc = s.coll.allreduce(buf, count, dtype, (void*)s.stream, s.coll.user);
   if (rc != 0) throw Error(IG_EINTERNAL, "allreduce callback failed");
@@ -321,7 +328,7 @@ static void allreduce(Session& s, void* buf, uint64_t count, int dtype) {
 // totals only might reach 2^32 (c5: 3 GB per pass -> 1.5 GB).
 template <typename CT>
 static void allreduce_table(Session& s, CT* t, uint64_t n) {
-  if (!s.has_coll || s.coll.world <= 1) return;
+  if (!coll_active(s)) return;
   if constexpr (sizeof(CT) == 8) {
     static const bool no_narrow = getenv("IG_NO_NARROW_ALLREDUCE") != nullptr;
     if (!no_narrow && n && n % 4 == 0) {
@@ -1151,11 +1158,27 @@ std::vector<uint64_t> plan_batches(Session& s) {
 // Host corpus: offsets/units/tiles first, then the bytes in sequence-aligned
 // batches on a copy stream (one event per batch); the dense pass consumes the
 // batches as they land, so most of the H2D hides behind counting.
+static bool page_locked(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
 static void load_and_run(Session& s, const ig_corpus& c, const ig_params& p, ig_result* out) {
   validate(p);
   if (c.location == IG_DEVICE) {
     load_corpus(s, c, true);
     run(s, p, out);
+    return;
+  }
+  if (c.num_seqs && c.offsets[c.num_seqs] && !page_locked(c.data)) {
+    // pageable: a DMA from it would stage synchronously before the run
+    // starts; host threads stream it through pinned slabs instead
+    std::vector<uint64_t> hoff(c.offsets, c.offsets + c.num_seqs + 1);
+    run_host_streamed(s, c.data, nullptr, hoff, p, out);
     return;
   }
   load_corpus(s, c, false);
@@ -1283,6 +1306,33 @@ int ig_topk_ngrams(const ig_corpus* corpus, const ig_params* params, ig_result* 
     ig_session* s = create(params->device, nullptr, nullptr);
     try {
       load_and_run(*s, *corpus, *params, out);
+    } catch (...) {
+      delete s;
+      throw;
+    }
+    delete s;
+  });
+}
+
+int ig_topk_ngrams_seqs(const uint8_t* const* seqs, const uint64_t* lens, uint64_t num_seqs,
+                        const ig_params* params, ig_result* out, char* err, size_t err_len) {
+  return guarded(err, err_len, [&] {
+    if ((num_seqs && (!seqs || !lens)) || !params || !out) throw Error(IG_ECONFIG, "null argument");
+    validate(*params);
+    std::vector<uint64_t> hoff(num_seqs + 1, 0);
+    for (uint64_t q = 0; q < num_seqs; ++q) {
+      if (lens[q] && !seqs[q]) throw Error(IG_ECONFIG, "null sequence pointer");
+      hoff[q + 1] = hoff[q] + lens[q];
+    }
+    ig_session* s = create(params->device, nullptr, nullptr);
+    try {
+      if (hoff[num_seqs]) {
+        run_host_streamed(*s, nullptr, seqs, hoff, *params, out);
+      } else {  // no bytes: the ordinary path (empty-corpus semantics)
+        static const uint8_t none = 0;
+        ig_corpus c{&none, hoff.data(), num_seqs, IG_HOST};
+        load_and_run(*s, c, *params, out);
+      }
     } catch (...) {
       delete s;
       throw;

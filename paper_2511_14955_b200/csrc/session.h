@@ -85,8 +85,12 @@ struct Session {
   // pinned staging slabs of the file loader (ingest.cu), created on first use
   void* slabs = nullptr;
   void (*slabs_free)(void*) = nullptr;
+  // the library's own NCCL communicator (nccl.cu), when it made one
+  void* nccl = nullptr;
+  void (*nccl_free)(void*) = nullptr;
 
   ~Session() {
+    if (nccl && nccl_free) nccl_free(nccl);
     if (slabs && slabs_free) slabs_free(slabs);
     for (auto e : events) cudaEventDestroy(e);
     for (auto e : batch_events) cudaEventDestroy(e);
@@ -192,6 +196,11 @@ void finish_corpus(Session& s, std::vector<uint64_t>& hoff);
 void check_offsets(const std::vector<uint64_t>& hoff);
 void run(Session& s, const ig_params& p, ig_result* out);
 std::vector<uint64_t> plan_batches(Session& s);
+// A run over a host corpus that is not page-locked: `mem` (contiguous) or
+// `seqs` (one pointer per sequence), offsets `hoff`; bytes stream through
+// pinned slabs on host threads while the dense pass counts (ingest.cu).
+void run_host_streamed(Session& s, const uint8_t* mem, const uint8_t* const* seqs,
+                       std::vector<uint64_t>& hoff, const ig_params& p, ig_result* out);
 template <typename CT>
 void count_once_exact(Session& s, uint32_t L, const DevPrefixSet& ps, uint64_t cap, CT* table);
 void init_select(Session& s);

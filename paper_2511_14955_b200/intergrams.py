@@ -276,18 +276,59 @@ def run_intergrams(corpus, cfg: IntergramConfig) -> IntergramsResult:
             return _result(out)
         finally:
             N.lib().ig_result_free(C.byref(out))
-    c = as_corpus(corpus)
     lib = N.lib()
     err = C.create_string_buffer(1024)
     out = N.ig_result()
-    view = c._view()
     params = cfg._params()
+    if isinstance(corpus, (list, tuple)) and all(isinstance(q, (bytes, bytearray, str))
+                                                 for q in corpus):
+        # the reference's in-memory corpus (make_memory_corpus): sequences
+        # gathered in place by the library (ig_topk_ngrams_seqs), no packing
+        seqs = [q.encode("latin-1") if isinstance(q, str) else bytes(q) for q in corpus]
+        m = len(seqs)
+        ptrs = (C.c_void_p * max(m, 1))(*[C.cast(C.c_char_p(q), C.c_void_p) for q in seqs])
+        lens = (C.c_uint64 * max(m, 1))(*[len(q) for q in seqs])
+        rc = lib.ig_topk_ngrams_seqs(ptrs, lens, m, C.byref(params), C.byref(out), err, len(err))
+        _raise(rc, err)
+        try:
+            return _result(out)
+        finally:
+            lib.ig_result_free(C.byref(out))
+    c = as_corpus(corpus)
+    view = c._view()
     rc = lib.ig_topk_ngrams(C.byref(view), C.byref(params), C.byref(out), err, len(err))
     _raise(rc, err)
     try:
         return _result(out)
     finally:
         lib.ig_result_free(C.byref(out))
+
+
+def nccl_unique_id() -> bytes:
+    """ig_nccl_unique_id: the 128-byte id rank 0 hands to every rank."""
+    buf = C.create_string_buffer(128)
+    err = C.create_string_buffer(1024)
+    _raise(N.lib().ig_nccl_unique_id(buf, err, len(err)), err)
+    return buf.raw
+
+
+def run_intergrams_multi(corpus, cfg: IntergramConfig, devices) -> IntergramsResult:
+    """run_intergrams over several GPUs of this process (ig_topk_ngrams_multi):
+    whole-sequence shards balanced by bytes, one NCCL all-reduce per pass."""
+    cfg.validate()
+    c = as_corpus(corpus)
+    devs = (C.c_int32 * len(devices))(*[int(d) for d in devices])
+    err = C.create_string_buffer(1024)
+    out = N.ig_result()
+    view = c._view()
+    params = cfg._params()
+    rc = N.lib().ig_topk_ngrams_multi(C.byref(view), devs, len(devices), C.byref(params),
+                                      C.byref(out), err, len(err))
+    _raise(rc, err)
+    try:
+        return _result(out)
+    finally:
+        N.lib().ig_result_free(C.byref(out))
 
 
 def count_dense(corpus, n: int, mode: CountMode, device: int = -1) -> np.ndarray:
@@ -498,14 +539,26 @@ class Session:
     """A device session with the corpus resident in HBM (ig_session_*)."""
 
     def __init__(self, device: int = 0, stream: int = 0,
-                 collective: Optional[N.ig_collective] = None):
+                 collective: Optional[N.ig_collective] = None,
+                 nccl: Optional[dict] = None):
+        """nccl: {"rank", "world", "id" (128 bytes from nccl_unique_id() on
+        rank 0), "bytes_total", "seqs_total"} — the session's table all-reduces
+        go through the library's own NCCL communicator (ig_session_create_nccl)."""
         self._lib = N.lib()
         self._h = C.c_void_p()
         self._coll = collective  # keep the callback alive
         err = C.create_string_buffer(1024)
-        rc = self._lib.ig_session_create(device, C.c_void_p(stream) if stream else None,
-                                         C.byref(collective) if collective else None,
-                                         C.byref(self._h), err, len(err))
+        st = C.c_void_p(stream) if stream else None
+        if nccl is not None:
+            uid = bytes(nccl["id"])
+            assert len(uid) == 128
+            rc = self._lib.ig_session_create_nccl(
+                device, st, int(nccl["rank"]), int(nccl["world"]), uid,
+                int(nccl["bytes_total"]), int(nccl["seqs_total"]), C.byref(self._h), err, len(err))
+        else:
+            rc = self._lib.ig_session_create(device, st,
+                                             C.byref(collective) if collective else None,
+                                             C.byref(self._h), err, len(err))
         _raise(rc, err)
 
     def load(self, corpus=None, *, data_ptr: int = 0, offsets_ptr: int = 0, num_seqs: int = 0,

@@ -23,9 +23,9 @@ def _free_port():
     return port
 
 
-def _bench(config, extra_env, torchrun):
+def _bench(config, extra_env, torchrun, collective="torch"):
     args = ["bench.py", "--config", config, "--seqs", "24", "--steps", "1", "--warmup", "3",
-            "--no-cpu-baseline", "--no-e2e"]
+            "--no-cpu-baseline", "--no-e2e", "--collective", collective]
     if torchrun:
         args = ["-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1",
                 "--master-addr", "127.0.0.1", "--master-port", str(_free_port())] + args
@@ -50,3 +50,50 @@ def test_bench_collective_hook_equals_single(gpu_lib, config, calls_per_pass):
     passes = max(coll["config"]["n"], 3) - 2
     assert coll["collective"]["allreduce_calls"] == 4 * passes * calls_per_pass
     assert coll["result_digest"] == plain["result_digest"]
+
+
+# The library's own communicator (ig_nccl_unique_id -> broadcast over the
+# torch group -> ig_session_create_nccl): every pass table goes through
+# ncclAllReduce on the session stream (a 1-rank group here, forced on).
+@pytest.mark.parametrize("config", ["c2", "c3"])
+def test_bench_library_nccl_equals_single(gpu_lib, config):
+    env = {"IG_FORCE_U64": "1"} if config == "c3" else {}
+    plain = _bench(config, env, torchrun=False, collective="lib")
+    coll = _bench(config, dict(env, IG_BENCH_FORCE_COLLECTIVE="1"), torchrun=True,
+                  collective="lib")
+    assert plain["collective"] is None
+    assert coll["collective"]["owner"].startswith("library")
+    assert coll["result_digest"] == plain["result_digest"]
+
+
+MULTI = r"""
+import os, sys, json
+import numpy as np
+sys.path.insert(0, %r)
+from paper_2511_14955_b200 import intergrams as ig, synth as S
+data, off = S.generate(S.scaled(S.CONFIGS["c2"], num_seqs=40, seq_len=200_000))
+out = {}
+for mode in (0, 1):
+    cfg = ig.IntergramConfig(n=6, k=2000, z=1.5, mode=ig.CountMode(mode))
+    a = ig.run_intergrams(ig.Corpus(data, off), cfg)
+    b = ig.run_intergrams_multi(ig.Corpus(data, off), cfg, devices=[0])
+    out[mode] = bool(np.array_equal(a.keys, b.keys) and np.array_equal(a.counts, b.counts))
+try:
+    ig.run_intergrams_multi(ig.Corpus(data, off), cfg, devices=[])
+    out["empty"] = "no error"
+except ig.ConfigError:
+    out["empty"] = "ConfigError"
+print(json.dumps(out))
+"""
+
+
+def test_multi_device_entry_point_one_gpu(gpu_lib):
+    # ig_topk_ngrams_multi on the one GPU of the box: ncclCommInitAll over
+    # [0], one session per device on its own thread, the all-reduce forced at
+    # world 1 so every pass table really goes through NCCL
+    env = dict(os.environ, IG_COLLECTIVE_AT_WORLD1="1")
+    out = subprocess.run([sys.executable, "-c", MULTI % ROOT], env=env, capture_output=True,
+                         text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    res = json.loads(out.stdout.strip().splitlines()[-1])
+    assert res == {"0": True, "1": True, "empty": "ConfigError"}
