@@ -111,8 +111,13 @@ inline IntergramsResult convert(const ig_result& r) {
   out.topk.reserve(r.len);
   for (uint64_t i = 0; i < r.len; ++i) {
     std::string g(r.gram_len, '\0');
-    for (uint32_t b = 0; b < r.gram_len; ++b)
-      g[b] = static_cast<char>((r.keys[i] >> (8 * (r.gram_len - 1 - b))) & 0xff);
+    if (r.grams) {  // every n (the only form for n > 8)
+      for (uint32_t b = 0; b < r.gram_len; ++b)
+        g[b] = static_cast<char>(r.grams[i * r.gram_len + b]);
+    } else {
+      for (uint32_t b = 0; b < r.gram_len; ++b)
+        g[b] = static_cast<char>((r.keys[i] >> (8 * (r.gram_len - 1 - b))) & 0xff);
+    }
     out.topk.push_back(GramCount{std::move(g), r.counts[i]});
   }
   for (uint32_t i = 0; i < r.num_passes; ++i) {

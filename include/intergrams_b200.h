@@ -60,8 +60,10 @@ extern "C" {
 #define IG_HOST 0
 #define IG_DEVICE 1
 
-/* Largest gram length the packed-u64 path supports.  run_intergrams with
- * n > IG_MAX_N returns IG_ECONFIG. */
+/* Largest gram length of the packed-u64 key forms (ig_result.keys,
+ * extend_pass, naive / hashgram / featurize).  run_intergrams itself takes
+ * any n, as the reference does (intergrams.cpp:37-42): grams longer than 8
+ * bytes come back in ig_result.grams only. */
 #define IG_MAX_N 8
 
 typedef struct {
@@ -105,6 +107,8 @@ typedef struct {
   ig_pass_stat* passes;
   uint32_t num_passes;
   char* diagnostics;       /* '\n'-separated, NUL-terminated */
+  uint8_t* grams;          /* len * gram_len gram bytes, canonical order (every n;
+                              for n > 8 the only form: keys is NULL) */
 } ig_result;
 
 /* Optional cross-rank hook for multi-GPU runs (one process per GPU).  The

@@ -270,6 +270,32 @@ def ref_run(data: np.ndarray, off: np.ndarray, n: int, k: int, z: float, mode: i
             secs.value, err.value.decode())
 
 
+def ref_run_grams(data: np.ndarray, off: np.ndarray, n: int, k: int, z: float, mode: int,
+                  workers: int = 0):
+    """ig_ref::run_intergrams for any n -> (rc, grams (len, n) uint8, counts,
+    passes, diagnostics, err): the gram bytes themselves (n > 8 does not fit
+    the packed keys ref_run returns)."""
+    L = ref()
+    grams = np.zeros(max(k * n, 1), np.uint8)
+    counts = np.zeros(k, np.uint64)
+    ln = C.c_uint64(0)
+    passes = (igref_pass * 64)()
+    np_ = C.c_uint32(0)
+    diag = C.create_string_buffer(8192)
+    err = C.create_string_buffer(512)
+    secs = C.c_double(0)
+    rc = L.igref_run_intergrams(_ptr(data), off.ctypes.data, off.size - 1, n, k, z, mode, workers,
+                                grams.ctypes.data, counts.ctypes.data, C.byref(ln), passes, 64,
+                                C.byref(np_), diag, len(diag), C.byref(secs), err, len(err))
+    m = ln.value
+    rows = [dict(label=passes[i].label.decode(), gram_len=passes[i].gram_len,
+                 bytes_processed=passes[i].bytes_processed,
+                 candidate_space=passes[i].candidate_space, retained=passes[i].retained,
+                 retained_short=bool(passes[i].retained_short)) for i in range(np_.value)]
+    return (rc, grams[:m * n].reshape(m, n).copy(), counts[:m], rows,
+            [d for d in diag.value.decode().split("\n") if d], err.value.decode())
+
+
 def ref_run_file(path: str, chunk_size: int, n: int, k: int, z: float, mode: int,
                  workers: int = 0):
     """ig_ref::run_intergrams over a file corpus (one root; chunk_size records,

@@ -42,7 +42,7 @@ class ig_result(C.Structure):
     _fields_ = [("len", C.c_uint64), ("gram_len", C.c_uint32),
                 ("keys", C.POINTER(C.c_uint64)), ("counts", C.POINTER(C.c_uint64)),
                 ("passes", C.POINTER(ig_pass_stat)), ("num_passes", C.c_uint32),
-                ("diagnostics", C.c_char_p)]
+                ("diagnostics", C.c_char_p), ("grams", C.POINTER(C.c_uint8))]
 
 
 class ig_hashgram_params(C.Structure):

@@ -49,7 +49,8 @@ enum EmitKind {
   kEmitBucket = 1,     // its hash bucket (hash-gramming pass 1)
   kEmitKeptGram = 2,   // grams of kept buckets (hash-gramming pass 2)
   kEmitVocab = 3,      // vocabulary hits (featurize)
-  kEmitCandidate = 4   // extension-pass candidate index rank * 256 + last byte
+  kEmitCandidate = 4,  // extension-pass candidate index rank * 256 + last byte
+  kEmitChain = 5       // the same for j >= 9 byte grams (rank chain, below)
 };
 
 struct EmitSpec {
@@ -67,6 +68,10 @@ struct EmitSpec {
   const uint32_t* vcols = nullptr;  // column per slot, ~0u = empty
   uint32_t vlg = 0;
   DevPrefixSet ps;  // kEmitCandidate: open-addressing survivor set (p = rank)
+  // kEmitChain: ps holds the 8-byte survivors (p = rank in key order) and
+  // remap[L - 9][p * 256 + byte] is the rank of an L-byte survivor in id
+  // (= byte) order, ~0u when the L-gram did not survive
+  const uint32_t* const* remap = nullptr;
 };
 
 __host__ __device__ inline uint64_t bswap64(uint64_t x) {
@@ -171,7 +176,8 @@ __device__ __forceinline__ uint32_t eval_thread(const EmitSpec& sp, uint64_t chu
         const uint32_t l32 = __funnelshift_r(w[wi], w[wi + 1], sh);
         const uint32_t h32 = __funnelshift_r(w[wi + 1], w[wi + 2], sh);
         const uint64_t le = (((uint64_t)h32 << 32) | l32) & nmask;
-        const uint64_t key = bswap64(le) >> (64 - 8 * n);  // big-endian packed gram
+        // big-endian packed gram (its first 8 bytes when n > 8)
+        const uint64_t key = n >= 8 ? bswap64(le) : bswap64(le) >> (64 - 8 * n);
         bool hit = true;
         uint64_t v = key;
         if (KIND == kEmitBucket) {
@@ -186,6 +192,15 @@ __device__ __forceinline__ uint32_t eval_thread(const EmitSpec& sp, uint64_t chu
           const uint32_t r = survivor_rank(sp.ps, key >> 8);
           hit = r != 0xffffffffu;
           v = (uint64_t)r * 256 + (key & 0xff);
+        } else if (KIND == kEmitChain) {
+          // the (n-1)-byte prefix's rank, walked up from its first 8 bytes
+          // (a trie below depth 8, as PrefixTrie::lookup walks it byte by
+          // byte, trie.cpp:139-160)
+          uint32_t r = survivor_rank(sp.ps, key);
+          for (uint32_t L = 9; L < n && r != 0xffffffffu; ++L)
+            r = __ldg(sp.remap[L - 9] + ((uint64_t)r * 256 + sp.data[g + L - 1]));
+          hit = r != 0xffffffffu;
+          v = (uint64_t)r * 256 + sp.data[g + n - 1];
         }
         if (hit) {
           mask |= 1u << i;
@@ -448,7 +463,8 @@ void fill_result(ig_result* out, uint32_t n, const std::vector<uint64_t>& keys,
   out->counts = (uint64_t*)malloc((len + 1) * 8);
   out->passes = (ig_pass_stat*)malloc((rows.size() + 1) * sizeof(ig_pass_stat));
   out->diagnostics = (char*)malloc(1);
-  if (!out->keys || !out->counts || !out->passes || !out->diagnostics) {
+  out->grams = (uint8_t*)malloc(len * n + 1);
+  if (!out->keys || !out->counts || !out->passes || !out->diagnostics || !out->grams) {
     ig_result_free(out);
     throw Error(IG_EINTERNAL, "host allocation failed");
   }
@@ -456,6 +472,8 @@ void fill_result(ig_result* out, uint32_t n, const std::vector<uint64_t>& keys,
     memcpy(out->keys, keys.data(), len * 8);
     memcpy(out->counts, counts.data(), len * 8);
   }
+  for (uint64_t i = 0; i < len; ++i)
+    for (uint32_t b = 0; b < n; ++b) out->grams[i * n + b] = (uint8_t)(keys[i] >> (8 * (n - 1 - b)));
   for (size_t i = 0; i < rows.size(); ++i) {
     out->passes[i] = rows[i].st;
     if (tm) out->passes[i].seconds = tm->seconds(rows[i].ev);
@@ -498,6 +516,42 @@ void count_once_exact(Session& s, uint32_t L, const DevPrefixSet& ps, uint64_t c
 }
 template void count_once_exact<uint32_t>(Session&, uint32_t, const DevPrefixSet&, uint64_t,
                                          uint32_t*);
+
+// Extension pass j >= 9 (grams longer than the packed u64 keys), both count
+// modes, by sorting: every position whose (j-1)-byte prefix survived emits
+// (rank * 256 + last byte[, sequence]); ids, counts and selection are the
+// reference's (intergrams.cpp:44-66), since ranks follow byte order.
+template <typename CT>
+void count_chain_exact(Session& s, uint32_t j, const DevPrefixSet& ps8,
+                       const uint32_t* const* remap, int mode, uint64_t cap, CT* table) {
+  EmitSpec sp;
+  sp.n = j;
+  sp.ps = ps8;
+  sp.remap = remap;
+  const uint64_t U = exact_count<kEmitChain>(s, sp, mode, bits_for(cap ? cap - 1 : 0));
+  if (U == 0) return;
+  k_put_counts<CT><<<grid_of(U), 256, 0, s.stream>>>(
+      static_cast<const uint64_t*>(s.ex.acc_keys.p), static_cast<const uint64_t*>(s.ex.acc_counts.p),
+      U, table);
+  IGB_LAUNCHED(&s);
+}
+template void count_chain_exact<uint32_t>(Session&, uint32_t, const DevPrefixSet&,
+                                          const uint32_t* const*, int, uint64_t, uint32_t*);
+template void count_chain_exact<unsigned long long>(Session&, uint32_t, const DevPrefixSet&,
+                                                    const uint32_t* const*, int, uint64_t,
+                                                    unsigned long long*);
+
+// remap[ids[r]] = r for the survivors sorted by id (the table was set to ~0u).
+__global__ void k_scatter_rank(const uint64_t* __restrict__ ids, uint64_t n,
+                               uint32_t* __restrict__ remap) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) remap[ids[i]] = (uint32_t)i;
+}
+
+void launch_scatter_rank(const uint64_t* sorted_ids, uint64_t n, uint32_t* remap,
+                         cudaStream_t st) {
+  if (n) k_scatter_rank<<<grid_of(n), 256, 0, st>>>(sorted_ids, n, remap);
+}
 template void count_once_exact<unsigned long long>(Session&, uint32_t, const DevPrefixSet&,
                                                    uint64_t, unsigned long long*);
 

@@ -227,7 +227,7 @@ int ig_topk_ngrams_multi(const ig_corpus* corpus, const int32_t* devices, int32_
       for (int i = 1; i < ndev; ++i) {
         const ig_result& a = rs[0];
         const ig_result& b = rs[(size_t)i];
-        if (a.len != b.len || memcmp(a.keys, b.keys, a.len * 8) ||
+        if (a.len != b.len || memcmp(a.grams, b.grams, a.len * a.gram_len) ||
             memcmp(a.counts, b.counts, a.len * 8)) {
           first = std::make_exception_ptr(
               Error(IG_EINTERNAL, "devices disagree on the top-k list"));

@@ -41,8 +41,6 @@ void validate(const ig_params& p) {
   if (p.flush_batch_size < 1) throw Error(IG_ECONFIG, "flush batch size must be >= 1");
   if (p.mode != IG_MODE_ONCE && p.mode != IG_MODE_ALL)
     throw Error(IG_ECONFIG, "count mode must be ONCE (0) or ALL (1)");
-  if (p.n > IG_MAX_N)
-    throw Error(IG_ECONFIG, "gram length n above 8 is not supported by the packed-u64 GPU path");
 }
 
 static uint64_t k_prime(const ig_params& p) {
@@ -972,6 +970,15 @@ static void run_t(Session& s, const ig_params& p, ig_result* out) {
   uint64_t* out_keys_d = nullptr;
   uint64_t* out_counts_d = nullptr;
   uint64_t out_len = 0;
+  // grams longer than 8 bytes (passes j >= 9): the 8-byte survivors (p =
+  // rank in key order) and per later level the survivor ids in id order
+  // plus an id -> rank table; a j-gram's prefix rank is walked up from its
+  // first 8 bytes, and since every rank follows byte order, ids (p * 256 +
+  // last byte) order the grams as their bytes do (intergrams.cpp:56-59)
+  DevPrefixSet ps8{};
+  uint64_t ns8 = 0;
+  std::vector<const uint32_t*> remap_ptrs;
+  std::vector<uint64_t> level_len;  // survivors of levels 9 .. j-1
 
   if (n <= 3) {  // intergrams.cpp:105-113
     ev = tm.begin();
@@ -1017,20 +1024,67 @@ static void run_t(Session& s, const ig_params& p, ig_result* out) {
       // an empty survivor list is a depth-0 trie (trie.cpp:23) and the
       // extension pass rejects it (intergrams.cpp:46-48)
       if (ns == 0) throw Error(IG_ECONFIG, "extension pass needs a trie of depth j-1");
-      if (hmask[0]) {
+      const bool chain = j >= 9;
+      if (hmask[0] && !chain) {
         P.ps.hit_in = j >= 5 ? hmask[(j - 1) & 1] : nullptr;
         P.ps.hit_out = j < n ? hmask[j & 1] : nullptr;
+      }
+      // count-all: a j-gram occurs at most as often as its (j-1)-byte prefix
+      // (each occurrence ends one byte after one of the prefix's), so when
+      // pass j-1's largest global count (its first survivor) is below 2^32,
+      // pass j counts into a u32 table over the whole corpus: no < 4 GiB
+      // segments, no scratch widening, half the selection bytes.  Every
+      // rank sees the same global bound, so table layouts still agree.
+      bool narrow = false;
+      if constexpr (sizeof(CT) == 8) {
+        if (p.mode == IG_MODE_ALL && !getenv("IG_FORCE_U64")) {
+          uint64_t top = 0;
+          d2h(s, &top, sc, sizeof(top));
+          narrow = top < 0xffffffffull;
+        }
       }
       ev = tm.begin();
       const uint64_t cap = 256 * ns;
       // fused histogram of the next pass's owners, sized for its largest
       // possible prefix count min(k', 256 * this pass's survivors)
-      next_lg = fuse_lg >= 0 && j < n ? (int32_t)predicted_lgno(std::min<uint64_t>(kp, 256 * ns))
-                                      : -1;
+      next_lg = fuse_lg >= 0 && j < n && j < 8
+                    ? (int32_t)predicted_lgno(std::min<uint64_t>(kp, 256 * ns))
+                    : -1;  // (passes j >= 9 do not route)
       if (next_lg > (int32_t)kMaxFusedLg) next_lg = -1;
-      CT* ct = count_pass<CT>(s, false, j, p.mode, &P, tcap, km, next_lg);
-      IGB_CUDA(cudaGetLastError());
-      allreduce_table<CT>(s, ct, tcap);
+      void* ct = nullptr;
+      if (chain) {
+        tcap = cap;
+        km = KeyMap{};  // table index = id = key (byte order)
+        auto go = [&](auto* tag) -> void* {
+          using T = std::remove_pointer_t<decltype(tag)>;
+          T* t = s.table.as<T>(tcap);
+          IGB_CUDA(cudaMemsetAsync(t, 0, tcap * sizeof(T), s.stream));
+          count_chain_exact<T>(s, j, ps8, static_cast<const uint32_t* const*>(s.chain_ptrs.p),
+                               p.mode, tcap, t);
+          IGB_CUDA(cudaGetLastError());
+          allreduce_table<T>(s, t, tcap);
+          return t;
+        };
+        ct = narrow ? go((uint32_t*)nullptr) : go((CT*)nullptr);
+      } else if (narrow) {
+        ct = count_pass<uint32_t>(s, false, j, p.mode, &P, tcap, km, next_lg);
+        IGB_CUDA(cudaGetLastError());
+        allreduce_table<uint32_t>(s, static_cast<uint32_t*>(ct), tcap);
+      } else {
+        ct = count_pass<CT>(s, false, j, p.mode, &P, tcap, km, next_lg);
+        IGB_CUDA(cudaGetLastError());
+        allreduce_table<CT>(s, static_cast<CT*>(ct), tcap);
+      }
+      int kbits = 8 * (int)j;
+      if (chain) {
+        kbits = 1;
+        while (kbits < 64 && ((tcap - 1) >> kbits) != 0) ++kbits;
+      }
+      auto select = [&](uint64_t kk, uint64_t* ok, uint64_t* oc) {
+        return narrow ? timed_select<uint32_t>(s, static_cast<uint32_t*>(ct), tcap, kk, km,
+                                               kbits, ok, oc)
+                      : timed_select<CT>(s, static_cast<CT*>(ct), tcap, kk, km, kbits, ok, oc);
+      };
       tm.end(ev);
       rows.push_back(
           make_row(std::to_string(j) + "-gram pass", j, total_bytes, cap, 0, false, ev));
@@ -1040,7 +1094,7 @@ static void run_t(Session& s, const ig_params& p, ig_result* out) {
         uint64_t ncap = std::min<uint64_t>(kp, cap);
         uint64_t* nk = s.next_keys.as<uint64_t>(ncap + 1);
         uint64_t* nc = s.next_counts.as<uint64_t>(ncap + 1);
-        uint64_t nn = timed_select<CT>(s, ct, tcap, kp, km, 8 * j, nk, nc);
+        uint64_t nn = select(kp, nk, nc);
         shrt = nn < kp;
         if (shrt)
           diag += "pass " + std::to_string(j) + " retained " + std::to_string(nn) +
@@ -1048,8 +1102,33 @@ static void run_t(Session& s, const ig_params& p, ig_result* out) {
         s.surv_keys.swap(s.next_keys);
         s.surv_counts.swap(s.next_counts);
         sk = nk;
+        sc = nc;
         ns = nn;
-        P = prepare_prefix(s, sk, ns, j, p.mode, owner_bits(next_lg, ns));
+        if (j == 8) {  // the next pass walks ranks from these 8-byte survivors
+          ps8 = build_prefix_set(s, sk, ns, 8);
+          ns8 = ns;
+        } else if (j > 8) {  // level j: survivor ids in id order, id -> rank
+          if (s.chain_ids.size() <= j) {
+            s.chain_ids.resize(j + 1);
+            s.chain_remap.resize(j + 1);
+          }
+          if (!s.chain_ids[j]) s.chain_ids[j].reset(new DevBuf());
+          if (!s.chain_remap[j]) s.chain_remap[j].reset(new DevBuf());
+          uint64_t* sid = s.chain_ids[j]->as<uint64_t>(ns + 1);
+          uint32_t* rk = s.chain_ranks.as<uint32_t>(2 * ns + 2);
+          sort_keys_by_value(sk, (uint32_t)ns, kbits, sid, rk, rk + ns + 1, s.chain_sort_tmp,
+                             s.stream);
+          uint32_t* rm = s.chain_remap[j]->as<uint32_t>(tcap);
+          IGB_CUDA(cudaMemsetAsync(rm, 0xff, tcap * sizeof(uint32_t), s.stream));
+          launch_scatter_rank(sid, ns, rm, s.stream);
+          s.launches += 3;
+          remap_ptrs.push_back(rm);
+          level_len.push_back(ns);
+          const uint32_t** dp = s.chain_ptrs.as<const uint32_t*>(remap_ptrs.size());
+          h2d(s, dp, remap_ptrs.data(), remap_ptrs.size() * sizeof(void*));
+        } else {
+          P = prepare_prefix(s, sk, ns, j, p.mode, owner_bits(next_lg, ns));
+        }
         tm.end(ev);
         rows.push_back(make_row("top-zk " + std::to_string(j) + "-grams/trie building", j, 0, 0,
                                 ns, shrt, ev));
@@ -1057,7 +1136,7 @@ static void run_t(Session& s, const ig_params& p, ig_result* out) {
         uint64_t ocap = std::min<uint64_t>(p.k, cap);
         out_keys_d = s.next_keys.as<uint64_t>(ocap + 1);
         out_counts_d = s.next_counts.as<uint64_t>(ocap + 1);
-        out_len = timed_select<CT>(s, ct, tcap, p.k, km, 8 * j, out_keys_d, out_counts_d);
+        out_len = select(p.k, out_keys_d, out_counts_d);
         tm.end(ev);
         rows.push_back(
             make_row("top-k " + std::to_string(j) + "-grams", j, 0, 0, out_len, false, ev));
@@ -1070,15 +1149,44 @@ static void run_t(Session& s, const ig_params& p, ig_result* out) {
   out->gram_len = n;
   out->keys = (uint64_t*)malloc((out_len + 1) * sizeof(uint64_t));
   out->counts = (uint64_t*)malloc((out_len + 1) * sizeof(uint64_t));
+  out->grams = (uint8_t*)malloc(out_len * n + 1);
   out->passes = (ig_pass_stat*)malloc(rows.size() * sizeof(ig_pass_stat));
   out->diagnostics = (char*)malloc(diag.size() + 1);
-  if (!out->keys || !out->counts || !out->passes || !out->diagnostics)
+  if (!out->keys || !out->counts || !out->grams || !out->passes || !out->diagnostics)
     throw Error(IG_EINTERNAL, "host allocation failed");
   if (out_len) {
     d2h(s, out->keys, out_keys_d, out_len * sizeof(uint64_t));
     d2h(s, out->counts, out_counts_d, out_len * sizeof(uint64_t));
   }
   IGB_CUDA(cudaStreamSynchronize(s.stream));
+  if (n <= 8) {
+    for (uint64_t i = 0; i < out_len; ++i)
+      for (uint32_t b = 0; b < n; ++b)
+        out->grams[i * n + b] = (uint8_t)(out->keys[i] >> (8 * (n - 1 - b)));
+  } else {
+    // keys are ids p * 256 + last byte: walk each down the levels to its
+    // first 8 bytes (the trie path, trie.cpp:139-160)
+    std::vector<uint64_t> k8(ns8);
+    if (ns8) d2h(s, k8.data(), ps8.pkeys, ns8 * sizeof(uint64_t));
+    std::vector<std::vector<uint64_t>> lv(level_len.size());
+    for (size_t L = 0; L < level_len.size(); ++L) {
+      lv[L].resize(level_len[L]);
+      if (level_len[L])
+        d2h(s, lv[L].data(), s.chain_ids[9 + L]->p, level_len[L] * sizeof(uint64_t));
+    }
+    for (uint64_t i = 0; i < out_len; ++i) {
+      uint8_t* g = out->grams + i * n;
+      uint64_t id = out->keys[i];
+      for (uint32_t L = n; L > 8; --L) {
+        g[L - 1] = (uint8_t)(id & 255);
+        const uint64_t r = id >> 8;  // rank at level L - 1
+        id = L - 1 > 8 ? lv[L - 1 - 9][r] : k8[r];
+      }
+      for (uint32_t b = 0; b < 8; ++b) g[b] = (uint8_t)(id >> (8 * (7 - b)));
+    }
+    free(out->keys);
+    out->keys = nullptr;  // n > 8: the grams do not fit packed u64 keys
+  }
   for (size_t i = 0; i < rows.size(); ++i) {
     rows[i].st.seconds = tm.seconds(rows[i].ev);
     out->passes[i] = rows[i].st;
@@ -1235,6 +1343,7 @@ void ig_result_free(ig_result* r) {
   if (!r) return;
   free(r->keys);
   free(r->counts);
+  free(r->grams);
   free(r->passes);
   free(r->diagnostics);
   r->keys = nullptr;

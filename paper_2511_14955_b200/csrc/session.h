@@ -9,6 +9,7 @@
 
 #include <cstdio>
 #include <functional>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -58,6 +59,10 @@ struct Session {
   DevBuf hot_keys, hot_ids, hot_work, hot_bounds;  // count-all hot-gram tables (§3.2e)
   DevBuf sort_keys, sort_vals, sort_tmp;           // count-all survivors in key order
   DevBuf hitmask[2];  // count-all hit chaining (ping-pong by pass parity)
+  // grams longer than 8 bytes (passes j >= 9): per level L >= 9 the survivor
+  // ids in id order and the id -> rank table; the device array of tables
+  std::vector<std::unique_ptr<DevBuf>> chain_ids, chain_remap;
+  DevBuf chain_ptrs, chain_ranks, chain_sort_tmp;
   DevBuf surv_keys, surv_counts, next_keys, next_counts;
   DevBuf pkeys, hkeys, hidx, hpacked, owner, owner_cnt, owner_start, cursor, rank_of_p;
   DevBuf sel_state, sel_hist, sel_scalar, units, unit_first;
@@ -203,6 +208,13 @@ void run_host_streamed(Session& s, const uint8_t* mem, const uint8_t* const* seq
                        std::vector<uint64_t>& hoff, const ig_params& p, ig_result* out);
 template <typename CT>
 void count_once_exact(Session& s, uint32_t L, const DevPrefixSet& ps, uint64_t cap, CT* table);
+// Extension pass j >= 9 (exact.cu): ranks walked from the 8-byte survivors
+// (ps8) through the per-level id -> rank tables (remap, device array).
+template <typename CT>
+void count_chain_exact(Session& s, uint32_t j, const DevPrefixSet& ps8,
+                       const uint32_t* const* remap, int mode, uint64_t cap, CT* table);
+void launch_scatter_rank(const uint64_t* sorted_ids, uint64_t n, uint32_t* remap,
+                         cudaStream_t st);
 void init_select(Session& s);
 
 }  // namespace igb

@@ -97,8 +97,9 @@ class IntergramsResult:
     topk: List[GramCount]
     passes: List[PassResult]
     diagnostics: List[str]
-    keys: np.ndarray = field(default=None, repr=False)
+    keys: np.ndarray = field(default=None, repr=False)  # packed u64 (n <= 8; None above)
     counts: np.ndarray = field(default=None, repr=False)
+    grams: np.ndarray = field(default=None, repr=False)  # (len, n) uint8, every n
 
 
 @dataclass
@@ -244,12 +245,22 @@ def _result(r: N.ig_result, materialize: bool = True) -> IntergramsResult:
     """materialize=False keeps the list as numpy keys/counts only (topk = [])."""
     n = int(r.len)
     gl = int(r.gram_len)
-    keys = np.ctypeslib.as_array(r.keys, shape=(max(n, 1),))[:n].copy() if n else \
-        np.zeros(0, np.uint64)
     counts = np.ctypeslib.as_array(r.counts, shape=(max(n, 1),))[:n].copy() if n else \
         np.zeros(0, np.uint64)
-    topk = [GramCount(key_to_gram(int(k), gl), int(c)) for k, c in zip(keys, counts)] \
-        if materialize else []
+    grams = None
+    if r.grams and n:
+        grams = np.ctypeslib.as_array(r.grams, shape=(n * gl,)).copy().reshape(n, gl)
+    elif r.grams or gl > 8:
+        grams = np.zeros((0, gl), np.uint8)
+    if r.keys:
+        keys = np.ctypeslib.as_array(r.keys, shape=(max(n, 1),))[:n].copy() if n else \
+            np.zeros(0, np.uint64)
+        topk = [GramCount(key_to_gram(int(k), gl), int(c)) for k, c in zip(keys, counts)] \
+            if materialize else []
+    else:  # n > 8: grams only
+        keys = None
+        topk = [GramCount(bytes(g), int(c)) for g, c in zip(grams, counts)] \
+            if materialize else []
     passes = []
     for i in range(int(r.num_passes)):
         p = r.passes[i]
@@ -257,7 +268,8 @@ def _result(r: N.ig_result, materialize: bool = True) -> IntergramsResult:
                                  int(p.bytes_processed), int(p.candidate_space),
                                  int(p.retained), bool(p.retained_short)))
     diag = (r.diagnostics or b"").decode()
-    return IntergramsResult(topk, passes, [d for d in diag.split("\n") if d], keys, counts)
+    return IntergramsResult(topk, passes, [d for d in diag.split("\n") if d], keys, counts,
+                            grams)
 
 
 def run_intergrams(corpus, cfg: IntergramConfig) -> IntergramsResult:
@@ -402,8 +414,11 @@ def shard_range(offsets: np.ndarray, rank: int, world: int) -> Tuple[int, int]:
 
 def run_result_topk(r: IntergramsResult, n: int) -> List[GramCount]:
     """The GramCount list of a result (materialised from keys/counts if needed)."""
-    if r.topk or r.keys is None:
+    if r.topk:
         return r.topk
+    if r.keys is None:
+        return [GramCount(bytes(g), int(c)) for g, c in zip(r.grams, r.counts)] \
+            if r.grams is not None else r.topk
     return [GramCount(key_to_gram(int(k), n), int(c)) for k, c in zip(r.keys, r.counts)]
 
 

@@ -40,8 +40,7 @@ def test_version():
 
 
 @pytest.mark.parametrize("n,k,z,msg", [(0, 1, 1.0, "gram length"), (4, 0, 1.0, "k must"),
-                                       (4, 1, 0.5, "oversample"), (4, 1, float("nan"), "oversample"),
-                                       (9, 1, 1.5, "above 8")])
+                                       (4, 1, 0.5, "oversample"), (4, 1, float("nan"), "oversample")])
 def test_invalid_config_rejected_before_device(n, k, z, msg):
     corpus = ig.make_memory_corpus([b"abcdefgh"])
     params = N.ig_params(n=n, k=k, z=z, mode=0, flush_batch_size=8, device=-1)
@@ -89,3 +88,17 @@ def test_shard_range_partitions_whole_sequences(world):
     total = int(off[-1])
     for a, b in got:  # byte balance within one sequence of the ideal cut
         assert abs(int(off[b] - off[a]) - total / world) <= 2 * lens.max() + 1
+
+
+@pytest.mark.parametrize("n", [9, 16, 64])
+def test_long_grams_pass_validation(n):
+    # the reference takes any n (intergrams.cpp:37-42): no ConfigError (on a
+    # box without a GPU the call then fails at the device, not in validation)
+    corpus = ig.make_memory_corpus([b"abcdefghijklmnop"])
+    params = N.ig_params(n=n, k=3, z=1.5, mode=0, flush_batch_size=8, device=-1)
+    out = N.ig_result()
+    err = C.create_string_buffer(256)
+    rc = N.lib().ig_topk_ngrams(C.byref(corpus._view()), C.byref(params), C.byref(out), err, 256)
+    assert rc != N.IG_ECONFIG, err.value
+    if rc == N.IG_OK:
+        N.lib().ig_result_free(C.byref(out))

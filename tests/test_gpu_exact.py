@@ -170,3 +170,19 @@ def test_c2_once_counts_equal_featurize_popcounts(gpu_lib):
     m = ig.featurize(c, r.topk)
     pops = m.column_popcounts()
     assert pops == [g.count for g in r.topk]
+
+
+def test_hashgram_large_b_equals_oracle(gpu_lib):
+    # the corpora of the reference's own test_hashgram.cpp:86-101 (B = 2^40,
+    # n = 4, k = 8, count-once, seed 7): the GPU path equals the reference
+    # algorithm (oracle) there; the reference binary itself cannot allocate
+    # CountTable(2^40) (tests/test_ref_unit_tests.py)
+    rng = O.Mt64(1234)
+    for _ in range(10):
+        d, off = O.csr(O.random_corpus(rng, 10, 100, 4))
+        r = ig.run_hashgram(corpus_of(d, off), ig.HashgramConfig(
+            buckets=1 << 40, n=4, k=8, mode=ONCE, seed=7))
+        rc, keys, counts, kept, ex = O.oracle_hashgram(d, off, 4, 8, 0, 1 << 40, 7)
+        assert rc == 0
+        assert as_tsv(r.topk) == util.tsv(keys, counts, 4)
+        assert r.passes[1].retained == kept and r.passes[2].retained == ex
