@@ -284,6 +284,29 @@ __device__ __forceinline__ uint32_t hlookup_packed(const uint64_t* __restrict__ 
   }
 }
 
+__device__ __forceinline__ uint32_t hlookup_packed_from(const uint64_t* __restrict__ tab,
+                                                     uint32_t lgS, uint32_t ib, uint64_t key,
+                                                     uint32_t h) {
+  const uint32_t mask = (1u << lgS) - 1;
+  for (;;) {
+    const uint64_t e = __ldg(tab + h);
+    if (e == kEmptyKey) return 0xffffffffu;
+    if ((e >> ib) == key) return (uint32_t)(e & ((1ull << ib) - 1));
+    h = (h + 1) & mask;
+  }
+}
+
+__device__ __forceinline__ uint32_t hlookup_wide_from(const uint64_t* __restrict__ wide,
+                                                   uint32_t lgS, uint64_t key, uint32_t h) {
+  const uint32_t mask = (1u << lgS) - 1;
+  for (;;) {
+    const ulonglong2 e = __ldg(reinterpret_cast<const ulonglong2*>(wide) + h);
+    if (e.x == key) return (uint32_t)e.y;
+    if (e.x == kEmptyKey) return 0xffffffffu;
+    h = (h + 1) & mask;
+  }
+}
+
 __device__ __forceinline__ uint32_t hlookup_wide(const uint64_t* __restrict__ wide, uint32_t lgS,
                                                  uint64_t key) {
   const uint32_t mask = (1u << lgS) - 1;
@@ -300,8 +323,51 @@ __device__ __forceinline__ uint32_t hlookup_wide(const uint64_t* __restrict__ wi
 // global prefix set, 4 {key, p} slots, 5 rank bitmap of 3-byte prefixes.
 // CT: pass table (hot flushes); CC: cold REDs (CT itself, or a u32
 // per-segment scratch when CT is u64).
-template <int KIND, int L, int TAB, typename CT, typename CC>
-__global__ void __launch_bounds__(1024, 1)
+// Resolves one cold position's probe whose first slot `e` (slot h) is
+// already loaded; later slots (a collision chain, rare at load <= 0.5) are
+// read in order.
+template <int TAB>
+__device__ __forceinline__ uint32_t hresolve(const uint64_t* __restrict__ ptab,
+                                             const DevPrefixSet& ps, uint64_t pk, uint32_t h,
+                                             ulonglong2 e) {
+  if constexpr (TAB == 5) {
+    const uint64_t bit = 1ull << (pk & 63);
+    return (e.x & bit) ? (uint32_t)e.y + (uint32_t)__popcll(e.x & (bit - 1)) : 0xffffffffu;
+  } else if constexpr (TAB == 3) {
+    if (e.x == kEmptyKey) return 0xffffffffu;
+    if ((e.x >> ps.ib) == pk) return (uint32_t)(e.x & ((1ull << ps.ib) - 1));
+    return hlookup_packed_from(ptab, ps.lgS, ps.ib, pk, (h + 1) & ((1u << ps.lgS) - 1));
+  } else {
+    if (e.x == pk) return (uint32_t)e.y;
+    if (e.x == kEmptyKey) return 0xffffffffu;
+    return hlookup_wide_from(ptab, ps.lgS, pk, (h + 1) & ((1u << ps.lgS) - 1));
+  }
+}
+
+// First probe slot of a cold position: TAB 5 the rank-bitmap word pair, 3 a
+// packed slot, 4 a {key, p} slot.
+template <int TAB>
+__device__ __forceinline__ ulonglong2 hfirst(const uint64_t* __restrict__ ptab,
+                                             const DevPrefixSet& ps, uint64_t pk, uint32_t& h) {
+  if constexpr (TAB == 5) {
+    h = 0;
+    return __ldg(reinterpret_cast<const ulonglong2*>(ptab) + (pk >> 6));
+  } else if constexpr (TAB == 3) {
+    h = hash_slot(pk, ps.lgS);
+    return make_ulonglong2(__ldg(ptab + h), 0ull);
+  } else {
+    h = hash_slot(pk, ps.lgS);
+    return __ldg(reinterpret_cast<const ulonglong2*>(ptab) + h);
+  }
+}
+
+// Threads per CTA: 1024 (64 registers) for the serial kernel; the phased
+// probes keep PB first slots live per lane, so 768 threads (80 registers).
+template <bool PH>
+constexpr int hot_threads() { return PH ? 768 : 1024; }
+
+template <int KIND, int L, int TAB, typename CT, typename CC, bool PH = false>
+__global__ void __launch_bounds__(hot_threads<PH>(), 1)
     k_count_hot(DevCorpus c, DevPrefixSet ps, const uint64_t* __restrict__ ptab, HotSweep hw,
                 CT* __restrict__ table, CC* __restrict__ cold) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -363,6 +429,64 @@ __global__ void __launch_bounds__(1024, 1)
         vm &= (mk << 1) | (((lane == 0 ? mk >> 16 : up) >> 15) & 1u);
       }
       uint32_t hm = 0;
+      if constexpr (PH && KIND == 1) {
+        // phase 1: the shared-memory hot table; positions not found there
+        // (in this slice) are left in `cm`
+        uint32_t cm = 0;
+        hstatic_for<0, 16>([&](auto tc) {
+          constexpr int T = decltype(tc)::value;
+          if ((vm >> T) & 1u) {
+            const uint64_t key = hkey8_at<T>(s) & hgram_mask<L>();
+            const uint64_t sk = key >> 8;
+            if (sk >= lo && sk < hi) {
+              const uint32_t b = hot_bucket(key, hw.lgnb);
+              const ulonglong2 e = skeys[b];
+              const uint32_t slot = e.x == key ? 2 * b : (e.y == key ? 2 * b + 1 : 0xffffffffu);
+              if (slot != 0xffffffffu) {
+                atomicAdd(scnt + slot, 1u);
+                hm |= 1u << T;
+              } else {
+                cm |= 1u << T;
+              }
+            }
+          }
+        });
+        // phase 2: the L2 prefix probes of the cold positions, PB first
+        // slots in flight at once (one L2 round trip per group instead of
+        // one per position), then one RED per hit.  The window words pass
+        // an optimisation barrier so phase 2 recomputes its keys (a few ALU
+        // ops) instead of keeping phase 1's 16 keys live.
+#pragma unroll
+        for (int i = 0; i < 7; ++i) asm volatile("" : "+r"(s.W[i]));
+        constexpr int PB = 4;
+        hstatic_for<0, 16 / PB>([&](auto gc) {
+          constexpr int G = decltype(gc)::value;
+          if ((cm >> (G * PB)) & ((1u << PB) - 1u)) {
+            ulonglong2 e[PB];
+            uint32_t h[PB];
+            hstatic_for<0, PB>([&](auto ic) {
+              constexpr int I = decltype(ic)::value;
+              constexpr int T = G * PB + I;
+              if ((cm >> T) & 1u) {
+                const uint64_t key = hkey8_at<T>(s) & hgram_mask<L>();
+                e[I] = hfirst<TAB>(ptab, ps, key >> 8, h[I]);
+              }
+            });
+            hstatic_for<0, PB>([&](auto ic) {
+              constexpr int I = decltype(ic)::value;
+              constexpr int T = G * PB + I;
+              if ((cm >> T) & 1u) {
+                const uint64_t key = hkey8_at<T>(s) & hgram_mask<L>();
+                const uint32_t p = hresolve<TAB>(ptab, ps, key >> 8, h[I], e[I]);
+                if (p != 0xffffffffu) {
+                  atomicAdd(cold + ((uint64_t)p * 256 + (uint32_t)(key & 0xff)), (CC)1);
+                  hm |= 1u << T;
+                }
+              }
+            });
+          }
+        });
+      } else
       hstatic_for<0, 16>([&](auto tc) {
         constexpr int T = decltype(tc)::value;
         if ((vm >> T) & 1u) {
@@ -417,8 +541,7 @@ void launch_count_hot(const DevCorpus& c, const DevPrefixSet& ps, bool dense, ui
                       const HotSweep& hw, CT* table, CC* cold, int num_sms, cudaStream_t st) {
   if (c.ntiles <= c.tile0) return;
   const size_t smem = hot_smem(hw.lgnb);
-  const int threads = 1024;
-  auto go = [&](auto kern, const uint64_t* ptab) {
+  auto go = [&](auto kern, const uint64_t* ptab, int threads = 1024) {
     IGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per = 0;
     IGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, threads, smem));
@@ -435,11 +558,21 @@ void launch_count_hot(const DevCorpus& c, const DevPrefixSet& ps, bool dense, ui
     }
     return;
   }
-#define IGB_HOT_J(J)                                                             \
-  case J:                                                                        \
-    if (J == 4 && ps.rankbits) go(k_count_hot<1, J, 5, CT, CC>, ps.rankbits);    \
-    else if (ps.packed) go(k_count_hot<1, J, 3, CT, CC>, ps.packed);             \
-    else go(k_count_hot<1, J, 4, CT, CC>, ps.wide);                              \
+  // phased probes (cold positions' first L2 slots issued together); the
+  // one-position-at-a-time kernel stays behind IG_HOT_SERIAL=1
+  static const bool serial = getenv("IG_HOT_SERIAL") != nullptr;
+#define IGB_HOT_J(J)                                                                     \
+  case J:                                                                                \
+    if (J == 4 && ps.rankbits) {                                                         \
+      if (serial) go(k_count_hot<1, J, 5, CT, CC>, ps.rankbits);                         \
+      else go(k_count_hot<1, J, 5, CT, CC, true>, ps.rankbits, hot_threads<true>());                          \
+    } else if (ps.packed) {                                                              \
+      if (serial) go(k_count_hot<1, J, 3, CT, CC>, ps.packed);                           \
+      else go(k_count_hot<1, J, 3, CT, CC, true>, ps.packed, 768);                          \
+    } else {                                                                             \
+      if (serial) go(k_count_hot<1, J, 4, CT, CC>, ps.wide);                             \
+      else go(k_count_hot<1, J, 4, CT, CC, true>, ps.wide, 768);                            \
+    }                                                                                    \
     break;
   switch (L) {
     IGB_HOT_J(2) IGB_HOT_J(3) IGB_HOT_J(4) IGB_HOT_J(5) IGB_HOT_J(6) IGB_HOT_J(7) IGB_HOT_J(8)

@@ -272,9 +272,10 @@ def _result(r: N.ig_result, materialize: bool = True) -> IntergramsResult:
                             grams)
 
 
-def run_intergrams(corpus, cfg: IntergramConfig) -> IntergramsResult:
+def run_intergrams(corpus, cfg: IntergramConfig, materialize: bool = True) -> IntergramsResult:
     """run_intergrams (intergrams.hpp:74-75) on the GPU.  A CorpusSpec is read
-    from disk by the library (pinned slabs -> HBM, ig_topk_ngrams_files)."""
+    from disk by the library (pinned slabs -> HBM, ig_topk_ngrams_files).
+    materialize=False: the list as numpy keys/grams/counts only."""
     cfg.validate()
     if isinstance(corpus, CorpusSpec):
         spec, _keep = corpus._native()
@@ -285,7 +286,7 @@ def run_intergrams(corpus, cfg: IntergramConfig) -> IntergramsResult:
                                           len(err))
         _raise(rc, err)
         try:
-            return _result(out)
+            return _result(out, materialize)
         finally:
             N.lib().ig_result_free(C.byref(out))
     lib = N.lib()
@@ -303,7 +304,7 @@ def run_intergrams(corpus, cfg: IntergramConfig) -> IntergramsResult:
         rc = lib.ig_topk_ngrams_seqs(ptrs, lens, m, C.byref(params), C.byref(out), err, len(err))
         _raise(rc, err)
         try:
-            return _result(out)
+            return _result(out, materialize)
         finally:
             lib.ig_result_free(C.byref(out))
     c = as_corpus(corpus)
@@ -311,7 +312,7 @@ def run_intergrams(corpus, cfg: IntergramConfig) -> IntergramsResult:
     rc = lib.ig_topk_ngrams(C.byref(view), C.byref(params), C.byref(out), err, len(err))
     _raise(rc, err)
     try:
-        return _result(out)
+        return _result(out, materialize)
     finally:
         lib.ig_result_free(C.byref(out))
 

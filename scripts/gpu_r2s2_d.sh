@@ -1,0 +1,22 @@
+# call d: serial vs phased cold probes on c3 (bench + ncu of the 6-gram sweep),
+# fixed tests, long-gram tests
+set -x
+cd "${GRAFT_REPO_ROOT:-/root/repo}"
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_long_grams.py tests/test_gpu_host_paths.py tests/test_gpu_multirank.py tests/test_gpu_count_all_paths.py -q -rf > gpurun_out/pytest_new.txt 2>&1; echo rc_new=$?
+tail -5 gpurun_out/pytest_new.txt
+for env in "IG_HOT_SERIAL=1" "IG_HOT_PHASED=1"; do
+  env $env timeout 900 python bench.py --no-cpu-baseline --no-e2e > gpurun_out/bench_$env.json 2> gpurun_out/bench_$env.err; echo rc=$?
+  python -c "
+import json; j=json.loads(open('gpurun_out/bench_$env.json').read().strip().splitlines()[-1]); print('$env', round(j['value'],2), round(j['ms_per_step'],1), j['result_digest'], {k: round(v,1) for k,v in j['step_breakdown_ms'].items() if 'pass' in k})"
+done
+for env in "IG_HOT_SERIAL=1" "IG_HOT_PHASED=1"; do
+  env $env timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_count_hot --launch-skip 7 -c 1 -o gpurun_out/hot6_$env python bench.py --profile-run > gpurun_out/ncu_$env.log 2>&1
+  echo rc_ncu=$?
+  ncu -i gpurun_out/hot6_$env.ncu-rep --page details > gpurun_out/hot6_${env}_details.txt 2>/dev/null
+  ncu -i gpurun_out/hot6_$env.ncu-rep --page raw --csv > gpurun_out/hot6_${env}_raw.csv 2>/dev/null
+  ncu -i gpurun_out/hot6_$env.ncu-rep --page source --csv > gpurun_out/hot6_${env}_source.csv 2>/dev/null
+  rm -f gpurun_out/hot6_$env.ncu-rep
+done
+gzip -f gpurun_out/*_source.csv gpurun_out/*_raw.csv
+du -sh gpurun_out

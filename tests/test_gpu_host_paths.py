@@ -72,8 +72,17 @@ def test_host_corpus_paths_equal_reference(gpu_lib, n, k, mode, path):
 
 def test_seqs_entry_point_edge_cases(gpu_lib):
     cfg = ig.IntergramConfig(n=4, k=10, z=1.5, mode=ig.CountMode.kAll)
-    assert len(ig.run_intergrams([], cfg).keys) == 0
-    assert len(ig.run_intergrams([b"", b""], cfg).keys) == 0
+    # no bytes: the dense pass keeps nothing and the 4-gram pass has a
+    # depth-0 trie, a ConfigError on the reference too (intergrams.cpp:46-48)
+    for empty in ([], [b"", b""]):
+        rc = O.ref_run_grams(np.zeros(0, np.uint8), np.zeros(len(empty) + 1, np.uint64),
+                             4, 10, 1.5, 1, 0)[0]
+        assert rc == 2
+        with pytest.raises(ig.ConfigError):
+            ig.run_intergrams(empty, cfg)
+    cfg3 = ig.IntergramConfig(n=3, k=10, z=1.5, mode=ig.CountMode.kAll)
+    assert len(ig.run_intergrams([], cfg3).counts) == 0
+    assert len(ig.run_intergrams([b"", b""], cfg3).counts) == 0
     r = ig.run_intergrams([b"abcdabcd", b"", b"cdab"], cfg)
     rc, keys, counts, _, _ = O.oracle_run(np.frombuffer(b"abcdabcdcdab", np.uint8),
                                           np.array([0, 8, 8, 12], np.uint64), 4, 10, 1.5, 1)

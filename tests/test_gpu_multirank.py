@@ -87,10 +87,16 @@ def test_two_ranks_equal_one(gpu_lib, name, n, k, mode):
                [p.bytes_processed for p in single.passes]
 
 
-def test_two_ranks_u64_tables_narrowed(gpu_lib):
+@pytest.mark.parametrize("force_u64", [False, True])
+def test_two_ranks_u64_tables_narrowed(gpu_lib, monkeypatch, force_u64):
     """Count-all with a total that might reach 2^32 (bytes_total 8 GiB): the
-    tables are u64, and each pass's all-reduce goes through the hook as one
-    u64 bound (sum of the per-rank maxima) followed by the table as u32."""
+    dense table is u64, and its all-reduce goes through the hook as one u64
+    bound (sum of the per-rank maxima) followed by the table as u32.  Every
+    extension pass's counts are bounded by the previous pass's top count,
+    so those tables are u32 from the start (one call each) -- unless u64
+    tables are forced, when every pass takes the bound + u32 route."""
+    if force_u64:
+        monkeypatch.setenv("IG_FORCE_U64", "1")
     cfg = S.scaled(S.CONFIGS["c5"], num_seqs=16, seq_len=65536)
     data, off = S.generate(cfg)
     icfg = ig.IntergramConfig(n=6, k=300, z=1.5, mode=ig.CountMode.kAll)
@@ -116,8 +122,10 @@ def test_two_ranks_u64_tables_narrowed(gpu_lib):
     for t in ts:
         t.join(timeout=300)
     passes = 6 - 2
-    assert ar.calls == 2 * passes
-    assert [d for d, _ in ar.dtypes] == [1, 0] * passes  # bound (u64), then the table (u32)
+    # bound (u64), then the table (u32)
+    want = [1, 0] * passes if force_u64 else [1, 0] + [0] * (passes - 1)
+    assert ar.calls == len(want)
+    assert [d for d, _ in ar.dtypes] == want
     assert all(c == 1 for d, c in ar.dtypes if d == 1)
     for r in range(2):
         assert results[r] is not None
