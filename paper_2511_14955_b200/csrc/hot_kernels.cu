@@ -323,6 +323,43 @@ __device__ __forceinline__ uint32_t hlookup_wide(const uint64_t* __restrict__ wi
 // global prefix set, 4 {key, p} slots, 5 rank bitmap of 3-byte prefixes.
 // CT: pass table (hot flushes); CC: cold REDs (CT itself, or a u32
 // per-segment scratch when CT is u64).
+// A probe that reads whole buckets from the key's (4-aligned) home: TAB 3
+// four packed slots (one 32-byte sector, two 16-byte loads) per step, TAB 4
+// two {key, p} slots, TAB 5 the rank-bitmap word pair (no probing).  The
+// first empty slot ends a miss (linear probing, no deletions).
+template <int TAB>
+__device__ __forceinline__ uint32_t hlookup_bucket(const uint64_t* __restrict__ ptab,
+                                                   const DevPrefixSet& ps, uint64_t pk) {
+  if constexpr (TAB == 5) {
+    return hlookup_rank(ptab, (uint32_t)pk);
+  } else if constexpr (TAB == 3) {
+    const uint32_t mask = (1u << ps.lgS) - 1;
+    const uint64_t pmask = (1ull << ps.ib) - 1;
+    for (uint32_t h = hash_slot(pk, ps.lgS);; h = (h + 4) & mask) {
+      const ulonglong2* b = reinterpret_cast<const ulonglong2*>(ptab + h);
+      const ulonglong2 x = __ldg(b), y = __ldg(b + 1);
+      if (x.x == kEmptyKey) return 0xffffffffu;
+      if ((x.x >> ps.ib) == pk) return (uint32_t)(x.x & pmask);
+      if (x.y == kEmptyKey) return 0xffffffffu;
+      if ((x.y >> ps.ib) == pk) return (uint32_t)(x.y & pmask);
+      if (y.x == kEmptyKey) return 0xffffffffu;
+      if ((y.x >> ps.ib) == pk) return (uint32_t)(y.x & pmask);
+      if (y.y == kEmptyKey) return 0xffffffffu;
+      if ((y.y >> ps.ib) == pk) return (uint32_t)(y.y & pmask);
+    }
+  } else {
+    const uint32_t mask = (1u << ps.lgS) - 1;
+    for (uint32_t h = hash_slot(pk, ps.lgS);; h = (h + 2) & mask) {
+      const ulonglong2* b = reinterpret_cast<const ulonglong2*>(ptab) + h;
+      const ulonglong2 x = __ldg(b), y = __ldg(b + 1);
+      if (x.x == pk) return (uint32_t)x.y;
+      if (x.x == kEmptyKey) return 0xffffffffu;
+      if (y.x == pk) return (uint32_t)y.y;
+      if (y.x == kEmptyKey) return 0xffffffffu;
+    }
+  }
+}
+
 // Resolves one cold position's probe whose first slot `e` (slot h) is
 // already loaded; later slots (a collision chain, rare at load <= 0.5) are
 // read in order.
@@ -361,10 +398,13 @@ __device__ __forceinline__ ulonglong2 hfirst(const uint64_t* __restrict__ ptab,
   }
 }
 
-// Threads per CTA: 1024 (64 registers) for the serial kernel; the phased
-// probes keep PB first slots live per lane, so 768 threads (80 registers).
+// Per-warp cold queue of the extension sweep (PH): kHotQ gram keys and
+// positions, and the hit bits its drains found, per lane.
+constexpr int kHotQ = 64;
+constexpr size_t kHotQWarpBytes = kHotQ * 8 + kHotQ * 2 + 32 * 4;
+
 template <bool PH>
-constexpr int hot_threads() { return PH ? 768 : 1024; }
+constexpr int hot_threads() { return 1024; }
 
 template <int KIND, int L, int TAB, typename CT, typename CC, bool PH = false>
 __global__ void __launch_bounds__(hot_threads<PH>(), 1)
@@ -379,11 +419,37 @@ __global__ void __launch_bounds__(hot_threads<PH>(), 1)
     for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) skeys[i] = gk[i];
     for (uint32_t i = threadIdx.x; i < 2 * nb; i += blockDim.x) scnt[i] = 0;
   }
-  __syncthreads();
   const int lane = threadIdx.x & 31;
+  // this warp's cold queue (extension sweep with queued probes)
+  unsigned char* qbase =
+      smem_raw + ((size_t)nb * 24) + (size_t)(threadIdx.x >> 5) * kHotQWarpBytes;
+  uint64_t* qkey = reinterpret_cast<uint64_t*>(qbase);
+  uint16_t* qpos = reinterpret_cast<uint16_t*>(qbase + kHotQ * 8);
+  uint32_t* qhit = reinterpret_cast<uint32_t*>(qbase + kHotQ * 10);
+  uint32_t qhead = 0, qtail = 0;  // warp-uniform
+  const uint32_t lt_mask = (1u << lane) - 1u;
+  if constexpr (PH && KIND == 1) qhit[lane] = 0;
+  const bool sliced = hw.sliced;
+  __syncthreads();
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   const uint64_t lo = hw.bounds[0], hi = hw.bounds[1];  // this slice's key range
   const bool chain = KIND == 1 && ps.hit_in != nullptr;
+  // cnt queued positions from the head, one per lane: bucket probe in L2,
+  // one RED per hit, its hit bit into qhit
+  auto drain = [&](uint32_t cnt) {
+    if (lane < cnt) {
+      const uint32_t qi = (qhead + lane) & (kHotQ - 1);
+      const uint64_t key = qkey[qi];
+      const uint32_t pos = qpos[qi];
+      const uint32_t p = hlookup_bucket<TAB>(ptab, ps, key >> 8);
+      if (p != 0xffffffffu) {
+        atomicAdd(cold + ((uint64_t)p * 256 + (uint32_t)(key & 0xff)), (CC)1);
+        atomicOr(qhit + (pos >> 4), 1u << (pos & 15));
+      }
+    }
+    qhead += cnt;
+    __syncwarp();
+  };
   uint64_t t = c.tile0 + ((blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5);
   if (t < c.ntiles) {
     // the next tile's loads stay in flight while the current one is counted
@@ -430,15 +496,18 @@ __global__ void __launch_bounds__(hot_threads<PH>(), 1)
       }
       uint32_t hm = 0;
       if constexpr (PH && KIND == 1) {
-        // phase 1: the shared-memory hot table; positions not found there
-        // (in this slice) are left in `cm`
-        uint32_t cm = 0;
+        // hot grams in shared memory; the others go to this warp's queue
+        // (ballot-compacted), drained 32 at a time with every lane probing
+        // one position: the L2 probes of a whole tile then cost a few round
+        // trips with full warps instead of one divergent round trip per T
         hstatic_for<0, 16>([&](auto tc) {
           constexpr int T = decltype(tc)::value;
+          bool cq = false;
+          uint64_t key = 0;
           if ((vm >> T) & 1u) {
-            const uint64_t key = hkey8_at<T>(s) & hgram_mask<L>();
+            key = hkey8_at<T>(s) & hgram_mask<L>();
             const uint64_t sk = key >> 8;
-            if (sk >= lo && sk < hi) {
+            if (!sliced || (sk >= lo && sk < hi)) {
               const uint32_t b = hot_bucket(key, hw.lgnb);
               const ulonglong2 e = skeys[b];
               const uint32_t slot = e.x == key ? 2 * b : (e.y == key ? 2 * b + 1 : 0xffffffffu);
@@ -446,53 +515,36 @@ __global__ void __launch_bounds__(hot_threads<PH>(), 1)
                 atomicAdd(scnt + slot, 1u);
                 hm |= 1u << T;
               } else {
-                cm |= 1u << T;
+                cq = true;
               }
             }
           }
-        });
-        // phase 2: the L2 prefix probes of the cold positions, PB first
-        // slots in flight at once (one L2 round trip per group instead of
-        // one per position), then one RED per hit.  The window words pass
-        // an optimisation barrier so phase 2 recomputes its keys (a few ALU
-        // ops) instead of keeping phase 1's 16 keys live.
-#pragma unroll
-        for (int i = 0; i < 7; ++i) asm volatile("" : "+r"(s.W[i]));
-        constexpr int PB = 4;
-        hstatic_for<0, 16 / PB>([&](auto gc) {
-          constexpr int G = decltype(gc)::value;
-          if ((cm >> (G * PB)) & ((1u << PB) - 1u)) {
-            ulonglong2 e[PB];
-            uint32_t h[PB];
-            hstatic_for<0, PB>([&](auto ic) {
-              constexpr int I = decltype(ic)::value;
-              constexpr int T = G * PB + I;
-              if ((cm >> T) & 1u) {
-                const uint64_t key = hkey8_at<T>(s) & hgram_mask<L>();
-                e[I] = hfirst<TAB>(ptab, ps, key >> 8, h[I]);
-              }
-            });
-            hstatic_for<0, PB>([&](auto ic) {
-              constexpr int I = decltype(ic)::value;
-              constexpr int T = G * PB + I;
-              if ((cm >> T) & 1u) {
-                const uint64_t key = hkey8_at<T>(s) & hgram_mask<L>();
-                const uint32_t p = hresolve<TAB>(ptab, ps, key >> 8, h[I], e[I]);
-                if (p != 0xffffffffu) {
-                  atomicAdd(cold + ((uint64_t)p * 256 + (uint32_t)(key & 0xff)), (CC)1);
-                  hm |= 1u << T;
-                }
-              }
-            });
+          const uint32_t bal = __ballot_sync(0xffffffffu, cq);
+          if (cq) {
+            const uint32_t qi = (qtail + __popc(bal & lt_mask)) & (kHotQ - 1);
+            qkey[qi] = key;
+            qpos[qi] = (uint16_t)((lane << 4) | T);
+          }
+          qtail += __popc(bal);
+          if (qtail - qhead >= 32) {
+            __syncwarp();
+            drain(32u);
           }
         });
+        if (qtail != qhead) {
+          __syncwarp();
+          drain(qtail - qhead);
+        }
+        __syncwarp();
+        hm |= qhit[lane];
+        qhit[lane] = 0;
       } else
       hstatic_for<0, 16>([&](auto tc) {
         constexpr int T = decltype(tc)::value;
         if ((vm >> T) & 1u) {
           const uint64_t key = hkey8_at<T>(s) & hgram_mask<L>();
           const uint64_t sk = KIND == 1 ? key >> 8 : key;
-          if (sk >= lo && sk < hi) {
+          if (!sliced || (sk >= lo && sk < hi)) {
             const uint32_t b = hot_bucket(key, hw.lgnb);
             const ulonglong2 e = skeys[b];
             const uint32_t slot = e.x == key ? 2 * b : (e.y == key ? 2 * b + 1 : 0xffffffffu);
@@ -535,13 +587,17 @@ __global__ void __launch_bounds__(hot_threads<PH>(), 1)
 }
 
 size_t hot_smem(uint32_t lgnb) { return ((size_t)1 << lgnb) * 24; }
+static size_t hot_smem_q(uint32_t lgnb, int threads) {
+  return hot_smem(lgnb) + (size_t)(threads / 32) * kHotQWarpBytes;
+}
 
 template <typename CT, typename CC>
 void launch_count_hot(const DevCorpus& c, const DevPrefixSet& ps, bool dense, uint32_t L,
                       const HotSweep& hw, CT* table, CC* cold, int num_sms, cudaStream_t st) {
   if (c.ntiles <= c.tile0) return;
-  const size_t smem = hot_smem(hw.lgnb);
-  auto go = [&](auto kern, const uint64_t* ptab, int threads = 1024) {
+  auto go = [&](auto kern, const uint64_t* ptab, bool queued = false) {
+    const int threads = 1024;
+    const size_t smem = queued ? hot_smem_q(hw.lgnb, threads) : hot_smem(hw.lgnb);
     IGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per = 0;
     IGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, threads, smem));
@@ -558,20 +614,20 @@ void launch_count_hot(const DevCorpus& c, const DevPrefixSet& ps, bool dense, ui
     }
     return;
   }
-  // phased probes (cold positions' first L2 slots issued together); the
-  // one-position-at-a-time kernel stays behind IG_HOT_SERIAL=1
+  // queued cold probes (ballot-compacted per warp, probed 32 at a time);
+  // the one-position-at-a-time kernel stays behind IG_HOT_SERIAL=1
   static const bool serial = getenv("IG_HOT_SERIAL") != nullptr;
 #define IGB_HOT_J(J)                                                                     \
   case J:                                                                                \
     if (J == 4 && ps.rankbits) {                                                         \
       if (serial) go(k_count_hot<1, J, 5, CT, CC>, ps.rankbits);                         \
-      else go(k_count_hot<1, J, 5, CT, CC, true>, ps.rankbits, hot_threads<true>());                          \
+      else go(k_count_hot<1, J, 5, CT, CC, true>, ps.rankbits, true);                          \
     } else if (ps.packed) {                                                              \
       if (serial) go(k_count_hot<1, J, 3, CT, CC>, ps.packed);                           \
-      else go(k_count_hot<1, J, 3, CT, CC, true>, ps.packed, 768);                          \
+      else go(k_count_hot<1, J, 3, CT, CC, true>, ps.packed, true);                          \
     } else {                                                                             \
       if (serial) go(k_count_hot<1, J, 4, CT, CC>, ps.wide);                             \
-      else go(k_count_hot<1, J, 4, CT, CC, true>, ps.wide, 768);                            \
+      else go(k_count_hot<1, J, 4, CT, CC, true>, ps.wide, true);                            \
     }                                                                                    \
     break;
   switch (L) {

@@ -205,8 +205,11 @@ struct DevPrefixSet {
   uint16_t* hit_out = nullptr;       // this pass's hits (read by the next pass), or null
 };
 
+// Home slot of a key in an open-addressing table of 2^lgS slots: always a
+// multiple of 4, so a probe can read whole 4-slot (32-byte) buckets while a
+// slot-by-slot linear probe from the same home stays valid.
 __host__ __device__ inline uint32_t hash_slot(uint64_t key, uint32_t lgS) {
-  return lgS == 0 ? 0u : (uint32_t)((key * 0x9E3779B97F4A7C15ull) >> (64 - lgS));
+  return lgS <= 2 ? 0u : (uint32_t)((key * 0x9E3779B97F4A7C15ull) >> (64 - lgS)) & ~3u;
 }
 
 // Owner slice of a prefix key (count-once passes): first byte xor last byte.

@@ -79,6 +79,7 @@ struct HotSweep {
   uint32_t lgnb = 0;
   const uint64_t* bounds = nullptr;  // device, 2 values
   bool first = true;
+  bool sliced = false;  // more than one slice: check the key range
 };
 size_t hot_smem(uint32_t lgnb);
 // Hot set of each slice from the (sample) counts in table[0, cap).  pkeys:

@@ -256,7 +256,7 @@ static DevPrefixSet build_prefix_set(Session& s, const uint64_t* keys, uint64_t 
     gs[o + 1] = gs[o] + gc[o];
     mx = std::max(mx, gc[o]);
   }
-  uint32_t lgS = 1;
+  uint32_t lgS = 2;  // >= one 4-slot bucket (hash_slot)
   while ((1ull << lgS) < 2ull * std::max<uint32_t>(mx, 1)) ++lgS;
   const uint32_t S = 1u << lgS;
   // recompute owners at width G (owner16 & (G-1) == owner_G)
@@ -605,6 +605,7 @@ static void count_all_hot(Session& s, bool dense, uint32_t L, const Prefix* P, C
       hw.lgnb = lgnb;
       hw.bounds = bounds + i;
       hw.first = i == 0;
+      hw.sliced = S > 1;
       const size_t ev = s.kt.begin(IG_KF_COUNT_ALL, s.stream);
       launch_count_hot(dc, ps, dense, L, hw, t, cold, s.num_sms, s.stream);
       s.kt.end(ev, s.stream);
