@@ -323,6 +323,30 @@ __device__ __forceinline__ uint32_t hlookup_wide(const uint64_t* __restrict__ wi
 // global prefix set, 4 {key, p} slots, 5 rank bitmap of 3-byte prefixes.
 // CT: pass table (hot flushes); CC: cold REDs (CT itself, or a u32
 // per-segment scratch when CT is u64).
+// Shared-memory accesses by 32-bit shared address (the extension sweep's
+// branch-free inner loop): a 16-byte load, and a predicated add / stores.
+__device__ __forceinline__ ulonglong2 lds_u64x2(uint32_t a) {
+  ulonglong2 v;
+  asm("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(v.x), "=l"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void red_shared_if(uint32_t a, bool p) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\t@q red.shared.add.u32 [%0], 1;\n\t}"
+               :: "r"(a), "r"((uint32_t)p) : "memory");
+}
+__device__ __forceinline__ void st_shared_u64_if(uint32_t a, uint64_t v, bool p) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.shared.u64 [%0], %1;\n\t}"
+               :: "r"(a), "l"(v), "r"((uint32_t)p) : "memory");
+}
+__device__ __forceinline__ void st_shared_u32_if(uint32_t a, uint32_t v, bool p) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.shared.u32 [%0], %1;\n\t}"
+               :: "r"(a), "r"(v), "r"((uint32_t)p) : "memory");
+}
+__device__ __forceinline__ void st_shared_u16_if(uint32_t a, uint16_t v, bool p) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.shared.u16 [%0], %1;\n\t}"
+               :: "r"(a), "h"(v), "r"((uint32_t)p) : "memory");
+}
+
 // A probe that reads whole buckets from the key's (4-aligned) home: TAB 3
 // four packed slots (one 32-byte sector, two 16-byte loads) per step, TAB 4
 // two {key, p} slots, TAB 5 the rank-bitmap word pair (no probing).  The
@@ -401,7 +425,7 @@ __device__ __forceinline__ ulonglong2 hfirst(const uint64_t* __restrict__ ptab,
 // Per-warp cold queue of the extension sweep (PH): kHotQ gram keys and
 // positions, and the hit bits its drains found, per lane.
 constexpr int kHotQ = 64;
-constexpr size_t kHotQWarpBytes = kHotQ * 8 + kHotQ * 2 + 32 * 4;
+constexpr size_t kHotQWarpBytes = kHotQ * 8 + kHotQ * 4 + 32 * 4;
 
 template <bool PH>
 constexpr int hot_threads() { return 1024; }
@@ -424,8 +448,12 @@ __global__ void __launch_bounds__(hot_threads<PH>(), 1)
   unsigned char* qbase =
       smem_raw + ((size_t)nb * 24) + (size_t)(threadIdx.x >> 5) * kHotQWarpBytes;
   uint64_t* qkey = reinterpret_cast<uint64_t*>(qbase);
-  uint16_t* qpos = reinterpret_cast<uint16_t*>(qbase + kHotQ * 8);
-  uint32_t* qhit = reinterpret_cast<uint32_t*>(qbase + kHotQ * 10);
+  uint32_t* qpos = reinterpret_cast<uint32_t*>(qbase + kHotQ * 8);
+  uint32_t* qhit = reinterpret_cast<uint32_t*>(qbase + kHotQ * 12);
+  const uint32_t s_keys = (uint32_t)__cvta_generic_to_shared(skeys);
+  const uint32_t s_cnt = (uint32_t)__cvta_generic_to_shared(scnt);
+  const uint32_t s_qkey = (uint32_t)__cvta_generic_to_shared(qkey);
+  const uint32_t s_qpos = (uint32_t)__cvta_generic_to_shared(qpos);
   uint32_t qhead = 0, qtail = 0;  // warp-uniform
   const uint32_t lt_mask = (1u << lane) - 1u;
   if constexpr (PH && KIND == 1) qhit[lane] = 0;
@@ -434,21 +462,76 @@ __global__ void __launch_bounds__(hot_threads<PH>(), 1)
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   const uint64_t lo = hw.bounds[0], hi = hw.bounds[1];  // this slice's key range
   const bool chain = KIND == 1 && ps.hit_in != nullptr;
-  // cnt queued positions from the head, one per lane: bucket probe in L2,
-  // one RED per hit, its hit bit into qhit
-  auto drain = [&](uint32_t cnt) {
+  // Queue drains are software-pipelined: drain_issue takes 32 queued
+  // positions (one per lane) and starts their first bucket loads; they are
+  // resolved (compare, RED, hit bit) by drain_resolve at the next drain, a
+  // few positions later, so the L2 round trip overlaps hot-path work.  A
+  // position carries its tile's iteration number k: if its tile is still
+  // the current one its hit bit goes to qhit (merged into the tile's
+  // hit-mask store), else straight into hit_out with an atomic OR.
+  const uint64_t tfirst = c.tile0 + ((blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5);
+  uint32_t kcur = 0;          // iteration number of the current tile
+  bool pf = false;            // a probe in flight on this lane
+  uint64_t pfkey = 0;
+  uint32_t pfpos = 0;
+  ulonglong2 pfa = make_ulonglong2(0, 0), pfb = make_ulonglong2(0, 0);
+  auto drain_resolve = [&]() {
+    if (pf) {
+      uint32_t p;
+      const uint64_t pk = pfkey >> 8;
+      if constexpr (TAB == 3) {
+        const uint64_t pmask = (1ull << ps.ib) - 1;
+        const uint64_t sl[4] = {pfa.x, pfa.y, pfb.x, pfb.y};
+        p = 0xfffffffeu;  // undecided
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if (p == 0xfffffffeu) {
+            if (sl[i] == kEmptyKey) p = 0xffffffffu;
+            else if ((sl[i] >> ps.ib) == pk) p = (uint32_t)(sl[i] & pmask);
+          }
+        if (p == 0xfffffffeu)  // a full bucket: continue from the next one
+          p = hlookup_packed_from(ptab, ps.lgS, ps.ib, pk,
+                                  (hash_slot(pk, ps.lgS) + 4) & ((1u << ps.lgS) - 1));
+      } else {
+        if (pfa.x == pk) p = (uint32_t)pfa.y;
+        else if (pfa.x == kEmptyKey) p = 0xffffffffu;
+        else if (pfb.x == pk) p = (uint32_t)pfb.y;
+        else if (pfb.x == kEmptyKey) p = 0xffffffffu;
+        else p = hlookup_wide_from(ptab, ps.lgS, pk,
+                                   (hash_slot(pk, ps.lgS) + 2) & ((1u << ps.lgS) - 1));
+      }
+      if (p != 0xffffffffu) {
+        atomicAdd(cold + ((uint64_t)p * 256 + (uint32_t)(pfkey & 0xff)), (CC)1);
+        const uint32_t k = pfpos >> 9, el = (pfpos >> 4) & 31, bit = 1u << (pfpos & 15);
+        if (k == kcur) {
+          atomicOr(qhit + el, bit);
+        } else if (ps.hit_out != nullptr) {  // its tile is done: OR into hit_out
+          const uint64_t wi = (tfirst + (uint64_t)k * nwarps) * 32 + el;
+          atomicOr(reinterpret_cast<unsigned int*>(ps.hit_out) + (wi >> 1), bit << (16 * (wi & 1)));
+        }
+      }
+      pf = false;
+    }
+  };
+  auto drain_issue = [&](uint32_t cnt) {
     if (lane < cnt) {
       const uint32_t qi = (qhead + lane) & (kHotQ - 1);
-      const uint64_t key = qkey[qi];
-      const uint32_t pos = qpos[qi];
-      const uint32_t p = hlookup_bucket<TAB>(ptab, ps, key >> 8);
-      if (p != 0xffffffffu) {
-        atomicAdd(cold + ((uint64_t)p * 256 + (uint32_t)(key & 0xff)), (CC)1);
-        atomicOr(qhit + (pos >> 4), 1u << (pos & 15));
-      }
+      pfkey = qkey[qi];
+      pfpos = qpos[qi];
+      const uint64_t pk = pfkey >> 8;
+      const uint32_t hh = hash_slot(pk, ps.lgS);
+      const ulonglong2* bk = TAB == 3 ? reinterpret_cast<const ulonglong2*>(ptab + hh)
+                                      : reinterpret_cast<const ulonglong2*>(ptab) + hh;
+      pfa = __ldg(bk);
+      pfb = __ldg(bk + 1);
+      pf = true;
     }
     qhead += cnt;
     __syncwarp();
+  };
+  auto drain = [&](uint32_t cnt) {
+    drain_resolve();
+    drain_issue(cnt);
   };
   uint64_t t = c.tile0 + ((blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5);
   if (t < c.ntiles) {
@@ -502,39 +585,32 @@ __global__ void __launch_bounds__(hot_threads<PH>(), 1)
         // trips with full warps instead of one divergent round trip per T
         hstatic_for<0, 16>([&](auto tc) {
           constexpr int T = decltype(tc)::value;
-          bool cq = false;
-          uint64_t key = 0;
-          if ((vm >> T) & 1u) {
-            key = hkey8_at<T>(s) & hgram_mask<L>();
+          // branch-free: every position is looked up (an invalid one's
+          // result is masked), the shared add and the queue stores are
+          // predicated, and shared addresses are 32-bit from one base
+          const uint64_t key = hkey8_at<T>(s) & hgram_mask<L>();
+          bool v = (vm >> T) & 1u;
+          if (sliced) {
             const uint64_t sk = key >> 8;
-            if (!sliced || (sk >= lo && sk < hi)) {
-              const uint32_t b = hot_bucket(key, hw.lgnb);
-              const ulonglong2 e = skeys[b];
-              const uint32_t slot = e.x == key ? 2 * b : (e.y == key ? 2 * b + 1 : 0xffffffffu);
-              if (slot != 0xffffffffu) {
-                atomicAdd(scnt + slot, 1u);
-                hm |= 1u << T;
-              } else {
-                cq = true;
-              }
-            }
+            v = v && sk >= lo && sk < hi;
           }
+          const uint32_t b = hot_bucket(key, hw.lgnb);
+          const ulonglong2 e = lds_u64x2(s_keys + b * 16);
+          const bool h1 = e.y == key;
+          const bool hot = v && (e.x == key || h1);
+          red_shared_if(s_cnt + (2 * b + (uint32_t)h1) * 4, hot);
+          hm |= (uint32_t)hot << T;
+          const bool cq = v && !hot;
           const uint32_t bal = __ballot_sync(0xffffffffu, cq);
-          if (cq) {
-            const uint32_t qi = (qtail + __popc(bal & lt_mask)) & (kHotQ - 1);
-            qkey[qi] = key;
-            qpos[qi] = (uint16_t)((lane << 4) | T);
-          }
+          const uint32_t qi = (qtail + __popc(bal & lt_mask)) & (kHotQ - 1);
+          st_shared_u64_if(s_qkey + qi * 8, key, cq);
+          st_shared_u32_if(s_qpos + qi * 4, (kcur << 9) | (lane << 4) | T, cq);
           qtail += __popc(bal);
           if (qtail - qhead >= 32) {
             __syncwarp();
             drain(32u);
           }
         });
-        if (qtail != qhead) {
-          __syncwarp();
-          drain(qtail - qhead);
-        }
         __syncwarp();
         hm |= qhit[lane];
         qhit[lane] = 0;
@@ -577,6 +653,17 @@ __global__ void __launch_bounds__(hot_threads<PH>(), 1)
       h = hn;
       d = dn;
       mk = mkn;
+      ++kcur;
+    }
+  }
+  if constexpr (PH && KIND == 1) {  // the warp's last probes: every tile is done
+    __syncwarp();
+    ++kcur;
+    drain_resolve();
+    while (qtail != qhead) {
+      const uint32_t n = qtail - qhead < 32u ? qtail - qhead : 32u;
+      drain_issue(n);
+      drain_resolve();
     }
   }
   __syncthreads();
@@ -619,9 +706,8 @@ void launch_count_hot(const DevCorpus& c, const DevPrefixSet& ps, bool dense, ui
   static const bool serial = getenv("IG_HOT_SERIAL") != nullptr;
 #define IGB_HOT_J(J)                                                                     \
   case J:                                                                                \
-    if (J == 4 && ps.rankbits) {                                                         \
-      if (serial) go(k_count_hot<1, J, 5, CT, CC>, ps.rankbits);                         \
-      else go(k_count_hot<1, J, 5, CT, CC, true>, ps.rankbits, true);                          \
+    if (J == 4 && ps.rankbits) {  /* one load per probe: no queue needed */             \
+      go(k_count_hot<1, J, 5, CT, CC>, ps.rankbits);                                     \
     } else if (ps.packed) {                                                              \
       if (serial) go(k_count_hot<1, J, 3, CT, CC>, ps.packed);                           \
       else go(k_count_hot<1, J, 3, CT, CC, true>, ps.packed, true);                          \
