@@ -284,7 +284,7 @@ __device__ __forceinline__ uint32_t hlookup_packed(const uint64_t* __restrict__ 
   }
 }
 
-__device__ __forceinline__ uint32_t hlookup_packed_from(const uint64_t* __restrict__ tab,
+__device__ __noinline__ uint32_t hlookup_packed_from(const uint64_t* __restrict__ tab,
                                                      uint32_t lgS, uint32_t ib, uint64_t key,
                                                      uint32_t h) {
   const uint32_t mask = (1u << lgS) - 1;
@@ -296,7 +296,7 @@ __device__ __forceinline__ uint32_t hlookup_packed_from(const uint64_t* __restri
   }
 }
 
-__device__ __forceinline__ uint32_t hlookup_wide_from(const uint64_t* __restrict__ wide,
+__device__ __noinline__ uint32_t hlookup_wide_from(const uint64_t* __restrict__ wide,
                                                    uint32_t lgS, uint64_t key, uint32_t h) {
   const uint32_t mask = (1u << lgS) - 1;
   for (;;) {
@@ -583,34 +583,52 @@ __global__ void __launch_bounds__(hot_threads<PH>(), 1)
         // (ballot-compacted), drained 32 at a time with every lane probing
         // one position: the L2 probes of a whole tile then cost a few round
         // trips with full warps instead of one divergent round trip per T
-        hstatic_for<0, 16>([&](auto tc) {
-          constexpr int T = decltype(tc)::value;
-          // branch-free: every position is looked up (an invalid one's
-          // result is masked), the shared add and the queue stores are
-          // predicated, and shared addresses are 32-bit from one base
-          const uint64_t key = hkey8_at<T>(s) & hgram_mask<L>();
-          bool v = (vm >> T) & 1u;
-          if (sliced) {
-            const uint64_t sk = key >> 8;
-            v = v && sk >= lo && sk < hi;
-          }
-          const uint32_t b = hot_bucket(key, hw.lgnb);
-          const ulonglong2 e = lds_u64x2(s_keys + b * 16);
-          const bool h1 = e.y == key;
-          const bool hot = v && (e.x == key || h1);
-          red_shared_if(s_cnt + (2 * b + (uint32_t)h1) * 4, hot);
-          hm |= (uint32_t)hot << T;
-          const bool cq = v && !hot;
-          const uint32_t bal = __ballot_sync(0xffffffffu, cq);
-          const uint32_t qi = (qtail + __popc(bal & lt_mask)) & (kHotQ - 1);
-          st_shared_u64_if(s_qkey + qi * 8, key, cq);
-          st_shared_u32_if(s_qpos + qi * 4, (kcur << 9) | (lane << 4) | T, cq);
-          qtail += __popc(bal);
-          if (qtail - qhead >= 32) {
-            __syncwarp();
-            drain(32u);
-          }
-        });
+        // a runtime loop over 4 groups of 4 positions (the window words
+        // rotate by one per group), so the drain code exists 4 times, not 16
+        uint32_t q0 = s.W[0], q1 = s.W[1], q2 = s.W[2], q3 = s.W[3], q4 = s.W[4], q5 = s.W[5];
+#pragma unroll 1
+        for (int g = 0; g < 4; ++g) {
+          hstatic_for<0, 4>([&](auto ic) {
+            constexpr int I = decltype(ic)::value;
+            constexpr int o = I + 1, wi = o / 4, sh = 8 * (o % 4);
+            const uint32_t w0 = wi == 0 ? q0 : q1, w1 = wi == 0 ? q1 : q2, w2 = wi == 0 ? q2 : q3;
+            const uint32_t klo = sh ? __funnelshift_r(w0, w1, sh) : w0;
+            const uint32_t khi = sh ? __funnelshift_r(w1, w2, sh) : w1;
+            const uint64_t key = (((uint64_t)__byte_perm(klo, 0, 0x0123) << 32) |
+                                  (uint64_t)__byte_perm(khi, 0, 0x0123)) & hgram_mask<L>();
+            const uint32_t T = 4 * g + I;
+            // branch-free: every position is looked up (an invalid one's
+            // result is masked), the shared add and the queue stores are
+            // predicated, and shared addresses are 32-bit from one base
+            bool v = (vm >> T) & 1u;
+            if (sliced) {
+              const uint64_t sk = key >> 8;
+              v = v && sk >= lo && sk < hi;
+            }
+            const uint32_t b = hot_bucket(key, hw.lgnb);
+            const ulonglong2 e = lds_u64x2(s_keys + b * 16);
+            const bool h1 = e.y == key;
+            const bool hot = v && (e.x == key || h1);
+            red_shared_if(s_cnt + (2 * b + (uint32_t)h1) * 4, hot);
+            hm |= (uint32_t)hot << T;
+            const bool cq = v && !hot;
+            const uint32_t bal = __ballot_sync(0xffffffffu, cq);
+            const uint32_t qi = (qtail + __popc(bal & lt_mask)) & (kHotQ - 1);
+            st_shared_u64_if(s_qkey + qi * 8, key, cq);
+            st_shared_u32_if(s_qpos + qi * 4, (kcur << 9) | (lane << 4) | T, cq);
+            qtail += __popc(bal);
+            if (qtail - qhead >= 32) {
+              __syncwarp();
+              drain(32u);
+            }
+          });
+          q0 = q1;
+          q1 = q2;
+          q2 = q3;
+          q3 = q4;
+          q4 = q5;
+          q5 = 0;
+        }
         __syncwarp();
         hm |= qhit[lane];
         qhit[lane] = 0;
