@@ -46,8 +46,11 @@ namespace igb {
 constexpr uint64_t kHotMul = 0xA24BAED4963EE407ull;  // bucket hash (odd)
 constexpr int kHotBins = 128;                        // semi-log count bins
 
+// Bucket of a hot-table key: a 32-bit mix of both key halves (4 ALU ops in
+// the sweep's inner loop instead of a 64-bit multiply).
 __host__ __device__ __forceinline__ uint32_t hot_bucket(uint64_t key, uint32_t lgnb) {
-  return (uint32_t)((key * kHotMul) >> (64 - lgnb));
+  const uint32_t h = (uint32_t)key * 0x9E3779B1u ^ (uint32_t)(key >> 32) * 0x85EBCA77u;
+  return (h ^ (h >> 15)) >> (32 - lgnb);
 }
 
 // Semi-log bin of a count c >= 1: 2 * floor(log2 c) + the next bit.
@@ -325,6 +328,10 @@ __device__ __forceinline__ uint32_t hlookup_wide(const uint64_t* __restrict__ wi
 // per-segment scratch when CT is u64).
 // Shared-memory accesses by 32-bit shared address (the extension sweep's
 // branch-free inner loop): a 16-byte load, and a predicated add / stores.
+__device__ __forceinline__ uint32_t opaque_u32(uint32_t x) {
+  asm volatile("mov.b32 %0, %0;" : "+r"(x));
+  return x;
+}
 __device__ __forceinline__ ulonglong2 lds_u64x2(uint32_t a) {
   ulonglong2 v;
   asm("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(v.x), "=l"(v.y) : "r"(a));
@@ -450,10 +457,13 @@ __global__ void __launch_bounds__(hot_threads<PH>(), 1)
   uint64_t* qkey = reinterpret_cast<uint64_t*>(qbase);
   uint32_t* qpos = reinterpret_cast<uint32_t*>(qbase + kHotQ * 8);
   uint32_t* qhit = reinterpret_cast<uint32_t*>(qbase + kHotQ * 12);
-  const uint32_t s_keys = (uint32_t)__cvta_generic_to_shared(skeys);
-  const uint32_t s_cnt = (uint32_t)__cvta_generic_to_shared(scnt);
-  const uint32_t s_qkey = (uint32_t)__cvta_generic_to_shared(qkey);
-  const uint32_t s_qpos = (uint32_t)__cvta_generic_to_shared(qpos);
+  // 32-bit shared addresses, made opaque so the compiler keeps them in
+  // registers instead of rebuilding the shared window base at every use
+  const uint32_t s_keys = opaque_u32((uint32_t)__cvta_generic_to_shared(skeys));
+  const uint32_t s_cnt = opaque_u32((uint32_t)__cvta_generic_to_shared(scnt));
+  const uint32_t s_qkey = opaque_u32((uint32_t)__cvta_generic_to_shared(qkey));
+  const uint32_t s_qpos = opaque_u32((uint32_t)__cvta_generic_to_shared(qpos));
+  const uint32_t lgnb_s = 32 - hw.lgnb;
   uint32_t qhead = 0, qtail = 0;  // warp-uniform
   const uint32_t lt_mask = (1u << lane) - 1u;
   if constexpr (PH && KIND == 1) qhit[lane] = 0;
@@ -600,18 +610,19 @@ __global__ void __launch_bounds__(hot_threads<PH>(), 1)
             // branch-free: every position is looked up (an invalid one's
             // result is masked), the shared add and the queue stores are
             // predicated, and shared addresses are 32-bit from one base
-            bool v = (vm >> T) & 1u;
+            uint32_t v = (vm >> T) & 1u;
             if (sliced) {
               const uint64_t sk = key >> 8;
-              v = v && sk >= lo && sk < hi;
+              v &= (uint32_t)(sk >= lo && sk < hi);
             }
-            const uint32_t b = hot_bucket(key, hw.lgnb);
+            const uint32_t hh = (uint32_t)key * 0x9E3779B1u ^ (uint32_t)(key >> 32) * 0x85EBCA77u;
+            const uint32_t b = (hh ^ (hh >> 15)) >> lgnb_s;  // hot_bucket
             const ulonglong2 e = lds_u64x2(s_keys + b * 16);
-            const bool h1 = e.y == key;
-            const bool hot = v && (e.x == key || h1);
-            red_shared_if(s_cnt + (2 * b + (uint32_t)h1) * 4, hot);
-            hm |= (uint32_t)hot << T;
-            const bool cq = v && !hot;
+            const uint32_t h1 = (uint32_t)(e.y == key);
+            const uint32_t hot = v & ((uint32_t)(e.x == key) | h1);
+            red_shared_if(s_cnt + (2 * b + h1) * 4, hot != 0);
+            hm |= hot << T;
+            const bool cq = (v & ~hot) != 0;
             const uint32_t bal = __ballot_sync(0xffffffffu, cq);
             const uint32_t qi = (qtail + __popc(bal & lt_mask)) & (kHotQ - 1);
             st_shared_u64_if(s_qkey + qi * 8, key, cq);
