@@ -184,6 +184,11 @@ IG_API int ig_session_create_nccl(int32_t device, void* cuda_stream, int32_t ran
 IG_API int ig_topk_ngrams_multi(const ig_corpus* corpus, const int32_t* devices, int32_t ndev,
                                 const ig_params* params, ig_result* out, char* err,
                                 size_t err_len);
+/* Debugging: with IG_GUARD=1 in the environment every device buffer carries
+ * guard bytes and every call checks them afterwards (out-of-bounds device
+ * writes become IG_EINTERNAL).  ig_guard_selftest writes byte `at` of a
+ * 100-byte guarded buffer and runs that check. */
+IG_API int ig_guard_selftest(int32_t device, int64_t at, char* err, size_t err_len);
 /* Kernel launches issued by the session so far (for launch accounting). */
 IG_API uint64_t ig_session_launches(const ig_session* s);
 

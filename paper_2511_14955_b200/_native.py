@@ -91,6 +91,7 @@ SYMBOLS = [
                                       C.POINTER(ig_result), C.c_char_p, C.c_size_t]),
     ("ig_session_launches", C.c_uint64, [C.c_void_p]),
     ("ig_nccl_unique_id", C.c_int, [C.c_char_p, C.c_char_p, C.c_size_t]),
+    ("ig_guard_selftest", C.c_int, [C.c_int32, C.c_int64, C.c_char_p, C.c_size_t]),
     ("ig_session_create_nccl", C.c_int, [C.c_int32, C.c_void_p, C.c_int32, C.c_int32,
                                          C.c_char_p, C.c_uint64, C.c_uint64,
                                          C.POINTER(C.c_void_p), C.c_char_p, C.c_size_t]),

@@ -16,6 +16,9 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <mutex>
+#include <set>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -57,33 +60,92 @@ constexpr int kFrontPad = 16;
 constexpr int kBackPad = 1024;
 constexpr size_t kMaxOnceSmem = 227 * 1024;  // dynamic smem per CTA (sm_100a)
 
+// Guarded allocation (IG_GUARD=1; the stand-in for compute-sanitizer, which
+// this GPU pool does not allow): every DevBuf gets kGuardBytes of 0xA5 in
+// front of and behind its bytes, and check_guards() (after every run / load /
+// exact call in this mode) throws when a kernel wrote into one.
+constexpr size_t kGuardBytes = 4096;
+struct DevBuf;
+inline bool guard_mode() {
+  static const bool g = getenv("IG_GUARD") != nullptr;
+  return g;
+}
+struct GuardRegistry {
+  std::mutex mu;
+  std::set<DevBuf*> live;
+  static GuardRegistry& get() {
+    static GuardRegistry* r = new GuardRegistry();  // outlives every DevBuf
+    return *r;
+  }
+};
+
 // Grow-only device buffer.
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
+  void* base = nullptr;  // allocation start (p - kGuardBytes in guard mode)
   DevBuf() = default;
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
   void swap(DevBuf& o) noexcept {
     std::swap(p, o.p);
     std::swap(bytes, o.bytes);
+    std::swap(base, o.base);
+  }
+  void release() {
+    if (base) cudaFree(base);
+    if (base && guard_mode()) {
+      std::lock_guard<std::mutex> lk(GuardRegistry::get().mu);
+      GuardRegistry::get().live.erase(this);
+    }
+    p = base = nullptr;
+    bytes = 0;
   }
   void* get(size_t need) {
     if (need > bytes) {
-      if (p) cudaFree(p);
-      p = nullptr;
-      bytes = 0;
-      IGB_CUDA(cudaMalloc(&p, need ? need : 16));
-      bytes = need ? need : 16;
+      release();
+      const size_t n = need ? need : 16;
+      if (guard_mode()) {
+        IGB_CUDA(cudaMalloc(&base, n + 2 * kGuardBytes));
+        IGB_CUDA(cudaMemset(base, 0xA5, kGuardBytes));
+        IGB_CUDA(cudaMemset(static_cast<char*>(base) + kGuardBytes + n, 0xA5, kGuardBytes));
+        p = static_cast<char*>(base) + kGuardBytes;
+        std::lock_guard<std::mutex> lk(GuardRegistry::get().mu);
+        GuardRegistry::get().live.insert(this);
+      } else {
+        IGB_CUDA(cudaMalloc(&base, n));
+        p = base;
+      }
+      bytes = n;
     }
     return p;
   }
   template <typename T>
   T* as(size_t count) { return static_cast<T*>(get(count * sizeof(T))); }
-  ~DevBuf() {
-    if (p) cudaFree(p);
-  }
+  ~DevBuf() { release(); }
 };
+
+// Throws when any live guarded buffer's guard bytes changed (a device write
+// out of bounds).  Synchronises the device.  No-op unless IG_GUARD is set.
+inline void check_guards(const char* where) {
+  if (!guard_mode()) return;
+  IGB_CUDA(cudaDeviceSynchronize());
+  std::lock_guard<std::mutex> lk(GuardRegistry::get().mu);
+  std::vector<unsigned char> h(kGuardBytes);
+  for (DevBuf* b : GuardRegistry::get().live) {
+    for (int side = 0; side < 2; ++side) {
+      const char* g = side == 0 ? static_cast<const char*>(b->base)
+                                : static_cast<const char*>(b->p) + b->bytes;
+      IGB_CUDA(cudaMemcpy(h.data(), g, kGuardBytes, cudaMemcpyDeviceToHost));
+      for (size_t i = 0; i < kGuardBytes; ++i)
+        if (h[i] != 0xA5)
+          throw Error(IG_EINTERNAL, std::string("guard bytes overwritten ") +
+                                        (side ? "behind" : "in front of") + " a device buffer of " +
+                                        std::to_string(b->bytes) + " bytes (" + where + ", offset " +
+                                        std::to_string(i) + ")");
+    }
+  }
+}
 
 // Grow-only mapped pinned host staging.  Every small host<->device transfer
 // of a run goes through it and is moved by a kernel (zero-copy), not a copy

@@ -1613,3 +1613,22 @@ void ig_shard_range(const uint64_t* offsets, uint64_t num_seqs, int32_t rank, in
 }
 
 }  // extern "C"
+
+// ---- IG_GUARD self-test: a kernel writes byte `at` of a 100-byte buffer
+// (at >= 100: past its end, at < 0: before it); the guard check must report
+// exactly the out-of-bounds writes.
+namespace igb {
+__global__ void k_poke(uint8_t* p, int64_t at) { p[at] = 0x5A; }
+}  // namespace igb
+
+extern "C" int ig_guard_selftest(int32_t device, int64_t at, char* err, size_t err_len) {
+  return guarded(err, err_len, [&] {
+    if (!guard_mode()) throw Error(IG_ECONFIG, "IG_GUARD is not set");
+    IGB_CUDA(cudaSetDevice(device));
+    DevBuf b;
+    uint8_t* p = b.as<uint8_t>(100);
+    k_poke<<<1, 1>>>(p, at);
+    IGB_CUDA(cudaGetLastError());
+    check_guards("self-test");
+  });
+}

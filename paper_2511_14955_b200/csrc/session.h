@@ -115,6 +115,14 @@ template <typename F>
 inline int guarded(char* err, size_t len, F&& f) {
   try {
     f();
+    if (guard_mode()) {  // IG_GUARD: no kernel of this call wrote out of bounds
+      bool any;
+      {
+        std::lock_guard<std::mutex> lk(GuardRegistry::get().mu);
+        any = !GuardRegistry::get().live.empty();
+      }
+      if (any) check_guards("C-ABI call");
+    }
     if (err && len) err[0] = 0;
     return IG_OK;
   } catch (const Error& e) {
