@@ -332,6 +332,12 @@ __device__ __forceinline__ uint32_t opaque_u32(uint32_t x) {
   asm volatile("mov.b32 %0, %0;" : "+r"(x));
   return x;
 }
+__device__ __forceinline__ uint64_t lds_u64_if(uint32_t a, bool p) {
+  uint64_t v = 0;
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.shared.u64 %0, [%1];\n\t}"
+               : "+l"(v) : "r"(a), "r"((uint32_t)p));
+  return v;
+}
 __device__ __forceinline__ ulonglong2 lds_u64x2(uint32_t a) {
   ulonglong2 v;
   asm("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(v.x), "=l"(v.y) : "r"(a));
@@ -447,7 +453,18 @@ __global__ void __launch_bounds__(hot_threads<PH>(), 1)
   uint32_t* scnt = reinterpret_cast<uint32_t*>(smem_raw + (size_t)nb * 16);
   {
     const ulonglong2* gk = reinterpret_cast<const ulonglong2*>(hw.keys);
-    for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) skeys[i] = gk[i];
+    if constexpr (PH && KIND == 1) {
+      // split ways: way-0 keys [0, nb), way-1 keys [nb, 2 nb) (8-byte loads;
+      // the second only when the first misses)
+      uint64_t* k0 = reinterpret_cast<uint64_t*>(skeys);
+      for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) {
+        const ulonglong2 e = gk[i];
+        k0[i] = e.x;
+        k0[nb + i] = e.y;
+      }
+    } else {
+      for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) skeys[i] = gk[i];
+    }
     for (uint32_t i = threadIdx.x; i < 2 * nb; i += blockDim.x) scnt[i] = 0;
   }
   const int lane = threadIdx.x & 31;
@@ -617,9 +634,13 @@ __global__ void __launch_bounds__(hot_threads<PH>(), 1)
             }
             const uint32_t hh = (uint32_t)key * 0x9E3779B1u ^ (uint32_t)(key >> 32) * 0x85EBCA77u;
             const uint32_t b = (hh ^ (hh >> 15)) >> lgnb_s;  // hot_bucket
-            const ulonglong2 e = lds_u64x2(s_keys + b * 16);
-            const uint32_t h1 = (uint32_t)(e.y == key);
-            const uint32_t hot = v & ((uint32_t)(e.x == key) | h1);
+            // predicated 8-byte loads: lanes without a valid position (or
+            // whose way-0 key matched) add no shared-memory wavefronts
+            const uint64_t k0 = lds_u64_if(s_keys + b * 8, v != 0);
+            const uint32_t m0 = v & (uint32_t)(k0 == key);
+            const uint64_t k1 = lds_u64_if(s_keys + (nb + b) * 8, (v & ~m0) != 0);
+            const uint32_t h1 = (v & ~m0) & (uint32_t)(k1 == key);
+            const uint32_t hot = m0 | h1;
             red_shared_if(s_cnt + (2 * b + h1) * 4, hot != 0);
             hm |= hot << T;
             const bool cq = (v & ~hot) != 0;
