@@ -506,7 +506,10 @@ __global__ void __launch_bounds__(hot_threads<PH>(), 1)
     if (pf) {
       uint32_t p;
       const uint64_t pk = pfkey >> 8;
-      if constexpr (TAB == 3) {
+      if constexpr (TAB == 5) {
+        const uint64_t bit = 1ull << (pk & 63);
+        p = (pfa.x & bit) ? (uint32_t)pfa.y + (uint32_t)__popcll(pfa.x & (bit - 1)) : 0xffffffffu;
+      } else if constexpr (TAB == 3) {
         const uint64_t pmask = (1ull << ps.ib) - 1;
         const uint64_t sl[4] = {pfa.x, pfa.y, pfb.x, pfb.y};
         p = 0xfffffffeu;  // undecided
@@ -546,11 +549,17 @@ __global__ void __launch_bounds__(hot_threads<PH>(), 1)
       pfkey = qkey[qi];
       pfpos = qpos[qi];
       const uint64_t pk = pfkey >> 8;
-      const uint32_t hh = hash_slot(pk, ps.lgS);
-      const ulonglong2* bk = TAB == 3 ? reinterpret_cast<const ulonglong2*>(ptab + hh)
-                                      : reinterpret_cast<const ulonglong2*>(ptab) + hh;
-      pfa = __ldg(bk);
-      pfb = __ldg(bk + 1);
+      if constexpr (TAB == 5) {  // rank bitmap: one 16-byte word pair
+        pfa = __ldg(reinterpret_cast<const ulonglong2*>(ptab) + (pk >> 6));
+      } else {
+        const uint32_t hh = hash_slot(pk, ps.lgS);
+        const ulonglong2* bk = TAB == 3 ? reinterpret_cast<const ulonglong2*>(ptab + hh)
+                                        : reinterpret_cast<const ulonglong2*>(ptab) + hh;
+        // the 32-byte bucket in one 256-bit load (homes are 32-byte aligned)
+        asm volatile("ld.global.nc.v4.u64 {%0, %1, %2, %3}, [%4];"
+                     : "=l"(pfa.x), "=l"(pfa.y), "=l"(pfb.x), "=l"(pfb.y)
+                     : "l"(bk));
+      }
       pf = true;
     }
     qhead += cnt;
@@ -754,10 +763,12 @@ void launch_count_hot(const DevCorpus& c, const DevPrefixSet& ps, bool dense, ui
   // queued cold probes (ballot-compacted per warp, probed 32 at a time);
   // the one-position-at-a-time kernel stays behind IG_HOT_SERIAL=1
   static const bool serial = getenv("IG_HOT_SERIAL") != nullptr;
+  static const bool q5 = getenv("IG_HOT_Q5") != nullptr;  // queued rank-bitmap pass (experiment)
 #define IGB_HOT_J(J)                                                                     \
   case J:                                                                                \
-    if (J == 4 && ps.rankbits) {  /* one load per probe: no queue needed */             \
-      go(k_count_hot<1, J, 5, CT, CC>, ps.rankbits);                                     \
+    if (J == 4 && ps.rankbits) {  /* one load per probe */                              \
+      if (serial || !q5) go(k_count_hot<1, J, 5, CT, CC>, ps.rankbits);                  \
+      else go(k_count_hot<1, J, 5, CT, CC, true>, ps.rankbits, true);                    \
     } else if (ps.packed) {                                                              \
       if (serial) go(k_count_hot<1, J, 3, CT, CC>, ps.packed);                           \
       else go(k_count_hot<1, J, 3, CT, CC, true>, ps.packed, true);                          \
