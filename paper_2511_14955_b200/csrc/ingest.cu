@@ -26,6 +26,7 @@
 #include <cstring>
 #include <exception>
 #include <filesystem>
+#include <map>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -113,6 +114,7 @@ struct Slabs {
   void* host[kSlabs] = {};
   cudaEvent_t done[kSlabs] = {};
   int64_t item[kSlabs];  // last item staged in the slab (-1: none)
+  int device = 0;
   std::mutex mu;
   std::condition_variable cv;
   ~Slabs() {
@@ -123,15 +125,53 @@ struct Slabs {
   }
 };
 
+// Pinned slab sets are pooled per process: allocating 16 x 32 MiB of pinned
+// memory costs ~0.3 s, which would dominate a one-shot call on a small
+// corpus.  A session borrows a set on first use and returns it when it is
+// destroyed; concurrent sessions get sets of their own.
+struct SlabPool {
+  std::mutex mu;
+  std::map<int, std::vector<Slabs*>> free;  // by device (the events belong to one)
+  static SlabPool& get() {
+    static SlabPool* p = new SlabPool();  // never destroyed: sets live for the process
+    return *p;
+  }
+};
+
+void return_slabs(void* p) {
+  auto* sl = static_cast<Slabs*>(p);
+  SlabPool& pool = SlabPool::get();
+  std::lock_guard<std::mutex> lk(pool.mu);
+  pool.free[sl->device].push_back(sl);
+}
+
 Slabs& slabs_of(Session& s) {
   if (!s.slabs) {
-    auto* sl = new Slabs();
-    s.slabs = sl;
-    s.slabs_free = [](void* p) { delete static_cast<Slabs*>(p); };
-    for (int i = 0; i < kSlabs; ++i) {
-      IGB_CUDA(cudaHostAlloc(&sl->host[i], kSlabBytes, cudaHostAllocDefault));
-      IGB_CUDA(cudaEventCreateWithFlags(&sl->done[i], cudaEventDisableTiming));
+    Slabs* sl = nullptr;
+    {
+      SlabPool& pool = SlabPool::get();
+      std::lock_guard<std::mutex> lk(pool.mu);
+      auto& v = pool.free[s.device];
+      if (!v.empty()) {
+        sl = v.back();
+        v.pop_back();
+      }
     }
+    if (!sl) {
+      sl = new Slabs();
+      sl->device = s.device;
+      try {
+        for (int i = 0; i < kSlabs; ++i) {
+          IGB_CUDA(cudaHostAlloc(&sl->host[i], kSlabBytes, cudaHostAllocPortable));
+          IGB_CUDA(cudaEventCreateWithFlags(&sl->done[i], cudaEventDisableTiming));
+        }
+      } catch (...) {
+        delete sl;
+        throw;
+      }
+    }
+    s.slabs = sl;
+    s.slabs_free = return_slabs;
   }
   return *static_cast<Slabs*>(s.slabs);
 }
