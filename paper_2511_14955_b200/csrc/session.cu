@@ -521,7 +521,7 @@ static void short_pass(Session& s, int kind, uint32_t L, const RouteParams& rp, 
 }
 
 // ---- count-all with sampled hot-gram tables
-static constexpr uint64_t kHotMinTiles = 1ull << 16;  // 32 MiB: below, the plain kernel
+static constexpr uint64_t kHotMinTiles = 1ull << 19;  // 256 MiB: below, the plain kernel
 
 static uint64_t env_u64(const char* name, uint64_t dflt) {
   const char* v = getenv(name);
