@@ -560,6 +560,14 @@ def main():
                 traffic = json.load(f).get(f"{cfg.name}:{dom}")
         except Exception:
             traffic = None
+    ceiling = None
+    cp = os.path.join(ROOT, "profiles", "ceiling.json")
+    if os.path.exists(cp):
+        try:
+            with open(cp) as f:
+                ceiling = json.load(f).get(f"{cfg.name}:{dom}")
+        except Exception:
+            ceiling = None
     step_breakdown = {}
     for step in rows:
         for p in step:
@@ -659,6 +667,7 @@ def main():
                          "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": local_bytes,
                          "avg_launch_ms": dom_avg_ms},
+            "ceiling": ceiling,
             "step_breakdown_ms": step_breakdown,
             "kernel_breakdown": kernel_breakdown,
             "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches,

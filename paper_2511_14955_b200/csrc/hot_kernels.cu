@@ -338,12 +338,6 @@ __device__ __forceinline__ uint64_t lds_u64_if(uint32_t a, bool p) {
                : "+l"(v) : "r"(a), "r"((uint32_t)p));
   return v;
 }
-__device__ __forceinline__ ulonglong2 ldg_u64x2_if(const ulonglong2* a, bool p) {
-  ulonglong2 v = make_ulonglong2(0, 0);
-  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %3, 0;\n\t@q ld.global.nc.v2.u64 {%0, %1}, [%2];\n\t}"
-               : "+l"(v.x), "+l"(v.y) : "l"(a), "r"((uint32_t)p));
-  return v;
-}
 __device__ __forceinline__ ulonglong2 lds_u64x2(uint32_t a) {
   ulonglong2 v;
   asm("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(v.x), "=l"(v.y) : "r"(a));
@@ -630,57 +624,6 @@ __global__ void __launch_bounds__(hot_threads<PH>(), 1)
         uint32_t q0 = s.W[0], q1 = s.W[1], q2 = s.W[2], q3 = s.W[3], q4 = s.W[4], q5 = s.W[5];
 #pragma unroll 1
         for (int g = 0; g < 4; ++g) {
-          auto gkey = [&](auto ic) -> uint64_t {  // the gram ending at group position I
-            constexpr int I = decltype(ic)::value;
-            constexpr int o = I + 1, wi = o / 4, sh = 8 * (o % 4);
-            const uint32_t w0 = wi == 0 ? q0 : q1, w1 = wi == 0 ? q1 : q2, w2 = wi == 0 ? q2 : q3;
-            const uint32_t klo = sh ? __funnelshift_r(w0, w1, sh) : w0;
-            const uint32_t khi = sh ? __funnelshift_r(w1, w2, sh) : w1;
-            return (((uint64_t)__byte_perm(klo, 0, 0x0123) << 32) |
-                    (uint64_t)__byte_perm(khi, 0, 0x0123)) & hgram_mask<L>();
-          };
-          if constexpr (TAB == 5) {
-            // rank-bitmap prefixes need no probing: the group's cold positions
-            // load their rank word pairs together (one L2 round trip per
-            // group), then resolve; no queue
-            ulonglong2 re[4];
-            uint32_t cm = 0;
-            hstatic_for<0, 4>([&](auto ic) {
-              constexpr int I = decltype(ic)::value;
-              const uint64_t key = gkey(ic);
-              const uint32_t T = 4 * g + I;
-              uint32_t v = (vm >> T) & 1u;
-              if (sliced) {
-                const uint64_t sk = key >> 8;
-                v &= (uint32_t)(sk >= lo && sk < hi);
-              }
-              const uint32_t hh = (uint32_t)key * 0x9E3779B1u ^ (uint32_t)(key >> 32) * 0x85EBCA77u;
-              const uint32_t b = (hh ^ (hh >> 15)) >> lgnb_s;
-              const uint64_t k0 = lds_u64_if(s_keys + b * 8, v != 0);
-              const uint32_t m0 = v & (uint32_t)(k0 == key);
-              const uint64_t k1 = lds_u64_if(s_keys + (nb + b) * 8, (v & ~m0) != 0);
-              const uint32_t h1 = (v & ~m0) & (uint32_t)(k1 == key);
-              const uint32_t hot = m0 | h1;
-              red_shared_if(s_cnt + (2 * b + h1) * 4, hot != 0);
-              hm |= hot << T;
-              const uint32_t cq = v & ~hot & 1u;
-              cm |= cq << I;
-              re[I] = ldg_u64x2_if(reinterpret_cast<const ulonglong2*>(ptab) + ((key >> 8) >> 6),
-                                   cq != 0);
-            });
-            hstatic_for<0, 4>([&](auto ic) {
-              constexpr int I = decltype(ic)::value;
-              if ((cm >> I) & 1u) {
-                const uint64_t key = gkey(ic);
-                const uint64_t bit = 1ull << ((key >> 8) & 63);
-                if (re[I].x & bit) {
-                  const uint32_t p = (uint32_t)re[I].y + (uint32_t)__popcll(re[I].x & (bit - 1));
-                  atomicAdd(cold + ((uint64_t)p * 256 + (uint32_t)(key & 0xff)), (CC)1);
-                  hm |= 1u << (4 * g + I);
-                }
-              }
-            });
-          } else
           hstatic_for<0, 4>([&](auto ic) {
             constexpr int I = decltype(ic)::value;
             constexpr int o = I + 1, wi = o / 4, sh = 8 * (o % 4);
@@ -820,12 +763,10 @@ void launch_count_hot(const DevCorpus& c, const DevPrefixSet& ps, bool dense, ui
   // queued cold probes (ballot-compacted per warp, probed 32 at a time);
   // the one-position-at-a-time kernel stays behind IG_HOT_SERIAL=1
   static const bool serial = getenv("IG_HOT_SERIAL") != nullptr;
-  static const bool q5 = getenv("IG_HOT_Q5") != nullptr;  // queued rank-bitmap pass (experiment)
 #define IGB_HOT_J(J)                                                                     \
   case J:                                                                                \
-    if (J == 4 && ps.rankbits) {  /* one load per probe */                              \
-      if (serial || !q5) go(k_count_hot<1, J, 5, CT, CC>, ps.rankbits);                  \
-      else go(k_count_hot<1, J, 5, CT, CC, true>, ps.rankbits, true);                    \
+    if (J == 4 && ps.rankbits) {  /* one load per probe: the serial kernel is faster */ \
+      go(k_count_hot<1, J, 5, CT, CC>, ps.rankbits);                                     \
     } else if (ps.packed) {                                                              \
       if (serial) go(k_count_hot<1, J, 3, CT, CC>, ps.packed);                           \
       else go(k_count_hot<1, J, 3, CT, CC, true>, ps.packed, true);                          \

@@ -593,14 +593,14 @@ int ig_topk_ngrams_files(const ig_file_corpus* spec, const ig_params* params, ig
   return guarded(err, err_len, [&] {
     if (!spec || !params || !out) throw Error(IG_ECONFIG, "null argument");
     validate(*params);
-    ig_session* s = create(params->device, nullptr, nullptr);
+    ig_session* s = acquire_oneshot(params->device);
     try {
       run_files(*s, *spec, *params, out);
     } catch (...) {
       delete s;
       throw;
     }
-    delete s;
+    release_oneshot(s);
   });
 }
 

@@ -18,6 +18,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <string>
+#include <map>
+#include <mutex>
 #include <vector>
 
 #include "ig_internal.cuh"
@@ -1408,19 +1410,71 @@ void ig_session_destroy(ig_session* s) {
   delete s;
 }
 
+}  // extern "C"
+
+// One-shot entry points (ig_topk_ngrams*, the C++ run_intergrams) reuse an
+// idle session per device instead of creating one per call: creating and
+// destroying a session (stream, events, mapped pinned arena, every device
+// buffer) costs ~0.1 s, which dominated a call on a small corpus.  A session
+// that held a corpus above 1 GiB is destroyed instead of kept, so a finished
+// large run does not pin its HBM; one that threw is never reused.
+namespace igb {
+namespace {
+struct OneShotPool {
+  std::mutex mu;
+  std::map<int, ig_session*> idle;
+  static OneShotPool& get() {
+    static OneShotPool* p = new OneShotPool();
+    return *p;
+  }
+};
+}  // namespace
+
+ig_session* acquire_oneshot(int32_t device) {
+  if (device < 0) IGB_CUDA(cudaGetDevice(&device));
+  {
+    OneShotPool& p = OneShotPool::get();
+    std::lock_guard<std::mutex> lk(p.mu);
+    auto it = p.idle.find(device);
+    if (it != p.idle.end() && it->second) {
+      ig_session* s = it->second;
+      it->second = nullptr;
+      return s;
+    }
+  }
+  return create(device, nullptr, nullptr);
+}
+
+void release_oneshot(ig_session* s) {
+  if (!s) return;
+  if (s->dc.total <= (1ull << 30) && !getenv("IG_NO_SESSION_POOL")) {
+    OneShotPool& p = OneShotPool::get();
+    std::lock_guard<std::mutex> lk(p.mu);
+    ig_session*& slot = p.idle[s->device];
+    if (!slot) {
+      slot = s;
+      return;
+    }
+  }
+  ig_session_destroy(s);
+}
+}  // namespace igb
+
+extern "C" {
+
 int ig_topk_ngrams(const ig_corpus* corpus, const ig_params* params, ig_result* out, char* err,
                    size_t err_len) {
   return guarded(err, err_len, [&] {
     if (!corpus || !params || !out) throw Error(IG_ECONFIG, "null argument");
     validate(*params);
-    ig_session* s = create(params->device, nullptr, nullptr);
+    ig_session* s = acquire_oneshot(params->device);
     try {
       load_and_run(*s, *corpus, *params, out);
     } catch (...) {
       delete s;
       throw;
     }
-    delete s;
+    release_oneshot(s);
   });
 }
 
@@ -1434,7 +1488,7 @@ int ig_topk_ngrams_seqs(const uint8_t* const* seqs, const uint64_t* lens, uint64
       if (lens[q] && !seqs[q]) throw Error(IG_ECONFIG, "null sequence pointer");
       hoff[q + 1] = hoff[q] + lens[q];
     }
-    ig_session* s = create(params->device, nullptr, nullptr);
+    ig_session* s = acquire_oneshot(params->device);
     try {
       if (hoff[num_seqs]) {
         run_host_streamed(*s, nullptr, seqs, hoff, *params, out);
@@ -1447,7 +1501,7 @@ int ig_topk_ngrams_seqs(const uint8_t* const* seqs, const uint64_t* lens, uint64
       delete s;
       throw;
     }
-    delete s;
+    release_oneshot(s);
   });
 }
 

@@ -232,4 +232,8 @@ struct ig_session : igb::Session {};
 
 namespace igb {
 ig_session* create(int32_t device, void* stream, const ig_collective* coll);
+// An idle session of `device` for a one-shot call (or a new one), and its
+// return (kept for the next call unless it held a corpus above 1 GiB).
+ig_session* acquire_oneshot(int32_t device);
+void release_oneshot(ig_session* s);
 }  // namespace igb
