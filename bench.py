@@ -74,8 +74,9 @@ REASON_BITS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_pow
 
 class ClockSampler:
     """SM clock and throttle reasons sampled DURING the timed region: NVML
-    polled from a thread every ~2 ms (short regions such as c1's still get
-    samples), else nvidia-smi -lms 100."""
+    polled from a thread (every ~2 ms for the first samples so that short
+    regions such as c1's still get some, then every 50 ms), else
+    nvidia-smi -lms 100."""
 
     def __init__(self, index: int):
         self.index = index
@@ -120,7 +121,10 @@ class ClockSampler:
                 self.samples.append((float(s[0]), float(s[1]), int(s[2])))
             except Exception:
                 return
-            self.stop.wait(0.002)
+            # dense at first (a 7 ms c1 region still gets samples), then
+            # every 50 ms: each NVML query takes driver locks the launching
+            # thread also needs, and 2 ms polling cost a c3 step ~20 ms
+            self.stop.wait(0.002 if len(self.samples) < 8 else 0.05)
 
     def _read(self):
         for line in self.proc.stdout:
@@ -523,12 +527,17 @@ def main():
     with ClockSampler(local) as clk:
         barrier()
         ev0.record(stream)
+        step_evs = []
         for _ in range(args.steps):
             res = sess.run(icfg, materialize=False)  # list lands in host numpy arrays
             rows.append(res.passes)
+            step_evs.append(torch.cuda.Event(enable_timing=True))
+            step_evs[-1].record(stream)
         ev1.record(stream)
         barrier()
     ms = ev0.elapsed_time(ev1) / args.steps
+    log("ms of each timed step:", [round(a.elapsed_time(b), 2)
+                                   for a, b in zip([ev0] + step_evs[:-1], step_evs)])
     kstats = sess.kernel_stats(reset=True)
     sess.set_profiling(False)
     launches = (sess.launches - l0) // args.steps

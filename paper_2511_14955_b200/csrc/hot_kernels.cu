@@ -618,61 +618,99 @@ __global__ void __launch_bounds__(hot_threads<PH>(), 1)
         // hot grams in shared memory; the others go to this warp's queue
         // (ballot-compacted), drained 32 at a time with every lane probing
         // one position: the L2 probes of a whole tile then cost a few round
-        // trips with full warps instead of one divergent round trip per T
-        // a runtime loop over 4 groups of 4 positions (the window words
-        // rotate by one per group), so the drain code exists 4 times, not 16
-        uint32_t q0 = s.W[0], q1 = s.W[1], q2 = s.W[2], q3 = s.W[3], q4 = s.W[4], q5 = s.W[5];
+        // trips with full warps instead of one divergent round trip per T.
+        // One position of every lane (v: the lane has one): branch-free, the
+        // shared add and the queue stores are predicated, and shared
+        // addresses are 32-bit from one base
+        auto step = [&](uint64_t key, uint32_t T, uint32_t v) {
+          if (sliced) {
+            const uint64_t sk = key >> 8;
+            v &= (uint32_t)(sk >= lo && sk < hi);
+          }
+          const uint32_t hh = (uint32_t)key * 0x9E3779B1u ^ (uint32_t)(key >> 32) * 0x85EBCA77u;
+          const uint32_t b = (hh ^ (hh >> 15)) >> lgnb_s;  // hot_bucket
+          // predicated 8-byte loads: lanes without a valid position (or
+          // whose way-0 key matched) add no shared-memory wavefronts
+          const uint64_t k0 = lds_u64_if(s_keys + b * 8, v != 0);
+          const uint32_t m0 = v & (uint32_t)(k0 == key);
+          const uint64_t k1 = lds_u64_if(s_keys + (nb + b) * 8, (v & ~m0) != 0);
+          const uint32_t h1 = (v & ~m0) & (uint32_t)(k1 == key);
+          const uint32_t hot = m0 | h1;
+          red_shared_if(s_cnt + (2 * b + h1) * 4, hot != 0);
+          hm |= hot << T;
+          const bool cq = (v & ~hot) != 0;
+          const uint32_t bal = __ballot_sync(0xffffffffu, cq);
+          const uint32_t qi = (qtail + __popc(bal & lt_mask)) & (kHotQ - 1);
+          st_shared_u64_if(s_qkey + qi * 8, key, cq);
+          st_shared_u32_if(s_qpos + qi * 4, (kcur << 9) | (lane << 4) | T, cq);
+          qtail += __popc(bal);
+          if (qtail - qhead >= 32) {
+            __syncwarp();
+            drain(32u);
+          }
+        };
+        // the most live positions any lane holds (hit chaining leaves few on
+        // a sparse pass: c5's 6- to 8-gram passes keep ~10 % of the tiles,
+        // its 5-gram pass ~9 % of the positions of the others)
+        const uint32_t iters = __reduce_max_sync(0xffffffffu, (uint32_t)__popc(vm));
+        if (iters == 0) {
+          // a dead tile costs one reduction
+        } else if (iters <= hw.sparse_iters) {
+          // sparse tile: every lane walks its own live positions, so the
+          // tile costs max-popcount steps instead of 16; the key comes out
+          // of the window at a runtime offset (word selects + funnel shifts)
+          uint32_t rem = vm;
 #pragma unroll 1
-        for (int g = 0; g < 4; ++g) {
-          hstatic_for<0, 4>([&](auto ic) {
-            constexpr int I = decltype(ic)::value;
-            constexpr int o = I + 1, wi = o / 4, sh = 8 * (o % 4);
-            const uint32_t w0 = wi == 0 ? q0 : q1, w1 = wi == 0 ? q1 : q2, w2 = wi == 0 ? q2 : q3;
-            const uint32_t klo = sh ? __funnelshift_r(w0, w1, sh) : w0;
-            const uint32_t khi = sh ? __funnelshift_r(w1, w2, sh) : w1;
+          for (uint32_t it = 0; it < iters; ++it) {
+            const uint32_t has = rem != 0;
+            const uint32_t T = has ? (uint32_t)__ffs((int)rem) - 1u : 0u;
+            rem &= rem - 1;
+            const uint32_t o = T + 1, wi = o >> 2, sh = 8 * (o & 3);
+            uint32_t x0 = (wi & 2) ? s.W[2] : s.W[0], x1 = (wi & 2) ? s.W[3] : s.W[1];
+            uint32_t x2 = (wi & 2) ? s.W[4] : s.W[2], x3 = (wi & 2) ? s.W[5] : s.W[3];
+            if (wi & 4) {
+              x0 = s.W[4];
+              x1 = s.W[5];
+              x2 = 0;
+              x3 = 0;
+            }
+            const uint32_t a0 = (wi & 1) ? x1 : x0, a1 = (wi & 1) ? x2 : x1, a2 = (wi & 1) ? x3 : x2;
+            const uint32_t klo = __funnelshift_r(a0, a1, sh), khi = __funnelshift_r(a1, a2, sh);
             const uint64_t key = (((uint64_t)__byte_perm(klo, 0, 0x0123) << 32) |
                                   (uint64_t)__byte_perm(khi, 0, 0x0123)) & hgram_mask<L>();
-            const uint32_t T = 4 * g + I;
-            // branch-free: every position is looked up (an invalid one's
-            // result is masked), the shared add and the queue stores are
-            // predicated, and shared addresses are 32-bit from one base
-            uint32_t v = (vm >> T) & 1u;
-            if (sliced) {
-              const uint64_t sk = key >> 8;
-              v &= (uint32_t)(sk >= lo && sk < hi);
-            }
-            const uint32_t hh = (uint32_t)key * 0x9E3779B1u ^ (uint32_t)(key >> 32) * 0x85EBCA77u;
-            const uint32_t b = (hh ^ (hh >> 15)) >> lgnb_s;  // hot_bucket
-            // predicated 8-byte loads: lanes without a valid position (or
-            // whose way-0 key matched) add no shared-memory wavefronts
-            const uint64_t k0 = lds_u64_if(s_keys + b * 8, v != 0);
-            const uint32_t m0 = v & (uint32_t)(k0 == key);
-            const uint64_t k1 = lds_u64_if(s_keys + (nb + b) * 8, (v & ~m0) != 0);
-            const uint32_t h1 = (v & ~m0) & (uint32_t)(k1 == key);
-            const uint32_t hot = m0 | h1;
-            red_shared_if(s_cnt + (2 * b + h1) * 4, hot != 0);
-            hm |= hot << T;
-            const bool cq = (v & ~hot) != 0;
-            const uint32_t bal = __ballot_sync(0xffffffffu, cq);
-            const uint32_t qi = (qtail + __popc(bal & lt_mask)) & (kHotQ - 1);
-            st_shared_u64_if(s_qkey + qi * 8, key, cq);
-            st_shared_u32_if(s_qpos + qi * 4, (kcur << 9) | (lane << 4) | T, cq);
-            qtail += __popc(bal);
-            if (qtail - qhead >= 32) {
-              __syncwarp();
-              drain(32u);
-            }
-          });
-          q0 = q1;
-          q1 = q2;
-          q2 = q3;
-          q3 = q4;
-          q4 = q5;
-          q5 = 0;
+            step(key, T, has);
+          }
+          __syncwarp();
+          hm |= qhit[lane];
+          qhit[lane] = 0;
+        } else {
+          // a runtime loop over 4 groups of 4 positions (the window words
+          // rotate by one per group), so the drain code exists 4 times, not 16
+          uint32_t q0 = s.W[0], q1 = s.W[1], q2 = s.W[2], q3 = s.W[3], q4 = s.W[4], q5 = s.W[5];
+#pragma unroll 1
+          for (int g = 0; g < 4; ++g) {
+            hstatic_for<0, 4>([&](auto ic) {
+              constexpr int I = decltype(ic)::value;
+              constexpr int o = I + 1, wi = o / 4, sh = 8 * (o % 4);
+              const uint32_t w0 = wi == 0 ? q0 : q1, w1 = wi == 0 ? q1 : q2, w2 = wi == 0 ? q2 : q3;
+              const uint32_t klo = sh ? __funnelshift_r(w0, w1, sh) : w0;
+              const uint32_t khi = sh ? __funnelshift_r(w1, w2, sh) : w1;
+              const uint64_t key = (((uint64_t)__byte_perm(klo, 0, 0x0123) << 32) |
+                                    (uint64_t)__byte_perm(khi, 0, 0x0123)) & hgram_mask<L>();
+              const uint32_t T = 4 * g + I;
+              step(key, T, (vm >> T) & 1u);
+            });
+            q0 = q1;
+            q1 = q2;
+            q2 = q3;
+            q3 = q4;
+            q4 = q5;
+            q5 = 0;
+          }
+          __syncwarp();
+          hm |= qhit[lane];
+          qhit[lane] = 0;
         }
-        __syncwarp();
-        hm |= qhit[lane];
-        qhit[lane] = 0;
       } else
       hstatic_for<0, 16>([&](auto tc) {
         constexpr int T = decltype(tc)::value;

@@ -80,6 +80,9 @@ struct HotSweep {
   const uint64_t* bounds = nullptr;  // device, 2 values
   bool first = true;
   bool sliced = false;  // more than one slice: check the key range
+  // queued extension sweep: a tile whose lanes hold at most this many live
+  // positions each is walked live position by live position (0: never)
+  uint32_t sparse_iters = 10;
 };
 size_t hot_smem(uint32_t lgnb);
 // Hot set of each slice from the (sample) counts in table[0, cap).  pkeys:

@@ -608,6 +608,7 @@ static void count_all_hot(Session& s, bool dense, uint32_t L, const Prefix* P, C
       hw.bounds = bounds + i;
       hw.first = i == 0;
       hw.sliced = S > 1;
+      hw.sparse_iters = (uint32_t)env_u64("IG_SPARSE_ITERS", 10);
       const size_t ev = s.kt.begin(IG_KF_COUNT_ALL, s.stream);
       launch_count_hot(dc, ps, dense, L, hw, t, cold, s.num_sms, s.stream);
       s.kt.end(ev, s.stream);

@@ -64,7 +64,11 @@ TOGGLES = [{}, {"IG_NO_HIT_CHAIN": "1"}, {"IG_NO_RANK_BITMAP": "1"},
            {"IG_NO_HIT_CHAIN": "1", "IG_NO_RANK_BITMAP": "1"},
            HOT, HOT_SMALL, HOT_U64, {**HOT_SMALL, "IG_NO_HIT_CHAIN": "1"},
            {**HOT, "IG_NO_RANK_BITMAP": "1", "IG_HOT_SLICES": "3"},
-           {"IG_FORCE_U64": "1", "IG_SEG_TILES": "777", "IG_NO_HOT": "1"}]
+           {"IG_FORCE_U64": "1", "IG_SEG_TILES": "777", "IG_NO_HOT": "1"},
+           # queued sweep: never / always walk a tile live position by live
+           # position (the default does for tiles with <= 10 per lane)
+           {**HOT, "IG_SPARSE_ITERS": "0"}, {**HOT, "IG_SPARSE_ITERS": "16"},
+           {**HOT_SMALL, "IG_SPARSE_ITERS": "16"}]
 
 
 def run_with_env(env, fn):
