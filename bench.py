@@ -84,6 +84,7 @@ class ClockSampler:
         self.proc = None
         self.stop = threading.Event()
         self.t = None
+        self.period = float(os.environ.get("IG_CLOCK_POLL_MS", "50")) * 1e-3
 
     def __enter__(self):
         try:
@@ -124,7 +125,7 @@ class ClockSampler:
             # dense at first (a 7 ms c1 region still gets samples), then
             # every 50 ms: each NVML query takes driver locks the launching
             # thread also needs, and 2 ms polling cost a c3 step ~20 ms
-            self.stop.wait(0.002 if len(self.samples) < 8 else 0.05)
+            self.stop.wait(0.002 if len(self.samples) < 8 else self.period)
 
     def _read(self):
         for line in self.proc.stdout:

@@ -443,7 +443,7 @@ constexpr size_t kHotQWarpBytes = kHotQ * 8 + kHotQ * 4 + 32 * 4;
 template <bool PH>
 constexpr int hot_threads() { return 1024; }
 
-template <int KIND, int L, int TAB, typename CT, typename CC, bool PH = false>
+template <int KIND, int L, int TAB, typename CT, typename CC, bool PH = false, bool SP = false>
 __global__ void __launch_bounds__(hot_threads<PH>(), 1)
     k_count_hot(DevCorpus c, DevPrefixSet ps, const uint64_t* __restrict__ ptab, HotSweep hw,
                 CT* __restrict__ table, CC* __restrict__ cold) {
@@ -489,6 +489,7 @@ __global__ void __launch_bounds__(hot_threads<PH>(), 1)
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   const uint64_t lo = hw.bounds[0], hi = hw.bounds[1];  // this slice's key range
   const bool chain = KIND == 1 && ps.hit_in != nullptr;
+  const bool sparse = SP && chain;  // a sparse pass
   // Queue drains are software-pipelined: drain_issue takes 32 queued
   // positions (one per lane) and starts their first bucket loads; they are
   // resolved (compare, RED, hit bit) by drain_resolve at the next drain, a
@@ -571,29 +572,48 @@ __global__ void __launch_bounds__(hot_threads<PH>(), 1)
   };
   uint64_t t = c.tile0 + ((blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5);
   if (t < c.ntiles) {
-    // the next tile's loads stay in flight while the current one is counted
-    uint4 v = __ldcs(reinterpret_cast<const uint4*>(c.data + t * kTileBytes + lane * 16));
+    // the next tile's loads stay in flight while the current one is counted.
+    // On a sparse pass (ps.sparse: the previous pass hit fewer than half of
+    // the positions) the masks run one tile further ahead, and a tile whose
+    // mask is empty (no position of it was counted by the previous pass)
+    // never reads its corpus bytes: c5's 6- to 8-gram passes touch ~10 % of
+    // the 64 GiB.
+    auto mask_at = [&](uint64_t tt) -> uint32_t {
+      uint32_t m = __ldcs(ps.hit_in + tt * 32 + lane);
+      m |= (lane == 0 ? (uint32_t)__ldcs(ps.hit_in + tt * 32 - 1) : 0xffffu) << 16;
+      return m;
+    };
+    auto live_of = [&](uint32_t m) -> bool {  // warp-uniform
+      return __any_sync(0xffffffffu, (lane == 0 ? m : (m & 0xffffu)) != 0);
+    };
+    uint32_t mk = chain ? mask_at(t) : 0xffffffffu;
+    uint4 v = make_uint4(0, 0, 0, 0);
     uint2 h = make_uint2(0, 0);
-    if (lane == 0) h = *reinterpret_cast<const uint2*>(c.data + t * kTileBytes - 8);
-    uint32_t d = __ldg(c.tile_seq + t);
-    uint32_t mk = 0xffffffffu;
-    if (chain) {
-      mk = __ldcs(ps.hit_in + t * 32 + lane);
-      mk |= (lane == 0 ? (uint32_t)__ldcs(ps.hit_in + t * 32 - 1) : 0xffffu) << 16;
+    uint32_t d = 0x80000000u;  // dead tile: "all positions valid" & an empty mask
+    if (!sparse || live_of(mk)) {
+      v = __ldcs(reinterpret_cast<const uint4*>(c.data + t * kTileBytes + lane * 16));
+      if (lane == 0) h = *reinterpret_cast<const uint2*>(c.data + t * kTileBytes - 8);
+      d = __ldg(c.tile_seq + t);
     }
+    // sparse: the mask of tile t + nwarps (else unused: loaded with its tile)
+    uint32_t mkn = (sparse && t + nwarps < c.ntiles) ? mask_at(t + nwarps) : 0xffffffffu;
     for (;;) {
       const uint64_t tn = t + nwarps;
       uint4 vn = make_uint4(0, 0, 0, 0);
       uint2 hn = make_uint2(0, 0);
-      uint32_t dn = 0, mkn = 0xffffffffu;
-      if (tn < c.ntiles) {
+      uint32_t dn = 0x80000000u, mknn = 0xffffffffu;
+      if (sparse) {
+        if (tn < c.ntiles && live_of(mkn)) {
+          vn = __ldcs(reinterpret_cast<const uint4*>(c.data + tn * kTileBytes + lane * 16));
+          if (lane == 0) hn = *reinterpret_cast<const uint2*>(c.data + tn * kTileBytes - 8);
+          dn = __ldg(c.tile_seq + tn);
+        }
+        if (tn + nwarps < c.ntiles) mknn = mask_at(tn + nwarps);
+      } else if (tn < c.ntiles) {
         vn = __ldcs(reinterpret_cast<const uint4*>(c.data + tn * kTileBytes + lane * 16));
         if (lane == 0) hn = *reinterpret_cast<const uint2*>(c.data + tn * kTileBytes - 8);
         dn = __ldg(c.tile_seq + tn);
-        if (chain) {
-          mkn = __ldcs(ps.hit_in + tn * 32 + lane);
-          mkn |= (lane == 0 ? (uint32_t)__ldcs(ps.hit_in + tn * 32 - 1) : 0xffffu) << 16;
-        }
+        if (chain) mkn = mask_at(tn);
       }
       HSeg s;
       s.W[2] = v.x;
@@ -649,41 +669,48 @@ __global__ void __launch_bounds__(hot_threads<PH>(), 1)
             drain(32u);
           }
         };
-        // the most live positions any lane holds (hit chaining leaves few on
-        // a sparse pass: c5's 6- to 8-gram passes keep ~10 % of the tiles,
-        // its 5-gram pass ~9 % of the positions of the others)
-        const uint32_t iters = __reduce_max_sync(0xffffffffu, (uint32_t)__popc(vm));
-        if (iters == 0) {
-          // a dead tile costs one reduction
-        } else if (iters <= hw.sparse_iters) {
-          // sparse tile: every lane walks its own live positions, so the
-          // tile costs max-popcount steps instead of 16; the key comes out
-          // of the window at a runtime offset (word selects + funnel shifts)
-          uint32_t rem = vm;
+        bool dense_tile = true;
+        if constexpr (SP) {
+          // the most live positions any lane holds (hit chaining leaves few
+          // on a sparse pass: c5's 6- to 8-gram passes keep ~10 % of the
+          // tiles, its 5-gram pass ~9 % of the positions of the others)
+          const uint32_t iters =
+              sparse ? __reduce_max_sync(0xffffffffu, (uint32_t)__popc(vm)) : 16u;
+          if (iters == 0) {
+            dense_tile = false;  // a dead tile costs one reduction
+          } else if (iters <= hw.sparse_iters) {
+            // sparse tile: every lane walks its own live positions, so the
+            // tile costs max-popcount steps instead of 16; the key comes out
+            // of the window at a runtime offset (word selects + funnel shifts)
+            dense_tile = false;
+            uint32_t rem = vm;
 #pragma unroll 1
-          for (uint32_t it = 0; it < iters; ++it) {
-            const uint32_t has = rem != 0;
-            const uint32_t T = has ? (uint32_t)__ffs((int)rem) - 1u : 0u;
-            rem &= rem - 1;
-            const uint32_t o = T + 1, wi = o >> 2, sh = 8 * (o & 3);
-            uint32_t x0 = (wi & 2) ? s.W[2] : s.W[0], x1 = (wi & 2) ? s.W[3] : s.W[1];
-            uint32_t x2 = (wi & 2) ? s.W[4] : s.W[2], x3 = (wi & 2) ? s.W[5] : s.W[3];
-            if (wi & 4) {
-              x0 = s.W[4];
-              x1 = s.W[5];
-              x2 = 0;
-              x3 = 0;
+            for (uint32_t it = 0; it < iters; ++it) {
+              const uint32_t has = rem != 0;
+              const uint32_t T = has ? (uint32_t)__ffs((int)rem) - 1u : 0u;
+              rem &= rem - 1;
+              const uint32_t o = T + 1, wi = o >> 2, sh = 8 * (o & 3);
+              uint32_t x0 = (wi & 2) ? s.W[2] : s.W[0], x1 = (wi & 2) ? s.W[3] : s.W[1];
+              uint32_t x2 = (wi & 2) ? s.W[4] : s.W[2], x3 = (wi & 2) ? s.W[5] : s.W[3];
+              if (wi & 4) {
+                x0 = s.W[4];
+                x1 = s.W[5];
+                x2 = 0;
+                x3 = 0;
+              }
+              const uint32_t a0 = (wi & 1) ? x1 : x0, a1 = (wi & 1) ? x2 : x1,
+                             a2 = (wi & 1) ? x3 : x2;
+              const uint32_t klo = __funnelshift_r(a0, a1, sh), khi = __funnelshift_r(a1, a2, sh);
+              const uint64_t key = (((uint64_t)__byte_perm(klo, 0, 0x0123) << 32) |
+                                    (uint64_t)__byte_perm(khi, 0, 0x0123)) & hgram_mask<L>();
+              step(key, T, has);
             }
-            const uint32_t a0 = (wi & 1) ? x1 : x0, a1 = (wi & 1) ? x2 : x1, a2 = (wi & 1) ? x3 : x2;
-            const uint32_t klo = __funnelshift_r(a0, a1, sh), khi = __funnelshift_r(a1, a2, sh);
-            const uint64_t key = (((uint64_t)__byte_perm(klo, 0, 0x0123) << 32) |
-                                  (uint64_t)__byte_perm(khi, 0, 0x0123)) & hgram_mask<L>();
-            step(key, T, has);
+            __syncwarp();
+            hm |= qhit[lane];
+            qhit[lane] = 0;
           }
-          __syncwarp();
-          hm |= qhit[lane];
-          qhit[lane] = 0;
-        } else {
+        }
+        if (dense_tile) {
           // a runtime loop over 4 groups of 4 positions (the window words
           // rotate by one per group), so the drain code exists 4 times, not 16
           uint32_t q0 = s.W[0], q1 = s.W[1], q2 = s.W[2], q3 = s.W[3], q4 = s.W[4], q5 = s.W[5];
@@ -750,6 +777,7 @@ __global__ void __launch_bounds__(hot_threads<PH>(), 1)
       h = hn;
       d = dn;
       mk = mkn;
+      if (sparse) mkn = mknn;
       ++kcur;
     }
   }
@@ -801,16 +829,33 @@ void launch_count_hot(const DevCorpus& c, const DevPrefixSet& ps, bool dense, ui
   // queued cold probes (ballot-compacted per warp, probed 32 at a time);
   // the one-position-at-a-time kernel stays behind IG_HOT_SERIAL=1
   static const bool serial = getenv("IG_HOT_SERIAL") != nullptr;
+  // the sparse variant (dead / sparse tiles, mask-gated corpus loads) is a
+  // second kernel, so the dense sweep's loop stays inside the instruction
+  // cache; only u32 tables (every chained pass of a < 2^32-count corpus)
+  constexpr bool kSparseTypes = sizeof(CT) == 4 && sizeof(CC) == 4;
+  const bool sp = ps.sparse && ps.hit_in != nullptr && kSparseTypes && !serial;
 #define IGB_HOT_J(J)                                                                     \
   case J:                                                                                \
     if (J == 4 && ps.rankbits) {  /* one load per probe: the serial kernel is faster */ \
       go(k_count_hot<1, J, 5, CT, CC>, ps.rankbits);                                     \
     } else if (ps.packed) {                                                              \
+      if constexpr (kSparseTypes && J >= 5) {                                            \
+        if (sp) {                                                                        \
+          go(k_count_hot<1, J, 3, CT, CC, true, true>, ps.packed, true);                 \
+          break;                                                                         \
+        }                                                                                \
+      }                                                                                  \
       if (serial) go(k_count_hot<1, J, 3, CT, CC>, ps.packed);                           \
-      else go(k_count_hot<1, J, 3, CT, CC, true>, ps.packed, true);                          \
+      else go(k_count_hot<1, J, 3, CT, CC, true>, ps.packed, true);                      \
     } else {                                                                             \
+      if constexpr (kSparseTypes && J >= 5) {                                            \
+        if (sp) {                                                                        \
+          go(k_count_hot<1, J, 4, CT, CC, true, true>, ps.wide, true);                   \
+          break;                                                                         \
+        }                                                                                \
+      }                                                                                  \
       if (serial) go(k_count_hot<1, J, 4, CT, CC>, ps.wide);                             \
-      else go(k_count_hot<1, J, 4, CT, CC, true>, ps.wide, true);                            \
+      else go(k_count_hot<1, J, 4, CT, CC, true>, ps.wide, true);                        \
     }                                                                                    \
     break;
   switch (L) {

@@ -265,6 +265,10 @@ struct DevPrefixSet {
   // was counted by the pass that wrote it.  hit_in[-1] is readable (zero).
   const uint16_t* hit_in = nullptr;  // previous extension pass's hits, or null
   uint16_t* hit_out = nullptr;       // this pass's hits (read by the next pass), or null
+  // hot sweeps (hot_kernels.cu): the previous pass hit fewer than half of the
+  // positions, so this one takes the sparse kernel (mask-gated corpus loads,
+  // dead tiles skipped, sparse tiles walked live position by live position)
+  bool sparse = false;
 };
 
 // Home slot of a key in an open-addressing table of 2^lgS slots: always a

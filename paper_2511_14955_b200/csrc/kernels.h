@@ -218,7 +218,8 @@ struct SelectCtx {
   DevBuf tmp_keys, tmp_counts, cub_tmp;
   uint64_t launches = 0;
   SelState* h_state = nullptr;            // pinned host mirrors (no pageable copies)
-  unsigned long long* h_scalar = nullptr;
+  unsigned long long* h_scalar = nullptr;  // mapped pinned: {max, sum}
+  unsigned long long last_sum = 0;  // sum of the last selected table's counts
   SelectCtx() = default;
   SelectCtx(const SelectCtx&) = delete;
   SelectCtx& operator=(const SelectCtx&) = delete;

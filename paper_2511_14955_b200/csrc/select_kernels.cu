@@ -55,18 +55,27 @@ __device__ __forceinline__ void load4<unsigned long long>(const unsigned long lo
   c[3] = b.y;
 }
 
-// max count (for the number of digit passes) — one u64 per block, then atomicMax.
+// max count (for the number of digit passes) and the sum of all counts (the
+// occurrences the pass counted: the next pass's sparse switch) — per warp,
+// then atomicMax / atomicAdd into out[0] / out[1].
 template <typename CT>
 __global__ void k_max(const CT* __restrict__ t, uint64_t cap4, unsigned long long* out) {
-  uint64_t mx = 0;
+  uint64_t mx = 0, sum = 0;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < cap4;
        i += (uint64_t)gridDim.x * blockDim.x) {
     uint64_t c[4];
     load4<CT>(t, i * 4, c);
     mx = max(max(mx, c[0]), max(c[1], max(c[2], c[3])));
+    sum += c[0] + c[1] + c[2] + c[3];
   }
-  for (int d = 16; d; d >>= 1) mx = max(mx, (uint64_t)__shfl_xor_sync(0xffffffffu, mx, d));
-  if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)mx);
+  for (int d = 16; d; d >>= 1) {
+    mx = max(mx, (uint64_t)__shfl_xor_sync(0xffffffffu, mx, d));
+    sum += (uint64_t)__shfl_xor_sync(0xffffffffu, sum, d);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(out, (unsigned long long)mx);
+    if (sum) atomicAdd(out + 1, (unsigned long long)sum);
+  }
 }
 
 // Histogram of digit (v >> shift) & 255 over the entries still in play.
@@ -202,13 +211,14 @@ uint64_t select_topk(SelectCtx& x, const CT* table, uint64_t cap, uint64_t k, Ke
   k_set_state<<<1, 1, 0, s>>>(x.state, init);  // by value: no host copy
   x.launches++;
   IGB_CUDA(cudaMemsetAsync(x.hist, 0, 256 * sizeof(uint32_t), s));
-  IGB_CUDA(cudaMemsetAsync(x.scalar, 0, sizeof(unsigned long long), s));
+  IGB_CUDA(cudaMemsetAsync(x.scalar, 0, 2 * sizeof(unsigned long long), s));
   k_max<CT><<<blocks, threads, 0, s>>>(table, cap4, x.scalar);
   x.launches++;
-  launch_copy(x.h_scalar, x.scalar, sizeof(unsigned long long), s);  // mapped pinned
+  launch_copy(x.h_scalar, x.scalar, 2 * sizeof(unsigned long long), s);  // mapped pinned
   x.launches++;
   IGB_CUDA(cudaStreamSynchronize(s));
-  const unsigned long long mx = *x.h_scalar;
+  const unsigned long long mx = x.h_scalar[0];
+  x.last_sum = x.h_scalar[1];
   if (mx == 0) return 0;  // all-zero table: empty result (counting.cpp:72)
   const int cbits = bits_of(mx);
   const int cpasses = (cbits + 7) / 8;

@@ -213,10 +213,10 @@ void init_select(Session& s) {
   s.sel.num_sms = s.num_sms;
   s.sel.state = s.sel_state.as<SelState>(1);
   s.sel.hist = s.sel_hist.as<uint32_t>(256);
-  s.sel.scalar = s.sel_scalar.as<unsigned long long>(1);
+  s.sel.scalar = s.sel_scalar.as<unsigned long long>(2);  // max, sum
   if (!s.sel.h_state) {
     IGB_CUDA(cudaHostAlloc(&s.sel.h_state, sizeof(SelState), cudaHostAllocMapped));
-    IGB_CUDA(cudaHostAlloc(&s.sel.h_scalar, sizeof(unsigned long long), cudaHostAllocMapped));
+    IGB_CUDA(cudaHostAlloc(&s.sel.h_scalar, 2 * sizeof(unsigned long long), cudaHostAllocMapped));
   }
 }
 
@@ -1032,6 +1032,12 @@ static void run_t(Session& s, const ig_params& p, ig_result* out) {
       if (hmask[0] && !chain) {
         P.ps.hit_in = j >= 5 ? hmask[(j - 1) & 1] : nullptr;
         P.ps.hit_out = j < n ? hmask[j & 1] : nullptr;
+        // sparse switch of the hot sweeps: on when pass j-1
+        // counted fewer than half of the positions (the sum of its table,
+        // which its selection read anyway; global on every rank).
+        // IG_SPARSE=0/1 forces it.
+        P.ps.sparse = P.ps.hit_in && 2 * s.sel.last_sum < total_bytes;
+        if (const char* f = getenv("IG_SPARSE")) P.ps.sparse = P.ps.hit_in && f[0] != '0';
       }
       // count-all: a j-gram occurs at most as often as its (j-1)-byte prefix
       // (each occurrence ends one byte after one of the prefix's), so when

@@ -68,7 +68,9 @@ TOGGLES = [{}, {"IG_NO_HIT_CHAIN": "1"}, {"IG_NO_RANK_BITMAP": "1"},
            # queued sweep: never / always walk a tile live position by live
            # position (the default does for tiles with <= 10 per lane)
            {**HOT, "IG_SPARSE_ITERS": "0"}, {**HOT, "IG_SPARSE_ITERS": "16"},
-           {**HOT_SMALL, "IG_SPARSE_ITERS": "16"}]
+           {**HOT_SMALL, "IG_SPARSE_ITERS": "16"},
+           # the sparse switch forced on (every chained pass) / off
+           {**HOT, "IG_SPARSE": "1"}, {**HOT, "IG_SPARSE": "0"}]
 
 
 def run_with_env(env, fn):
