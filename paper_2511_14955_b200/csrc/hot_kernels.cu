@@ -49,8 +49,9 @@ constexpr int kHotBins = 128;                        // semi-log count bins
 // Bucket of a hot-table key: a 32-bit mix of both key halves (4 ALU ops in
 // the sweep's inner loop instead of a 64-bit multiply).
 __host__ __device__ __forceinline__ uint32_t hot_bucket(uint64_t key, uint32_t lgnb) {
-  const uint32_t h = (uint32_t)key * 0x9E3779B1u ^ (uint32_t)(key >> 32) * 0x85EBCA77u;
-  return (h ^ (h >> 15)) >> (32 - lgnb);
+  // the top bits of a sum of two odd-multiplier products: 2 IMAD + 1 shift
+  const uint32_t h = (uint32_t)key * 0x9E3779B1u + (uint32_t)(key >> 32) * 0x85EBCA77u;
+  return h >> (32 - lgnb);
 }
 
 // Semi-log bin of a count c >= 1: 2 * floor(log2 c) + the next bit.
@@ -480,7 +481,8 @@ __global__ void __launch_bounds__(hot_threads<PH>(), 1)
   const uint32_t s_cnt = opaque_u32((uint32_t)__cvta_generic_to_shared(scnt));
   const uint32_t s_qkey = opaque_u32((uint32_t)__cvta_generic_to_shared(qkey));
   const uint32_t s_qpos = opaque_u32((uint32_t)__cvta_generic_to_shared(qpos));
-  const uint32_t lgnb_s = 32 - hw.lgnb;
+  const uint32_t lgnb_s = opaque_u32(32 - hw.lgnb);
+  const uint32_t s_keys1 = opaque_u32(s_keys + nb * 8);  // way-1 keys
   uint32_t qhead = 0, qtail = 0;  // warp-uniform
   const uint32_t lt_mask = (1u << lane) - 1u;
   if constexpr (PH && KIND == 1) qhit[lane] = 0;
@@ -511,25 +513,29 @@ __global__ void __launch_bounds__(hot_threads<PH>(), 1)
         const uint64_t bit = 1ull << (pk & 63);
         p = (pfa.x & bit) ? (uint32_t)pfa.y + (uint32_t)__popcll(pfa.x & (bit - 1)) : 0xffffffffu;
       } else if constexpr (TAB == 3) {
-        const uint64_t pmask = (1ull << ps.ib) - 1;
-        const uint64_t sl[4] = {pfa.x, pfa.y, pfb.x, pfb.y};
-        p = 0xfffffffeu;  // undecided
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-          if (p == 0xfffffffeu) {
-            if (sl[i] == kEmptyKey) p = 0xffffffffu;
-            else if ((sl[i] >> ps.ib) == pk) p = (uint32_t)(sl[i] & pmask);
-          }
+        // branch-free over the 4 slots of the bucket: a slot holds
+        // (key << ib) | rank, so slot ^ (pk << ib) < 2^ib is a match and its
+        // low word the rank (ib < 32: ranks are u32).  Linear probing
+        // without deletions: the key cannot lie beyond an empty slot, so
+        // match -> hit, else any empty slot -> miss, else the next bucket.
+        const uint64_t pks = pk << ps.ib, lim = 1ull << ps.ib;
+        const uint64_t x0 = pfa.x ^ pks, x1 = pfa.y ^ pks, x2 = pfb.x ^ pks, x3 = pfb.y ^ pks;
+        const bool m0 = x0 < lim, m1 = x1 < lim, m2 = x2 < lim, m3 = x3 < lim;
+        const bool anye = (pfa.x == kEmptyKey) | (pfa.y == kEmptyKey) | (pfb.x == kEmptyKey) |
+                          (pfb.y == kEmptyKey);
+        const uint32_t pv = m0 ? (uint32_t)x0 : m1 ? (uint32_t)x1 : m2 ? (uint32_t)x2 : (uint32_t)x3;
+        p = (m0 | m1 | m2 | m3) ? pv : (anye ? 0xffffffffu : 0xfffffffeu);
         if (p == 0xfffffffeu)  // a full bucket: continue from the next one
           p = hlookup_packed_from(ptab, ps.lgS, ps.ib, pk,
                                   (hash_slot(pk, ps.lgS) + 4) & ((1u << ps.lgS) - 1));
       } else {
-        if (pfa.x == pk) p = (uint32_t)pfa.y;
-        else if (pfa.x == kEmptyKey) p = 0xffffffffu;
-        else if (pfb.x == pk) p = (uint32_t)pfb.y;
-        else if (pfb.x == kEmptyKey) p = 0xffffffffu;
-        else p = hlookup_wide_from(ptab, ps.lgS, pk,
-                                   (hash_slot(pk, ps.lgS) + 2) & ((1u << ps.lgS) - 1));
+        // two {key, p} slots, branch-free (same argument as the packed bucket)
+        const bool m0 = pfa.x == pk, m1 = pfb.x == pk;
+        const bool anye = (pfa.x == kEmptyKey) | (pfb.x == kEmptyKey);
+        p = m0 ? (uint32_t)pfa.y : m1 ? (uint32_t)pfb.y : anye ? 0xffffffffu : 0xfffffffeu;
+        if (p == 0xfffffffeu)  // both slots taken by other keys: the next bucket
+          p = hlookup_wide_from(ptab, ps.lgS, pk,
+                                (hash_slot(pk, ps.lgS) + 2) & ((1u << ps.lgS) - 1));
       }
       if (p != 0xffffffffu) {
         atomicAdd(cold + ((uint64_t)p * 256 + (uint32_t)(pfkey & 0xff)), (CC)1);
@@ -642,18 +648,16 @@ __global__ void __launch_bounds__(hot_threads<PH>(), 1)
         // One position of every lane (v: the lane has one): branch-free, the
         // shared add and the queue stores are predicated, and shared
         // addresses are 32-bit from one base
+        // (one slice only: launch_count_hot sends sliced sweeps, which need
+        // tables above IG_HOT_SLICE_MB = 4 GiB, to the serial kernel)
         auto step = [&](uint64_t key, uint32_t T, uint32_t v) {
-          if (sliced) {
-            const uint64_t sk = key >> 8;
-            v &= (uint32_t)(sk >= lo && sk < hi);
-          }
-          const uint32_t hh = (uint32_t)key * 0x9E3779B1u ^ (uint32_t)(key >> 32) * 0x85EBCA77u;
-          const uint32_t b = (hh ^ (hh >> 15)) >> lgnb_s;  // hot_bucket
+          const uint32_t hh = (uint32_t)key * 0x9E3779B1u + (uint32_t)(key >> 32) * 0x85EBCA77u;
+          const uint32_t b = hh >> lgnb_s;  // hot_bucket
           // predicated 8-byte loads: lanes without a valid position (or
           // whose way-0 key matched) add no shared-memory wavefronts
           const uint64_t k0 = lds_u64_if(s_keys + b * 8, v != 0);
           const uint32_t m0 = v & (uint32_t)(k0 == key);
-          const uint64_t k1 = lds_u64_if(s_keys + (nb + b) * 8, (v & ~m0) != 0);
+          const uint64_t k1 = lds_u64_if(s_keys1 + b * 8, (v & ~m0) != 0);
           const uint32_t h1 = (v & ~m0) & (uint32_t)(k1 == key);
           const uint32_t hot = m0 | h1;
           red_shared_if(s_cnt + (2 * b + h1) * 4, hot != 0);
@@ -828,11 +832,12 @@ void launch_count_hot(const DevCorpus& c, const DevPrefixSet& ps, bool dense, ui
   }
   // queued cold probes (ballot-compacted per warp, probed 32 at a time);
   // the one-position-at-a-time kernel stays behind IG_HOT_SERIAL=1
-  static const bool serial = getenv("IG_HOT_SERIAL") != nullptr;
+  static const bool serial_env = getenv("IG_HOT_SERIAL") != nullptr;
   // the sparse variant (dead / sparse tiles, mask-gated corpus loads) is a
   // second kernel, so the dense sweep's loop stays inside the instruction
   // cache; only u32 tables (every chained pass of a < 2^32-count corpus)
   constexpr bool kSparseTypes = sizeof(CT) == 4 && sizeof(CC) == 4;
+  const bool serial = serial_env || hw.sliced;  // the queued sweep handles one slice
   const bool sp = ps.sparse && ps.hit_in != nullptr && kSparseTypes && !serial;
 #define IGB_HOT_J(J)                                                                     \
   case J:                                                                                \
