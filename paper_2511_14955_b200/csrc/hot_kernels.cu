@@ -482,6 +482,7 @@ __global__ void __launch_bounds__(hot_threads<PH>(), 1)
   const uint32_t s_qkey = opaque_u32((uint32_t)__cvta_generic_to_shared(qkey));
   const uint32_t s_qpos = opaque_u32((uint32_t)__cvta_generic_to_shared(qpos));
   const uint32_t lgnb_s = opaque_u32(32 - hw.lgnb);
+  const uint32_t slot_sh = opaque_u32(64 - ps.lgS);  // hash_slot's shift
   const uint32_t s_keys1 = opaque_u32(s_keys + nb * 8);  // way-1 keys
   uint32_t qhead = 0, qtail = 0;  // warp-uniform
   const uint32_t lt_mask = (1u << lane) - 1u;
@@ -559,7 +560,9 @@ __global__ void __launch_bounds__(hot_threads<PH>(), 1)
       if constexpr (TAB == 5) {  // rank bitmap: one 16-byte word pair
         pfa = __ldg(reinterpret_cast<const ulonglong2*>(ptab) + (pk >> 6));
       } else {
-        const uint32_t hh = hash_slot(pk, ps.lgS);
+        // hash_slot(pk, lgS) with the shift in a register (lgS >= 3 here:
+        // tables that fit shared memory take the plain kernel)
+        const uint32_t hh = (uint32_t)((pk * 0x9E3779B97F4A7C15ull) >> slot_sh) & ~3u;
         const ulonglong2* bk = TAB == 3 ? reinterpret_cast<const ulonglong2*>(ptab + hh)
                                         : reinterpret_cast<const ulonglong2*>(ptab) + hh;
         // the 32-byte bucket in one 256-bit load (homes are 32-byte aligned)
@@ -650,19 +653,20 @@ __global__ void __launch_bounds__(hot_threads<PH>(), 1)
         // addresses are 32-bit from one base
         // (one slice only: launch_count_hot sends sliced sweeps, which need
         // tables above IG_HOT_SLICE_MB = 4 GiB, to the serial kernel)
-        auto step = [&](uint64_t key, uint32_t T, uint32_t v) {
+        auto step = [&](uint64_t key, uint32_t T, bool v) {
           const uint32_t hh = (uint32_t)key * 0x9E3779B1u + (uint32_t)(key >> 32) * 0x85EBCA77u;
-          const uint32_t b = hh >> lgnb_s;  // hot_bucket
+          const uint32_t b8 = (hh >> lgnb_s) * 8;  // hot_bucket * 8
           // predicated 8-byte loads: lanes without a valid position (or
           // whose way-0 key matched) add no shared-memory wavefronts
-          const uint64_t k0 = lds_u64_if(s_keys + b * 8, v != 0);
-          const uint32_t m0 = v & (uint32_t)(k0 == key);
-          const uint64_t k1 = lds_u64_if(s_keys1 + b * 8, (v & ~m0) != 0);
-          const uint32_t h1 = (v & ~m0) & (uint32_t)(k1 == key);
-          const uint32_t hot = m0 | h1;
-          red_shared_if(s_cnt + (2 * b + h1) * 4, hot != 0);
-          hm |= hot << T;
-          const bool cq = (v & ~hot) != 0;
+          const uint64_t k0 = lds_u64_if(s_keys + b8, v);
+          const bool m0 = v && k0 == key;
+          const bool n1 = v && !m0;
+          const uint64_t k1 = lds_u64_if(s_keys1 + b8, n1);
+          const bool h1 = n1 && k1 == key;
+          const bool hot = m0 || h1;
+          red_shared_if(s_cnt + b8 + (h1 ? 4u : 0u), hot);  // counter 2 * bucket + way
+          if (hot) hm |= 1u << T;
+          const bool cq = v && !hot;
           const uint32_t bal = __ballot_sync(0xffffffffu, cq);
           const uint32_t qi = (qtail + __popc(bal & lt_mask)) & (kHotQ - 1);
           st_shared_u64_if(s_qkey + qi * 8, key, cq);
@@ -707,7 +711,7 @@ __global__ void __launch_bounds__(hot_threads<PH>(), 1)
               const uint32_t klo = __funnelshift_r(a0, a1, sh), khi = __funnelshift_r(a1, a2, sh);
               const uint64_t key = (((uint64_t)__byte_perm(klo, 0, 0x0123) << 32) |
                                     (uint64_t)__byte_perm(khi, 0, 0x0123)) & hgram_mask<L>();
-              step(key, T, has);
+              step(key, T, has != 0);
             }
             __syncwarp();
             hm |= qhit[lane];
@@ -729,7 +733,7 @@ __global__ void __launch_bounds__(hot_threads<PH>(), 1)
               const uint64_t key = (((uint64_t)__byte_perm(klo, 0, 0x0123) << 32) |
                                     (uint64_t)__byte_perm(khi, 0, 0x0123)) & hgram_mask<L>();
               const uint32_t T = 4 * g + I;
-              step(key, T, (vm >> T) & 1u);
+              step(key, T, ((vm >> T) & 1u) != 0);
             });
             q0 = q1;
             q1 = q2;
