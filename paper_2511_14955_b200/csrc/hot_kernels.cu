@@ -141,6 +141,10 @@ __global__ void k_hot_best(const unsigned long long* __restrict__ cand,
     const uint32_t s = (uint32_t)(g / ccap), i = (uint32_t)(g % ccap);
     if (i >= min(ncand[s], ccap)) continue;
     const unsigned long long v = cand[g];
+    if (way < 0) {  // direct: the way is the next hash bit
+      atomicMax(best + (uint64_t)s * nb * 2 + hot_bucket(kf(v & 0xffffffffu), lgnb + 1), v);
+      continue;
+    }
     const uint32_t b = hot_bucket(kf(v & 0xffffffffu), lgnb);
     unsigned long long* bk = best + ((uint64_t)s * nb + b) * 2;
     if (way == 1 && bk[0] == v) continue;
@@ -170,7 +174,8 @@ __global__ void k_hot_fill(const unsigned long long* __restrict__ best, uint32_t
 
 template <typename CT>
 void build_hot_set(const CT* table, uint64_t cap, const HotSliceIds& sl, const uint64_t* pkeys,
-                   uint32_t lgnb, HotSet& hs, DevBuf& work, int num_sms, cudaStream_t st) {
+                   uint32_t lgnb, HotSet& hs, DevBuf& work, int num_sms, cudaStream_t st,
+                   bool direct) {
   const uint32_t S = sl.S, nb = 1u << lgnb;
   const uint32_t ccap = 2 * nb * 2;  // candidates per slice: twice the slots
   // work layout: hist | thr | ncand | cand | best
@@ -192,20 +197,25 @@ void build_hot_set(const CT* table, uint64_t cap, const HotSliceIds& sl, const u
   k_hot_collect<CT><<<gb ? gb : 1, 256, 0, st>>>(table, cap, sl, thr, ccap, nc, cand);
   const HotKeyFn kf{pkeys};
   const unsigned cb = (unsigned)std::min<uint64_t>(((uint64_t)S * ccap + 255) / 256, 4096);
-  k_hot_best<<<cb, 256, 0, st>>>(cand, nc, S, ccap, kf, lgnb, 0, best);
-  k_hot_best<<<cb, 256, 0, st>>>(cand, nc, S, ccap, kf, lgnb, 1, best);
+  if (direct) {
+    k_hot_best<<<cb, 256, 0, st>>>(cand, nc, S, ccap, kf, lgnb, -1, best);
+  } else {
+    k_hot_best<<<cb, 256, 0, st>>>(cand, nc, S, ccap, kf, lgnb, 0, best);
+    k_hot_best<<<cb, 256, 0, st>>>(cand, nc, S, ccap, kf, lgnb, 1, best);
+  }
   const unsigned fb = (unsigned)std::min<uint64_t>(((uint64_t)S * nb * 2 + 255) / 256, 4096);
   k_hot_fill<<<fb, 256, 0, st>>>(best, S, kf, lgnb, hs.keys, hs.ids);
   hs.S = S;
   hs.lgnb = lgnb;
+  hs.direct = direct;
 }
 
 template void build_hot_set<uint32_t>(const uint32_t*, uint64_t, const HotSliceIds&,
                                       const uint64_t*, uint32_t, HotSet&, DevBuf&, int,
-                                      cudaStream_t);
+                                      cudaStream_t, bool);
 template void build_hot_set<unsigned long long>(const unsigned long long*, uint64_t,
                                                 const HotSliceIds&, const uint64_t*, uint32_t,
-                                                HotSet&, DevBuf&, int, cudaStream_t);
+                                                HotSet&, DevBuf&, int, cudaStream_t, bool);
 
 // ---------------------------------------------------------------- sweep
 
@@ -455,14 +465,9 @@ __global__ void __launch_bounds__(hot_threads<PH>(), 1)
   {
     const ulonglong2* gk = reinterpret_cast<const ulonglong2*>(hw.keys);
     if constexpr (PH && KIND == 1) {
-      // split ways: way-0 keys [0, nb), way-1 keys [nb, 2 nb) (8-byte loads;
-      // the second only when the first misses)
-      uint64_t* k0 = reinterpret_cast<uint64_t*>(skeys);
-      for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) {
-        const ulonglong2 e = gk[i];
-        k0[i] = e.x;
-        k0[nb + i] = e.y;
-      }
+      // a direct table (HotSet::direct): 2 nb slots, slot = the top
+      // lgnb + 1 hash bits, one 8-byte load per lookup
+      for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) skeys[i] = gk[i];
     } else {
       for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) skeys[i] = gk[i];
     }
@@ -481,9 +486,8 @@ __global__ void __launch_bounds__(hot_threads<PH>(), 1)
   const uint32_t s_cnt = opaque_u32((uint32_t)__cvta_generic_to_shared(scnt));
   const uint32_t s_qkey = opaque_u32((uint32_t)__cvta_generic_to_shared(qkey));
   const uint32_t s_qpos = opaque_u32((uint32_t)__cvta_generic_to_shared(qpos));
-  const uint32_t lgnb_s = opaque_u32(32 - hw.lgnb);
+  const uint32_t lgnb_s = opaque_u32(31 - hw.lgnb);  // slot = hash >> lgnb_s (lgnb + 1 bits)
   const uint32_t slot_sh = opaque_u32(64 - ps.lgS);  // hash_slot's shift
-  const uint32_t s_keys1 = opaque_u32(s_keys + nb * 8);  // way-1 keys
   uint32_t qhead = 0, qtail = 0;  // warp-uniform
   const uint32_t lt_mask = (1u << lane) - 1u;
   if constexpr (PH && KIND == 1) qhit[lane] = 0;
@@ -655,16 +659,12 @@ __global__ void __launch_bounds__(hot_threads<PH>(), 1)
         // tables above IG_HOT_SLICE_MB = 4 GiB, to the serial kernel)
         auto step = [&](uint64_t key, uint32_t T, bool v) {
           const uint32_t hh = (uint32_t)key * 0x9E3779B1u + (uint32_t)(key >> 32) * 0x85EBCA77u;
-          const uint32_t b8 = (hh >> lgnb_s) * 8;  // hot_bucket * 8
-          // predicated 8-byte loads: lanes without a valid position (or
-          // whose way-0 key matched) add no shared-memory wavefronts
-          const uint64_t k0 = lds_u64_if(s_keys + b8, v);
-          const bool m0 = v && k0 == key;
-          const bool n1 = v && !m0;
-          const uint64_t k1 = lds_u64_if(s_keys1 + b8, n1);
-          const bool h1 = n1 && k1 == key;
-          const bool hot = m0 || h1;
-          red_shared_if(s_cnt + b8 + (h1 ? 4u : 0u), hot);  // counter 2 * bucket + way
+          const uint32_t sl = hh >> lgnb_s;  // direct slot = 2 * hot_bucket + way bit
+          // a predicated 8-byte load: lanes without a valid position add no
+          // shared-memory wavefronts
+          const uint64_t k0 = lds_u64_if(s_keys + sl * 8, v);
+          const bool hot = v && k0 == key;
+          red_shared_if(s_cnt + sl * 4, hot);
           if (hot) hm |= 1u << T;
           const bool cq = v && !hot;
           const uint32_t bal = __ballot_sync(0xffffffffu, cq);
@@ -807,6 +807,15 @@ __global__ void __launch_bounds__(hot_threads<PH>(), 1)
 }
 
 size_t hot_smem(uint32_t lgnb) { return ((size_t)1 << lgnb) * 24; }
+
+bool hot_sweep_queued(const DevPrefixSet& ps, bool dense, uint32_t L, bool sliced) {
+  static const bool off = getenv("IG_HOT_SERIAL") != nullptr || getenv("IG_HOT_TWOWAY") != nullptr;
+  if (off || dense || sliced) return false;
+  // the rank-bitmap (4-gram) pass: serial kernel unless IG_HOT_Q5 (experiment)
+  static const bool q5 = getenv("IG_HOT_Q5") != nullptr;
+  if (L == 4 && ps.rankbits) return q5;
+  return ps.packed != nullptr || ps.wide != nullptr;
+}
 static size_t hot_smem_q(uint32_t lgnb, int threads) {
   return hot_smem(lgnb) + (size_t)(threads / 32) * kHotQWarpBytes;
 }
@@ -841,11 +850,18 @@ void launch_count_hot(const DevCorpus& c, const DevPrefixSet& ps, bool dense, ui
   // second kernel, so the dense sweep's loop stays inside the instruction
   // cache; only u32 tables (every chained pass of a < 2^32-count corpus)
   constexpr bool kSparseTypes = sizeof(CT) == 4 && sizeof(CC) == 4;
-  const bool serial = serial_env || hw.sliced;  // the queued sweep handles one slice
+  // the queued sweep handles one slice and reads a direct table
+  const bool serial = serial_env || hw.sliced || !hw.direct;
   const bool sp = ps.sparse && ps.hit_in != nullptr && kSparseTypes && !serial;
 #define IGB_HOT_J(J)                                                                     \
   case J:                                                                                \
     if (J == 4 && ps.rankbits) {  /* one load per probe: the serial kernel is faster */ \
+      if constexpr (J == 4) {                                                            \
+        if (!serial) {                                                                   \
+          go(k_count_hot<1, 4, 5, CT, CC, true>, ps.rankbits, true);                     \
+          break;                                                                         \
+        }                                                                                \
+      }                                                                                  \
       go(k_count_hot<1, J, 5, CT, CC>, ps.rankbits);                                     \
     } else if (ps.packed) {                                                              \
       if constexpr (kSparseTypes && J >= 5) {                                            \

@@ -66,6 +66,10 @@ struct HotSliceIds {
 // Per slice: 2^lgnb two-way buckets of gram keys and their table ids.
 struct HotSet {
   uint32_t S = 1, lgnb = 0;
+  // direct: a key may only sit in way (next hash bit) of its bucket, i.e. the
+  // table is 2 << lgnb direct-mapped slots (the queued sweep reads one slot);
+  // two-way lookups still find every key
+  bool direct = false;
   uint64_t* keys = nullptr;  // [S][2 << lgnb]
   uint32_t* ids = nullptr;   // [S][2 << lgnb] (~0u: empty slot)
 };
@@ -83,13 +87,17 @@ struct HotSweep {
   // queued extension sweep: a tile whose lanes hold at most this many live
   // positions each is walked live position by live position (0: never)
   uint32_t sparse_iters = 10;
+  bool direct = false;  // HotSet::direct
 };
+// Whether launch_count_hot takes the queued sweep (which wants a direct table).
+bool hot_sweep_queued(const DevPrefixSet& ps, bool dense, uint32_t L, bool sliced);
 size_t hot_smem(uint32_t lgnb);
 // Hot set of each slice from the (sample) counts in table[0, cap).  pkeys:
 // gram key of id = (pkeys[id >> 8] << 8) | (id & 255), or null (key = id).
 template <typename CT>
 void build_hot_set(const CT* table, uint64_t cap, const HotSliceIds& sl, const uint64_t* pkeys,
-                   uint32_t lgnb, HotSet& hs, DevBuf& work, int num_sms, cudaStream_t st);
+                   uint32_t lgnb, HotSet& hs, DevBuf& work, int num_sms, cudaStream_t st,
+                   bool direct = false);
 template <typename CT, typename CC>
 void launch_count_hot(const DevCorpus& c, const DevPrefixSet& ps, bool dense, uint32_t L,
                       const HotSweep& hw, CT* table, CC* cold, int num_sms, cudaStream_t st);

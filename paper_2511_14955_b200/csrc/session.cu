@@ -593,9 +593,10 @@ static void count_all_hot(Session& s, bool dense, uint32_t L, const Prefix* P, C
   const size_t slots = (size_t)S * (2u << lgnb);
   hs.keys = s.hot_keys.as<uint64_t>(slots);
   hs.ids = s.hot_ids.as<uint32_t>(slots);
+  const bool direct = hot_sweep_queued(dense ? DevPrefixSet{} : P->ps, dense, L, S > 1);
   build_hot_set<uint32_t>(sample, tcap, sl, dense ? nullptr : P->ps.pkeys, lgnb, hs, s.hot_work,
-                          s.num_sms, s.stream);
-  s.launches += 6;
+                          s.num_sms, s.stream, direct);
+  s.launches += direct ? 5 : 6;
   // 4. sweeps: per < 2^32-position segment when the table is u64 (cold REDs
   // into a u32 scratch, widened after the segment), once per slice
   const DevPrefixSet& ps = dense ? DevPrefixSet{} : P->ps;
@@ -608,6 +609,7 @@ static void count_all_hot(Session& s, bool dense, uint32_t L, const Prefix* P, C
       hw.bounds = bounds + i;
       hw.first = i == 0;
       hw.sliced = S > 1;
+      hw.direct = hs.direct;
       hw.sparse_iters = (uint32_t)env_u64("IG_SPARSE_ITERS", 10);
       const size_t ev = s.kt.begin(IG_KF_COUNT_ALL, s.stream);
       launch_count_hot(dc, ps, dense, L, hw, t, cold, s.num_sms, s.stream);
