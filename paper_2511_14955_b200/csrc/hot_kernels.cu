@@ -746,6 +746,48 @@ __global__ void __launch_bounds__(hot_threads<PH>(), 1)
           hm |= qhit[lane];
           qhit[lane] = 0;
         }
+      } else if (KIND == 0 && hw.direct) {
+        // dense pass over a direct table (one slice), branch-free: one
+        // predicated 8-byte load and compare, a predicated shared add for a
+        // hot gram, a predicated RED for any other
+        hstatic_for<0, 16>([&](auto tc) {
+          constexpr int T = decltype(tc)::value;
+          const bool v = ((vm >> T) & 1u) != 0;
+          const uint64_t key = hkey8_at<T>(s) & hgram_mask<L>();
+          const uint32_t hh = (uint32_t)key * 0x9E3779B1u + (uint32_t)(key >> 32) * 0x85EBCA77u;
+          const uint32_t sl = hh >> lgnb_s;
+          const uint64_t k0 = lds_u64_if(s_keys + sl * 8, v);
+          const bool hot = v && k0 == key;
+          red_shared_if(s_cnt + sl * 4, hot);
+          if (v && !hot) atomicAdd(cold + key, (CC)1);
+        });
+      } else if (KIND == 1 && TAB == 5 && hw.direct) {
+        // the rank-bitmap (4-gram) pass over a direct table (one slice),
+        // branch-free: the hot lookup as above; any other position loads its
+        // 3-byte prefix's {bits, rank} pair (predicated), and a set bit is one
+        // RED at rank * 256 + last byte.  The 16 positions' loads are
+        // independent, so they overlap without a queue.
+        hstatic_for<0, 16>([&](auto tc) {
+          constexpr int T = decltype(tc)::value;
+          const bool v = ((vm >> T) & 1u) != 0;
+          const uint64_t key = hkey8_at<T>(s) & hgram_mask<L>();
+          const uint32_t hh = (uint32_t)key * 0x9E3779B1u + (uint32_t)(key >> 32) * 0x85EBCA77u;
+          const uint32_t sl = hh >> lgnb_s;
+          const uint64_t k0 = lds_u64_if(s_keys + sl * 8, v);
+          const bool hot = v && k0 == key;
+          red_shared_if(s_cnt + sl * 4, hot);
+          const bool cq = v && !hot;
+          const uint32_t pre = (uint32_t)(key >> 8);
+          ulonglong2 e = make_ulonglong2(0, 0);
+          if (cq) e = __ldg(reinterpret_cast<const ulonglong2*>(ptab) + (pre >> 6));
+          const uint64_t bit = 1ull << (pre & 63);
+          const bool hit = (e.x & bit) != 0;  // (e = 0 unless cq)
+          if (hit) {
+            const uint32_t p = (uint32_t)e.y + (uint32_t)__popcll(e.x & (bit - 1));
+            atomicAdd(cold + ((uint64_t)p * 256 + (uint32_t)(key & 0xff)), (CC)1);
+          }
+          if (hot || hit) hm |= 1u << T;
+        });
       } else
       hstatic_for<0, 16>([&](auto tc) {
         constexpr int T = decltype(tc)::value;
@@ -810,10 +852,11 @@ size_t hot_smem(uint32_t lgnb) { return ((size_t)1 << lgnb) * 24; }
 
 bool hot_sweep_queued(const DevPrefixSet& ps, bool dense, uint32_t L, bool sliced) {
   static const bool off = getenv("IG_HOT_SERIAL") != nullptr || getenv("IG_HOT_TWOWAY") != nullptr;
-  if (off || dense || sliced) return false;
-  // the rank-bitmap (4-gram) pass: serial kernel unless IG_HOT_Q5 (experiment)
-  static const bool q5 = getenv("IG_HOT_Q5") != nullptr;
-  if (L == 4 && ps.rankbits) return q5;
+  if (off || sliced) return false;
+  if (dense) return true;  // the dense sweep's branch-free path reads a direct table too
+  // the rank-bitmap (4-gram) pass: the serial kernel's branch-free path (the
+  // queued sweep only with IG_HOT_Q5: slower)
+  if (L == 4 && ps.rankbits) return true;
   return ps.packed != nullptr || ps.wide != nullptr;
 }
 static size_t hot_smem_q(uint32_t lgnb, int threads) {
@@ -846,6 +889,7 @@ void launch_count_hot(const DevCorpus& c, const DevPrefixSet& ps, bool dense, ui
   // queued cold probes (ballot-compacted per warp, probed 32 at a time);
   // the one-position-at-a-time kernel stays behind IG_HOT_SERIAL=1
   static const bool serial_env = getenv("IG_HOT_SERIAL") != nullptr;
+  static const bool q5 = getenv("IG_HOT_Q5") != nullptr;  // queued rank-bitmap pass (experiment)
   // the sparse variant (dead / sparse tiles, mask-gated corpus loads) is a
   // second kernel, so the dense sweep's loop stays inside the instruction
   // cache; only u32 tables (every chained pass of a < 2^32-count corpus)
@@ -857,7 +901,7 @@ void launch_count_hot(const DevCorpus& c, const DevPrefixSet& ps, bool dense, ui
   case J:                                                                                \
     if (J == 4 && ps.rankbits) {  /* one load per probe: the serial kernel is faster */ \
       if constexpr (J == 4) {                                                            \
-        if (!serial) {                                                                   \
+        if (q5 && !serial) {                                                             \
           go(k_count_hot<1, 4, 5, CT, CC, true>, ps.rankbits, true);                     \
           break;                                                                         \
         }                                                                                \

@@ -89,7 +89,8 @@ struct HotSweep {
   uint32_t sparse_iters = 10;
   bool direct = false;  // HotSet::direct
 };
-// Whether launch_count_hot takes the queued sweep (which wants a direct table).
+// Whether this pass's sweep reads a direct table: the queued extension sweep
+// (launch_count_hot takes it exactly then) and the one-slice dense sweep.
 bool hot_sweep_queued(const DevPrefixSet& ps, bool dense, uint32_t L, bool sliced);
 size_t hot_smem(uint32_t lgnb);
 // Hot set of each slice from the (sample) counts in table[0, cap).  pkeys:
