@@ -603,7 +603,8 @@ __global__ void __launch_bounds__(hot_threads<PH>(), 1)
     uint4 v = make_uint4(0, 0, 0, 0);
     uint2 h = make_uint2(0, 0);
     uint32_t d = 0x80000000u;  // dead tile: "all positions valid" & an empty mask
-    if (!sparse || live_of(mk)) {
+    bool cur_live = !sparse || live_of(mk);  // warp-uniform: the tile has a live position
+    if (cur_live) {
       v = __ldcs(reinterpret_cast<const uint4*>(c.data + t * kTileBytes + lane * 16));
       if (lane == 0) h = *reinterpret_cast<const uint2*>(c.data + t * kTileBytes - 8);
       d = __ldg(c.tile_seq + t);
@@ -615,8 +616,10 @@ __global__ void __launch_bounds__(hot_threads<PH>(), 1)
       uint4 vn = make_uint4(0, 0, 0, 0);
       uint2 hn = make_uint2(0, 0);
       uint32_t dn = 0x80000000u, mknn = 0xffffffffu;
+      bool next_live = true;
       if (sparse) {
-        if (tn < c.ntiles && live_of(mkn)) {
+        next_live = tn < c.ntiles && live_of(mkn);
+        if (next_live) {
           vn = __ldcs(reinterpret_cast<const uint4*>(c.data + tn * kTileBytes + lane * 16));
           if (lane == 0) hn = *reinterpret_cast<const uint2*>(c.data + tn * kTileBytes - 8);
           dn = __ldg(c.tile_seq + tn);
@@ -628,6 +631,8 @@ __global__ void __launch_bounds__(hot_threads<PH>(), 1)
         dn = __ldg(c.tile_seq + tn);
         if (chain) mkn = mask_at(tn);
       }
+      uint32_t hm = 0;
+      if (!SP || cur_live) {  // (a dead tile of a sparse pass: only its zero hit-mask word)
       HSeg s;
       s.W[2] = v.x;
       s.W[3] = v.y;
@@ -646,7 +651,6 @@ __global__ void __launch_bounds__(hot_threads<PH>(), 1)
         const uint32_t up = __shfl_up_sync(0xffffffffu, mk, 1);
         vm &= (mk << 1) | (((lane == 0 ? mk >> 16 : up) >> 15) & 1u);
       }
-      uint32_t hm = 0;
       if constexpr (PH && KIND == 1) {
         // hot grams in shared memory; the others go to this warp's queue
         // (ballot-compacted), drained 32 at a time with every lane probing
@@ -816,6 +820,7 @@ __global__ void __launch_bounds__(hot_threads<PH>(), 1)
           }
         }
       });
+      }
       if (KIND == 1 && ps.hit_out != nullptr) {
         uint16_t* w = ps.hit_out + t * 32 + lane;
         if (hw.first) __stcs(w, (uint16_t)hm);  // slice 0 writes every word
@@ -828,6 +833,7 @@ __global__ void __launch_bounds__(hot_threads<PH>(), 1)
       d = dn;
       mk = mkn;
       if (sparse) mkn = mknn;
+      cur_live = next_live;
       ++kcur;
     }
   }
