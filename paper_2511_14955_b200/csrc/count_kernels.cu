@@ -147,9 +147,10 @@ __device__ __forceinline__ uint32_t valid_mask_one(int64_t b0, int64_t s0, int64
 // Returns p or 0xffffffff.  Slices: keys[o*S .. o*S+S).
 __device__ __forceinline__ uint32_t prefix_lookup(const uint64_t* __restrict__ hkeys,
                                                   const uint32_t* __restrict__ hidx, uint32_t S,
-                                                  uint32_t lgS, uint32_t o, uint64_t key) {
+                                                  uint32_t lgS, uint32_t o, uint64_t key,
+                                                  uint32_t hmask = ~3u) {
   const uint64_t* kk = hkeys + (size_t)o * S;
-  uint32_t h = hash_slot(key, lgS);
+  uint32_t h = hash_slot(key, lgS, hmask);
   for (;;) {
     const uint64_t k = __ldg(kk + h);
     if (k == key) return __ldg(hidx + (size_t)o * S + h);
@@ -176,9 +177,9 @@ __device__ __forceinline__ uint32_t lookup_packed(const uint64_t* tab, uint32_t 
 
 // The same probe over {key, p} 16-byte slots: one 16-byte load per probe.
 __device__ __forceinline__ uint32_t lookup_wide(const uint64_t* __restrict__ wide, uint32_t lgS,
-                                                uint64_t key) {
+                                                uint64_t key, uint32_t hmask) {
   const uint32_t mask = (1u << lgS) - 1;
-  uint32_t h = hash_slot(key, lgS);
+  uint32_t h = hash_slot(key, lgS, hmask);
   for (;;) {
     const ulonglong2 e = __ldg(reinterpret_cast<const ulonglong2*>(wide) + h);
     if (e.x == key) return (uint32_t)e.y;
@@ -438,9 +439,9 @@ __global__ void __launch_bounds__(512, 3) k_count_all(DevCorpus c, DevPrefixSet 
             uint32_t p;
             if constexpr (TAB == 1) p = lookup_packed(s_tab, ps.lgS, ps.ib, key >> 8);
             else if constexpr (TAB == 3) p = lookup_packed<true>(packed, ps.lgS, ps.ib, key >> 8);
-            else if constexpr (TAB == 4) p = lookup_wide(packed, ps.lgS, key >> 8);
+            else if constexpr (TAB == 4) p = lookup_wide(packed, ps.lgS, key >> 8, ps.hmask);
             else if constexpr (TAB == 5) p = lookup_rank(packed, (uint32_t)(key >> 8));
-            else p = prefix_lookup(ps.hkeys, ps.hidx, ps.S, ps.lgS, 0, key >> 8);
+            else p = prefix_lookup(ps.hkeys, ps.hidx, ps.S, ps.lgS, 0, key >> 8, ps.hmask);
             if (p != 0xffffffffu) {
               count_one<CT>(p * 256 + (uint32_t)(key & 0xff), tag, hcnt, table);
               hm |= 1u << T;
@@ -701,7 +702,8 @@ __global__ void k_prefix_insert(const uint64_t* __restrict__ keys, uint32_t K,
                                 uint32_t* __restrict__ cursor, uint32_t S, uint32_t lgS,
                                 uint64_t* __restrict__ hkeys, uint32_t* __restrict__ hidx,
                                 uint64_t* __restrict__ pkeys, uint32_t* __restrict__ rank_of_p,
-                                bool S_single, const uint32_t* __restrict__ ranks) {
+                                bool S_single, const uint32_t* __restrict__ ranks,
+                                uint32_t hmask) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < K; i += gridDim.x * blockDim.x) {
     const uint32_t o = owner[i];
     // single slice (count-all): p = rank, identical on every rank of a
@@ -711,7 +713,7 @@ __global__ void k_prefix_insert(const uint64_t* __restrict__ keys, uint32_t K,
     pkeys[p] = key;
     rank_of_p[p] = ranks ? ranks[i] : i;
     unsigned long long* kk = reinterpret_cast<unsigned long long*>(hkeys + (size_t)o * S);
-    uint32_t h = hash_slot(key, lgS);
+    uint32_t h = hash_slot(key, lgS, hmask);
     for (;;) {
       const unsigned long long prev = atomicCAS(kk + h, (unsigned long long)kEmptyKey,
                                                 (unsigned long long)key);
@@ -735,12 +737,12 @@ void launch_prefix_owner(const uint64_t* keys, uint32_t K, uint32_t plen, uint32
 void launch_prefix_insert(const uint64_t* keys, uint32_t K, const uint32_t* owner,
                           const uint32_t* owner_start, uint32_t* cursor, uint32_t S, uint32_t lgS,
                           uint64_t* hkeys, uint32_t* hidx, uint64_t* pkeys, uint32_t* rank_of_p,
-                          cudaStream_t st, const uint32_t* ranks) {
+                          cudaStream_t st, const uint32_t* ranks, uint32_t hmask) {
   if (!K) return;
   const unsigned blocks = (K + 255) / 256;
   k_prefix_insert<<<blocks < 4096 ? blocks : 4096, 256, 0, st>>>(
       keys, K, owner, owner_start, cursor, S, lgS, hkeys, hidx, pkeys, rank_of_p,
-      owner_start == nullptr, ranks);
+      owner_start == nullptr, ranks, hmask);
 }
 
 }  // namespace igb

@@ -130,7 +130,7 @@ __device__ __forceinline__ uint32_t vocab_col(const EmitSpec& sp, uint64_t key) 
 }
 
 __device__ __forceinline__ uint32_t survivor_rank(const DevPrefixSet& ps, uint64_t key) {
-  uint32_t h = hash_slot(key, ps.lgS);
+  uint32_t h = hash_slot(key, ps.lgS, ps.hmask);
   for (;;) {
     const uint64_t k = ps.hkeys[h];
     if (k == key) return ps.hidx[h];

@@ -322,9 +322,9 @@ __device__ __noinline__ uint32_t hlookup_wide_from(const uint64_t* __restrict__ 
 }
 
 __device__ __forceinline__ uint32_t hlookup_wide(const uint64_t* __restrict__ wide, uint32_t lgS,
-                                                 uint64_t key) {
+                                                 uint64_t key, uint32_t hmask) {
   const uint32_t mask = (1u << lgS) - 1;
-  uint32_t h = hash_slot(key, lgS);
+  uint32_t h = hash_slot(key, lgS, hmask);
   for (;;) {
     const ulonglong2 e = __ldg(reinterpret_cast<const ulonglong2*>(wide) + h);
     if (e.x == key) return (uint32_t)e.y;
@@ -397,7 +397,7 @@ __device__ __forceinline__ uint32_t hlookup_bucket(const uint64_t* __restrict__ 
     }
   } else {
     const uint32_t mask = (1u << ps.lgS) - 1;
-    for (uint32_t h = hash_slot(pk, ps.lgS);; h = (h + 2) & mask) {
+    for (uint32_t h = hash_slot(pk, ps.lgS, ps.hmask);; h = (h + 2) & mask) {
       const ulonglong2* b = reinterpret_cast<const ulonglong2*>(ptab) + h;
       const ulonglong2 x = __ldg(b), y = __ldg(b + 1);
       if (x.x == pk) return (uint32_t)x.y;
@@ -441,7 +441,7 @@ __device__ __forceinline__ ulonglong2 hfirst(const uint64_t* __restrict__ ptab,
     h = hash_slot(pk, ps.lgS);
     return make_ulonglong2(__ldg(ptab + h), 0ull);
   } else {
-    h = hash_slot(pk, ps.lgS);
+    h = hash_slot(pk, ps.lgS, ps.hmask);
     return __ldg(reinterpret_cast<const ulonglong2*>(ptab) + h);
   }
 }
@@ -488,6 +488,7 @@ __global__ void __launch_bounds__(hot_threads<PH>(), 1)
   const uint32_t s_qpos = opaque_u32((uint32_t)__cvta_generic_to_shared(qpos));
   const uint32_t lgnb_s = opaque_u32(31 - hw.lgnb);  // slot = hash >> lgnb_s (lgnb + 1 bits)
   const uint32_t slot_sh = opaque_u32(64 - ps.lgS);  // hash_slot's shift
+  const uint32_t slot_hm = TAB == 4 ? ps.hmask : ~3u;  // and its home alignment
   uint32_t qhead = 0, qtail = 0;  // warp-uniform
   const uint32_t lt_mask = (1u << lane) - 1u;
   if constexpr (PH && KIND == 1) qhit[lane] = 0;
@@ -540,7 +541,7 @@ __global__ void __launch_bounds__(hot_threads<PH>(), 1)
         p = m0 ? (uint32_t)pfa.y : m1 ? (uint32_t)pfb.y : anye ? 0xffffffffu : 0xfffffffeu;
         if (p == 0xfffffffeu)  // both slots taken by other keys: the next bucket
           p = hlookup_wide_from(ptab, ps.lgS, pk,
-                                (hash_slot(pk, ps.lgS) + 2) & ((1u << ps.lgS) - 1));
+                                (hash_slot(pk, ps.lgS, ps.hmask) + 2) & ((1u << ps.lgS) - 1));
       }
       if (p != 0xffffffffu) {
         atomicAdd(cold + ((uint64_t)p * 256 + (uint32_t)(pfkey & 0xff)), (CC)1);
@@ -566,7 +567,7 @@ __global__ void __launch_bounds__(hot_threads<PH>(), 1)
       } else {
         // hash_slot(pk, lgS) with the shift in a register (lgS >= 3 here:
         // tables that fit shared memory take the plain kernel)
-        const uint32_t hh = (uint32_t)((pk * 0x9E3779B97F4A7C15ull) >> slot_sh) & ~3u;
+        const uint32_t hh = (uint32_t)((pk * 0x9E3779B97F4A7C15ull) >> slot_sh) & slot_hm;
         const ulonglong2* bk = TAB == 3 ? reinterpret_cast<const ulonglong2*>(ptab + hh)
                                         : reinterpret_cast<const ulonglong2*>(ptab) + hh;
         // the 32-byte bucket in one 256-bit load (homes are 32-byte aligned)
@@ -810,7 +811,7 @@ __global__ void __launch_bounds__(hot_threads<PH>(), 1)
             } else {
               uint32_t p;
               if constexpr (TAB == 3) p = hlookup_packed(ptab, ps.lgS, ps.ib, key >> 8);
-              else if constexpr (TAB == 4) p = hlookup_wide(ptab, ps.lgS, key >> 8);
+              else if constexpr (TAB == 4) p = hlookup_wide(ptab, ps.lgS, key >> 8, ps.hmask);
               else p = hlookup_rank(ptab, (uint32_t)(key >> 8));
               if (p != 0xffffffffu) {
                 atomicAdd(cold + ((uint64_t)p * 256 + (uint32_t)(key & 0xff)), (CC)1);

@@ -255,6 +255,7 @@ struct DevPrefixSet {
   uint32_t plen = 0;       // prefix length (j-1)
   uint32_t max_owner = 0;  // largest owner slice size
   uint32_t ib = 0;         // local-index bits of a packed entry
+  uint32_t hmask = ~3u;    // home alignment of the open-addressing slots (hash_slot)
   const uint64_t* packed = nullptr;  // [G*S] (key << ib) | local, or null
   const uint64_t* wide = nullptr;    // [2*S] {key, p} slots (G == 1), or null
   // 3-byte prefixes (the first extension pass): {bits, rank} pairs over the
@@ -274,8 +275,10 @@ struct DevPrefixSet {
 // Home slot of a key in an open-addressing table of 2^lgS slots: always a
 // multiple of 4, so a probe can read whole 4-slot (32-byte) buckets while a
 // slot-by-slot linear probe from the same home stays valid.
-__host__ __device__ inline uint32_t hash_slot(uint64_t key, uint32_t lgS) {
-  return lgS <= 2 ? 0u : (uint32_t)((key * 0x9E3779B97F4A7C15ull) >> (64 - lgS)) & ~3u;
+// hmask: ~3u (4-aligned homes: packed 8-byte slots, a 32-byte bucket holds 4)
+// or ~1u (2-aligned: {key, p} 16-byte slots, a 32-byte bucket holds 2).
+__host__ __device__ inline uint32_t hash_slot(uint64_t key, uint32_t lgS, uint32_t hmask = ~3u) {
+  return lgS <= 2 ? 0u : (uint32_t)((key * 0x9E3779B97F4A7C15ull) >> (64 - lgS)) & hmask;
 }
 
 // Owner slice of a prefix key (count-once passes): first byte xor last byte.

@@ -28,7 +28,8 @@ void launch_prefix_owner(const uint64_t* keys, uint32_t K, uint32_t plen, uint32
 void launch_prefix_insert(const uint64_t* keys, uint32_t K, const uint32_t* owner,
                           const uint32_t* owner_start, uint32_t* cursor, uint32_t S, uint32_t lgS,
                           uint64_t* hkeys, uint32_t* hidx, uint64_t* pkeys, uint32_t* rank_of_p,
-                          cudaStream_t st, const uint32_t* ranks = nullptr);
+                          cudaStream_t st, const uint32_t* ranks = nullptr,
+                          uint32_t hmask = ~3u);
 // keys[0..K) ascending (key_bits significant bits) with their input indices
 void sort_keys_by_value(const uint64_t* keys, uint32_t K, uint32_t key_bits, uint64_t* out_keys,
                         uint32_t* out_ranks, uint32_t* tmp_ranks, DevBuf& tmp, cudaStream_t st);

@@ -271,6 +271,13 @@ static DevPrefixSet build_prefix_set(Session& s, const uint64_t* keys, uint64_t 
   uint64_t* pk = s.pkeys.as<uint64_t>(K + 1);
   uint32_t* rp = s.rank_of_p.as<uint32_t>(K + 1);
   IGB_CUDA(cudaMemsetAsync(hk, 0xff, (size_t)G * S * sizeof(uint64_t), s.stream));
+  // a set that will be read as {key, p} 16-byte slots (key and index do not
+  // pack into 64 bits) gets 2-aligned homes: a 32-byte probe holds 2 slots
+  {
+    uint32_t ibw = 1;
+    while ((1ull << ibw) <= mx) ++ibw;
+    ps.hmask = (8 * plen + ibw > 64 && G == 1) ? ~1u : ~3u;
+  }
   // p = rank in key order (deterministic on every GPU; hot-gram slices of
   // the pass table are then contiguous p ranges)
   uint64_t* sk = s.sort_keys.as<uint64_t>(K + 1);
@@ -278,7 +285,7 @@ static DevPrefixSet build_prefix_set(Session& s, const uint64_t* keys, uint64_t 
   sort_keys_by_value(keys, (uint32_t)K, 8 * plen, sk, sr, sr + K + 1, s.sort_tmp, s.stream);
   s.launches += 2;
   launch_prefix_insert(sk, (uint32_t)K, owner, G == 1 ? nullptr : ostart, cursor, S, lgS, hk, hi,
-                       pk, rp, s.stream, sr);
+                       pk, rp, s.stream, sr, ps.hmask);
   s.launches++;
   ps.pkeys = pk;
   ps.hkeys = hk;
