@@ -6,7 +6,7 @@
 // proj/src/intergrams.cpp:44-66, id = p * 256 + last byte when the (j-1)-byte
 // prefix is survivor p).  Only the way the additions reach the table changes:
 //
-//   1. sample  — 1/64 of the 512-byte tiles (t % 64 == 0) are counted by the
+//   1. sample  — every 16th to 256th 512-byte tile (~64 MiB) is counted by the
 //                plain kernel into a scratch table (thrown away after step 2;
 //                the sweeps count every tile, sampled ones included).
 //   2. select  — per slice of the table's id range, the ids with the largest

@@ -57,7 +57,7 @@ void launch_rank_prefix(const uint64_t* keys, uint32_t K, uint64_t* rankbits, ui
                         uint32_t* rank_of_p, cudaStream_t st);
 
 // --- count-all with sampled hot-gram tables (hot_kernels.cu)
-constexpr uint32_t kHotSampleStride = 64;  // sample tiles: t % 64 == 0
+constexpr uint32_t kHotSampleStrideMin = 16, kHotSampleStrideMax = 256;  // sample tiles: t % stride == 0
 constexpr int kMaxHotSlices = 8;
 // Slices of a pass table's id range: slice s = ids [lo[s], lo[s+1]).
 struct HotSliceIds {

@@ -578,14 +578,18 @@ static void count_all_hot(Session& s, bool dense, uint32_t L, const Prefix* P, C
     launch_slice_bounds(P->ps.pkeys, (uint32_t)K, S, bounds, s.stream);
     s.launches++;
   }
-  // 1. sample: tiles t % 64 == 0, plain kernel, into a u32 scratch (< 2^32
-  // positions: 1/64 of the corpus); the sweeps below count every tile
+  // 1. sample: every stride-th tile, plain kernel, into a u32 scratch (< 2^32
+  // positions: at most 1/16 of the corpus); the sweeps below count every tile
   uint32_t* sample = s.scratch32.as<uint32_t>(tcap);
   IGB_CUDA(cudaMemsetAsync(sample, 0, tcap * 4, s.stream));
   {
     DevCorpus dc = s.dc;
     dc.tile0 = 0;
-    dc.tstride = kHotSampleStride;
+    // ~2^17 sample tiles (64 MiB): every 16th tile of a 1 GiB corpus, every
+    // 256th from 16 GiB up (c3: 64 -> 256 saved 6 ms per run, same hot sets)
+    const uint64_t want = std::max<uint64_t>(kHotSampleStrideMin,
+                                             std::min<uint64_t>(kHotSampleStrideMax, s.dc.ntiles >> 17));
+    dc.tstride = (uint32_t)env_u64("IG_HOT_SAMPLE_STRIDE", want);
     DevPrefixSet sps = dense ? DevPrefixSet{} : P->ps;
     sps.hit_out = nullptr;  // the sweeps write this pass's hit masks
     const size_t ev = s.kt.begin(IG_KF_COUNT_ALL, s.stream);
