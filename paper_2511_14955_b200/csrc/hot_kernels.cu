@@ -134,13 +134,15 @@ __global__ void k_hot_collect(const CT* __restrict__ t, uint64_t cap, HotSliceId
 __global__ void k_hot_best(const unsigned long long* __restrict__ cand,
                            const uint32_t* __restrict__ ncand, uint32_t S, uint32_t ccap,
                            HotKeyFn kf, uint32_t lgnb, int way,
-                           unsigned long long* __restrict__ best) {
+                           unsigned long long* __restrict__ best,
+                           unsigned long long drop_above) {
   const uint32_t nb = 1u << lgnb;
   for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < (uint64_t)S * ccap;
        g += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t s = (uint32_t)(g / ccap), i = (uint32_t)(g % ccap);
     if (i >= min(ncand[s], ccap)) continue;
     const unsigned long long v = cand[g];
+    if ((v >> 32) > drop_above) continue;  // experiment: the hottest grams stay cold
     if (way < 0) {  // direct: the way is the next hash bit
       atomicMax(best + (uint64_t)s * nb * 2 + hot_bucket(kf(v & 0xffffffffu), lgnb + 1), v);
       continue;
@@ -197,11 +199,15 @@ void build_hot_set(const CT* table, uint64_t cap, const HotSliceIds& sl, const u
   k_hot_collect<CT><<<gb ? gb : 1, 256, 0, st>>>(table, cap, sl, thr, ccap, nc, cand);
   const HotKeyFn kf{pkeys};
   const unsigned cb = (unsigned)std::min<uint64_t>(((uint64_t)S * ccap + 255) / 256, 4096);
+  // IG_HOT_DROP_ABOVE=c (experiment): candidates with a sample count above c
+  // are left out of the table, i.e. the hottest grams are counted by L2 REDs
+  static const char* drop_env = getenv("IG_HOT_DROP_ABOVE");
+  const unsigned long long drop = drop_env ? strtoull(drop_env, nullptr, 10) : ~0ull;
   if (direct) {
-    k_hot_best<<<cb, 256, 0, st>>>(cand, nc, S, ccap, kf, lgnb, -1, best);
+    k_hot_best<<<cb, 256, 0, st>>>(cand, nc, S, ccap, kf, lgnb, -1, best, drop);
   } else {
-    k_hot_best<<<cb, 256, 0, st>>>(cand, nc, S, ccap, kf, lgnb, 0, best);
-    k_hot_best<<<cb, 256, 0, st>>>(cand, nc, S, ccap, kf, lgnb, 1, best);
+    k_hot_best<<<cb, 256, 0, st>>>(cand, nc, S, ccap, kf, lgnb, 0, best, drop);
+    k_hot_best<<<cb, 256, 0, st>>>(cand, nc, S, ccap, kf, lgnb, 1, best, drop);
   }
   const unsigned fb = (unsigned)std::min<uint64_t>(((uint64_t)S * nb * 2 + 255) / 256, 4096);
   k_hot_fill<<<fb, 256, 0, st>>>(best, S, kf, lgnb, hs.keys, hs.ids);
