@@ -154,6 +154,26 @@ __global__ void k_hot_best(const unsigned long long* __restrict__ cand,
   }
 }
 
+// Direct tables: candidates with a sample count of at least `imp` that lost
+// their slot to a hotter key (they would be counted by same-address L2 REDs,
+// which serialise: c3's dense pass takes 400 ms instead of 38 with its few
+// hottest grams left out).  The host rebuilds two-way when any exists.
+__global__ void k_hot_lost(const unsigned long long* __restrict__ cand,
+                           const uint32_t* __restrict__ ncand, uint32_t S, uint32_t ccap,
+                           HotKeyFn kf, uint32_t lgnb, const unsigned long long* __restrict__ best,
+                           unsigned long long imp, uint32_t* __restrict__ lost) {
+  const uint32_t nb = 1u << lgnb;
+  for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < (uint64_t)S * ccap;
+       g += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t s = (uint32_t)(g / ccap), i = (uint32_t)(g % ccap);
+    if (i >= min(ncand[s], ccap)) continue;
+    const unsigned long long v = cand[g];
+    if ((v >> 32) < imp) continue;
+    if (best[(uint64_t)s * nb * 2 + hot_bucket(kf(v & 0xffffffffu), lgnb + 1)] != v)
+      atomicAdd(lost, 1u);
+  }
+}
+
 __global__ void k_hot_fill(const unsigned long long* __restrict__ best, uint32_t S, HotKeyFn kf,
                            uint32_t lgnb, uint64_t* __restrict__ keys, uint32_t* __restrict__ ids) {
   const uint32_t nb = 1u << lgnb;
@@ -177,7 +197,7 @@ __global__ void k_hot_fill(const unsigned long long* __restrict__ best, uint32_t
 template <typename CT>
 void build_hot_set(const CT* table, uint64_t cap, const HotSliceIds& sl, const uint64_t* pkeys,
                    uint32_t lgnb, HotSet& hs, DevBuf& work, int num_sms, cudaStream_t st,
-                   bool direct) {
+                   bool direct, uint64_t important) {
   const uint32_t S = sl.S, nb = 1u << lgnb;
   const uint32_t ccap = 2 * nb * 2;  // candidates per slice: twice the slots
   // work layout: hist | thr | ncand | cand | best
@@ -203,8 +223,12 @@ void build_hot_set(const CT* table, uint64_t cap, const HotSliceIds& sl, const u
   // are left out of the table, i.e. the hottest grams are counted by L2 REDs
   static const char* drop_env = getenv("IG_HOT_DROP_ABOVE");
   const unsigned long long drop = drop_env ? strtoull(drop_env, nullptr, 10) : ~0ull;
+  hs.lost = nullptr;
   if (direct) {
     k_hot_best<<<cb, 256, 0, st>>>(cand, nc, S, ccap, kf, lgnb, -1, best, drop);
+    hs.lost = nc + 15;  // (zeroed with the work header above)
+    k_hot_lost<<<cb, 256, 0, st>>>(cand, nc, S, ccap, kf, lgnb, best,
+                                   std::max<unsigned long long>(important, 1), hs.lost);
   } else {
     k_hot_best<<<cb, 256, 0, st>>>(cand, nc, S, ccap, kf, lgnb, 0, best, drop);
     k_hot_best<<<cb, 256, 0, st>>>(cand, nc, S, ccap, kf, lgnb, 1, best, drop);
@@ -218,10 +242,11 @@ void build_hot_set(const CT* table, uint64_t cap, const HotSliceIds& sl, const u
 
 template void build_hot_set<uint32_t>(const uint32_t*, uint64_t, const HotSliceIds&,
                                       const uint64_t*, uint32_t, HotSet&, DevBuf&, int,
-                                      cudaStream_t, bool);
+                                      cudaStream_t, bool, uint64_t);
 template void build_hot_set<unsigned long long>(const unsigned long long*, uint64_t,
                                                 const HotSliceIds&, const uint64_t*, uint32_t,
-                                                HotSet&, DevBuf&, int, cudaStream_t, bool);
+                                                HotSet&, DevBuf&, int, cudaStream_t, bool,
+                                                uint64_t);
 
 // ---------------------------------------------------------------- sweep
 

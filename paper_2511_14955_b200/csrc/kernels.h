@@ -71,6 +71,10 @@ struct HotSet {
   // table is 2 << lgnb direct-mapped slots (the queued sweep reads one slot);
   // two-way lookups still find every key
   bool direct = false;
+  // direct: device count of important candidates (sample count >= the
+  // builder's `important`) that lost their slot; the caller rebuilds two-way
+  // when it is not zero
+  uint32_t* lost = nullptr;
   uint64_t* keys = nullptr;  // [S][2 << lgnb]
   uint32_t* ids = nullptr;   // [S][2 << lgnb] (~0u: empty slot)
 };
@@ -99,7 +103,7 @@ size_t hot_smem(uint32_t lgnb);
 template <typename CT>
 void build_hot_set(const CT* table, uint64_t cap, const HotSliceIds& sl, const uint64_t* pkeys,
                    uint32_t lgnb, HotSet& hs, DevBuf& work, int num_sms, cudaStream_t st,
-                   bool direct = false);
+                   bool direct = false, uint64_t important = ~0ull);
 template <typename CT, typename CC>
 void launch_count_hot(const DevCorpus& c, const DevPrefixSet& ps, bool dense, uint32_t L,
                       const HotSweep& hw, CT* table, CC* cold, int num_sms, cudaStream_t st);

@@ -582,6 +582,7 @@ static void count_all_hot(Session& s, bool dense, uint32_t L, const Prefix* P, C
   // positions: at most 1/16 of the corpus); the sweeps below count every tile
   uint32_t* sample = s.scratch32.as<uint32_t>(tcap);
   IGB_CUDA(cudaMemsetAsync(sample, 0, tcap * 4, s.stream));
+  uint32_t sample_stride = kHotSampleStrideMin;
   {
     DevCorpus dc = s.dc;
     dc.tile0 = 0;
@@ -589,7 +590,8 @@ static void count_all_hot(Session& s, bool dense, uint32_t L, const Prefix* P, C
     // 256th from 16 GiB up (c3: 64 -> 256 saved 6 ms per run, same hot sets)
     const uint64_t want = std::max<uint64_t>(kHotSampleStrideMin,
                                              std::min<uint64_t>(kHotSampleStrideMax, s.dc.ntiles >> 17));
-    dc.tstride = (uint32_t)env_u64("IG_HOT_SAMPLE_STRIDE", want);
+    sample_stride = (uint32_t)env_u64("IG_HOT_SAMPLE_STRIDE", want);
+    dc.tstride = sample_stride;
     DevPrefixSet sps = dense ? DevPrefixSet{} : P->ps;
     sps.hit_out = nullptr;  // the sweeps write this pass's hit masks
     const size_t ev = s.kt.begin(IG_KF_COUNT_ALL, s.stream);
@@ -604,10 +606,25 @@ static void count_all_hot(Session& s, bool dense, uint32_t L, const Prefix* P, C
   const size_t slots = (size_t)S * (2u << lgnb);
   hs.keys = s.hot_keys.as<uint64_t>(slots);
   hs.ids = s.hot_ids.as<uint32_t>(slots);
-  const bool direct = hot_sweep_queued(dense ? DevPrefixSet{} : P->ps, dense, L, S > 1);
+  bool direct = hot_sweep_queued(dense ? DevPrefixSet{} : P->ps, dense, L, S > 1);
+  // a gram above ~1/1024 of the positions must not be left to same-address L2
+  // REDs: when a direct table (one slot per key) loses one to a hotter key,
+  // the table is rebuilt two-way and the pass takes the two-way kernels
+  const uint64_t sample_pos = (s.dc.ntiles / sample_stride + 1) * kTileBytes;
+  const uint64_t important = env_u64("IG_HOT_IMPORTANT", sample_pos >> 10);
   build_hot_set<uint32_t>(sample, tcap, sl, dense ? nullptr : P->ps.pkeys, lgnb, hs, s.hot_work,
-                          s.num_sms, s.stream, direct);
-  s.launches += direct ? 5 : 6;
+                          s.num_sms, s.stream, direct, important);
+  s.launches += 6;
+  if (direct) {
+    uint32_t lost = 0;
+    d2h(s, &lost, hs.lost, sizeof(lost));
+    if (lost) {
+      direct = false;
+      build_hot_set<uint32_t>(sample, tcap, sl, dense ? nullptr : P->ps.pkeys, lgnb, hs,
+                              s.hot_work, s.num_sms, s.stream, false, important);
+      s.launches += 6;
+    }
+  }
   // 4. sweeps: per < 2^32-position segment when the table is u64 (cold REDs
   // into a u32 scratch, widened after the segment), once per slice
   const DevPrefixSet& ps = dense ? DevPrefixSet{} : P->ps;

@@ -70,7 +70,10 @@ TOGGLES = [{}, {"IG_NO_HIT_CHAIN": "1"}, {"IG_NO_RANK_BITMAP": "1"},
            {**HOT, "IG_SPARSE_ITERS": "0"}, {**HOT, "IG_SPARSE_ITERS": "16"},
            {**HOT_SMALL, "IG_SPARSE_ITERS": "16"},
            # the sparse switch forced on (every chained pass) / off
-           {**HOT, "IG_SPARSE": "1"}, {**HOT, "IG_SPARSE": "0"}]
+           {**HOT, "IG_SPARSE": "1"}, {**HOT, "IG_SPARSE": "0"},
+           # direct hot tables: every candidate that loses its slot counts as
+           # important, so every pass falls back to the two-way build
+           {**HOT, "IG_HOT_IMPORTANT": "1"}, {**HOT, "IG_HOT_IMPORTANT": "1", "IG_SPARSE": "1"}]
 
 
 def run_with_env(env, fn):
