@@ -48,9 +48,13 @@ constexpr int kHotBins = 128;                        // semi-log count bins
 
 // Bucket of a hot-table key: a 32-bit mix of both key halves (4 ALU ops in
 // the sweep's inner loop instead of a 64-bit multiply).
-__host__ __device__ __forceinline__ uint32_t hot_bucket(uint64_t key, uint32_t lgnb) {
-  // the top bits of a sum of two odd-multiplier products: 2 IMAD + 1 shift
-  const uint32_t h = (uint32_t)key * 0x9E3779B1u + (uint32_t)(key >> 32) * 0x85EBCA77u;
+constexpr uint32_t kHotMul0 = 0x9E3779B1u;  // first multiplier of the low key word
+__host__ __device__ __forceinline__ uint32_t hot_bucket(uint64_t key, uint32_t lgnb,
+                                                        uint32_t mul) {
+  // the top bits of a sum of two odd-multiplier products: 2 IMAD + 1 shift.
+  // `mul` (odd) is the table's multiplier of the low key word: a rebuild with
+  // another one moves the keys apart that shared a slot.
+  const uint32_t h = (uint32_t)key * mul + (uint32_t)(key >> 32) * 0x85EBCA77u;
   return h >> (32 - lgnb);
 }
 
@@ -135,7 +139,7 @@ __global__ void k_hot_best(const unsigned long long* __restrict__ cand,
                            const uint32_t* __restrict__ ncand, uint32_t S, uint32_t ccap,
                            HotKeyFn kf, uint32_t lgnb, int way,
                            unsigned long long* __restrict__ best,
-                           unsigned long long drop_above) {
+                           unsigned long long drop_above, uint32_t mul) {
   const uint32_t nb = 1u << lgnb;
   for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < (uint64_t)S * ccap;
        g += (uint64_t)gridDim.x * blockDim.x) {
@@ -144,10 +148,10 @@ __global__ void k_hot_best(const unsigned long long* __restrict__ cand,
     const unsigned long long v = cand[g];
     if ((v >> 32) > drop_above) continue;  // experiment: the hottest grams stay cold
     if (way < 0) {  // direct: the way is the next hash bit
-      atomicMax(best + (uint64_t)s * nb * 2 + hot_bucket(kf(v & 0xffffffffu), lgnb + 1), v);
+      atomicMax(best + (uint64_t)s * nb * 2 + hot_bucket(kf(v & 0xffffffffu), lgnb + 1, mul), v);
       continue;
     }
-    const uint32_t b = hot_bucket(kf(v & 0xffffffffu), lgnb);
+    const uint32_t b = hot_bucket(kf(v & 0xffffffffu), lgnb, mul);
     unsigned long long* bk = best + ((uint64_t)s * nb + b) * 2;
     if (way == 1 && bk[0] == v) continue;
     atomicMax(bk + way, v);
@@ -161,7 +165,8 @@ __global__ void k_hot_best(const unsigned long long* __restrict__ cand,
 __global__ void k_hot_lost(const unsigned long long* __restrict__ cand,
                            const uint32_t* __restrict__ ncand, uint32_t S, uint32_t ccap,
                            HotKeyFn kf, uint32_t lgnb, const unsigned long long* __restrict__ best,
-                           unsigned long long imp, uint32_t* __restrict__ lost) {
+                           unsigned long long imp, uint32_t* __restrict__ lost, bool direct,
+                           uint32_t mul) {
   const uint32_t nb = 1u << lgnb;
   for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < (uint64_t)S * ccap;
        g += (uint64_t)gridDim.x * blockDim.x) {
@@ -169,13 +174,22 @@ __global__ void k_hot_lost(const unsigned long long* __restrict__ cand,
     if (i >= min(ncand[s], ccap)) continue;
     const unsigned long long v = cand[g];
     if ((v >> 32) < imp) continue;
-    if (best[(uint64_t)s * nb * 2 + hot_bucket(kf(v & 0xffffffffu), lgnb + 1)] != v)
-      atomicAdd(lost, 1u);
+    const unsigned long long* bs = best + (uint64_t)s * nb * 2;
+    const uint64_t key = kf(v & 0xffffffffu);
+    bool in;
+    if (direct) {
+      in = bs[hot_bucket(key, lgnb + 1, mul)] == v;
+    } else {
+      const uint32_t b = hot_bucket(key, lgnb, mul);
+      in = bs[2 * b] == v || bs[2 * b + 1] == v;
+    }
+    if (!in) atomicAdd(lost, 1u);
   }
 }
 
 __global__ void k_hot_fill(const unsigned long long* __restrict__ best, uint32_t S, HotKeyFn kf,
-                           uint32_t lgnb, uint64_t* __restrict__ keys, uint32_t* __restrict__ ids) {
+                           uint32_t lgnb, uint64_t* __restrict__ keys, uint32_t* __restrict__ ids,
+                           uint32_t mul) {
   const uint32_t nb = 1u << lgnb;
   for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < (uint64_t)S * nb * 2;
        g += (uint64_t)gridDim.x * blockDim.x) {
@@ -187,7 +201,7 @@ __global__ void k_hot_fill(const unsigned long long* __restrict__ best, uint32_t
     } else {
       // a key this bucket can never be asked for
       uint64_t k = ~0ull;
-      for (uint64_t c = 0; hot_bucket(k, lgnb) == b; ++c) k = c;
+      for (uint64_t c = 0; hot_bucket(k, lgnb, mul) == b; ++c) k = c;
       keys[g] = k;
       ids[g] = 0xffffffffu;
     }
@@ -197,7 +211,7 @@ __global__ void k_hot_fill(const unsigned long long* __restrict__ best, uint32_t
 template <typename CT>
 void build_hot_set(const CT* table, uint64_t cap, const HotSliceIds& sl, const uint64_t* pkeys,
                    uint32_t lgnb, HotSet& hs, DevBuf& work, int num_sms, cudaStream_t st,
-                   bool direct, uint64_t important) {
+                   bool direct, uint64_t important, uint32_t mul) {
   const uint32_t S = sl.S, nb = 1u << lgnb;
   const uint32_t ccap = 2 * nb * 2;  // candidates per slice: twice the slots
   // work layout: hist | thr | ncand | cand | best
@@ -223,30 +237,30 @@ void build_hot_set(const CT* table, uint64_t cap, const HotSliceIds& sl, const u
   // are left out of the table, i.e. the hottest grams are counted by L2 REDs
   static const char* drop_env = getenv("IG_HOT_DROP_ABOVE");
   const unsigned long long drop = drop_env ? strtoull(drop_env, nullptr, 10) : ~0ull;
-  hs.lost = nullptr;
   if (direct) {
-    k_hot_best<<<cb, 256, 0, st>>>(cand, nc, S, ccap, kf, lgnb, -1, best, drop);
-    hs.lost = nc + 15;  // (zeroed with the work header above)
-    k_hot_lost<<<cb, 256, 0, st>>>(cand, nc, S, ccap, kf, lgnb, best,
-                                   std::max<unsigned long long>(important, 1), hs.lost);
+    k_hot_best<<<cb, 256, 0, st>>>(cand, nc, S, ccap, kf, lgnb, -1, best, drop, mul);
   } else {
-    k_hot_best<<<cb, 256, 0, st>>>(cand, nc, S, ccap, kf, lgnb, 0, best, drop);
-    k_hot_best<<<cb, 256, 0, st>>>(cand, nc, S, ccap, kf, lgnb, 1, best, drop);
+    k_hot_best<<<cb, 256, 0, st>>>(cand, nc, S, ccap, kf, lgnb, 0, best, drop, mul);
+    k_hot_best<<<cb, 256, 0, st>>>(cand, nc, S, ccap, kf, lgnb, 1, best, drop, mul);
   }
+  hs.lost = nc + 15;  // (zeroed with the work header above)
+  k_hot_lost<<<cb, 256, 0, st>>>(cand, nc, S, ccap, kf, lgnb, best,
+                                 std::max<unsigned long long>(important, 1), hs.lost, direct, mul);
   const unsigned fb = (unsigned)std::min<uint64_t>(((uint64_t)S * nb * 2 + 255) / 256, 4096);
-  k_hot_fill<<<fb, 256, 0, st>>>(best, S, kf, lgnb, hs.keys, hs.ids);
+  k_hot_fill<<<fb, 256, 0, st>>>(best, S, kf, lgnb, hs.keys, hs.ids, mul);
   hs.S = S;
   hs.lgnb = lgnb;
   hs.direct = direct;
+  hs.mul = mul;
 }
 
 template void build_hot_set<uint32_t>(const uint32_t*, uint64_t, const HotSliceIds&,
                                       const uint64_t*, uint32_t, HotSet&, DevBuf&, int,
-                                      cudaStream_t, bool, uint64_t);
+                                      cudaStream_t, bool, uint64_t, uint32_t);
 template void build_hot_set<unsigned long long>(const unsigned long long*, uint64_t,
                                                 const HotSliceIds&, const uint64_t*, uint32_t,
                                                 HotSet&, DevBuf&, int, cudaStream_t, bool,
-                                                uint64_t);
+                                                uint64_t, uint32_t);
 
 // ---------------------------------------------------------------- sweep
 
@@ -518,6 +532,7 @@ __global__ void __launch_bounds__(hot_threads<PH>(), 1)
   const uint32_t s_qkey = opaque_u32((uint32_t)__cvta_generic_to_shared(qkey));
   const uint32_t s_qpos = opaque_u32((uint32_t)__cvta_generic_to_shared(qpos));
   const uint32_t lgnb_s = opaque_u32(31 - hw.lgnb);  // slot = hash >> lgnb_s (lgnb + 1 bits)
+  const uint32_t hmul = opaque_u32(hw.mul);          // the table's low-word multiplier
   const uint32_t slot_sh = opaque_u32(64 - ps.lgS);  // hash_slot's shift
   const uint32_t slot_hm = TAB == 4 ? ps.hmask : ~3u;  // and its home alignment
   uint32_t qhead = 0, qtail = 0;  // warp-uniform
@@ -694,7 +709,7 @@ __global__ void __launch_bounds__(hot_threads<PH>(), 1)
         // (one slice only: launch_count_hot sends sliced sweeps, which need
         // tables above IG_HOT_SLICE_MB = 4 GiB, to the serial kernel)
         auto step = [&](uint64_t key, uint32_t T, bool v) {
-          const uint32_t hh = (uint32_t)key * 0x9E3779B1u + (uint32_t)(key >> 32) * 0x85EBCA77u;
+          const uint32_t hh = (uint32_t)key * hmul + (uint32_t)(key >> 32) * 0x85EBCA77u;
           const uint32_t sl = hh >> lgnb_s;  // direct slot = 2 * hot_bucket + way bit
           // a predicated 8-byte load: lanes without a valid position add no
           // shared-memory wavefronts
@@ -790,7 +805,7 @@ __global__ void __launch_bounds__(hot_threads<PH>(), 1)
           constexpr int T = decltype(tc)::value;
           const bool v = ((vm >> T) & 1u) != 0;
           const uint64_t key = hkey8_at<T>(s) & hgram_mask<L>();
-          const uint32_t hh = (uint32_t)key * 0x9E3779B1u + (uint32_t)(key >> 32) * 0x85EBCA77u;
+          const uint32_t hh = (uint32_t)key * hmul + (uint32_t)(key >> 32) * 0x85EBCA77u;
           const uint32_t sl = hh >> lgnb_s;
           const uint64_t k0 = lds_u64_if(s_keys + sl * 8, v);
           const bool hot = v && k0 == key;
@@ -807,7 +822,7 @@ __global__ void __launch_bounds__(hot_threads<PH>(), 1)
           constexpr int T = decltype(tc)::value;
           const bool v = ((vm >> T) & 1u) != 0;
           const uint64_t key = hkey8_at<T>(s) & hgram_mask<L>();
-          const uint32_t hh = (uint32_t)key * 0x9E3779B1u + (uint32_t)(key >> 32) * 0x85EBCA77u;
+          const uint32_t hh = (uint32_t)key * hmul + (uint32_t)(key >> 32) * 0x85EBCA77u;
           const uint32_t sl = hh >> lgnb_s;
           const uint64_t k0 = lds_u64_if(s_keys + sl * 8, v);
           const bool hot = v && k0 == key;
@@ -831,7 +846,7 @@ __global__ void __launch_bounds__(hot_threads<PH>(), 1)
           const uint64_t key = hkey8_at<T>(s) & hgram_mask<L>();
           const uint64_t sk = KIND == 1 ? key >> 8 : key;
           if (!sliced || (sk >= lo && sk < hi)) {
-            const uint32_t b = hot_bucket(key, hw.lgnb);
+            const uint32_t b = hot_bucket(key, hw.lgnb, hmul);
             const ulonglong2 e = skeys[b];
             const uint32_t slot = e.x == key ? 2 * b : (e.y == key ? 2 * b + 1 : 0xffffffffu);
             if (slot != 0xffffffffu) {

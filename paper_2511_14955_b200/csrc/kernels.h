@@ -75,6 +75,7 @@ struct HotSet {
   // builder's `important`) that lost their slot; the caller rebuilds two-way
   // when it is not zero
   uint32_t* lost = nullptr;
+  uint32_t mul = 0x9E3779B1u;  // the table's multiplier of the low key word (hot_bucket)
   uint64_t* keys = nullptr;  // [S][2 << lgnb]
   uint32_t* ids = nullptr;   // [S][2 << lgnb] (~0u: empty slot)
 };
@@ -93,6 +94,7 @@ struct HotSweep {
   // positions each is walked live position by live position (0: never)
   uint32_t sparse_iters = 10;
   bool direct = false;  // HotSet::direct
+  uint32_t mul = 0x9E3779B1u;  // HotSet::mul
 };
 // Whether this pass's sweep reads a direct table: the queued extension sweep
 // (launch_count_hot takes it exactly then) and the one-slice dense sweep.
@@ -103,7 +105,7 @@ size_t hot_smem(uint32_t lgnb);
 template <typename CT>
 void build_hot_set(const CT* table, uint64_t cap, const HotSliceIds& sl, const uint64_t* pkeys,
                    uint32_t lgnb, HotSet& hs, DevBuf& work, int num_sms, cudaStream_t st,
-                   bool direct = false, uint64_t important = ~0ull);
+                   bool direct = false, uint64_t important = ~0ull, uint32_t mul = 0x9E3779B1u);
 template <typename CT, typename CC>
 void launch_count_hot(const DevCorpus& c, const DevPrefixSet& ps, bool dense, uint32_t L,
                       const HotSweep& hw, CT* table, CC* cold, int num_sms, cudaStream_t st);

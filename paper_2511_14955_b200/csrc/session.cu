@@ -612,17 +612,20 @@ static void count_all_hot(Session& s, bool dense, uint32_t L, const Prefix* P, C
   // the table is rebuilt two-way and the pass takes the two-way kernels
   const uint64_t sample_pos = (s.dc.ntiles / sample_stride + 1) * kTileBytes;
   const uint64_t important = env_u64("IG_HOT_IMPORTANT", sample_pos >> 10);
-  build_hot_set<uint32_t>(sample, tcap, sl, dense ? nullptr : P->ps.pkeys, lgnb, hs, s.hot_work,
-                          s.num_sms, s.stream, direct, important);
-  s.launches += 6;
-  if (direct) {
+  // up to 4 multipliers per table kind: a rebuild with another multiplier
+  // moves apart the keys that shared a slot; then (direct tables only) the
+  // two-way build, whose pass takes the two-way kernels
+  static const uint32_t kMuls[4] = {0x9E3779B1u, 0xC2B2AE3Du, 0x27D4EB2Fu, 0x165667B1u};
+  for (int attempt = 0;; ++attempt) {
+    build_hot_set<uint32_t>(sample, tcap, sl, dense ? nullptr : P->ps.pkeys, lgnb, hs,
+                            s.hot_work, s.num_sms, s.stream, direct, important, kMuls[attempt & 3]);
+    s.launches += 6 + (direct ? 0 : 1);
     uint32_t lost = 0;
     d2h(s, &lost, hs.lost, sizeof(lost));
-    if (lost) {
+    if (!lost) break;
+    if ((attempt & 3) == 3) {
+      if (!direct) break;  // every multiplier lost one: keep the last table
       direct = false;
-      build_hot_set<uint32_t>(sample, tcap, sl, dense ? nullptr : P->ps.pkeys, lgnb, hs,
-                              s.hot_work, s.num_sms, s.stream, false, important);
-      s.launches += 6;
     }
   }
   // 4. sweeps: per < 2^32-position segment when the table is u64 (cold REDs
@@ -638,6 +641,7 @@ static void count_all_hot(Session& s, bool dense, uint32_t L, const Prefix* P, C
       hw.first = i == 0;
       hw.sliced = S > 1;
       hw.direct = hs.direct;
+      hw.mul = hs.mul;
       hw.sparse_iters = (uint32_t)env_u64("IG_SPARSE_ITERS", 10);
       const size_t ev = s.kt.begin(IG_KF_COUNT_ALL, s.stream);
       launch_count_hot(dc, ps, dense, L, hw, t, cold, s.num_sms, s.stream);
